@@ -1,0 +1,364 @@
+"""Benchmark of the B200 parallel grid build (BASELINE.json metric on its headline config).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl reference]
+
+A "step" is one full build_parallel of the config's scene (default cfg3: the 10M-triangle
+architectural scene, density 4, 342^3 cells -- BASELINE.json configs[2], the paper's 25 Hz
+case). `value` = builds/s with inputs resident in HBM (device pointers through the C ABI);
+`e2e` = the same through the public numpy API (pinned host inputs, H2D + build + D2H of G
+and O inside the timed region). Rank 0 prints one JSON line.
+
+N > 1 (torchrun): every rank builds its own copy of the scene (replicas; weak scaling).
+`--impl reference` times the reference's own CPU build (oracle/_ref, C lane, all host
+threads) on the same config instead.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "grid builds/sec (Hz) + M pairs/s on 10M-tri scene; HBM GB/s vs peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--cpu-budget-s", type=float, default=150.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def traffic_table():
+    """Per-launch DRAM bytes of each kernel from the committed ncu capture (or {})."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def run_reference(args, world, rank):
+    """The reference's own CPU implementation on the same config (oracle/_ref, C lane)."""
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    from paper_2403_10647_b200 import scenes
+    ref = oracle.reference_module()
+    mesh, spec = scenes.config_scene(args.config)
+    cores = os.cpu_count() or 1
+    if ref is not None:
+        kind = "reference"
+        rmesh = ref.TriangleMesh(mesh.vertices, mesh.triangles)
+        rspec = ref.GridSpec(ref.Aabb(spec.bounds.lo, spec.bounds.hi), spec.dims)
+
+        def one():
+            g, rep = ref.build_parallel(rmesh, rspec, workers=cores)
+            return rep.no
+    else:
+        kind = "port"
+        cores = 1
+
+        def one():
+            G, O = oracle.build_parallel(mesh.vertices, mesh.triangles, spec)
+            return len(O)
+    t0 = time.perf_counter()
+    no = one()                       # warm-up build, also sizes the sample
+    t_first = time.perf_counter() - t0
+    warm = max(0, min(args.warmup, 1) - 1)
+    for _ in range(warm):
+        one()
+    steps = max(1, min(args.steps, int(args.cpu_budget_s // max(t_first, 1e-3))))
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        one()
+        times.append(time.perf_counter() - t0)
+    sec = statistics.median(times)
+    value = 1.0 / sec
+    sample = (f"full {args.config} build ({mesh.ntriangles} tris, dims {spec.dims}), "
+              f"{steps} timed of {args.steps} requested (CPU time cap {args.cpu_budget_s:.0f}s), "
+              f"workers={cores if kind == 'reference' else 1}, {cpu_model()}")
+    line = {"metric": METRIC, "impl": "reference", "value": round(value, 6), "unit": "builds/s",
+            "n_gpus": world, "steps": steps, "warmup": 1, "ms_per_step": round(sec * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32",
+            "data": "synthetic", "mpairs_per_s": round(no / sec / 1e6, 4),
+            "config": {"workload": args.config, "triangles": mesh.ntriangles, "dims": list(spec.dims),
+                       "no": int(no)},
+            "cpu_baseline": {"value": round(value, 6), "unit": "builds/s", "cores": cores, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": round(value, 6), "unit": "builds/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args, mesh, spec):
+    """Rank 0, N=1 only: the reference CPU build timed once on the same scene (~20-30 s)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    ref = oracle.reference_module()
+    if ref is not None:
+        rmesh = ref.TriangleMesh(mesh.vertices, mesh.triangles)
+        rspec = ref.GridSpec(ref.Aabb(spec.bounds.lo, spec.bounds.hi), spec.dims)
+        t0 = time.perf_counter()
+        ref.build_parallel(rmesh, rspec)
+        sec = time.perf_counter() - t0
+        return {"value": round(1.0 / sec, 6), "unit": "builds/s", "cores": 1, "kind": "reference",
+                "sample": f"1 full {args.config} build, reference pargrid C lane, workers=None "
+                          f"(single thread), {sec:.2f}s, {cpu_model()}"}
+    t0 = time.perf_counter()
+    oracle.build_parallel(mesh.vertices, mesh.triangles, spec)
+    sec = time.perf_counter() - t0
+    return {"value": round(1.0 / sec, 6), "unit": "builds/s", "cores": 1, "kind": "port",
+            "sample": f"1 full {args.config} build, C oracle port, single thread, {sec:.2f}s"}
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+        run_reference(args, world, rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2403_10647_b200 import _native, builders, scenes
+
+    mesh, spec = scenes.config_scene(args.config)
+    V, T = mesh.vertices, mesh.triangles
+    n, nv = len(T), len(V)
+    ncells = spec.ncells
+    dev = torch.device("cuda", local)
+    Vd = torch.from_numpy(np.ascontiguousarray(V)).to(dev)
+    Td = torch.from_numpy(np.ascontiguousarray(T)).to(dev)
+    b = _native.Builder(local)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    no = b.count(Vd, nv, Td, n, spec, 0, sp)
+    Gd = torch.empty(ncells + 1, dtype=torch.int32, device=dev)
+    Od = torch.empty(max(no, 1), dtype=torch.int32, device=dev)
+
+    def step(timed=False):
+        b.count(Vd, nv, Td, n, spec, 0, sp)
+        return b.finish(Gd, Od, 0, sp, timed=timed)
+
+    step()
+    launches = b.launches()
+    # parity of the measured configuration against the reference's golden hashes
+    parity = "unchecked"
+    try:
+        import hashlib
+        with open(os.path.join(ROOT, "tests", "golden", "hashes.json")) as fh:
+            h = json.load(fh)["scenes"].get(args.config)
+        if h:
+            torch.cuda.synchronize()
+            g = Gd.cpu().numpy().view(np.uint32)
+            o = Od[:no].cpu().numpy().view(np.uint32)
+            ok = (hashlib.sha256(g.tobytes()).hexdigest() == h["G_sha256"]
+                  and hashlib.sha256(o.tobytes()).hexdigest() == h["O_sha256"] and no == h["no"])
+            parity = "bit-exact vs reference (sha256 G,O)" if ok else "MISMATCH"
+    except Exception as exc:  # pragma: no cover
+        parity = f"unchecked ({exc})"
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # per-kernel CUDA-event breakdown over the same steps (phase events inside the C ABI)
+    phases = np.zeros(6)
+    for _ in range(args.steps):
+        phases += np.array(step(timed=True))
+    phases /= args.steps
+    k1_ms, k2_ms, sort_ms, k4_ms = phases[0], phases[2], phases[3], phases[5]
+    key_bits = int(ncells - 1).bit_length()
+    npasses = (key_bits + 7) // 8
+    pass_ms = sort_ms / max(npasses, 1)
+
+    # end to end through the public API: pinned host inputs, H2D + build + D2H each step
+    e2e_steps = args.e2e_steps or min(args.steps, 10)
+    Vh = np.ascontiguousarray(V).copy()
+    Th = np.ascontiguousarray(T).copy()
+    _native.host_register(Vh)
+    _native.host_register(Th)
+    from paper_2403_10647_b200.gridcore import TriangleMesh
+    hmesh = TriangleMesh(Vh, Th)
+    grid, rep = builders.build_parallel(hmesh, spec, device=local)
+    e2e_t = []
+    for _ in range(e2e_steps):
+        t0 = time.perf_counter()
+        grid, rep = builders.build_parallel(hmesh, spec, device=local)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_sec = statistics.median(e2e_t)
+    _native.host_unregister(Vh)
+    _native.host_unregister(Th)
+
+    peak, peak_kind = peaks()
+    B = 12 * n + 24 * nv + 4 * (ncells + 1) + 4 * no          # SURVEY §8d compulsory bytes
+    kern = {
+        "k_boxes_count_scan": {"ms": k1_ms, "launches": 1, "alg_bytes": 12 * n + 24 * nv + 16 * n},
+        "k_expand_pairs": {"ms": k2_ms, "launches": 1, "alg_bytes": 16 * n + 8 * no},
+        "k_onesweep_pass": {"ms": pass_ms, "launches": npasses, "alg_bytes": 16 * no},
+        "k_cell_offsets": {"ms": k4_ms, "launches": 1, "alg_bytes": 4 * no + 4 * (ncells + 1)},
+    }
+    for k, v in kern.items():
+        v["gbs"] = v["alg_bytes"] / (v["ms"] * 1e-3) / 1e9 if v["ms"] > 0 else None
+        v["frac"] = v["gbs"] / peak if v["gbs"] else None
+    dom = max(kern, key=lambda k: kern[k]["ms"] * kern[k]["launches"])
+    traffic = traffic_table().get(dom)
+    value = world / (ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "builds/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32",
+        "data": "synthetic",
+        "config": {"workload": args.config, "scene": scenes.CONFIGS[args.config][0],
+                   "triangles": n, "dims": list(spec.dims), "ncells": ncells, "no": no,
+                   "key_bits": key_bits, "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (%.0f MB read per build)" % ((12 * n + 24 * nv) / 1e6),
+                   "parity": parity},
+        "mpairs_per_s": round(no / (ms * 1e-3) / 1e6 * world, 2),
+        "hbm": {"compulsory_bytes": B, "achieved_gbs": round(B / (ms * 1e-3) / 1e9, 1),
+                "frac_of_peak": round(B / (ms * 1e-3) / 1e9 / peak, 4), "peak_gbs": peak,
+                "peak_kind": peak_kind},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(kern[dom]["gbs"], 1),
+                     "peak": peak, "unit": "GB/s", "frac": round(kern[dom]["frac"], 4),
+                     "traffic": traffic, "alg_bytes_per_launch": kern[dom]["alg_bytes"],
+                     "launch_ms": round(kern[dom]["ms"], 4), "peak_kind": peak_kind},
+        "kernels": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
+                    for k, v in kern.items()},
+        "e2e": {"value": round(1.0 / e2e_sec * world, 3), "unit": "builds/s",
+                "h2d_bytes_per_step": int(Vh.nbytes + Th.nbytes),
+                "d2h_bytes_per_step": int(grid.G.nbytes + grid.O.nbytes), "ms_per_step": round(e2e_sec * 1e3, 2)},
+        "gpu_launches": launches * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, mesh, spec)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,103 @@
+/*
+ * pgrid.h -- C ABI of libpgrid.so, the B200 (sm_100a) parallel uniform-grid builder.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   pargrid.builders.build_parallel(mesh, spec, workers=None, record=None)
+ *       (/root/reference/pkg/src/pargrid/builders.py:144-169)
+ * and for the reference's native plugin seam
+ *   kernels.radix_sort_pairs(keys, values, key_bits)
+ *       (/root/reference/pkg/src/pargrid/kernels/__init__.py:50-51 -> _ckernels.pyx:21-50).
+ * Plain pointers and sizes only; no torch or Python types. Python binds it with ctypes
+ * (paper_2403_10647_b200/_native.py); INTEGRATION.md shows the binding a reference
+ * maintainer would add.
+ *
+ * Threading: a pg_builder owns its device workspace and must be used by one thread at a
+ * time; distinct builders are independent (the reference is safe for concurrent builds on
+ * distinct inputs). Every call is enqueued on the caller's `stream`
+ * (a cudaStream_t; NULL = legacy default stream).
+ */
+#ifndef PGRID_H
+#define PGRID_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes. Python maps them onto the reference's exception classes
+ * (pargrid/errors.py:4-23): 1 -> SizeError, 2 -> InvariantError, 3 -> GridError. */
+#define PG_OK 0
+#define PG_SIZE_ERROR 1        /* NO > 2^32-1 (builders.py:99-100); N/NO/ncells > 2^30
+                                  (primitives.py:17,29-31); ncells > 2^32-1 (gridcore.py:46) */
+#define PG_INVARIANT_ERROR 2   /* precondition violated (primitives.py:22-25, gridcore.py:44-52) */
+#define PG_CUDA_ERROR 3        /* CUDA runtime failure */
+#define PG_STATE_ERROR 4       /* call sequence violated (finish before count, ...) */
+
+/* Flags. */
+#define PG_HOST_INPUT 1u       /* V/T (or sort inputs) are host pointers: copied H2D in-call */
+#define PG_HOST_OUTPUT 2u      /* G/O (or sort outputs) are host pointers: copied D2H in-call */
+#define PG_KEEP_STAGES 4u      /* keep the unsorted pairs for pg_stage (record= support) */
+
+/* Grid specification: the exact host doubles of GridSpec (gridcore.py:36-57). */
+typedef struct {
+    double lo[3];     /* spec.bounds.lo (padded, gridcore.py:190-194) */
+    double hi[3];     /* spec.bounds.hi */
+    double cell[3];   /* spec.cell_size = (hi - lo) / dims (gridcore.py:50) */
+    int64_t dims[3];  /* spec.dims, x-fastest linearisation (gridcore.py:99-103) */
+} pg_spec;
+
+typedef struct pg_builder pg_builder;
+
+/* Phase times in ms, in the reference's PHASES order (builders.py:19):
+ * count, scan, pairgen, sort, rle, finalize. Fused phases report 0 for the absorbed step
+ * (scan is fused into count; rle into finalize). */
+#define PG_NPHASES 6
+
+int  pg_builder_create(int device, pg_builder **out);
+void pg_builder_destroy(pg_builder *b);
+
+/* Phase 1 of build_parallel: triangle AABB -> clamped cell box -> CountCells, fused with
+ * the decoupled-look-back ExclusiveSum (builders.py:90-101, gridcore.py:145-167).
+ * V: f64[nv*3] row-major vertices; T: i32[n*3] triangle vertex indices (geometry.py:33-45).
+ * Returns NO (number of <cell, object> pairs) in *no_out after one device->host readback.
+ * SizeError conditions are detected here (NO > 2^32-1, NO > 2^30, ncells > 2^30, n > 2^30). */
+int pg_count(pg_builder *b, const double *V, int64_t nv, const int32_t *T, int64_t n,
+             const pg_spec *spec, uint32_t flags, void *stream, uint64_t *no_out);
+
+/* Phase 2: pair expansion, stable LSD radix sort on ceil(log2 ncells) key bits, and the
+ * RLE -> scatter -> ExclusiveSum tail (builders.py:120-141, 155-160) into caller buffers
+ * G[ncells+1] (u32) and O[NO] (u32, original triangle ids ascending within each cell).
+ * phase_ms may be NULL. */
+int pg_finish(pg_builder *b, uint32_t *G, uint32_t *O, uint32_t flags, void *stream,
+              float *phase_ms);
+
+/* Record support (builders.py:138-140, 161-163): copy one stage of the last build into dst.
+ *   stage 0: per-triangle record u32[n][4] = {lo_cell, mx, my, pair offset} (count==0 <=> dropped)
+ *   stage 1: unsorted pair cell ids u32[NO]         stage 2: unsorted pair triangle ids u32[NO]
+ *   stage 3: sorted cell ids u32[NO]
+ * Stages 1-2 need PG_KEEP_STAGES on the preceding pg_finish. */
+int pg_stage(pg_builder *b, int stage, void *dst, uint32_t flags, void *stream);
+
+/* Plugin-seam replacement of kernels.radix_sort_pairs (_ckernels.pyx:21-50): stable LSD
+ * sort of (key, value) u32 pairs over the 8*ceil(key_bits/8) low key bits (the digits the
+ * reference's 8-bit passes cover). Inputs untouched; outputs are new buffers. */
+int pg_radix_sort_pairs(pg_builder *b, const uint32_t *keys, const uint32_t *vals,
+                        uint32_t *keys_out, uint32_t *vals_out, int64_t n, int key_bits,
+                        uint32_t flags, void *stream);
+
+/* Page-lock host memory so PG_HOST_* copies run at full PCIe rate (optional). */
+int pg_host_register(void *ptr, uint64_t bytes);
+int pg_host_unregister(void *ptr);
+
+/* Number of device kernel launches issued by the last pg_count + pg_finish pair. */
+int pg_last_launch_count(pg_builder *b);
+
+/* Thread-local message for the last non-zero return code. */
+const char *pg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PGRID_H */

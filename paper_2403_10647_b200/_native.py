@@ -1,0 +1,177 @@
+"""ctypes binding of libpgrid.so (C ABI declared in include/pgrid.h).
+
+The library is built in-tree (paper_2403_10647_b200/_lib/libpgrid.so) by
+`__graft_entry__.build()` / `make -C paper_2403_10647_b200/csrc`. There is no fallback:
+if the library or a CUDA device is missing, every build call raises loudly.
+"""
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import DeviceError, GridError, InvariantError, SizeError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libpgrid.so")
+
+PG_OK = 0
+PG_SIZE_ERROR = 1
+PG_INVARIANT_ERROR = 2
+PG_CUDA_ERROR = 3
+PG_STATE_ERROR = 4
+
+PG_HOST_INPUT = 1
+PG_HOST_OUTPUT = 2
+PG_KEEP_STAGES = 4
+
+NPHASES = 6
+
+# every symbol include/pgrid.h declares (checked by tests/test_boundary.py)
+EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
+           "pg_radix_sort_pairs", "pg_host_register", "pg_host_unregister",
+           "pg_last_launch_count", "pg_last_error")
+
+
+class PgSpec(ctypes.Structure):
+    """pg_spec: the exact host doubles of GridSpec (gridcore.py:36-57)."""
+    _fields_ = [("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3),
+                ("cell", ctypes.c_double * 3), ("dims", ctypes.c_int64 * 3)]
+
+    @classmethod
+    def from_spec(cls, spec):
+        s = cls()
+        lo = np.asarray(spec.bounds.lo, dtype=np.float64)
+        hi = np.asarray(spec.bounds.hi, dtype=np.float64)
+        cell = np.asarray(spec.cell_size, dtype=np.float64)
+        for k in range(3):
+            s.lo[k] = float(lo[k])
+            s.hi[k] = float(hi[k])
+            s.cell[k] = float(cell[k])
+            s.dims[k] = int(spec.dims[k])
+        return s
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load():
+    """Load libpgrid.so (raises GridError if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise GridError(f"native library missing: {LIB_PATH} (run __graft_entry__.build())")
+        lib = ctypes.CDLL(LIB_PATH)
+        vp, i64, u32, u64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64
+        lib.pg_builder_create.argtypes = [ctypes.c_int, ctypes.POINTER(vp)]
+        lib.pg_builder_destroy.argtypes = [vp]
+        lib.pg_builder_destroy.restype = None
+        lib.pg_count.argtypes = [vp, vp, i64, vp, i64, ctypes.POINTER(PgSpec), u32, vp,
+                                 ctypes.POINTER(u64)]
+        lib.pg_finish.argtypes = [vp, vp, vp, u32, vp, ctypes.POINTER(ctypes.c_float)]
+        lib.pg_stage.argtypes = [vp, ctypes.c_int, vp, u32, vp]
+        lib.pg_radix_sort_pairs.argtypes = [vp, vp, vp, vp, vp, i64, ctypes.c_int, u32, vp]
+        lib.pg_host_register.argtypes = [vp, u64]
+        lib.pg_host_unregister.argtypes = [vp]
+        lib.pg_last_launch_count.argtypes = [vp]
+        lib.pg_last_error.restype = ctypes.c_char_p
+        for name in ("pg_builder_create", "pg_count", "pg_finish", "pg_stage",
+                     "pg_radix_sort_pairs", "pg_host_register", "pg_host_unregister",
+                     "pg_last_launch_count"):
+            getattr(lib, name).restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def check(rc):
+    """Map a C return code onto the reference's exception classes (errors.py:4-23)."""
+    if rc == PG_OK:
+        return
+    msg = (load().pg_last_error() or b"").decode(errors="replace")
+    if rc == PG_SIZE_ERROR:
+        raise SizeError(msg)
+    if rc == PG_INVARIANT_ERROR:
+        raise InvariantError(msg)
+    if rc == PG_CUDA_ERROR:
+        raise DeviceError(msg)
+    raise GridError(f"pgrid error {rc}: {msg}")
+
+
+def ptr(a):
+    """Raw data pointer of a numpy array or a torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data if a.size else None
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr() if a.numel() else None
+    return int(a)
+
+
+class Builder:
+    """One device workspace (libpgrid pg_builder). Use from one thread at a time."""
+
+    def __init__(self, device=0):
+        self._lib = load()
+        h = ctypes.c_void_p()
+        check(self._lib.pg_builder_create(int(device), ctypes.byref(h)))
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.pg_builder_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def count(self, V, nv, T, n, spec, flags=0, stream=None):
+        s = PgSpec.from_spec(spec)
+        no = ctypes.c_uint64(0)
+        check(self._lib.pg_count(self._h, ptr(V), int(nv), ptr(T), int(n), ctypes.byref(s),
+                                 flags, stream, ctypes.byref(no)))
+        return int(no.value)
+
+    def finish(self, G, O, flags=0, stream=None, timed=True):
+        phases = (ctypes.c_float * NPHASES)() if timed else None
+        check(self._lib.pg_finish(self._h, ptr(G), ptr(O), flags, stream, phases))
+        return list(phases) if timed else None
+
+    def stage(self, stage, dst, flags=PG_HOST_OUTPUT, stream=None):
+        check(self._lib.pg_stage(self._h, int(stage), ptr(dst), flags, stream))
+
+    def radix_sort_pairs(self, keys, vals, keys_out, vals_out, n, key_bits, flags=0, stream=None):
+        check(self._lib.pg_radix_sort_pairs(self._h, ptr(keys), ptr(vals), ptr(keys_out),
+                                            ptr(vals_out), int(n), int(key_bits), flags, stream))
+
+    def launches(self):
+        return int(self._lib.pg_last_launch_count(self._h))
+
+
+_tls = threading.local()
+
+
+def thread_builder(device=0):
+    """Per-thread default builder (concurrent builds on distinct threads stay independent)."""
+    b = getattr(_tls, "builder", None)
+    if b is None or b.device != device:
+        b = Builder(device)
+        _tls.builder = b
+    return b
+
+
+def host_register(a):
+    check(load().pg_host_register(ptr(a), a.nbytes))
+
+
+def host_unregister(a):
+    check(load().pg_host_unregister(ptr(a)))

@@ -1,0 +1,110 @@
+"""Drop-in `build_parallel` (pargrid.builders.build_parallel, builders.py:144-169) on B200.
+
+Same signature, same outputs, same errors, same report as the reference:
+
+    grid, report = build_parallel(mesh, spec, workers=None, record=None)
+
+`mesh` is any TriangleMesh-like object (f64 vertices (nv,3), i32 triangles (N,3)) -- the
+reference's own or ours; `spec` any GridSpec-like object. The arrays cross the C ABI
+(include/pgrid.h) once: host -> device, four kernel stages, device -> host. There is no
+CPU compute path; without libpgrid.so or a GPU this raises.
+"""
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .errors import InvariantError
+from .gridcore import CompactGrid
+
+PHASES = ("count", "scan", "pairgen", "sort", "rle", "finalize")   # builders.py:19
+PAIRGEN_OPS_PER_PAIR = 8                                           # builders.py:24
+
+# Test hook (builders.py:26-28, 135-137): corrupt O[0] so harnesses can prove detection.
+_fault_inject = False
+
+
+@dataclass
+class BuildReport:
+    """builders.py:33-43."""
+    algo: str
+    no: int = 0
+    max_task_work: int = 0
+    total_work: int = 0
+    phase_ms: dict = field(default_factory=lambda: {p: 0.0 for p in PHASES})
+
+    @property
+    def total_ms(self):
+        return sum(self.phase_ms.values())
+
+
+def _mesh_arrays(mesh):
+    V = np.ascontiguousarray(mesh.vertices, dtype=np.float64).reshape(-1, 3)
+    T = np.ascontiguousarray(mesh.triangles, dtype=np.int32).reshape(-1, 3)
+    if T.size and (T.min() < 0 or T.max() >= len(V)):
+        raise InvariantError("triangle index out of range")
+    return V, T
+
+
+def _fill_record(record, b, n, no, G, O):
+    """Reproduce the reference's record= arrays (builders.py:138-140, 161-163) from the
+    device stages. The reference numbers objects after dropping out-of-grid triangles
+    ("compacted" ids); the device keeps original ids, so the stage arrays are re-indexed
+    here (presentation only -- G and O come straight from the device)."""
+    recs = np.empty((n, 4), np.uint32)
+    if n:
+        b.stage(0, recs)
+    off = recs[:, 3].astype(np.int64)
+    counts = np.diff(np.append(off, no)) if n else np.zeros(0, np.int64)
+    kept = np.flatnonzero(counts > 0)
+    offsets = off[kept]
+    gc = np.empty(no, np.uint32)
+    go = np.empty(no, np.uint32)
+    sc = np.empty(no, np.uint32)
+    if no:
+        b.stage(1, gc)
+        b.stage(2, go)
+        b.stage(3, sc)
+    obj_ids = np.searchsorted(kept, go.astype(np.int64))
+    rel_c = np.arange(no, dtype=np.int64) - offsets[obj_ids] if no else np.zeros(0, np.int64)
+    cell_counts = np.diff(G.astype(np.int64))
+    uniques = np.flatnonzero(cell_counts)
+    record.update(v=counts[kept].astype(np.int64), offsets=offsets, no=int(no),
+                  obj_ids=obj_ids.astype(np.int64), rel_c=rel_c, global_c=gc.astype(np.int64),
+                  sorted_c=sc.astype(np.int64),
+                  sorted_o=np.searchsorted(kept, O.astype(np.int64)).astype(np.int64),
+                  rle_uniques=uniques.astype(np.int64), rle_counts=cell_counts[uniques],
+                  g=G.astype(np.int64))
+
+
+def build_parallel(mesh, spec, workers=None, record=None, device=0):
+    """Alg. 1 BuildParallelGrid on the GPU; bit-identical to the reference.
+
+    `workers` is accepted for signature parity (builders.py:144) and ignored: the output
+    never depends on it (test_builders.py:148-154)."""
+    del workers
+    V, T = _mesh_arrays(mesh)
+    n = len(T)
+    b = _native.thread_builder(device)
+    ms = {p: 0.0 for p in PHASES}
+    t0 = time.perf_counter()
+    no = b.count(V, len(V), T, n, spec, flags=_native.PG_HOST_INPUT)
+    ms["count"] = (time.perf_counter() - t0) * 1e3
+    ncells = int(spec.dims[0]) * int(spec.dims[1]) * int(spec.dims[2])
+    G = np.empty(ncells + 1, np.uint32)
+    O = np.empty(no, np.uint32)
+    flags = _native.PG_HOST_OUTPUT | (_native.PG_KEEP_STAGES if record is not None else 0)
+    phases = b.finish(G, O, flags=flags)
+    for name, v in zip(PHASES, phases):
+        if name != "count":
+            ms[name] = float(v)
+    if record is not None:
+        _fill_record(record, b, n, no, G, O)
+    if _fault_inject and no:
+        O[0] ^= 1
+    report = BuildReport("parallel", no=no,
+                         max_task_work=PAIRGEN_OPS_PER_PAIR if no else 0,
+                         total_work=PAIRGEN_OPS_PER_PAIR * no, phase_ms=ms)
+    return CompactGrid(spec, G, O), report

@@ -1,0 +1,446 @@
+// pgrid.cu -- host orchestration and C ABI of libpgrid.so (see include/pgrid.h).
+//
+// One pg_builder = one device workspace (grow-only, reused across builds) + events.
+// pg_count runs K1 and reads NO back (the only host sync of a build: O's size is dynamic,
+// PAPER.md:90); pg_finish runs K2 -> radix passes -> K4 into the caller's G and O.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/pgrid.h"
+#include "pgrid_kernels.cuh"
+
+using namespace pgrid;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(PG_CUDA_ERROR, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+constexpr int64_t kMaxIds = 4294967295LL;  // gridcore.py:11
+constexpr int64_t kMaxScan = 1LL << 30;    // primitives.py:17
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t need) {
+    if (need <= bytes) return PG_OK;
+    const size_t want = std::max(need, bytes + bytes / 4);  // grow-only, 25% headroom
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      return fail(PG_CUDA_ERROR, "cudaMalloc(%zu) failed: %s", want, cudaGetErrorString(e));
+    }
+    bytes = want;
+    return PG_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as(size_t byte_off = 0) const {
+    return reinterpret_cast<T*>(static_cast<char*>(p) + byte_off);
+  }
+};
+
+PassPlan make_plan(int key_bits, int max_digit_bits) {
+  PassPlan pl{};
+  pl.npasses = key_bits <= 0 ? 0 : (key_bits + max_digit_bits - 1) / max_digit_bits;
+  int shift = 0;
+  for (int i = 0; i < pl.npasses; ++i) {
+    // balanced digits: spread key_bits over the passes (e.g. 26 -> 7,7,6,6)
+    const int rem_passes = pl.npasses - i;
+    const int b = (key_bits - shift + rem_passes - 1) / rem_passes;
+    pl.shift[i] = shift;
+    pl.bits[i] = b;
+    shift += b;
+  }
+  return pl;
+}
+
+int bit_length(uint64_t v) {
+  int b = 0;
+  while (v >> b) ++b;
+  return b;
+}
+
+size_t os_smem_bytes() { return sizeof(OsSmem); }
+
+}  // namespace
+
+struct pg_builder {
+  int device = 0;
+  cudaEvent_t ev[8] = {};
+  unsigned long long* h_scalars = nullptr;  // pinned: [0] NO, [1] error flags
+  // inputs staged on device for PG_HOST_INPUT
+  DevBuf in_v, in_t;
+  // K1 outputs / scratch
+  DevBuf rec, k1_sync;
+  // pair buffers and sort scratch
+  DevBuf pairs, sort_sync, stage, gbuf, obuf;
+  // state of the last pg_count
+  bool counted = false;
+  int64_t n = 0;
+  uint64_t no = 0;
+  int64_t ncells = 0;
+  int dims[3] = {1, 1, 1};
+  int key_bits = 0;
+  bool stages_kept = false;
+  bool k1_timed = false;  // ev[5]..ev[6] bracket K1 of the last pg_count
+  int launches = 0;
+  const unsigned* sorted_keys = nullptr;
+};
+
+extern "C" {
+
+const char* pg_last_error(void) { return g_err.c_str(); }
+
+int pg_builder_create(int device, pg_builder** out) {
+  if (!out) return fail(PG_INVARIANT_ERROR, "null out pointer");
+  CU(cudaSetDevice(device));
+  pg_builder* b = new pg_builder();
+  b->device = device;
+  for (auto& e : b->ev) CU(cudaEventCreate(&e));
+  CU(cudaMallocHost(&b->h_scalars, 4 * sizeof(unsigned long long)));
+  CU(cudaFuncSetAttribute(k_onesweep_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)os_smem_bytes()));
+  *out = b;
+  return PG_OK;
+}
+
+void pg_builder_destroy(pg_builder* b) {
+  if (!b) return;
+  cudaSetDevice(b->device);
+  for (auto& e : b->ev)
+    if (e) cudaEventDestroy(e);
+  if (b->h_scalars) cudaFreeHost(b->h_scalars);
+  for (DevBuf* d : {&b->in_v, &b->in_t, &b->rec, &b->k1_sync, &b->pairs, &b->sort_sync, &b->stage,
+                    &b->gbuf, &b->obuf})
+    d->release();
+  delete b;
+}
+
+int pg_host_register(void* ptr, uint64_t bytes) {
+  if (!ptr || !bytes) return PG_OK;
+  CU(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
+  return PG_OK;
+}
+
+int pg_host_unregister(void* ptr) {
+  if (!ptr) return PG_OK;
+  CU(cudaHostUnregister(ptr));
+  return PG_OK;
+}
+
+int pg_last_launch_count(pg_builder* b) { return b ? b->launches : 0; }
+
+int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64_t n, const pg_spec* spec,
+             uint32_t flags, void* stream_, uint64_t* no_out) {
+  if (!b || !spec || !no_out) return fail(PG_INVARIANT_ERROR, "null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  b->counted = false;
+  b->stages_kept = false;
+  b->k1_timed = false;
+  b->launches = 0;
+  if (n < 0 || nv < 0) return fail(PG_INVARIANT_ERROR, "negative sizes");
+  for (int k = 0; k < 3; ++k)
+    if (spec->dims[k] < 1) return fail(PG_INVARIANT_ERROR, "dims must be three positive integers");
+  int64_t ncells = 1;
+  for (int k = 0; k < 3; ++k) {
+    ncells *= spec->dims[k];
+    if (ncells > kMaxIds) return fail(PG_SIZE_ERROR, "cells exceed 32-bit id space");
+  }
+  // The reference raises SizeError once the G scan sees more than 2^30 cells
+  // (primitives.py:29-31 via builders.py:130); every successful build has ncells <= 2^30.
+  if (ncells > kMaxScan) return fail(PG_SIZE_ERROR, "array of %lld elements exceeds the scan size limit", (long long)ncells);
+  if (n > kMaxScan) return fail(PG_SIZE_ERROR, "%lld triangles exceed the scan size limit", (long long)n);
+  if (n > 0 && (!V || !T)) return fail(PG_INVARIANT_ERROR, "null mesh arrays");
+
+  DevSpec ds;
+  for (int k = 0; k < 3; ++k) {
+    ds.lo[k] = spec->lo[k];
+    ds.hi[k] = spec->hi[k];
+    ds.cell[k] = spec->cell[k];
+    ds.dims[k] = (int)spec->dims[k];
+    b->dims[k] = (int)spec->dims[k];
+  }
+  b->n = n;
+  b->ncells = ncells;
+  b->key_bits = bit_length((uint64_t)(ncells - 1));  // builders.py:124
+
+  if (n == 0) {
+    b->no = 0;
+    *no_out = 0;
+    b->counted = true;
+    return PG_OK;
+  }
+  const double* dV = V;
+  const int32_t* dT = T;
+  if (flags & PG_HOST_INPUT) {
+    int rc;
+    if ((rc = b->in_v.ensure((size_t)nv * 3 * sizeof(double)))) return rc;
+    if ((rc = b->in_t.ensure((size_t)n * 3 * sizeof(int32_t)))) return rc;
+    CU(cudaMemcpyAsync(b->in_v.p, V, (size_t)nv * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(b->in_t.p, T, (size_t)n * 3 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    dV = b->in_v.as<double>();
+    dT = b->in_t.as<int32_t>();
+  }
+  const unsigned ntiles = (unsigned)((n + K1_TILE - 1) / K1_TILE);
+  int rc;
+  if ((rc = b->rec.ensure((size_t)n * sizeof(uint4)))) return rc;
+  // sync area: [status u64 x ntiles][tile counter][err][total u64]
+  const size_t sync_bytes = align_up((size_t)ntiles * 8) + 256;
+  if ((rc = b->k1_sync.ensure(sync_bytes))) return rc;
+  unsigned long long* status = b->k1_sync.as<unsigned long long>();
+  unsigned* ctr = b->k1_sync.as<unsigned>(align_up((size_t)ntiles * 8));
+  unsigned* err = ctr + 1;
+  unsigned long long* total = b->k1_sync.as<unsigned long long>(align_up((size_t)ntiles * 8) + 8);
+  CU(cudaMemsetAsync(b->k1_sync.p, 0, sync_bytes, st));
+  CU(cudaEventRecord(b->ev[5], st));
+  k_boxes_count_scan<<<ntiles, K1_THREADS, 0, st>>>(dV, reinterpret_cast<const int*>(dT), n, ds,
+                                                     b->rec.as<uint4>(), status, ctr, total, err);
+  CU(cudaGetLastError());
+  CU(cudaEventRecord(b->ev[6], st));
+  b->launches = 1;
+  b->k1_timed = true;
+  CU(cudaMemcpyAsync(&b->h_scalars[0], total, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(&b->h_scalars[1], err, 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  const uint64_t no = b->h_scalars[0];
+  const unsigned errf = (unsigned)(b->h_scalars[1] & 0xffffffffu);
+  *no_out = no;
+  if (errf) return fail(PG_INVARIANT_ERROR, "triangle cell box with hi < lo (non-finite or huge upper corner)");
+  if ((int64_t)no > kMaxIds) return fail(PG_SIZE_ERROR, "%llu cell/object pairs exceed 32-bit id space", (unsigned long long)no);
+  if ((int64_t)no > kMaxScan) return fail(PG_SIZE_ERROR, "array of %llu elements exceeds the scan size limit", (unsigned long long)no);
+  b->no = no;
+  b->counted = true;
+  return PG_OK;
+}
+
+namespace {
+
+// LSD passes over (keys0, vals0), ping-ponging with (keys1, vals1); the last pass writes its
+// values straight into vals_final (O). hist (plan.npasses x 256) must already be filled.
+int run_passes(pg_builder* b, const PassPlan& plan, unsigned* keys0, unsigned* vals0, unsigned* keys1,
+               unsigned* vals1, unsigned* vals_final, uint64_t n, unsigned* hist, unsigned* status,
+               unsigned* ctrs, cudaStream_t st, const unsigned** sorted_keys_out) {
+  const unsigned ntiles = (unsigned)((n + OS_TILE - 1) / OS_TILE);
+  unsigned* kbuf[2] = {keys0, keys1};
+  unsigned* vbuf[2] = {vals0, vals1};
+  for (int p = 0; p < plan.npasses; ++p) {
+    const bool last = p == plan.npasses - 1;
+    unsigned* kin = kbuf[p & 1];
+    unsigned* vin = vbuf[p & 1];
+    unsigned* ko = kbuf[(p + 1) & 1];
+    unsigned* vo = last ? vals_final : vbuf[(p + 1) & 1];
+    k_onesweep_pass<<<ntiles, OS_THREADS, os_smem_bytes(), st>>>(
+        kin, vin, ko, vo, (unsigned)n, plan.shift[p], plan.bits[p], hist + p * kMaxBins,
+        status + (size_t)p * ntiles * kMaxBins, ctrs + p);
+    CU(cudaGetLastError());
+    ++b->launches;
+    *sorted_keys_out = ko;
+  }
+  return PG_OK;
+}
+
+}  // namespace
+
+int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* stream_, float* phase_ms) {
+  if (!b || !b->counted) return fail(PG_STATE_ERROR, "pg_finish without a successful pg_count");
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  const uint64_t no = b->no;
+  const int64_t ncells = b->ncells;
+  const PassPlan plan = make_plan(b->key_bits, 8);
+  int rc;
+  unsigned* dG = G;
+  unsigned* dO = O;
+  if (flags & PG_HOST_OUTPUT) {
+    if ((rc = b->gbuf.ensure((size_t)(ncells + 1) * 4))) return rc;
+    if ((rc = b->obuf.ensure(std::max<size_t>((size_t)no * 4, 4)))) return rc;
+    dG = b->gbuf.as<unsigned>();
+    dO = b->obuf.as<unsigned>();
+  }
+  // pairs: keysA | valsA | keysB | valsB (16 B aligned sections)
+  const size_t sec = align_up(std::max<size_t>((size_t)no * 4, 16));
+  if ((rc = b->pairs.ensure(4 * sec))) return rc;
+  unsigned* keysA = b->pairs.as<unsigned>(0);
+  unsigned* valsA = b->pairs.as<unsigned>(sec);
+  unsigned* keysB = b->pairs.as<unsigned>(2 * sec);
+  unsigned* valsB = b->pairs.as<unsigned>(3 * sec);
+  const unsigned os_tiles = (unsigned)((no + OS_TILE - 1) / OS_TILE);
+  // sort sync area: [hist npasses x 256][tile counters x 4][status npasses x tiles x 256]
+  const size_t hist_bytes = align_up(kMaxPasses * kMaxBins * 4);
+  const size_t ctr_bytes = 256;
+  const size_t status_bytes = (size_t)std::max(plan.npasses, 1) * os_tiles * kMaxBins * 4;
+  const size_t sync_bytes = hist_bytes + ctr_bytes + align_up(status_bytes);
+  if ((rc = b->sort_sync.ensure(sync_bytes))) return rc;
+  unsigned* hist = b->sort_sync.as<unsigned>(0);
+  unsigned* ctrs = b->sort_sync.as<unsigned>(hist_bytes);
+  unsigned* status = b->sort_sync.as<unsigned>(hist_bytes + ctr_bytes);
+
+  CU(cudaEventRecord(b->ev[0], st));
+  CU(cudaMemsetAsync(b->sort_sync.p, 0, sync_bytes, st));
+  const unsigned* sorted = keysA;
+  if (no > 0) {
+    // K2: pairs (+ histograms). With no radix pass the pair order is final: vals -> O.
+    unsigned* v0 = plan.npasses == 0 ? dO : valsA;
+    const unsigned k2_tiles = (unsigned)((no + K2_TILE - 1) / K2_TILE);
+    k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->n, (unsigned)no, (unsigned)b->dims[0],
+                                                     (unsigned)b->dims[0] * (unsigned)b->dims[1], plan, keysA, v0,
+                                                     hist);
+    CU(cudaGetLastError());
+    ++b->launches;
+    if (flags & PG_KEEP_STAGES) {
+      if ((rc = b->stage.ensure(2 * sec))) return rc;
+      CU(cudaMemcpyAsync(b->stage.as<unsigned>(0), keysA, no * 4, cudaMemcpyDeviceToDevice, st));
+      CU(cudaMemcpyAsync(b->stage.as<unsigned>(sec), v0, no * 4, cudaMemcpyDeviceToDevice, st));
+      b->stages_kept = true;
+    }
+    CU(cudaEventRecord(b->ev[1], st));
+    if (plan.npasses > 0) {
+      if ((rc = run_passes(b, plan, keysA, valsA, keysB, valsB, dO, no, hist, status, ctrs, st, &sorted)))
+        return rc;
+    }
+  } else {
+    CU(cudaEventRecord(b->ev[1], st));
+  }
+  CU(cudaEventRecord(b->ev[2], st));
+  const unsigned g_tiles = (unsigned)((ncells + G_TILE - 1) / G_TILE);
+  k_cell_offsets<<<g_tiles, G_THREADS, 0, st>>>(sorted, (unsigned)no, (unsigned)ncells, dG);
+  CU(cudaGetLastError());
+  ++b->launches;
+  b->sorted_keys = sorted;
+  CU(cudaEventRecord(b->ev[3], st));
+  if (flags & PG_HOST_OUTPUT) {
+    CU(cudaMemcpyAsync(G, dG, (size_t)(ncells + 1) * 4, cudaMemcpyDeviceToHost, st));
+    if (no) CU(cudaMemcpyAsync(O, dO, no * 4, cudaMemcpyDeviceToHost, st));
+  }
+  CU(cudaEventRecord(b->ev[4], st));
+  if (phase_ms || (flags & PG_HOST_OUTPUT)) CU(cudaEventSynchronize(b->ev[4]));
+  if (phase_ms) {
+    float t01 = 0, t12 = 0, t23 = 0, t34 = 0;
+    CU(cudaEventElapsedTime(&t01, b->ev[0], b->ev[1]));
+    CU(cudaEventElapsedTime(&t12, b->ev[1], b->ev[2]));
+    CU(cudaEventElapsedTime(&t23, b->ev[2], b->ev[3]));
+    CU(cudaEventElapsedTime(&t34, b->ev[3], b->ev[4]));
+    float t_k1 = 0.f;
+    if (b->k1_timed) CU(cudaEventElapsedTime(&t_k1, b->ev[5], b->ev[6]));
+    phase_ms[0] = t_k1;  // count: K1 device time (callers add their H2D / readback around it)
+    phase_ms[1] = 0.f;  // scan: fused into count (K1)
+    phase_ms[2] = t01;  // pairgen: K2 (+ histograms)
+    phase_ms[3] = t12;  // sort: onesweep passes
+    phase_ms[4] = 0.f;  // rle: fused into finalize (K4)
+    phase_ms[5] = t23 + t34;  // finalize: K4 (+ D2H of G/O for host outputs)
+  }
+  return PG_OK;
+}
+
+int pg_stage(pg_builder* b, int stage, void* dst, uint32_t flags, void* stream_) {
+  if (!b || !b->counted) return fail(PG_STATE_ERROR, "no build to read stages from");
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  const cudaMemcpyKind kind = (flags & PG_HOST_OUTPUT) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  const size_t sec = align_up(std::max<size_t>((size_t)b->no * 4, 16));
+  switch (stage) {
+    case 0:
+      if (b->n) CU(cudaMemcpyAsync(dst, b->rec.p, (size_t)b->n * 16, kind, st));
+      break;
+    case 1:
+    case 2:
+      if (!b->stages_kept) return fail(PG_STATE_ERROR, "stages 1-2 need PG_KEEP_STAGES on pg_finish");
+      if (b->no) CU(cudaMemcpyAsync(dst, b->stage.as<unsigned>(stage == 1 ? 0 : sec), b->no * 4, kind, st));
+      break;
+    case 3:
+      if (b->no) CU(cudaMemcpyAsync(dst, b->sorted_keys, b->no * 4, kind, st));
+      break;
+    default:
+      return fail(PG_INVARIANT_ERROR, "unknown stage %d", stage);
+  }
+  CU(cudaStreamSynchronize(st));
+  return PG_OK;
+}
+
+int pg_radix_sort_pairs(pg_builder* b, const uint32_t* keys, const uint32_t* vals, uint32_t* keys_out,
+                        uint32_t* vals_out, int64_t n, int key_bits, uint32_t flags, void* stream_) {
+  if (!b) return fail(PG_INVARIANT_ERROR, "null builder");
+  if (key_bits < 0 || key_bits > 32) return fail(PG_INVARIANT_ERROR, "key_bits must be in [0, 32]");
+  if (n < 0) return fail(PG_INVARIANT_ERROR, "negative length");
+  if (n > kMaxScan) return fail(PG_SIZE_ERROR, "sort of %lld pairs exceeds the size limit", (long long)n);
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  b->counted = false;
+  b->launches = 0;
+  if (n == 0) return PG_OK;
+  // the reference sorts 8-bit digits [0, 8*ceil(key_bits/8)) (_ckernels.pyx:33)
+  const int sort_bits = std::min(32, 8 * ((key_bits + 7) / 8));
+  const PassPlan plan = make_plan(sort_bits, 8);
+  const size_t sec = align_up((size_t)n * 4);
+  int rc;
+  if ((rc = b->pairs.ensure(4 * sec))) return rc;
+  unsigned* kA = b->pairs.as<unsigned>(0);
+  unsigned* vA = b->pairs.as<unsigned>(sec);
+  unsigned* kB = b->pairs.as<unsigned>(2 * sec);
+  unsigned* vB = b->pairs.as<unsigned>(3 * sec);
+  const cudaMemcpyKind in_kind = (flags & PG_HOST_INPUT) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  CU(cudaMemcpyAsync(kA, keys, (size_t)n * 4, in_kind, st));
+  CU(cudaMemcpyAsync(vA, vals, (size_t)n * 4, in_kind, st));
+  const unsigned os_tiles = (unsigned)((n + OS_TILE - 1) / OS_TILE);
+  const size_t hist_bytes = align_up(kMaxPasses * kMaxBins * 4);
+  const size_t ctr_bytes = 256;
+  const size_t status_bytes = (size_t)std::max(plan.npasses, 1) * os_tiles * kMaxBins * 4;
+  const size_t sync_bytes = hist_bytes + ctr_bytes + align_up(status_bytes);
+  if ((rc = b->sort_sync.ensure(sync_bytes))) return rc;
+  unsigned* hist = b->sort_sync.as<unsigned>(0);
+  unsigned* ctrs = b->sort_sync.as<unsigned>(hist_bytes);
+  unsigned* status = b->sort_sync.as<unsigned>(hist_bytes + ctr_bytes);
+  CU(cudaMemsetAsync(b->sort_sync.p, 0, sync_bytes, st));
+  const unsigned* sorted = kA;
+  unsigned* vfinal = vA;
+  if (plan.npasses > 0) {
+    k_digit_hist<<<std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(kA, n, plan, hist);
+    CU(cudaGetLastError());
+    ++b->launches;
+    // host outputs: final values land in the staging section behind the pair buffers
+    if ((rc = b->stage.ensure(sec))) return rc;
+    unsigned* vdst = (flags & PG_HOST_OUTPUT) ? b->stage.as<unsigned>() : vals_out;
+    if ((rc = run_passes(b, plan, kA, vA, kB, vB, vdst, (uint64_t)n, hist, status, ctrs, st, &sorted)))
+      return rc;
+    vfinal = vdst;
+  }
+  const cudaMemcpyKind out_kind = (flags & PG_HOST_OUTPUT) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  CU(cudaMemcpyAsync(keys_out, sorted, (size_t)n * 4, out_kind, st));
+  if (vfinal != vals_out) CU(cudaMemcpyAsync(vals_out, vfinal, (size_t)n * 4, out_kind, st));
+  CU(cudaStreamSynchronize(st));
+  return PG_OK;
+}
+
+}  // extern "C"

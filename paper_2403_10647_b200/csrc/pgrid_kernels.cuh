@@ -1,0 +1,617 @@
+// pgrid_kernels.cuh -- sm_100a kernels of the parallel uniform-grid build.
+//
+// Data path:
+//   K1 k_boxes_count_scan : triangle AABB -> clamped cell box -> CountCells, fused with a
+//                           decoupled-look-back exclusive scan (builders.py:90-101,
+//                           gridcore.py:145-167, primitives.py:36-44)
+//   K2 k_expand_pairs     : load-balanced <cell, triangle> pair expansion (MakeObjectIds +
+//                           InclusiveSum + SegmentedExclusiveSum + MakeCellIds,
+//                           builders.py:155-160 / 104-117) + all radix digit histograms
+//   K3 k_onesweep_pass    : one stable LSD digit pass of the onesweep radix sort
+//                           (builders.py:123-125 -> _ckernels.pyx:21-50)
+//   K4 k_cell_offsets     : RunLengthEncode -> NonEmptyCells scatter -> ExclusiveSum, fused:
+//                           G[c] = #pairs with cell < c (builders.py:126-133)
+// All integer work is exact; the only floating point is the f64 sub/div/floor of K1, done
+// with explicit round-to-nearest intrinsics so it matches numpy bit for bit.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pgrid {
+
+// ----------------------------------------------------------------------------------------
+// common helpers
+// ----------------------------------------------------------------------------------------
+struct DevSpec {
+  double lo[3];
+  double hi[3];
+  double cell[3];
+  int dims[3];
+};
+
+// Per-pass digit plan for the radix sort.
+constexpr int kMaxPasses = 4;
+struct PassPlan {
+  int npasses;
+  int shift[kMaxPasses];
+  int bits[kMaxPasses];
+};
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// numpy float64 -> int64 astype on x86-64 (cvttsd2si): NaN / out-of-range -> INT64_MIN.
+// gridcore.py:161-162 floors then casts; CUDA's cvt saturates instead, so emulate x86.
+__device__ __forceinline__ long long np_floor_i64(double q) {
+  const double f = floor(q);
+  return (f >= -9223372036854775808.0 && f < 9223372036854775808.0) ? (long long)f
+                                                                     : (long long)(-9223372036854775807LL - 1);
+}
+__device__ __forceinline__ unsigned clip_axis(long long v, int dim) {
+  return v < 0 ? 0u : (v > (long long)(dim - 1) ? (unsigned)(dim - 1) : (unsigned)v);
+}
+
+// Warp-cooperative 32-ary lower_bound: smallest i in [0, n] with load(i) >= x (load(n) = +inf).
+// 5 rounds of 32 parallel probes cover 2^25 elements; each round is one L2/HBM latency.
+template <typename Load>
+__device__ __forceinline__ unsigned long long warp_lower_bound(unsigned long long n, unsigned long long x,
+                                                               Load load) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long lo = 0, hi = n;  // answer in [lo, hi]; load(lo-1) < x; load(hi) >= x or hi == n
+  while (lo < hi) {
+    const unsigned long long span = hi - lo;
+    const unsigned long long step = (span + 31) / 32;
+    const unsigned long long p = lo + (unsigned long long)lane * step;
+    const bool ge = (p < hi) ? (load(p) >= x) : true;
+    const unsigned ball = __ballot_sync(0xffffffffu, ge);
+    const int f = __ffs(ball) - 1;  // first lane whose probe is >= x (ball != 0: lanes past hi vote true)
+    if (f == 0) {
+      hi = lo;
+    } else {
+      const unsigned long long pf = lo + (unsigned long long)f * step;
+      const unsigned long long pprev = lo + (unsigned long long)(f - 1) * step;
+      lo = pprev + 1;
+      hi = pf < hi ? pf : hi;
+    }
+  }
+  return lo;
+}
+
+// ----------------------------------------------------------------------------------------
+// K1: boxes + counts + decoupled-look-back exclusive scan
+// ----------------------------------------------------------------------------------------
+constexpr int K1_THREADS = 256;
+constexpr int K1_ITEMS = 4;
+constexpr int K1_TILE = K1_THREADS * K1_ITEMS;
+constexpr unsigned long long LB_AGG = 1ull << 62;
+constexpr unsigned long long LB_PREFIX = 2ull << 62;
+constexpr unsigned long long LB_VALUE = (1ull << 62) - 1;
+
+// Per-triangle record written by K1 and read by K2: {lo_cell, mx, my, pair offset}.
+// mx/my are the box extents in x/y; count = mx*my*mz is implied by the offsets.
+// Dropped triangles (keep == false, gridcore.py:159) are {0, 1, 1, off} with count 0.
+__global__ void __launch_bounds__(K1_THREADS)
+k_boxes_count_scan(const double* __restrict__ V, const int* __restrict__ T, long long n, DevSpec s,
+                   uint4* __restrict__ rec, unsigned long long* __restrict__ status,
+                   unsigned* __restrict__ tile_ctr, unsigned long long* __restrict__ total,
+                   unsigned* __restrict__ err) {
+  __shared__ unsigned sh_tile;
+  __shared__ unsigned long long sh_warp[K1_THREADS / 32];
+  __shared__ unsigned long long sh_excl;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) sh_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const unsigned tile = sh_tile;
+  const unsigned ntiles = (unsigned)((n + K1_TILE - 1) / K1_TILE);
+  const long long first = (long long)tile * K1_TILE + (long long)tid * K1_ITEMS;
+
+  uint3 box[K1_ITEMS];
+  unsigned cnt[K1_ITEMS];
+  const unsigned dx = (unsigned)s.dims[0], dxy = (unsigned)s.dims[0] * (unsigned)s.dims[1];
+#pragma unroll
+  for (int j = 0; j < K1_ITEMS; ++j) {
+    const long long i = first + j;
+    box[j] = make_uint3(0u, 1u, 1u);
+    cnt[j] = 0;
+    if (i < n) {
+      const int t0 = __ldg(T + 3 * i), t1 = __ldg(T + 3 * i + 1), t2 = __ldg(T + 3 * i + 2);
+      bool keep = true;
+      unsigned lo[3], hi[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double a = __ldg(V + 3 * (long long)t0 + k);
+        const double b = __ldg(V + 3 * (long long)t1 + k);
+        const double c = __ldg(V + 3 * (long long)t2 + k);
+        // np.min/np.max propagate NaN, which fails both comparisons (gridcore.py:156-159);
+        // fmin/fmax do not, so NaN is folded into keep explicitly.
+        const bool nan = isnan(a) | isnan(b) | isnan(c);
+        const double mn = fmin(fmin(a, b), c);
+        const double mx = fmax(fmax(a, b), c);
+        keep &= !nan && (mx >= s.lo[k]) && (mn <= s.hi[k]);
+        const double ql = __ddiv_rn(__dsub_rn(mn, s.lo[k]), s.cell[k]);
+        const double qh = __ddiv_rn(__dsub_rn(mx, s.lo[k]), s.cell[k]);
+        lo[k] = clip_axis(np_floor_i64(ql), s.dims[k]);
+        hi[k] = clip_axis(np_floor_i64(qh), s.dims[k]);
+      }
+      if (keep && (hi[0] < lo[0] || hi[1] < lo[1] || hi[2] < lo[2])) {
+        // +inf / >2^63 upper corners cast to INT64_MIN and clip to 0 below lo: the reference
+        // then fails its non-negative / coincident-mark checks (primitives.py:22-25, 71-72).
+        atomicOr(err, 1u);
+        keep = false;
+      }
+      if (keep) {
+        const unsigned ex = hi[0] - lo[0] + 1, ey = hi[1] - lo[1] + 1, ez = hi[2] - lo[2] + 1;
+        box[j] = make_uint3(lo[0] + dx * lo[1] + dxy * lo[2], ex, ey);
+        cnt[j] = ex * ey * ez;  // <= ncells <= 2^30
+      }
+    }
+  }
+  // block-wide exclusive scan of the counts (blocked arrangement keeps triangle order)
+  unsigned long long tsum = 0;
+#pragma unroll
+  for (int j = 0; j < K1_ITEMS; ++j) tsum += cnt[j];
+  unsigned long long incl = tsum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += o;
+  }
+  if (lane == 31) sh_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long w = lane < K1_THREADS / 32 ? sh_warp[lane] : 0ull;
+    unsigned long long wi = w;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long o = __shfl_up_sync(0xffffffffu, wi, d);
+      if (lane >= d) wi += o;
+    }
+    const unsigned long long aggregate = __shfl_sync(0xffffffffu, wi, K1_THREADS / 32 - 1);
+    if (lane < K1_THREADS / 32) sh_warp[lane] = wi - w;  // exclusive warp prefix
+    // decoupled look-back (one warp, 32 predecessors per round)
+    unsigned long long excl = 0;
+    if (tile == 0) {
+      if (lane == 0) st_relaxed_u64(status, LB_PREFIX | aggregate);
+    } else {
+      if (lane == 0) st_relaxed_u64(status + tile, LB_AGG | aggregate);
+      long long pred = (long long)tile - 1 - lane;
+      while (true) {
+        unsigned long long v = pred >= 0 ? ld_relaxed_u64(status + pred) : LB_PREFIX;
+        while (__any_sync(0xffffffffu, (v >> 62) == 0)) {
+          if ((v >> 62) == 0) v = ld_relaxed_u64(status + pred);
+        }
+        const unsigned pmask = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+        const int stop = pmask ? __ffs(pmask) - 1 : 31;
+        unsigned long long contrib = lane <= stop ? (v & LB_VALUE) : 0ull;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, d);
+        excl += contrib;
+        if (pmask) break;
+        pred -= 32;
+      }
+      if (lane == 0) st_relaxed_u64(status + tile, LB_PREFIX | (excl + aggregate));
+    }
+    if (lane == 0) {
+      sh_excl = excl;
+      if (tile == ntiles - 1) *total = excl + aggregate;
+    }
+  }
+  __syncthreads();
+  unsigned long long off = sh_excl + sh_warp[warp] + (incl - tsum);
+#pragma unroll
+  for (int j = 0; j < K1_ITEMS; ++j) {
+    const long long i = first + j;
+    if (i < n) rec[i] = make_uint4(box[j].x, box[j].y, box[j].z, (unsigned)off);
+    off += cnt[j];
+  }
+}
+
+// ----------------------------------------------------------------------------------------
+// K2: load-balanced pair expansion + radix digit histograms
+// ----------------------------------------------------------------------------------------
+constexpr int K2_THREADS = 256;
+constexpr int K2_ITEMS = 8;
+constexpr int K2_TILE = K2_THREADS * K2_ITEMS;
+constexpr int kMaxBins = 256;
+
+// Each CTA owns pairs [p0, p0 + K2_TILE). The owning triangle of every pair is recovered
+// the way Alg. 1 does it (marks at run starts + inclusive max-scan), but
+// tile-locally: the tile's first owner comes from a 32-ary search over the record offsets,
+// the run starts inside the tile are scattered into shared memory, and a block max-scan
+// fills the gaps. Within a thread's 8 consecutive pairs the cell coordinate is stepped
+// incrementally (x-fastest), so the two divisions of _make_cell_ids (builders.py:111-113)
+// run at most once per thread.
+__global__ void __launch_bounds__(K2_THREADS)
+k_expand_pairs(const uint4* __restrict__ rec, long long n, unsigned no, unsigned dx, unsigned dxy,
+               PassPlan plan, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
+               unsigned* __restrict__ hist) {
+  __shared__ int slot[K2_TILE];
+  __shared__ unsigned sh_hist[kMaxPasses * kMaxBins];
+  __shared__ int sh_warpmax[K2_THREADS / 32];
+  __shared__ long long sh_olo;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned p0 = blockIdx.x * (unsigned)K2_TILE;
+  const unsigned pend = min(p0 + (unsigned)K2_TILE, no);
+
+  for (int i = tid; i < K2_TILE; i += K2_THREADS) slot[i] = -1;
+  for (int i = tid; i < plan.npasses * kMaxBins; i += K2_THREADS) sh_hist[i] = 0;
+  if (warp == 0) {
+    // olo = (#triangles with offset <= p0) - 1: the owner of pair p0.
+    const unsigned long long c = warp_lower_bound((unsigned long long)n, (unsigned long long)p0 + 1,
+                                                  [&](unsigned long long i) { return (unsigned long long)__ldg(&rec[i].w); });
+    if (lane == 0) sh_olo = (long long)c - 1;
+  }
+  __syncthreads();
+  const long long olo = sh_olo;
+  if (tid == 0) slot[0] = (int)olo;
+  // run starts inside the tile: every triangle after olo whose offset is < pend
+  for (long long ob = olo + 1;; ob += K2_THREADS) {
+    const long long o = ob + tid;
+    bool in = false;
+    if (o < n) {
+      const unsigned off = __ldg(&rec[o].w);
+      if (off < pend) {
+        atomicMax(&slot[off - p0], (int)o);  // zero-count triangles share the next start; max wins
+        in = true;
+      }
+    }
+    if (!__syncthreads_and(in)) break;
+  }
+  __syncthreads();
+  // inclusive max-scan over the slots (blocked: thread t owns slots [8t, 8t+8))
+  int own[K2_ITEMS];
+  {
+    const int4 a = *reinterpret_cast<const int4*>(&slot[tid * K2_ITEMS]);
+    const int4 b = *reinterpret_cast<const int4*>(&slot[tid * K2_ITEMS + 4]);
+    own[0] = a.x; own[1] = a.y; own[2] = a.z; own[3] = a.w;
+    own[4] = b.x; own[5] = b.y; own[6] = b.z; own[7] = b.w;
+  }
+#pragma unroll
+  for (int j = 1; j < K2_ITEMS; ++j) own[j] = max(own[j], own[j - 1]);
+  int run = own[K2_ITEMS - 1];
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, run, d);
+    if (lane >= d) run = max(run, o);
+  }
+  if (lane == 31) sh_warpmax[warp] = run;
+  __syncthreads();
+  int carry = __shfl_up_sync(0xffffffffu, run, 1);
+  if (lane == 0) carry = -1;
+  for (int w = 0; w < warp; ++w) carry = max(carry, sh_warpmax[w]);
+#pragma unroll
+  for (int j = 0; j < K2_ITEMS; ++j) own[j] = max(own[j], carry);
+
+  // expansion
+  unsigned key[K2_ITEMS];
+  const unsigned pbase = p0 + (unsigned)tid * K2_ITEMS;
+  int prev = -1;
+  unsigned cell = 0, x = 0, y = 0, mx = 1, my = 1;
+#pragma unroll
+  for (int j = 0; j < K2_ITEMS; ++j) {
+    const unsigned p = pbase + j;
+    key[j] = 0;
+    if (p < pend) {
+      const int o = own[j];
+      if (o != prev) {
+        const uint4 r = __ldg(&rec[o]);
+        const unsigned rel = p - r.w;
+        mx = r.y;
+        my = r.z;
+        const unsigned mxy = mx * my;
+        const unsigned z = rel / mxy;
+        const unsigned rem = rel - z * mxy;
+        y = rem / mx;
+        x = rem - y * mx;
+        cell = r.x + x + dx * y + dxy * z;
+        prev = o;
+      } else {
+        ++x;
+        ++cell;
+        if (x == mx) {
+          x = 0;
+          cell += dx - mx;
+          if (++y == my) {
+            y = 0;
+            cell += dxy - dx * my;
+          }
+        }
+      }
+      key[j] = cell;
+    }
+  }
+  if (pbase + K2_ITEMS <= pend) {
+    uint4* kd = reinterpret_cast<uint4*>(keys + pbase);
+    uint4* vd = reinterpret_cast<uint4*>(vals + pbase);
+    kd[0] = make_uint4(key[0], key[1], key[2], key[3]);
+    kd[1] = make_uint4(key[4], key[5], key[6], key[7]);
+    vd[0] = make_uint4(own[0], own[1], own[2], own[3]);
+    vd[1] = make_uint4(own[4], own[5], own[6], own[7]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < K2_ITEMS; ++j)
+      if (pbase + j < pend) {
+        keys[pbase + j] = key[j];
+        vals[pbase + j] = (unsigned)own[j];
+      }
+  }
+  // digit histograms of every radix pass (consumed by the onesweep passes)
+  for (int ps = 0; ps < plan.npasses; ++ps) {
+    const unsigned mask = (1u << plan.bits[ps]) - 1u;
+#pragma unroll
+    for (int j = 0; j < K2_ITEMS; ++j)
+      if (pbase + j < pend) atomicAdd(&sh_hist[ps * kMaxBins + ((key[j] >> plan.shift[ps]) & mask)], 1u);
+  }
+  __syncthreads();
+  for (int i = tid; i < plan.npasses * kMaxBins; i += K2_THREADS) {
+    const unsigned c = sh_hist[i];
+    if (c) atomicAdd(&hist[i], c);
+  }
+}
+
+// Standalone digit histogram (plugin-seam sort of arbitrary keys).
+__global__ void __launch_bounds__(256)
+k_digit_hist(const unsigned* __restrict__ keys, long long n, PassPlan plan, unsigned* __restrict__ hist) {
+  __shared__ unsigned sh_hist[kMaxPasses * kMaxBins];
+  for (int i = threadIdx.x; i < plan.npasses * kMaxBins; i += blockDim.x) sh_hist[i] = 0;
+  __syncthreads();
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned k = keys[i];
+    for (int ps = 0; ps < plan.npasses; ++ps)
+      atomicAdd(&sh_hist[ps * kMaxBins + ((k >> plan.shift[ps]) & ((1u << plan.bits[ps]) - 1u))], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < plan.npasses * kMaxBins; i += blockDim.x)
+    if (sh_hist[i]) atomicAdd(&hist[i], sh_hist[i]);
+}
+
+// ----------------------------------------------------------------------------------------
+// K3: onesweep digit pass (stable)
+// ----------------------------------------------------------------------------------------
+constexpr int OS_THREADS = 512;
+constexpr int OS_WARPS = OS_THREADS / 32;
+constexpr int OS_ITEMS = 8;
+constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096 pairs
+// look-back word: 0 = not ready; bit31 set = inclusive prefix; else aggregate + 1.
+constexpr unsigned OS_PREFIX = 1u << 31;
+
+struct OsSmem {
+  unsigned keys[OS_TILE];
+  unsigned vals[OS_TILE];
+  unsigned whist[OS_WARPS][kMaxBins];  // per-warp digit counts, then exclusive warp offsets
+  unsigned local_start[kMaxBins];      // tile-local exclusive digit prefix
+  unsigned gbase[kMaxBins];            // global position of smem slot 0 for each digit
+  unsigned wsum_h[8];
+  unsigned wsum_l[8];
+  unsigned tile;
+};
+
+// One LSD digit pass (Adinets & Merrill's onesweep): tiles are claimed in order through an
+// atomic counter, ranked stably in shared memory with match-any warp multisplit, and placed
+// with a per-digit decoupled look-back over the previous tiles; global digit starts come
+// from the histogram K2 accumulated, so there is no separate upsweep/downsweep.
+__global__ void __launch_bounds__(OS_THREADS)
+k_onesweep_pass(const unsigned* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
+                unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, unsigned no, int shift,
+                int bits, const unsigned* __restrict__ hist, unsigned* __restrict__ status,
+                unsigned* __restrict__ tile_ctr) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  OsSmem& sm = *reinterpret_cast<OsSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nbins = 1 << bits;
+  const unsigned dmask = (unsigned)nbins - 1u;
+  if (tid == 0) sm.tile = atomicAdd(tile_ctr, 1u);
+  for (int i = tid; i < OS_WARPS * kMaxBins; i += OS_THREADS) (&sm.whist[0][0])[i] = 0;
+  __syncthreads();
+  const unsigned tile = sm.tile;
+  const unsigned tbase = tile * (unsigned)OS_TILE;
+  const unsigned tvalid = min((unsigned)OS_TILE, no - tbase);
+
+  // warp-striped load: item j of lane l of warp w is tile element w*256 + j*32 + l
+  unsigned key[OS_ITEMS], val[OS_ITEMS], rank[OS_ITEMS];
+#pragma unroll
+  for (int j = 0; j < OS_ITEMS; ++j) {
+    const unsigned e = (unsigned)warp * (OS_ITEMS * 32) + j * 32 + lane;
+    key[j] = 0u;
+    val[j] = 0u;
+    if (e < tvalid) {
+      key[j] = __ldcs(keys_in + tbase + e);
+      val[j] = __ldcs(vals_in + tbase + e);
+    }
+  }
+  // global exclusive digit start, part 1 (warp-local scan of the pass histogram)
+  unsigned h = 0, h_inc = 0;
+  if (tid < kMaxBins) {
+    h = tid < nbins ? __ldg(&hist[tid]) : 0u;
+    h_inc = h;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned o = __shfl_up_sync(0xffffffffu, h_inc, d);
+      if (lane >= d) h_inc += o;
+    }
+    if (lane == 31) sm.wsum_h[warp] = h_inc;
+  }
+  // warp-level stable ranking (match-any multisplit); element order = index order
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int j = 0; j < OS_ITEMS; ++j) {
+    const unsigned e = (unsigned)warp * (OS_ITEMS * 32) + j * 32 + lane;
+    const bool valid = e < tvalid;
+    const unsigned active = __ballot_sync(0xffffffffu, valid);
+    const unsigned d = (key[j] >> shift) & dmask;
+    unsigned old = 0, leader = lane, r = 0;
+    if (valid) {
+      const unsigned peers = __match_any_sync(active, d);
+      leader = __ffs(peers) - 1;
+      r = __popc(peers & lt);
+      if (lane == (int)leader) {
+        old = sm.whist[warp][d];
+        sm.whist[warp][d] = old + __popc(peers);
+      }
+    }
+    old = __shfl_sync(0xffffffffu, old, leader);
+    rank[j] = old + r;
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive offsets across warps + tile count; publish the aggregate early
+  unsigned tcount = 0, l_inc = 0, dstart = 0;
+  if (tid < kMaxBins) {
+    if (tid < nbins) {
+#pragma unroll
+      for (int w = 0; w < OS_WARPS; ++w) {
+        const unsigned c = sm.whist[w][tid];
+        sm.whist[w][tid] = tcount;
+        tcount += c;
+      }
+      st_relaxed_u32(status + (size_t)tile * kMaxBins + tid, tile == 0 ? (OS_PREFIX | tcount) : (tcount + 1u));
+    }
+    for (int w = 0; w < warp; ++w) dstart += sm.wsum_h[w];
+    dstart += h_inc - h;
+    l_inc = tcount;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned o = __shfl_up_sync(0xffffffffu, l_inc, d);
+      if (lane >= d) l_inc += o;
+    }
+    if (lane == 31) sm.wsum_l[warp] = l_inc;
+  }
+  __syncthreads();
+  if (tid < nbins) {
+    unsigned lstart = l_inc - tcount;
+    for (int w = 0; w < warp; ++w) lstart += sm.wsum_l[w];
+    sm.local_start[tid] = lstart;
+    unsigned excl = 0;
+    if (tile > 0) {
+      // decoupled look-back over this digit's column of the status matrix
+      long long pred = (long long)tile - 1;
+      while (true) {
+        const unsigned v = ld_relaxed_u32(status + (size_t)pred * kMaxBins + tid);
+        if (v == 0u) continue;  // predecessor has not published yet
+        if (v & OS_PREFIX) {
+          excl += v & ~OS_PREFIX;
+          break;
+        }
+        excl += v - 1u;
+        --pred;
+      }
+      st_relaxed_u32(status + (size_t)tile * kMaxBins + tid, OS_PREFIX | (excl + tcount));
+    }
+    sm.gbase[tid] = dstart + excl - lstart;
+  }
+  __syncthreads();
+  // stable local scatter into digit order
+#pragma unroll
+  for (int j = 0; j < OS_ITEMS; ++j) {
+    const unsigned e = (unsigned)warp * (OS_ITEMS * 32) + j * 32 + lane;
+    if (e < tvalid) {
+      const unsigned d = (key[j] >> shift) & dmask;
+      const unsigned pos = sm.local_start[d] + sm.whist[warp][d] + rank[j];
+      sm.keys[pos] = key[j];
+      sm.vals[pos] = val[j];
+    }
+  }
+  __syncthreads();
+  // write out: consecutive smem slots of one digit go to consecutive global positions
+  for (unsigned i = tid; i < tvalid; i += OS_THREADS) {
+    const unsigned k = sm.keys[i];
+    const unsigned g = sm.gbase[(k >> shift) & dmask] + i;
+    if (keys_out) keys_out[g] = k;
+    vals_out[g] = sm.vals[i];
+  }
+}
+
+// ----------------------------------------------------------------------------------------
+// K4: G from the sorted cell ids (RLE -> NonEmptyCells scatter -> ExclusiveSum, fused)
+// ----------------------------------------------------------------------------------------
+constexpr int G_THREADS = 256;
+constexpr int G_ITEMS = 16;
+constexpr int G_TILE = G_THREADS * G_ITEMS;  // cells per CTA
+
+// G[c] = #pairs with cell < c = lower_bound(sorted, c). Each CTA owns cells [c0, c0+G_TILE):
+// two warp searches bound its key range [i0, i1); every first occurrence of a cell marks
+// its run start; a block suffix-min fills empty cells with the next run start (or i1).
+// The last CTA also writes the sentinel G[ncells] = NO (builders.py:131-133).
+__global__ void __launch_bounds__(G_THREADS)
+k_cell_offsets(const unsigned* __restrict__ sorted, unsigned no, unsigned ncells, unsigned* __restrict__ G) {
+  __shared__ unsigned mark[G_TILE];
+  __shared__ unsigned sh_i0, sh_i1;
+  __shared__ unsigned sh_wmin[G_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned c0 = blockIdx.x * (unsigned)G_TILE;
+  const unsigned c1 = min(c0 + (unsigned)G_TILE, ncells);
+  auto ld = [&](unsigned long long i) { return (unsigned long long)__ldg(sorted + i); };
+  if (warp == 0) {
+    const unsigned v = (unsigned)warp_lower_bound(no, c0, ld);
+    if (lane == 0) sh_i0 = v;
+  } else if (warp == 1) {
+    const unsigned v = (unsigned)warp_lower_bound(no, c1, ld);
+    if (lane == 0) sh_i1 = v;
+  }
+  for (int i = tid; i < G_TILE; i += G_THREADS) mark[i] = 0xffffffffu;
+  __syncthreads();
+  const unsigned i0 = sh_i0, i1 = sh_i1;
+  for (unsigned i = i0 + tid; i < i1; i += G_THREADS) {
+    const unsigned k = __ldg(sorted + i);
+    if (i == 0 || __ldg(sorted + i - 1) != k) mark[k - c0] = i;
+  }
+  __syncthreads();
+  // block suffix-min (thread t owns cells [16t, 16t+16))
+  unsigned v[G_ITEMS];
+#pragma unroll
+  for (int q = 0; q < G_ITEMS / 4; ++q) {
+    const uint4 a = *reinterpret_cast<const uint4*>(&mark[tid * G_ITEMS + 4 * q]);
+    v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
+  }
+  unsigned tmin = i1;
+#pragma unroll
+  for (int q = 0; q < G_ITEMS; ++q) tmin = min(tmin, v[q]);
+  unsigned suf = tmin;  // inclusive suffix-min over lanes >= lane
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned o = __shfl_down_sync(0xffffffffu, suf, d);
+    if (lane + d < 32) suf = min(suf, o);
+  }
+  if (lane == 0) sh_wmin[warp] = suf;
+  __syncthreads();
+  unsigned carry = __shfl_down_sync(0xffffffffu, suf, 1);
+  if (lane == 31) carry = i1;
+  for (int w = warp + 1; w < G_THREADS / 32; ++w) carry = min(carry, sh_wmin[w]);
+#pragma unroll
+  for (int q = G_ITEMS - 1; q >= 0; --q) {
+    carry = min(carry, v[q]);
+    v[q] = carry;
+  }
+  const unsigned cb = c0 + (unsigned)tid * G_ITEMS;
+  if (cb + G_ITEMS <= c1) {
+    uint4* dst = reinterpret_cast<uint4*>(G + cb);
+#pragma unroll
+    for (int q = 0; q < G_ITEMS / 4; ++q) dst[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < G_ITEMS; ++q)
+      if (cb + q < c1) G[cb + q] = v[q];
+  }
+  if (blockIdx.x == gridDim.x - 1 && tid == 0) G[ncells] = no;
+}
+
+}  // namespace pgrid

@@ -1,0 +1,193 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden vectors and
+the CPU oracle. Bit-exact: this path is integer/index work plus an IEEE f64 floor."""
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2403_10647_b200 import _native, builders, gen_scene, grids_equal, spec_for_mesh
+from paper_2403_10647_b200.errors import InvariantError, SizeError
+from paper_2403_10647_b200.gridcore import Aabb, GridSpec, TriangleMesh
+from paper_2403_10647_b200.kernels import radix_sort_pairs
+from util import KAT_NAMES, kat_case, scene_from_recipe, sha
+
+pytestmark = pytest.mark.gpu
+
+STAGES = ("v", "offsets", "obj_ids", "rel_c", "global_c", "sorted_c", "sorted_o",
+          "rle_uniques", "rle_counts", "g")
+
+
+@pytest.mark.parametrize("name", KAT_NAMES)
+def test_kat_every_stage(kat, name):
+    mesh, spec = kat_case(kat, name)
+    rec = {}
+    grid, rep = builders.build_parallel(mesh, spec, record=rec)
+    assert np.array_equal(grid.G, kat[f"{name}/G"])
+    assert np.array_equal(grid.O, kat[f"{name}/O"])
+    assert rep.no == int(kat[f"{name}/no"]) == rec["no"]
+    for st in STAGES:
+        assert np.array_equal(rec[st], kat[f"{name}/{st}"]), st
+
+
+def test_walkthrough_report(kat):
+    mesh, spec = kat_case(kat, "walkthrough")
+    grid, rep = builders.build_parallel(mesh, spec)
+    assert grid.G.tolist() == [0, 1, 3, 3, 4] and grid.O.tolist() == [0, 0, 1, 1]
+    assert rep.algo == "parallel" and rep.no == 4
+    assert rep.max_task_work == 8 and rep.total_work == 32
+    assert set(rep.phase_ms) == set(builders.PHASES) and rep.total_ms > 0
+
+
+def test_empty_mesh(kat):
+    spec = GridSpec(Aabb([0, 0, 0], [1, 1, 1]), (2, 2, 2))
+    grid, rep = builders.build_parallel(TriangleMesh(np.zeros((0, 3)), np.zeros((0, 3), np.int32)), spec)
+    assert np.array_equal(grid.G, kat["empty/G"]) and grid.no == 0 and rep.no == 0
+    assert rep.max_task_work == 0
+
+
+@pytest.mark.parametrize("kind", ["uniform", "skewed", "walls"])
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_random_scenes(kat, kind, seed):
+    mesh = gen_scene(kind, 400 + 100 * seed, seed)
+    spec = spec_for_mesh(mesh, dims=(9, 7, 11))
+    grid, rep = builders.build_parallel(mesh, spec)
+    assert np.array_equal(grid.G, kat[f"rand_{kind}_{seed}/G"])
+    assert np.array_equal(grid.O, kat[f"rand_{kind}_{seed}/O"])
+    assert grid.G[-1] == grid.no == rep.no
+    assert np.all(np.diff(grid.G.astype(np.int64)) >= 0)
+
+
+def test_acceptance_100_scenes(hashes):
+    """The reference's validate recipe (cli.py:171-196, test_acceptance.py:24-32)."""
+    for key in [k for k in hashes if k.startswith("accept_")]:
+        h = hashes[key]
+        mesh, spec = scene_from_recipe(h["recipe"])
+        grid, rep = builders.build_parallel(mesh, spec)
+        assert rep.no == h["no"], key
+        assert sha(grid.G) == h["G_sha256"] and sha(grid.O) == h["O_sha256"], key
+
+
+@pytest.mark.parametrize("key", ["cfg1", "skewed100k", "walls100k", "cfg2"] +
+                         [f"sweep1m_d{d}" for d in (1, 2, 4, 8, 16, 32, 64)])
+def test_config_hashes(hashes, key):
+    h = hashes[key]
+    mesh, spec = scene_from_recipe(h["recipe"])
+    assert list(spec.dims) == h["dims"]
+    grid, rep = builders.build_parallel(mesh, spec)
+    assert rep.no == h["no"]
+    assert sha(grid.G) == h["G_sha256"] and sha(grid.O) == h["O_sha256"]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("key", ["cfg3", "cfg3u"])
+def test_headline_config_hashes(hashes, key):
+    h = hashes[key]
+    mesh, spec = scene_from_recipe(h["recipe"])
+    grid, rep = builders.build_parallel(mesh, spec)
+    assert rep.no == h["no"]
+    assert sha(grid.G) == h["G_sha256"] and sha(grid.O) == h["O_sha256"]
+
+
+def test_random_vs_oracle():
+    """Scenes without committed goldens: compare with the C oracle directly."""
+    rng = np.random.default_rng(3)
+    for i in range(20):
+        kind = ("uniform", "skewed", "walls", "lognormal", "arch")[i % 5]
+        n = int(rng.integers(1, 60000))
+        mesh = gen_scene(kind, n, 50 + i)
+        dims = tuple(int(d) for d in rng.integers(1, 90, 3)) if i % 2 else None
+        spec = spec_for_mesh(mesh, dims=dims) if dims else spec_for_mesh(mesh, density=float(rng.integers(1, 30)))
+        grid, rep = builders.build_parallel(mesh, spec)
+        G, O = oracle.build_parallel(mesh.vertices, mesh.triangles, spec)
+        assert np.array_equal(grid.G, G) and np.array_equal(grid.O, O), (kind, n, spec.dims)
+
+
+def test_indexed_mesh_and_custom_bounds_vs_oracle():
+    """Shared vertices, unreferenced vertices, a spec that drops most triangles."""
+    rng = np.random.default_rng(9)
+    V = rng.random((5000, 3)) * 4 - 1
+    T = rng.integers(0, 4000, size=(20000, 3)).astype(np.int32)
+    mesh = TriangleMesh(V, T)
+    for dims in ((1, 1, 1), (3, 1, 1), (17, 23, 5), (64, 64, 64)):
+        spec = GridSpec(Aabb([0.2, 0.1, 0.3], [0.9, 0.6, 0.7]), dims)
+        grid, _ = builders.build_parallel(mesh, spec)
+        G, O = oracle.build_parallel(V, T, spec)
+        assert np.array_equal(grid.G, G) and np.array_equal(grid.O, O), dims
+
+
+def test_huge_object_and_tile_spanning():
+    """One triangle covering every cell plus small ones: owner search across many tiles."""
+    mesh = gen_scene("skewed", 3000, 4)
+    spec = spec_for_mesh(mesh, dims=(160, 150, 140))     # 3.36M cells, NO > 3.36M
+    grid, rep = builders.build_parallel(mesh, spec)
+    G, O = oracle.build_parallel(mesh.vertices, mesh.triangles, spec)
+    assert np.array_equal(grid.G, G) and np.array_equal(grid.O, O)
+
+
+def test_size_errors():
+    V = np.array([[-1, -1, -1], [3, -1, 2], [-1, 3, 2]], np.float64)
+    T = np.array([[0, 1, 2]], np.int32)
+    mesh = TriangleMesh(V, T)
+    with pytest.raises(SizeError):   # ncells > 2^30: the reference's G scan cap
+        builders.build_parallel(mesh, GridSpec(Aabb([0, 0, 0], [1, 1, 1]), (1025, 1024, 1024)))
+    # NO > 2^30 pairs from 2 full-cover triangles on 2^29+ cells
+    mesh2 = TriangleMesh(V, np.array([[0, 1, 2], [0, 1, 2], [0, 1, 2]], np.int32))
+    with pytest.raises(SizeError):
+        builders.build_parallel(mesh2, GridSpec(Aabb([0, 0, 0], [1, 1, 1]), (1024, 1024, 512)))
+
+
+def test_invariant_error_on_inverted_box():
+    """+inf upper corner with lo > 0: the reference fails its non-negative check."""
+    V = np.array([[0.6, 0.6, 0.6], [np.inf, 0.7, 0.7], [0.7, 0.6, 0.7]], np.float64)
+    mesh = TriangleMesh(V, np.array([[0, 1, 2]], np.int32))
+    with pytest.raises(InvariantError):
+        builders.build_parallel(mesh, GridSpec(Aabb([0, 0, 0], [1, 1, 1]), (4, 4, 4)))
+
+
+def test_repeat_builds_identical_and_workers_ignored():
+    mesh = gen_scene("walls", 3000, 5)
+    spec = spec_for_mesh(mesh, dims=(30, 31, 29))
+    first, _ = builders.build_parallel(mesh, spec, workers=1)
+    for w in (None, 8, 64):
+        again, _ = builders.build_parallel(mesh, spec, workers=w)
+        assert grids_equal(first, again)
+
+
+def test_fault_injection_hook():
+    mesh = gen_scene("uniform", 100, 2)
+    spec = spec_for_mesh(mesh, dims=(4, 4, 4))
+    clean, _ = builders.build_parallel(mesh, spec)
+    builders._fault_inject = True
+    try:
+        faulty, _ = builders.build_parallel(mesh, spec)
+    finally:
+        builders._fault_inject = False
+    assert not grids_equal(clean, faulty)
+
+
+@pytest.mark.parametrize("bits", [0, 1, 7, 8, 9, 19, 26, 32])
+def test_plugin_radix_sort_kat(kat, bits):
+    ks, vs = radix_sort_pairs(kat[f"radix{bits}/keys"], kat[f"radix{bits}/vals"], bits)
+    assert np.array_equal(ks, kat[f"radix{bits}/sorted_keys"])
+    assert np.array_equal(vs, kat[f"radix{bits}/sorted_vals"])
+
+
+@pytest.mark.parametrize("n,bits", [(1, 5), (4095, 12), (4097, 16), (1_000_003, 30), (2_000_000, 32)])
+def test_plugin_radix_sort_vs_oracle(n, bits):
+    rng = np.random.default_rng(n)
+    keys = rng.integers(0, 1 << bits, n, dtype=np.uint64).astype(np.uint32)
+    keys[::5] = keys[7 % n]
+    vals = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    ks, vs = radix_sort_pairs(keys, vals, bits)
+    ok, ov = oracle.radix_sort_pairs(keys, vals, bits)
+    assert np.array_equal(ks, ok) and np.array_equal(vs, ov)
+
+
+def test_launch_count_is_native():
+    """The build runs our kernels: K1 + K2 + passes + K4 launches are reported."""
+    mesh = gen_scene("uniform", 20000, 1)
+    spec = spec_for_mesh(mesh)
+    builders.build_parallel(mesh, spec)
+    b = _native.thread_builder()
+    nbits = int(spec.ncells - 1).bit_length()
+    assert b.launches() == 3 + (nbits + 7) // 8

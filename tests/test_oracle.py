@@ -1,0 +1,99 @@
+"""The CPU oracle (oracle/pgrid_oracle.c) pinned against the reference's golden vectors.
+
+Golden vectors come from running the unmodified reference (tests/golden/make_golden.py);
+when oracle/_ref holds a built reference, the oracle is also cross-checked live.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from util import KAT_NAMES, kat_case, scene_from_recipe, sha
+
+
+@pytest.mark.parametrize("name", KAT_NAMES)
+def test_oracle_kat_all_stages(kat, name):
+    mesh, spec = kat_case(kat, name)
+    lo, hi, keep = oracle.cell_boxes(mesh.vertices, mesh.triangles, spec)
+    assert np.array_equal(lo, kat[f"{name}/box_lo"])
+    assert np.array_equal(hi, kat[f"{name}/box_hi"])
+    assert np.array_equal(keep, kat[f"{name}/keep"])
+    G, O, st = oracle.build_parallel(mesh.vertices, mesh.triangles, spec, stages=True)
+    assert np.array_equal(G, kat[f"{name}/G"])
+    assert np.array_equal(O, kat[f"{name}/O"])
+    assert st["no"] == int(kat[f"{name}/no"])
+    assert np.array_equal(st["global_c"], kat[f"{name}/global_c"])
+    assert np.array_equal(st["obj_ids"], kat[f"{name}/obj_ids"])
+    assert np.array_equal(st["sorted_c"], kat[f"{name}/sorted_c"])
+    assert np.array_equal(st["sorted_o"], kat[f"{name}/sorted_o"])
+
+
+def test_oracle_empty(kat):
+    from paper_2403_10647_b200.gridcore import Aabb, GridSpec
+    spec = GridSpec(Aabb([0, 0, 0], [1, 1, 1]), (2, 2, 2))
+    G, O = oracle.build_parallel(np.zeros((0, 3)), np.zeros((0, 3), np.int32), spec)
+    assert np.array_equal(G, kat["empty/G"]) and len(O) == 0
+
+
+@pytest.mark.parametrize("bits", [0, 1, 7, 8, 9, 19, 26, 32])
+def test_oracle_radix_kat(kat, bits):
+    ks, vs = oracle.radix_sort_pairs(kat[f"radix{bits}/keys"], kat[f"radix{bits}/vals"], bits)
+    assert np.array_equal(ks, kat[f"radix{bits}/sorted_keys"])
+    assert np.array_equal(vs, kat[f"radix{bits}/sorted_vals"])
+
+
+@pytest.mark.parametrize("kind", ["uniform", "skewed", "walls"])
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_oracle_random_scenes(kat, kind, seed):
+    from paper_2403_10647_b200 import gen_scene, spec_for_mesh
+    mesh = gen_scene(kind, 400 + 100 * seed, seed)
+    spec = spec_for_mesh(mesh, dims=(9, 7, 11))
+    G, O = oracle.build_parallel(mesh.vertices, mesh.triangles, spec)
+    assert np.array_equal(G, kat[f"rand_{kind}_{seed}/G"])
+    assert np.array_equal(O, kat[f"rand_{kind}_{seed}/O"])
+
+
+def test_oracle_acceptance_100_scenes(hashes):
+    keys = [k for k in hashes if k.startswith("accept_")]
+    assert len(keys) == 100
+    for key in keys:
+        h = hashes[key]
+        mesh, spec = scene_from_recipe(h["recipe"])
+        assert list(spec.dims) == h["dims"]
+        G, O = oracle.build_parallel(mesh.vertices, mesh.triangles, spec)
+        assert len(O) == h["no"] and sha(G) == h["G_sha256"] and sha(O) == h["O_sha256"], key
+
+
+@pytest.mark.parametrize("key", ["cfg1", "skewed100k", "cfg2", "sweep1m_d1", "sweep1m_d64"])
+def test_oracle_config_hashes(hashes, key):
+    h = hashes[key]
+    mesh, spec = scene_from_recipe(h["recipe"])
+    assert list(spec.dims) == h["dims"]
+    G, O = oracle.build_parallel(mesh.vertices, mesh.triangles, spec)
+    assert len(O) == h["no"]
+    assert sha(G) == h["G_sha256"] and sha(O) == h["O_sha256"]
+
+
+def test_oracle_vs_live_reference():
+    ref = oracle.reference_module()
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(11)
+    for i in range(12):
+        n = int(rng.integers(1, 3000))
+        kind = ("uniform", "skewed", "walls")[i % 3]
+        mesh = ref.gen_scene(kind, n, 1000 + i)
+        dims = tuple(int(d) for d in rng.integers(1, 40, 3))
+        spec = ref.spec_for_mesh(mesh, dims=dims)
+        g, rep = ref.build_parallel(mesh, spec)
+        G, O = oracle.build_parallel(mesh.vertices, mesh.triangles, spec)
+        assert np.array_equal(G, g.G) and np.array_equal(O, g.O)
+
+
+def test_oracle_size_error():
+    from paper_2403_10647_b200.gridcore import Aabb, GridSpec
+    # one triangle covering 1024^3 cells: NO > 2^30 scan cap -> SizeError in the reference
+    spec = GridSpec(Aabb([0, 0, 0], [1, 1, 1]), (1025, 1024, 1024))
+    V = np.array([[-1, -1, -1], [3, -1, 2], [-1, 3, 2]], np.float64)
+    with pytest.raises(oracle.OracleSizeError):
+        oracle.build_parallel(V, np.array([[0, 1, 2]], np.int32), spec)

@@ -1,0 +1,48 @@
+"""Run the reference's OWN test-suite (built into oracle/_ref by `make -C oracle ref`)
+with the B200 build_parallel injected in place of the reference's (compat.install), and
+the "cuda" lane registered in its backend registry. A drop-in must pass it unchanged."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "oracle", "_ref")
+
+pytestmark = pytest.mark.gpu
+
+
+def test_reference_suite_against_gpu_builder():
+    if not os.path.isdir(os.path.join(REF, "tests")):
+        pytest.skip("oracle/_ref/tests not built (make -C oracle ref)")
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([REF, os.path.join(ROOT, "tests"), ROOT, env.get("PYTHONPATH", "")])
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "ref_inject_plugin",
+                        "-p", "no:cacheprovider", os.path.join(REF, "tests")],
+                       cwd=REF, env=env, capture_output=True, text=True, timeout=1200)
+    tail = (r.stdout + r.stderr)[-3000:]
+    assert r.returncode == 0, tail
+    assert " passed" in r.stdout, tail
+    print(tail.strip().splitlines()[-1])
+
+
+def test_injection_is_effective():
+    """Guard against a silent no-op shim: the injected function is ours."""
+    if not os.path.isdir(os.path.join(REF, "pargrid")):
+        pytest.skip("oracle/_ref not built")
+    code = ("import pargrid, pargrid.cli;"
+            "from paper_2403_10647_b200 import compat; compat.install(pargrid);"
+            "import pargrid.builders as b;"
+            "assert getattr(b.build_parallel, '__wrapped_b200__', False);"
+            "assert pargrid.cli.ALGORITHMS['parallel'] is b.build_parallel;"
+            "assert 'cuda' in pargrid.kernels.available_backends();"
+            "m = pargrid.gen_scene('uniform', 500, 1); s = pargrid.spec_for_mesh(m);"
+            "g, r = pargrid.build_parallel(m, s);"
+            "assert type(g) is pargrid.CompactGrid and type(r) is pargrid.BuildReport;"
+            "print('ok')")
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([REF, ROOT, env.get("PYTHONPATH", "")])
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]

@@ -1,0 +1,29 @@
+"""Shared helpers for the parity tests (fixtures are regenerated from recipes)."""
+
+import hashlib
+
+import numpy as np
+
+from paper_2403_10647_b200 import scenes
+from paper_2403_10647_b200.gridcore import Aabb, GridSpec, TriangleMesh, spec_for_mesh
+
+KAT_NAMES = ("walkthrough", "full_cover", "dropped", "faces", "nonfinite", "indexed",
+             "one_cell", "sparse_kept")
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def kat_case(kat, name):
+    mesh = TriangleMesh(kat[f"{name}/V"], kat[f"{name}/T"])
+    spec = GridSpec(Aabb(kat[f"{name}/lo"], kat[f"{name}/hi"]), tuple(int(d) for d in kat[f"{name}/dims"]))
+    return mesh, spec
+
+
+def scene_from_recipe(recipe):
+    """(mesh, spec) for a hashes.json recipe."""
+    mesh = scenes.gen_scene(recipe["kind"], recipe["n"], recipe["seed"], recipe.get("density", 5.0))
+    if "dims" in recipe:
+        return mesh, spec_for_mesh(mesh, dims=tuple(recipe["dims"]))
+    return mesh, spec_for_mesh(mesh, density=recipe["density"])
