@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -93,6 +94,25 @@ int bit_length(uint64_t v) {
 }
 
 size_t os_smem_bytes() { return sizeof(OsSmem); }
+
+// PGRID_SYNC_DEBUG=1: synchronise after every launch so a fault names its kernel.
+bool sync_debug() {
+  static const bool on = [] {
+    const char* e = getenv("PGRID_SYNC_DEBUG");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
+
+#define LAUNCHED(name, st)                                                                         \
+  do {                                                                                             \
+    CU(cudaGetLastError());                                                                        \
+    if (sync_debug()) {                                                                            \
+      cudaError_t e2_ = cudaStreamSynchronize(st);                                                 \
+      if (e2_ != cudaSuccess)                                                                      \
+        return fail(PG_CUDA_ERROR, "kernel %s failed: %s", name, cudaGetErrorString(e2_));         \
+    }                                                                                              \
+  } while (0)
 
 }  // namespace
 
@@ -227,7 +247,7 @@ int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64
   CU(cudaEventRecord(b->ev[5], st));
   k_boxes_count_scan<<<ntiles, K1_THREADS, 0, st>>>(dV, reinterpret_cast<const int*>(dT), n, ds,
                                                      b->rec.as<uint4>(), status, ctr, total, err);
-  CU(cudaGetLastError());
+  LAUNCHED("k_boxes_count_scan", st);
   CU(cudaEventRecord(b->ev[6], st));
   b->launches = 1;
   b->k1_timed = true;
@@ -264,7 +284,7 @@ int run_passes(pg_builder* b, const PassPlan& plan, unsigned* keys0, unsigned* v
     k_onesweep_pass<<<ntiles, OS_THREADS, os_smem_bytes(), st>>>(
         kin, vin, ko, vo, (unsigned)n, plan.shift[p], plan.bits[p], hist + p * kMaxBins,
         status + (size_t)p * ntiles * kMaxBins, ctrs + p);
-    CU(cudaGetLastError());
+    LAUNCHED("k_onesweep_pass", st);
     ++b->launches;
     *sorted_keys_out = ko;
   }
@@ -317,7 +337,7 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
     k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->n, (unsigned)no, (unsigned)b->dims[0],
                                                      (unsigned)b->dims[0] * (unsigned)b->dims[1], plan, keysA, v0,
                                                      hist);
-    CU(cudaGetLastError());
+    LAUNCHED("k_expand_pairs", st);
     ++b->launches;
     if (flags & PG_KEEP_STAGES) {
       if ((rc = b->stage.ensure(2 * sec))) return rc;
@@ -336,7 +356,7 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
   CU(cudaEventRecord(b->ev[2], st));
   const unsigned g_tiles = (unsigned)((ncells + G_TILE - 1) / G_TILE);
   k_cell_offsets<<<g_tiles, G_THREADS, 0, st>>>(sorted, (unsigned)no, (unsigned)ncells, dG);
-  CU(cudaGetLastError());
+  LAUNCHED("k_cell_offsets", st);
   ++b->launches;
   b->sorted_keys = sorted;
   CU(cudaEventRecord(b->ev[3], st));
@@ -427,7 +447,7 @@ int pg_radix_sort_pairs(pg_builder* b, const uint32_t* keys, const uint32_t* val
   unsigned* vfinal = vA;
   if (plan.npasses > 0) {
     k_digit_hist<<<std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(kA, n, plan, hist);
-    CU(cudaGetLastError());
+    LAUNCHED("k_digit_hist", st);
     ++b->launches;
     // host outputs: final values land in the staging section behind the pair buffers
     if ((rc = b->stage.ensure(sec))) return rc;

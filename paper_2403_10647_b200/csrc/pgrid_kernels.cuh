@@ -83,14 +83,17 @@ __device__ __forceinline__ unsigned long long warp_lower_bound(unsigned long lon
     const unsigned long long p = lo + (unsigned long long)lane * step;
     const bool ge = (p < hi) ? (load(p) >= x) : true;
     const unsigned ball = __ballot_sync(0xffffffffu, ge);
-    const int f = __ffs(ball) - 1;  // first lane whose probe is >= x (ball != 0: lanes past hi vote true)
+    // f = first lane whose probe is >= x; 32 if every probe is < x (then the answer is past
+    // lane 31's probe: all 32 probes can lie inside [lo, hi) when 31*step < span)
+    const int f = ball ? __ffs(ball) - 1 : 32;
     if (f == 0) {
       hi = lo;
     } else {
-      const unsigned long long pf = lo + (unsigned long long)f * step;
-      const unsigned long long pprev = lo + (unsigned long long)(f - 1) * step;
-      lo = pprev + 1;
-      hi = pf < hi ? pf : hi;
+      lo = lo + (unsigned long long)(f - 1) * step + 1;
+      if (f < 32) {
+        const unsigned long long pf = (lo - 1) + step;
+        hi = pf < hi ? pf : hi;
+      }
     }
   }
   return lo;
@@ -244,7 +247,7 @@ __global__ void __launch_bounds__(K2_THREADS)
 k_expand_pairs(const uint4* __restrict__ rec, long long n, unsigned no, unsigned dx, unsigned dxy,
                PassPlan plan, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
                unsigned* __restrict__ hist) {
-  __shared__ int slot[K2_TILE];
+  __shared__ __align__(16) int slot[K2_TILE];
   __shared__ unsigned sh_hist[kMaxPasses * kMaxBins];
   __shared__ int sh_warpmax[K2_THREADS / 32];
   __shared__ long long sh_olo;
@@ -553,7 +556,7 @@ constexpr int G_TILE = G_THREADS * G_ITEMS;  // cells per CTA
 // The last CTA also writes the sentinel G[ncells] = NO (builders.py:131-133).
 __global__ void __launch_bounds__(G_THREADS)
 k_cell_offsets(const unsigned* __restrict__ sorted, unsigned no, unsigned ncells, unsigned* __restrict__ G) {
-  __shared__ unsigned mark[G_TILE];
+  __shared__ __align__(16) unsigned mark[G_TILE];
   __shared__ unsigned sh_i0, sh_i1;
   __shared__ unsigned sh_wmin[G_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -105,10 +105,11 @@ def test_random_vs_oracle():
 def test_indexed_mesh_and_custom_bounds_vs_oracle():
     """Shared vertices, unreferenced vertices, a spec that drops most triangles."""
     rng = np.random.default_rng(9)
-    V = rng.random((5000, 3)) * 4 - 1
-    T = rng.integers(0, 4000, size=(20000, 3)).astype(np.int32)
+    V = rng.random((5000, 3)) * 1.4 - 0.2
+    T = rng.integers(0, 4000, size=(3000, 3)).astype(np.int32)
+    T[::5, 1:] = T[::5, :1] + rng.integers(0, 3, size=(600, 2))   # some small triangles
     mesh = TriangleMesh(V, T)
-    for dims in ((1, 1, 1), (3, 1, 1), (17, 23, 5), (64, 64, 64)):
+    for dims in ((1, 1, 1), (3, 1, 1), (17, 23, 5), (40, 30, 20)):
         spec = GridSpec(Aabb([0.2, 0.1, 0.3], [0.9, 0.6, 0.7]), dims)
         grid, _ = builders.build_parallel(mesh, spec)
         G, O = oracle.build_parallel(V, T, spec)
