@@ -290,7 +290,7 @@ def main():
     phases /= args.steps
     k1_ms, k2_ms, sort_ms, k4_ms = phases[0], phases[2], phases[3], phases[5]
     key_bits = int(ncells - 1).bit_length()
-    npasses = (key_bits + 7) // 8
+    npasses = max(launches - 3, 0)       # K1 + K2 + K4 + one launch per radix pass
     pass_ms = sort_ms / max(npasses, 1)
 
     # end to end through the public API: pinned host inputs, H2D + build + D2H each step

@@ -134,7 +134,8 @@ struct pg_builder {
   int dims[3] = {1, 1, 1};
   int key_bits = 0;
   bool stages_kept = false;
-  bool k1_timed = false;  // ev[5]..ev[6] bracket K1 of the last pg_count
+  bool k1_timed = false;
+  unsigned os_grid = 148;  // persistent onesweep CTAs (SMs x resident CTAs per SM)  // ev[5]..ev[6] bracket K1 of the last pg_count
   int launches = 0;
   const unsigned* sorted_keys = nullptr;
 };
@@ -151,6 +152,12 @@ int pg_builder_create(int device, pg_builder** out) {
   for (auto& e : b->ev) CU(cudaEventCreate(&e));
   CU(cudaMallocHost(&b->h_scalars, 4 * sizeof(unsigned long long)));
   CU(cudaFuncSetAttribute(k_onesweep_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)os_smem_bytes()));
+  {
+    int sms = 0, per_sm = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_onesweep_pass, OS_THREADS, os_smem_bytes()));
+    b->os_grid = (unsigned)std::max(1, sms * std::max(1, per_sm));
+  }
   *out = b;
   return PG_OK;
 }
@@ -281,7 +288,7 @@ int run_passes(pg_builder* b, const PassPlan& plan, unsigned* keys0, unsigned* v
     unsigned* vin = vbuf[p & 1];
     unsigned* ko = kbuf[(p + 1) & 1];
     unsigned* vo = last ? vals_final : vbuf[(p + 1) & 1];
-    k_onesweep_pass<<<ntiles, OS_THREADS, os_smem_bytes(), st>>>(
+    k_onesweep_pass<<<std::min(ntiles, b->os_grid), OS_THREADS, os_smem_bytes(), st>>>(
         kin, vin, ko, vo, (unsigned)n, plan.shift[p], plan.bits[p], hist + p * kMaxBins,
         status + (size_t)p * ntiles * kMaxBins, ctrs + p);
     LAUNCHED("k_onesweep_pass", st);
@@ -299,7 +306,7 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
   CU(cudaSetDevice(b->device));
   const uint64_t no = b->no;
   const int64_t ncells = b->ncells;
-  const PassPlan plan = make_plan(b->key_bits, 8);
+  const PassPlan plan = make_plan(b->key_bits, kMaxDigitBits);
   int rc;
   unsigned* dG = G;
   unsigned* dO = O;

@@ -234,7 +234,8 @@ k_boxes_count_scan(const double* __restrict__ V, const int* __restrict__ T, long
 constexpr int K2_THREADS = 256;
 constexpr int K2_ITEMS = 8;
 constexpr int K2_TILE = K2_THREADS * K2_ITEMS;
-constexpr int kMaxBins = 256;
+constexpr int kMaxDigitBits = 9;
+constexpr int kMaxBins = 1 << kMaxDigitBits;  // 512
 
 // Each CTA owns pairs [p0, p0 + K2_TILE). The owning triangle of every pair is recovered
 // the way Alg. 1 does it (marks at run starts + inclusive max-scan), but
@@ -398,21 +399,59 @@ constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096 pairs
 constexpr unsigned OS_PREFIX = 1u << 31;
 
 struct OsSmem {
-  unsigned keys[OS_TILE];
-  unsigned vals[OS_TILE];
+  unsigned buf[OS_TILE];               // tile in digit order: keys, then values
+  unsigned vstage[OS_TILE];            // values in input order (cp.async staging)
   unsigned whist[OS_WARPS][kMaxBins];  // per-warp digit counts, then exclusive warp offsets
+  unsigned dstart[kMaxBins];           // global exclusive digit start (from the histogram)
   unsigned local_start[kMaxBins];      // tile-local exclusive digit prefix
-  unsigned gbase[kMaxBins];            // global position of smem slot 0 for each digit
-  unsigned wsum_h[8];
-  unsigned wsum_l[8];
-  unsigned tile;
+  unsigned gbase[kMaxBins];            // global position of buf[0] for each digit
+  unsigned wsum[OS_WARPS];
+  unsigned tile, next_tile;
 };
 
-// One LSD digit pass (Adinets & Merrill's onesweep): tiles are claimed in order through an
-// atomic counter, ranked stably in shared memory with match-any warp multisplit, and placed
-// with a per-digit decoupled look-back over the previous tiles; global digit starts come
-// from the histogram K2 accumulated, so there is no separate upsweep/downsweep.
-__global__ void __launch_bounds__(OS_THREADS)
+__device__ __forceinline__ void cp_async4(void* smem, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_wait() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Block-wide exclusive scan of one value per thread (threads >= n contribute 0).
+__device__ __forceinline__ unsigned os_block_excl_scan(unsigned v, unsigned* wsum, unsigned& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned inc = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  unsigned add = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < OS_WARPS; ++w) {
+    const unsigned x = wsum[w];
+    add += w < warp ? x : 0u;
+    tot += x;
+  }
+  total = tot;
+  return add + inc - v;
+}
+
+// One LSD digit pass (Adinets & Merrill's onesweep), persistent: each CTA claims tiles in
+// order through an atomic counter (prefetching its next claim while it works), ranks a tile
+// stably in shared memory with match-any warp multisplit, and places it with a per-digit
+// decoupled look-back over the previous tiles. Global digit starts come from the histogram
+// K2 accumulated, so there is no upsweep. Values never occupy registers: cp.async stages
+// them in input order and they are permuted shared->shared after the keys are written.
+__global__ void __launch_bounds__(OS_THREADS, 2)
 k_onesweep_pass(const unsigned* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
                 unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, unsigned no, int shift,
                 int bits, const unsigned* __restrict__ hist, unsigned* __restrict__ status,
@@ -422,65 +461,77 @@ k_onesweep_pass(const unsigned* __restrict__ keys_in, const unsigned* __restrict
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nbins = 1 << bits;
   const unsigned dmask = (unsigned)nbins - 1u;
-  if (tid == 0) sm.tile = atomicAdd(tile_ctr, 1u);
-  for (int i = tid; i < OS_WARPS * kMaxBins; i += OS_THREADS) (&sm.whist[0][0])[i] = 0;
-  __syncthreads();
-  const unsigned tile = sm.tile;
-  const unsigned tbase = tile * (unsigned)OS_TILE;
-  const unsigned tvalid = min((unsigned)OS_TILE, no - tbase);
-
-  // warp-striped load: item j of lane l of warp w is tile element w*256 + j*32 + l
-  unsigned key[OS_ITEMS], val[OS_ITEMS], rank[OS_ITEMS];
-#pragma unroll
-  for (int j = 0; j < OS_ITEMS; ++j) {
-    const unsigned e = (unsigned)warp * (OS_ITEMS * 32) + j * 32 + lane;
-    key[j] = 0u;
-    val[j] = 0u;
-    if (e < tvalid) {
-      key[j] = __ldcs(keys_in + tbase + e);
-      val[j] = __ldcs(vals_in + tbase + e);
-    }
-  }
-  // global exclusive digit start, part 1 (warp-local scan of the pass histogram)
-  unsigned h = 0, h_inc = 0;
-  if (tid < kMaxBins) {
-    h = tid < nbins ? __ldg(&hist[tid]) : 0u;
-    h_inc = h;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const unsigned o = __shfl_up_sync(0xffffffffu, h_inc, d);
-      if (lane >= d) h_inc += o;
-    }
-    if (lane == 31) sm.wsum_h[warp] = h_inc;
-  }
-  // warp-level stable ranking (match-any multisplit); element order = index order
+  const unsigned ntiles = (no + OS_TILE - 1) / OS_TILE;
   const unsigned lt = lanemask_lt();
-#pragma unroll
-  for (int j = 0; j < OS_ITEMS; ++j) {
-    const unsigned e = (unsigned)warp * (OS_ITEMS * 32) + j * 32 + lane;
-    const bool valid = e < tvalid;
-    const unsigned active = __ballot_sync(0xffffffffu, valid);
-    const unsigned d = (key[j] >> shift) & dmask;
-    unsigned old = 0, leader = lane, r = 0;
-    if (valid) {
-      const unsigned peers = __match_any_sync(active, d);
-      leader = __ffs(peers) - 1;
-      r = __popc(peers & lt);
-      if (lane == (int)leader) {
-        old = sm.whist[warp][d];
-        sm.whist[warp][d] = old + __popc(peers);
-      }
-    }
-    old = __shfl_sync(0xffffffffu, old, leader);
-    rank[j] = old + r;
-    __syncwarp();
+
+  if (tid == 0) sm.tile = atomicAdd(tile_ctr, 1u);
+  {  // global exclusive digit starts, once per CTA
+    const unsigned h = tid < nbins ? __ldg(&hist[tid]) : 0u;
+    unsigned total;
+    const unsigned ex = os_block_excl_scan(h, sm.wsum, total);
+    if (tid < kMaxBins) sm.dstart[tid] = ex;
   }
   __syncthreads();
-  // per digit: exclusive offsets across warps + tile count; publish the aggregate early
-  unsigned tcount = 0, l_inc = 0, dstart = 0;
-  if (tid < kMaxBins) {
-    if (tid < nbins) {
+
+  while (true) {
+    const unsigned tile = sm.tile;
+    if (tile >= ntiles) break;
+    const unsigned tbase = tile * (unsigned)OS_TILE;
+    const unsigned tvalid = min((unsigned)OS_TILE, no - tbase);
+    // stage values (input order) asynchronously; claim the next tile early
+    if (tvalid == (unsigned)OS_TILE) {
+      for (int c = tid; c < OS_TILE / 4; c += OS_THREADS) cp_async16(&sm.vstage[4 * c], vals_in + tbase + 4 * c);
+    } else {
+      for (unsigned e = tid; e < tvalid; e += OS_THREADS) cp_async4(&sm.vstage[e], vals_in + tbase + e);
+    }
+    cp_async_commit();
+    if (tid == 0) sm.next_tile = atomicAdd(tile_ctr, 1u);
+    // each warp zeroes its own histogram row
+    for (int b = lane; b < nbins; b += 32) sm.whist[warp][b] = 0u;
+    // warp-striped keys: item j of lane l of warp w is tile element w*256 + j*32 + l
+    unsigned key[OS_ITEMS], dig[OS_ITEMS], peers[OS_ITEMS];
 #pragma unroll
+    for (int j = 0; j < OS_ITEMS; ++j) {
+      const unsigned e = (unsigned)warp * (OS_ITEMS * 32) + j * 32 + lane;
+      key[j] = e < tvalid ? __ldcs(keys_in + tbase + e) : 0u;
+    }
+    // peers (same-digit lanes) of every item via bit-sliced ballots (MATCH.ANY is MIO-bound)
+#pragma unroll
+    for (int j = 0; j < OS_ITEMS; ++j) {
+      const unsigned e = (unsigned)warp * (OS_ITEMS * 32) + j * 32 + lane;
+      unsigned pm = __ballot_sync(0xffffffffu, e < tvalid);
+      dig[j] = (key[j] >> shift) & dmask;
+#pragma unroll
+      for (int b = 0; b < kMaxDigitBits; ++b) {
+        if (b < bits) {
+          const bool set = (dig[j] >> b) & 1u;
+          const unsigned bb = __ballot_sync(0xffffffffu, set);
+          pm &= set ? bb : ~bb;
+        }
+      }
+      peers[j] = e < tvalid ? pm : 0u;
+    }
+    __syncwarp();
+    // warp-serial counting: rank = earlier same-digit items of this warp (index order)
+    unsigned rank[OS_ITEMS];
+#pragma unroll
+    for (int j = 0; j < OS_ITEMS; ++j) {
+      const unsigned pm = peers[j];
+      const int leader = pm ? __ffs(pm) - 1 : lane;
+      unsigned old = 0;
+      if (pm && lane == leader) {
+        old = sm.whist[warp][dig[j]];
+        sm.whist[warp][dig[j]] = old + __popc(pm);
+      }
+      old = __shfl_sync(0xffffffffu, old, leader);
+      rank[j] = old + __popc(pm & lt);
+      __syncwarp();
+    }
+    __syncthreads();
+    // per digit: exclusive offsets across warps + tile count; publish the aggregate early
+    unsigned tcount = 0;
+    if (tid < nbins) {
+#pragma unroll 4
       for (int w = 0; w < OS_WARPS; ++w) {
         const unsigned c = sm.whist[w][tid];
         sm.whist[w][tid] = tcount;
@@ -488,58 +539,78 @@ k_onesweep_pass(const unsigned* __restrict__ keys_in, const unsigned* __restrict
       }
       st_relaxed_u32(status + (size_t)tile * kMaxBins + tid, tile == 0 ? (OS_PREFIX | tcount) : (tcount + 1u));
     }
-    for (int w = 0; w < warp; ++w) dstart += sm.wsum_h[w];
-    dstart += h_inc - h;
-    l_inc = tcount;
+    unsigned tile_total;
+    const unsigned lstart = os_block_excl_scan(tcount, sm.wsum, tile_total);
+    if (tid < nbins) {
+      sm.local_start[tid] = lstart;
+      unsigned excl = 0;
+      if (tile > 0) {
+        // decoupled look-back over this digit's column of the status matrix, four
+        // predecessors per round trip; back off while a predecessor has not published
+        int pred = (int)tile - 1;
+        bool done = false;
+        while (!done) {
+          unsigned v[4];
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const unsigned o = __shfl_up_sync(0xffffffffu, l_inc, d);
-      if (lane >= d) l_inc += o;
-    }
-    if (lane == 31) sm.wsum_l[warp] = l_inc;
-  }
-  __syncthreads();
-  if (tid < nbins) {
-    unsigned lstart = l_inc - tcount;
-    for (int w = 0; w < warp; ++w) lstart += sm.wsum_l[w];
-    sm.local_start[tid] = lstart;
-    unsigned excl = 0;
-    if (tile > 0) {
-      // decoupled look-back over this digit's column of the status matrix
-      long long pred = (long long)tile - 1;
-      while (true) {
-        const unsigned v = ld_relaxed_u32(status + (size_t)pred * kMaxBins + tid);
-        if (v == 0u) continue;  // predecessor has not published yet
-        if (v & OS_PREFIX) {
-          excl += v & ~OS_PREFIX;
-          break;
+          for (int q = 0; q < 4; ++q)
+            v[q] = pred - q >= 0 ? ld_relaxed_u32(status + (size_t)(pred - q) * kMaxBins + tid) : OS_PREFIX;
+          int q = 0;
+          for (; q < 4; ++q) {
+            if (v[q] == 0u) break;  // not published yet: retry from here
+            if (v[q] & OS_PREFIX) {
+              excl += v[q] & ~OS_PREFIX;
+              done = true;
+              break;
+            }
+            excl += v[q] - 1u;
+          }
+          if (!done) {
+            pred -= q;
+            if (q < 4) __nanosleep(32);
+          }
         }
-        excl += v - 1u;
-        --pred;
+        st_relaxed_u32(status + (size_t)tile * kMaxBins + tid, OS_PREFIX | (excl + tcount));
       }
-      st_relaxed_u32(status + (size_t)tile * kMaxBins + tid, OS_PREFIX | (excl + tcount));
+      sm.gbase[tid] = sm.dstart[tid] + excl - lstart;
     }
-    sm.gbase[tid] = dstart + excl - lstart;
-  }
-  __syncthreads();
-  // stable local scatter into digit order
+    __syncthreads();
+    // keys: stable local scatter into digit order, then coalesced-run write-out
 #pragma unroll
-  for (int j = 0; j < OS_ITEMS; ++j) {
-    const unsigned e = (unsigned)warp * (OS_ITEMS * 32) + j * 32 + lane;
-    if (e < tvalid) {
-      const unsigned d = (key[j] >> shift) & dmask;
-      const unsigned pos = sm.local_start[d] + sm.whist[warp][d] + rank[j];
-      sm.keys[pos] = key[j];
-      sm.vals[pos] = val[j];
+    for (int j = 0; j < OS_ITEMS; ++j) {
+      const unsigned e = (unsigned)warp * (OS_ITEMS * 32) + j * 32 + lane;
+      if (e < tvalid) {
+        rank[j] += sm.local_start[dig[j]] + sm.whist[warp][dig[j]];  // rank -> tile position
+        sm.buf[rank[j]] = key[j];
+      }
     }
-  }
-  __syncthreads();
-  // write out: consecutive smem slots of one digit go to consecutive global positions
-  for (unsigned i = tid; i < tvalid; i += OS_THREADS) {
-    const unsigned k = sm.keys[i];
-    const unsigned g = sm.gbase[(k >> shift) & dmask] + i;
-    if (keys_out) keys_out[g] = k;
-    vals_out[g] = sm.vals[i];
+    __syncthreads();
+    unsigned gpos[OS_ITEMS];
+#pragma unroll
+    for (int r = 0; r < OS_ITEMS; ++r) {
+      const unsigned i = tid + r * OS_THREADS;
+      gpos[r] = 0;
+      if (i < tvalid) {
+        const unsigned k = sm.buf[i];
+        gpos[r] = sm.gbase[(k >> shift) & dmask] + i;
+        if (keys_out) keys_out[gpos[r]] = k;
+      }
+    }
+    cp_async_wait();
+    __syncthreads();
+    // values: shared->shared permutation with the same positions, then write-out
+#pragma unroll
+    for (int j = 0; j < OS_ITEMS; ++j) {
+      const unsigned e = (unsigned)warp * (OS_ITEMS * 32) + j * 32 + lane;
+      if (e < tvalid) sm.buf[rank[j]] = sm.vstage[e];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < OS_ITEMS; ++r) {
+      const unsigned i = tid + r * OS_THREADS;
+      if (i < tvalid) vals_out[gpos[r]] = sm.buf[i];
+    }
+    if (tid == 0) sm.tile = sm.next_tile;
+    __syncthreads();
   }
 }
 

@@ -191,4 +191,4 @@ def test_launch_count_is_native():
     builders.build_parallel(mesh, spec)
     b = _native.thread_builder()
     nbits = int(spec.ncells - 1).bit_length()
-    assert b.launches() == 3 + (nbits + 7) // 8
+    assert b.launches() == 3 + (nbits + 8) // 9     # 9-bit digits
