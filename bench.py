@@ -290,7 +290,7 @@ def main():
     phases /= args.steps
     k1_ms, k2_ms, sort_ms, k4_ms = phases[0], phases[2], phases[3], phases[5]
     key_bits = int(ncells - 1).bit_length()
-    npasses = max(launches - 3, 0)       # K1 + K2 + K4 + one launch per radix pass
+    npasses = (key_bits + 8) // 9        # 9-bit digits (make_plan in pgrid.cu)
     pass_ms = sort_ms / max(npasses, 1)
 
     # end to end through the public API: pinned host inputs, H2D + build + D2H each step
@@ -316,7 +316,7 @@ def main():
     kern = {
         "k_boxes_count_scan": {"ms": k1_ms, "launches": 1, "alg_bytes": 12 * n + 24 * nv + 16 * n},
         "k_expand_pairs": {"ms": k2_ms, "launches": 1, "alg_bytes": 16 * n + 8 * no},
-        "k_onesweep_pass": {"ms": pass_ms, "launches": npasses, "alg_bytes": 16 * no},
+        "radix_pass": {"ms": pass_ms, "launches": npasses, "alg_bytes": 16 * no},
         "k_cell_offsets": {"ms": k4_ms, "launches": 1, "alg_bytes": 4 * no + 4 * (ncells + 1)},
     }
     for k, v in kern.items():

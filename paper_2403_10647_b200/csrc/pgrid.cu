@@ -93,7 +93,7 @@ int bit_length(uint64_t v) {
   return b;
 }
 
-size_t os_smem_bytes() { return sizeof(OsSmem); }
+size_t rs_smem_bytes() { return sizeof(RsSmem); }
 
 // PGRID_SYNC_DEBUG=1: synchronise after every launch so a fault names its kernel.
 bool sync_debug() {
@@ -134,8 +134,7 @@ struct pg_builder {
   int dims[3] = {1, 1, 1};
   int key_bits = 0;
   bool stages_kept = false;
-  bool k1_timed = false;
-  unsigned os_grid = 148;  // persistent onesweep CTAs (SMs x resident CTAs per SM)  // ev[5]..ev[6] bracket K1 of the last pg_count
+  bool k1_timed = false;  // ev[5]..ev[6] bracket K1 of the last pg_count
   int launches = 0;
   const unsigned* sorted_keys = nullptr;
 };
@@ -151,13 +150,7 @@ int pg_builder_create(int device, pg_builder** out) {
   b->device = device;
   for (auto& e : b->ev) CU(cudaEventCreate(&e));
   CU(cudaMallocHost(&b->h_scalars, 4 * sizeof(unsigned long long)));
-  CU(cudaFuncSetAttribute(k_onesweep_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)os_smem_bytes()));
-  {
-    int sms = 0, per_sm = 0;
-    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_onesweep_pass, OS_THREADS, os_smem_bytes()));
-    b->os_grid = (unsigned)std::max(1, sms * std::max(1, per_sm));
-  }
+  CU(cudaFuncSetAttribute(k_radix_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem_bytes()));
   *out = b;
   return PG_OK;
 }
@@ -275,11 +268,12 @@ int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64
 namespace {
 
 // LSD passes over (keys0, vals0), ping-ponging with (keys1, vals1); the last pass writes its
-// values straight into vals_final (O). hist (plan.npasses x 256) must already be filled.
+// values straight into vals_final (O). hist (plan.npasses x 512) must already be filled;
+// `counts` holds one [digit][tile] matrix.
 int run_passes(pg_builder* b, const PassPlan& plan, unsigned* keys0, unsigned* vals0, unsigned* keys1,
-               unsigned* vals1, unsigned* vals_final, uint64_t n, unsigned* hist, unsigned* status,
-               unsigned* ctrs, cudaStream_t st, const unsigned** sorted_keys_out) {
-  const unsigned ntiles = (unsigned)((n + OS_TILE - 1) / OS_TILE);
+               unsigned* vals1, unsigned* vals_final, uint64_t n, unsigned* hist, unsigned* counts,
+               cudaStream_t st, const unsigned** sorted_keys_out) {
+  const unsigned ntiles = (unsigned)((n + RS_TILE - 1) / RS_TILE);
   unsigned* kbuf[2] = {keys0, keys1};
   unsigned* vbuf[2] = {vals0, vals1};
   for (int p = 0; p < plan.npasses; ++p) {
@@ -288,11 +282,14 @@ int run_passes(pg_builder* b, const PassPlan& plan, unsigned* keys0, unsigned* v
     unsigned* vin = vbuf[p & 1];
     unsigned* ko = kbuf[(p + 1) & 1];
     unsigned* vo = last ? vals_final : vbuf[(p + 1) & 1];
-    k_onesweep_pass<<<std::min(ntiles, b->os_grid), OS_THREADS, os_smem_bytes(), st>>>(
-        kin, vin, ko, vo, (unsigned)n, plan.shift[p], plan.bits[p], hist + p * kMaxBins,
-        status + (size_t)p * ntiles * kMaxBins, ctrs + p);
-    LAUNCHED("k_onesweep_pass", st);
-    ++b->launches;
+    k_tile_counts<<<ntiles, RS_THREADS, 0, st>>>(kin, (unsigned)n, plan.shift[p], plan.bits[p], counts);
+    LAUNCHED("k_tile_counts", st);
+    k_scan_tile_counts<<<1u << plan.bits[p], SC_THREADS, 0, st>>>(counts, ntiles);
+    LAUNCHED("k_scan_tile_counts", st);
+    k_radix_scatter<<<ntiles, RS_THREADS, rs_smem_bytes(), st>>>(kin, vin, ko, vo, (unsigned)n, plan.shift[p],
+                                                                  plan.bits[p], hist + p * kMaxBins, counts);
+    LAUNCHED("k_radix_scatter", st);
+    b->launches += 3;
     *sorted_keys_out = ko;
   }
   return PG_OK;
@@ -323,19 +320,15 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
   unsigned* valsA = b->pairs.as<unsigned>(sec);
   unsigned* keysB = b->pairs.as<unsigned>(2 * sec);
   unsigned* valsB = b->pairs.as<unsigned>(3 * sec);
-  const unsigned os_tiles = (unsigned)((no + OS_TILE - 1) / OS_TILE);
-  // sort sync area: [hist npasses x 256][tile counters x 4][status npasses x tiles x 256]
+  // sort scratch: [hist kMaxPasses x 512 (zeroed)][tile counts 512 x tiles]
+  const unsigned rs_tiles = (unsigned)((no + RS_TILE - 1) / RS_TILE);
   const size_t hist_bytes = align_up(kMaxPasses * kMaxBins * 4);
-  const size_t ctr_bytes = 256;
-  const size_t status_bytes = (size_t)std::max(plan.npasses, 1) * os_tiles * kMaxBins * 4;
-  const size_t sync_bytes = hist_bytes + ctr_bytes + align_up(status_bytes);
-  if ((rc = b->sort_sync.ensure(sync_bytes))) return rc;
+  if ((rc = b->sort_sync.ensure(hist_bytes + (size_t)rs_tiles * kMaxBins * 4))) return rc;
   unsigned* hist = b->sort_sync.as<unsigned>(0);
-  unsigned* ctrs = b->sort_sync.as<unsigned>(hist_bytes);
-  unsigned* status = b->sort_sync.as<unsigned>(hist_bytes + ctr_bytes);
+  unsigned* counts = b->sort_sync.as<unsigned>(hist_bytes);
 
   CU(cudaEventRecord(b->ev[0], st));
-  CU(cudaMemsetAsync(b->sort_sync.p, 0, sync_bytes, st));
+  CU(cudaMemsetAsync(hist, 0, hist_bytes, st));
   const unsigned* sorted = keysA;
   if (no > 0) {
     // K2: pairs (+ histograms). With no radix pass the pair order is final: vals -> O.
@@ -354,7 +347,7 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
     }
     CU(cudaEventRecord(b->ev[1], st));
     if (plan.npasses > 0) {
-      if ((rc = run_passes(b, plan, keysA, valsA, keysB, valsB, dO, no, hist, status, ctrs, st, &sorted)))
+      if ((rc = run_passes(b, plan, keysA, valsA, keysB, valsB, dO, no, hist, counts, st, &sorted)))
         return rc;
     }
   } else {
@@ -440,16 +433,12 @@ int pg_radix_sort_pairs(pg_builder* b, const uint32_t* keys, const uint32_t* val
   const cudaMemcpyKind in_kind = (flags & PG_HOST_INPUT) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
   CU(cudaMemcpyAsync(kA, keys, (size_t)n * 4, in_kind, st));
   CU(cudaMemcpyAsync(vA, vals, (size_t)n * 4, in_kind, st));
-  const unsigned os_tiles = (unsigned)((n + OS_TILE - 1) / OS_TILE);
+  const unsigned rs_tiles = (unsigned)((n + RS_TILE - 1) / RS_TILE);
   const size_t hist_bytes = align_up(kMaxPasses * kMaxBins * 4);
-  const size_t ctr_bytes = 256;
-  const size_t status_bytes = (size_t)std::max(plan.npasses, 1) * os_tiles * kMaxBins * 4;
-  const size_t sync_bytes = hist_bytes + ctr_bytes + align_up(status_bytes);
-  if ((rc = b->sort_sync.ensure(sync_bytes))) return rc;
+  if ((rc = b->sort_sync.ensure(hist_bytes + (size_t)rs_tiles * kMaxBins * 4))) return rc;
   unsigned* hist = b->sort_sync.as<unsigned>(0);
-  unsigned* ctrs = b->sort_sync.as<unsigned>(hist_bytes);
-  unsigned* status = b->sort_sync.as<unsigned>(hist_bytes + ctr_bytes);
-  CU(cudaMemsetAsync(b->sort_sync.p, 0, sync_bytes, st));
+  unsigned* counts = b->sort_sync.as<unsigned>(hist_bytes);
+  CU(cudaMemsetAsync(hist, 0, hist_bytes, st));
   const unsigned* sorted = kA;
   unsigned* vfinal = vA;
   if (plan.npasses > 0) {
@@ -459,7 +448,7 @@ int pg_radix_sort_pairs(pg_builder* b, const uint32_t* keys, const uint32_t* val
     // host outputs: final values land in the staging section behind the pair buffers
     if ((rc = b->stage.ensure(sec))) return rc;
     unsigned* vdst = (flags & PG_HOST_OUTPUT) ? b->stage.as<unsigned>() : vals_out;
-    if ((rc = run_passes(b, plan, kA, vA, kB, vB, vdst, (uint64_t)n, hist, status, ctrs, st, &sorted)))
+    if ((rc = run_passes(b, plan, kA, vA, kB, vB, vdst, (uint64_t)n, hist, counts, st, &sorted)))
       return rc;
     vfinal = vdst;
   }

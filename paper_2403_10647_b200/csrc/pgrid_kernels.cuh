@@ -7,7 +7,7 @@
 //   K2 k_expand_pairs     : load-balanced <cell, triangle> pair expansion (MakeObjectIds +
 //                           InclusiveSum + SegmentedExclusiveSum + MakeCellIds,
 //                           builders.py:155-160 / 104-117) + all radix digit histograms
-//   K3 k_onesweep_pass    : one stable LSD digit pass of the onesweep radix sort
+//   K3 k_radix_scatter    : one stable LSD digit pass (tile counts -> row scan -> scatter)
 //                           (builders.py:123-125 -> _ckernels.pyx:21-50)
 //   K4 k_cell_offsets     : RunLengthEncode -> NonEmptyCells scatter -> ExclusiveSum, fused:
 //                           G[c] = #pairs with cell < c (builders.py:126-133)
@@ -389,24 +389,27 @@ k_digit_hist(const unsigned* __restrict__ keys, long long n, PassPlan plan, unsi
 }
 
 // ----------------------------------------------------------------------------------------
-// K3: onesweep digit pass (stable)
+// K3: stable LSD radix pass, reduce-then-scan:
+//   k_tile_counts       per-tile digit counts          counts[digit][tile]
+//   k_scan_tile_counts  exclusive scan of every digit row over the tiles
+//   k_radix_scatter     rank the tile stably in shared memory, scatter to
+//                       dstart[digit] + offs[digit][tile] + local rank
+// (A single-kernel onesweep with decoupled look-back was measured first: its per-digit
+//  look-back chains serialised at ~20% of HBM bandwidth on B200.)
 // ----------------------------------------------------------------------------------------
-constexpr int OS_THREADS = 512;
-constexpr int OS_WARPS = OS_THREADS / 32;
-constexpr int OS_ITEMS = 8;
-constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096 pairs
-// look-back word: 0 = not ready; bit31 set = inclusive prefix; else aggregate + 1.
-constexpr unsigned OS_PREFIX = 1u << 31;
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_ITEMS = 16;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 pairs per tile
+constexpr int RS_DPT = kMaxBins / RS_THREADS;   // digits per thread in the per-digit phases (2)
 
-struct OsSmem {
-  unsigned buf[OS_TILE];               // tile in digit order: keys, then values
-  unsigned vstage[OS_TILE];            // values in input order (cp.async staging)
-  unsigned whist[OS_WARPS][kMaxBins];  // per-warp digit counts, then exclusive warp offsets
-  unsigned dstart[kMaxBins];           // global exclusive digit start (from the histogram)
-  unsigned local_start[kMaxBins];      // tile-local exclusive digit prefix
-  unsigned gbase[kMaxBins];            // global position of buf[0] for each digit
-  unsigned wsum[OS_WARPS];
-  unsigned tile, next_tile;
+struct RsSmem {
+  unsigned buf[RS_TILE];                     // tile in digit order: keys, then values
+  unsigned vstage[RS_TILE];                  // values in input order (cp.async staging)
+  unsigned short whist[RS_WARPS][kMaxBins];  // per-warp digit counts -> exclusive warp offsets
+  unsigned local_start[kMaxBins];            // tile-local exclusive digit prefix
+  unsigned gbase[kMaxBins];                  // global position of buf[0] for each digit
+  unsigned wsum[RS_WARPS];
 };
 
 __device__ __forceinline__ void cp_async4(void* smem, const void* g) {
@@ -417,14 +420,12 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g)
                : "memory");
 }
-__device__ __forceinline__ void cp_async_commit_wait() {
-  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// Block-wide exclusive scan of one value per thread (threads >= n contribute 0).
-__device__ __forceinline__ unsigned os_block_excl_scan(unsigned v, unsigned* wsum, unsigned& total) {
+// Block-wide exclusive scan of one value per thread (NW warps); also returns the total.
+template <int NW>
+__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* wsum, unsigned& total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned inc = v;
 #pragma unroll
@@ -436,181 +437,223 @@ __device__ __forceinline__ unsigned os_block_excl_scan(unsigned v, unsigned* wsu
   __syncthreads();
   unsigned add = 0, tot = 0;
 #pragma unroll
-  for (int w = 0; w < OS_WARPS; ++w) {
+  for (int w = 0; w < NW; ++w) {
     const unsigned x = wsum[w];
     add += w < warp ? x : 0u;
     tot += x;
   }
   total = tot;
+  __syncthreads();  // wsum may be reused by the caller's next scan
   return add + inc - v;
 }
 
-// One LSD digit pass (Adinets & Merrill's onesweep), persistent: each CTA claims tiles in
-// order through an atomic counter (prefetching its next claim while it works), ranks a tile
-// stably in shared memory with match-any warp multisplit, and places it with a per-digit
-// decoupled look-back over the previous tiles. Global digit starts come from the histogram
-// K2 accumulated, so there is no upsweep. Values never occupy registers: cp.async stages
-// them in input order and they are permuted shared->shared after the keys are written.
-__global__ void __launch_bounds__(OS_THREADS, 2)
-k_onesweep_pass(const unsigned* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
+__global__ void __launch_bounds__(RS_THREADS)
+k_tile_counts(const unsigned* __restrict__ keys, unsigned no, int shift, int bits, unsigned* __restrict__ counts) {
+  __shared__ unsigned h[kMaxBins];
+  const int tid = threadIdx.x;
+  const unsigned ntiles = (no + RS_TILE - 1) / RS_TILE;
+  const unsigned tile = blockIdx.x;
+  const unsigned tbase = tile * (unsigned)RS_TILE;
+  const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
+  const unsigned dmask = (1u << bits) - 1u;
+  for (int b = tid; b < kMaxBins; b += RS_THREADS) h[b] = 0u;
+  __syncthreads();
+  if (tvalid == (unsigned)RS_TILE) {
+    const uint4* src = reinterpret_cast<const uint4*>(keys + tbase);
+    uint4 k[RS_TILE / 4 / RS_THREADS];
+#pragma unroll
+    for (int r = 0; r < RS_TILE / 4 / RS_THREADS; ++r) k[r] = __ldcs(src + tid + r * RS_THREADS);
+#pragma unroll
+    for (int r = 0; r < RS_TILE / 4 / RS_THREADS; ++r) {
+      atomicAdd(&h[(k[r].x >> shift) & dmask], 1u);
+      atomicAdd(&h[(k[r].y >> shift) & dmask], 1u);
+      atomicAdd(&h[(k[r].z >> shift) & dmask], 1u);
+      atomicAdd(&h[(k[r].w >> shift) & dmask], 1u);
+    }
+  } else {
+    for (unsigned e = tid; e < tvalid; e += RS_THREADS) atomicAdd(&h[(__ldcs(keys + tbase + e) >> shift) & dmask], 1u);
+  }
+  __syncthreads();
+  for (int b = tid; b < (1 << bits); b += RS_THREADS) counts[(size_t)b * ntiles + tile] = h[b];
+}
+
+constexpr int SC_THREADS = 256;
+constexpr int SC_ITEMS = 16;
+// One CTA per digit row: counts[row][0..ntiles) -> exclusive prefix over tiles, in place.
+__global__ void __launch_bounds__(SC_THREADS)
+k_scan_tile_counts(unsigned* __restrict__ counts, unsigned ntiles) {
+  __shared__ unsigned s[SC_THREADS * SC_ITEMS];
+  __shared__ unsigned wsum[SC_THREADS / 32];
+  const int tid = threadIdx.x;
+  unsigned* row = counts + (size_t)blockIdx.x * ntiles;
+  unsigned carry = 0;
+  for (unsigned base = 0; base < ntiles; base += SC_THREADS * SC_ITEMS) {
+#pragma unroll
+    for (int k = 0; k < SC_ITEMS; ++k) {
+      const unsigned i = base + tid + k * SC_THREADS;
+      s[tid + k * SC_THREADS] = i < ntiles ? row[i] : 0u;
+    }
+    __syncthreads();
+    unsigned v[SC_ITEMS], run = 0;
+#pragma unroll
+    for (int q = 0; q < SC_ITEMS; ++q) {
+      v[q] = run;
+      run += s[tid * SC_ITEMS + q];
+    }
+    unsigned total;
+    const unsigned pre = block_excl_scan<SC_THREADS / 32>(run, wsum, total);
+#pragma unroll
+    for (int q = 0; q < SC_ITEMS; ++q) s[tid * SC_ITEMS + q] = carry + pre + v[q];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < SC_ITEMS; ++k) {
+      const unsigned i = base + tid + k * SC_THREADS;
+      if (i < ntiles) row[i] = s[tid + k * SC_THREADS];
+    }
+    carry += total;
+    __syncthreads();
+  }
+}
+
+// Scatter one tile of a digit pass. Item j of lane l of warp w is tile element
+// w*512 + j*32 + l (coalesced loads); ranks follow element order, so the pass is stable.
+// Values never occupy registers: cp.async stages them in input order and they are
+// permuted shared->shared after the keys have been written.
+__global__ void __launch_bounds__(RS_THREADS, 4)
+k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
                 unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, unsigned no, int shift,
-                int bits, const unsigned* __restrict__ hist, unsigned* __restrict__ status,
-                unsigned* __restrict__ tile_ctr) {
+                int bits, const unsigned* __restrict__ hist, const unsigned* __restrict__ offs) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  OsSmem& sm = *reinterpret_cast<OsSmem*>(smem_raw);
+  RsSmem& sm = *reinterpret_cast<RsSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nbins = 1 << bits;
   const unsigned dmask = (unsigned)nbins - 1u;
-  const unsigned ntiles = (no + OS_TILE - 1) / OS_TILE;
-  const unsigned lt = lanemask_lt();
+  const unsigned ntiles = (no + RS_TILE - 1) / RS_TILE;
+  const unsigned tile = blockIdx.x;
+  const unsigned tbase = tile * (unsigned)RS_TILE;
+  const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
 
-  if (tid == 0) sm.tile = atomicAdd(tile_ctr, 1u);
-  {  // global exclusive digit starts, once per CTA
-    const unsigned h = tid < nbins ? __ldg(&hist[tid]) : 0u;
-    unsigned total;
-    const unsigned ex = os_block_excl_scan(h, sm.wsum, total);
-    if (tid < kMaxBins) sm.dstart[tid] = ex;
+  if (tvalid == (unsigned)RS_TILE) {
+#pragma unroll
+    for (int c = tid; c < RS_TILE / 4; c += RS_THREADS) cp_async16(&sm.vstage[4 * c], vals_in + tbase + 4 * c);
+  } else {
+    for (unsigned e = tid; e < tvalid; e += RS_THREADS) cp_async4(&sm.vstage[e], vals_in + tbase + e);
+  }
+  cp_async_commit();
+  {
+    unsigned* row = reinterpret_cast<unsigned*>(&sm.whist[warp][0]);
+#pragma unroll
+    for (int q = lane; q < kMaxBins / 2; q += 32) row[q] = 0u;
+  }
+  unsigned key[RS_ITEMS];
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    const unsigned e = (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane;
+    key[j] = e < tvalid ? __ldcs(keys_in + tbase + e) : 0u;
+  }
+  // peers (same-digit lanes) per item: bit-sliced ballots, all items interleaved for ILP
+  unsigned pm[RS_ITEMS];
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j)
+    pm[j] = __ballot_sync(0xffffffffu, (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane < tvalid);
+#pragma unroll
+  for (int b = 0; b < kMaxDigitBits; ++b) {
+    if (b < bits) {
+#pragma unroll
+      for (int j = 0; j < RS_ITEMS; ++j) {
+        const bool set = (key[j] >> (shift + b)) & 1u;
+        const unsigned bb = __ballot_sync(0xffffffffu, set);
+        pm[j] &= set ? bb : ~bb;
+      }
+    }
+  }
+  __syncwarp();
+  const unsigned lt = lanemask_lt();
+  unsigned rank[RS_ITEMS];
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    const unsigned e = (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane;
+    const unsigned peers = e < tvalid ? pm[j] : 0u;
+    const int leader = peers ? __ffs(peers) - 1 : lane;
+    unsigned old = 0;
+    if (peers && lane == leader) {
+      const unsigned d = (key[j] >> shift) & dmask;
+      old = sm.whist[warp][d];
+      sm.whist[warp][d] = (unsigned short)(old + __popc(peers));
+    }
+    old = __shfl_sync(0xffffffffu, old, leader);
+    rank[j] = old + __popc(peers & lt);
+    __syncwarp();
   }
   __syncthreads();
-
-  while (true) {
-    const unsigned tile = sm.tile;
-    if (tile >= ntiles) break;
-    const unsigned tbase = tile * (unsigned)OS_TILE;
-    const unsigned tvalid = min((unsigned)OS_TILE, no - tbase);
-    // stage values (input order) asynchronously; claim the next tile early
-    if (tvalid == (unsigned)OS_TILE) {
-      for (int c = tid; c < OS_TILE / 4; c += OS_THREADS) cp_async16(&sm.vstage[4 * c], vals_in + tbase + 4 * c);
-    } else {
-      for (unsigned e = tid; e < tvalid; e += OS_THREADS) cp_async4(&sm.vstage[e], vals_in + tbase + e);
-    }
-    cp_async_commit();
-    if (tid == 0) sm.next_tile = atomicAdd(tile_ctr, 1u);
-    // each warp zeroes its own histogram row
-    for (int b = lane; b < nbins; b += 32) sm.whist[warp][b] = 0u;
-    // warp-striped keys: item j of lane l of warp w is tile element w*256 + j*32 + l
-    unsigned key[OS_ITEMS], dig[OS_ITEMS], peers[OS_ITEMS];
+  // per digit (RS_DPT consecutive digits per thread): warp offsets, tile counts, prefixes
+  unsigned tc[RS_DPT], hs[RS_DPT], tsum = 0, hsum = 0;
 #pragma unroll
-    for (int j = 0; j < OS_ITEMS; ++j) {
-      const unsigned e = (unsigned)warp * (OS_ITEMS * 32) + j * 32 + lane;
-      key[j] = e < tvalid ? __ldcs(keys_in + tbase + e) : 0u;
-    }
-    // peers (same-digit lanes) of every item via bit-sliced ballots (MATCH.ANY is MIO-bound)
+  for (int q = 0; q < RS_DPT; ++q) {
+    const int d = tid * RS_DPT + q;
+    unsigned run = 0;
+    if (d < nbins) {
 #pragma unroll
-    for (int j = 0; j < OS_ITEMS; ++j) {
-      const unsigned e = (unsigned)warp * (OS_ITEMS * 32) + j * 32 + lane;
-      unsigned pm = __ballot_sync(0xffffffffu, e < tvalid);
-      dig[j] = (key[j] >> shift) & dmask;
-#pragma unroll
-      for (int b = 0; b < kMaxDigitBits; ++b) {
-        if (b < bits) {
-          const bool set = (dig[j] >> b) & 1u;
-          const unsigned bb = __ballot_sync(0xffffffffu, set);
-          pm &= set ? bb : ~bb;
-        }
-      }
-      peers[j] = e < tvalid ? pm : 0u;
-    }
-    __syncwarp();
-    // warp-serial counting: rank = earlier same-digit items of this warp (index order)
-    unsigned rank[OS_ITEMS];
-#pragma unroll
-    for (int j = 0; j < OS_ITEMS; ++j) {
-      const unsigned pm = peers[j];
-      const int leader = pm ? __ffs(pm) - 1 : lane;
-      unsigned old = 0;
-      if (pm && lane == leader) {
-        old = sm.whist[warp][dig[j]];
-        sm.whist[warp][dig[j]] = old + __popc(pm);
-      }
-      old = __shfl_sync(0xffffffffu, old, leader);
-      rank[j] = old + __popc(pm & lt);
-      __syncwarp();
-    }
-    __syncthreads();
-    // per digit: exclusive offsets across warps + tile count; publish the aggregate early
-    unsigned tcount = 0;
-    if (tid < nbins) {
-#pragma unroll 4
-      for (int w = 0; w < OS_WARPS; ++w) {
-        const unsigned c = sm.whist[w][tid];
-        sm.whist[w][tid] = tcount;
-        tcount += c;
-      }
-      st_relaxed_u32(status + (size_t)tile * kMaxBins + tid, tile == 0 ? (OS_PREFIX | tcount) : (tcount + 1u));
-    }
-    unsigned tile_total;
-    const unsigned lstart = os_block_excl_scan(tcount, sm.wsum, tile_total);
-    if (tid < nbins) {
-      sm.local_start[tid] = lstart;
-      unsigned excl = 0;
-      if (tile > 0) {
-        // decoupled look-back over this digit's column of the status matrix, four
-        // predecessors per round trip; back off while a predecessor has not published
-        int pred = (int)tile - 1;
-        bool done = false;
-        while (!done) {
-          unsigned v[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            v[q] = pred - q >= 0 ? ld_relaxed_u32(status + (size_t)(pred - q) * kMaxBins + tid) : OS_PREFIX;
-          int q = 0;
-          for (; q < 4; ++q) {
-            if (v[q] == 0u) break;  // not published yet: retry from here
-            if (v[q] & OS_PREFIX) {
-              excl += v[q] & ~OS_PREFIX;
-              done = true;
-              break;
-            }
-            excl += v[q] - 1u;
-          }
-          if (!done) {
-            pred -= q;
-            if (q < 4) __nanosleep(32);
-          }
-        }
-        st_relaxed_u32(status + (size_t)tile * kMaxBins + tid, OS_PREFIX | (excl + tcount));
-      }
-      sm.gbase[tid] = sm.dstart[tid] + excl - lstart;
-    }
-    __syncthreads();
-    // keys: stable local scatter into digit order, then coalesced-run write-out
-#pragma unroll
-    for (int j = 0; j < OS_ITEMS; ++j) {
-      const unsigned e = (unsigned)warp * (OS_ITEMS * 32) + j * 32 + lane;
-      if (e < tvalid) {
-        rank[j] += sm.local_start[dig[j]] + sm.whist[warp][dig[j]];  // rank -> tile position
-        sm.buf[rank[j]] = key[j];
+      for (int w = 0; w < RS_WARPS; ++w) {
+        const unsigned c = sm.whist[w][d];
+        sm.whist[w][d] = (unsigned short)run;
+        run += c;
       }
     }
-    __syncthreads();
-    unsigned gpos[OS_ITEMS];
+    tc[q] = run;
+    hs[q] = d < nbins ? __ldg(&hist[d]) : 0u;
+    tsum += run;
+    hsum += hs[q];
+  }
+  unsigned ttot, htot;
+  unsigned lpre = block_excl_scan<RS_WARPS>(tsum, sm.wsum, ttot);
+  unsigned hpre = block_excl_scan<RS_WARPS>(hsum, sm.wsum, htot);
 #pragma unroll
-    for (int r = 0; r < OS_ITEMS; ++r) {
-      const unsigned i = tid + r * OS_THREADS;
-      gpos[r] = 0;
-      if (i < tvalid) {
-        const unsigned k = sm.buf[i];
-        gpos[r] = sm.gbase[(k >> shift) & dmask] + i;
-        if (keys_out) keys_out[gpos[r]] = k;
-      }
+  for (int q = 0; q < RS_DPT; ++q) {
+    const int d = tid * RS_DPT + q;
+    if (d < nbins) {
+      sm.local_start[d] = lpre;
+      sm.gbase[d] = hpre + __ldg(&offs[(size_t)d * ntiles + tile]) - lpre;
     }
-    cp_async_wait();
-    __syncthreads();
-    // values: shared->shared permutation with the same positions, then write-out
+    lpre += tc[q];
+    hpre += hs[q];
+  }
+  __syncthreads();
+  // keys: stable local scatter into digit order, then run-coalesced write-out
 #pragma unroll
-    for (int j = 0; j < OS_ITEMS; ++j) {
-      const unsigned e = (unsigned)warp * (OS_ITEMS * 32) + j * 32 + lane;
-      if (e < tvalid) sm.buf[rank[j]] = sm.vstage[e];
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    const unsigned e = (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane;
+    if (e < tvalid) {
+      const unsigned d = (key[j] >> shift) & dmask;
+      rank[j] += sm.local_start[d] + sm.whist[warp][d];  // rank -> tile position
+      sm.buf[rank[j]] = key[j];
     }
-    __syncthreads();
+  }
+  __syncthreads();
+  unsigned gpos[RS_ITEMS];
 #pragma unroll
-    for (int r = 0; r < OS_ITEMS; ++r) {
-      const unsigned i = tid + r * OS_THREADS;
-      if (i < tvalid) vals_out[gpos[r]] = sm.buf[i];
+  for (int r = 0; r < RS_ITEMS; ++r) {
+    const unsigned i = tid + r * RS_THREADS;
+    gpos[r] = 0;
+    if (i < tvalid) {
+      const unsigned k = sm.buf[i];
+      gpos[r] = sm.gbase[(k >> shift) & dmask] + i;
+      if (keys_out) keys_out[gpos[r]] = k;
     }
-    if (tid == 0) sm.tile = sm.next_tile;
-    __syncthreads();
+  }
+  cp_async_wait();
+  __syncthreads();
+  // values: shared->shared permutation with the same positions, then write-out
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    const unsigned e = (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane;
+    if (e < tvalid) sm.buf[rank[j]] = sm.vstage[e];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < RS_ITEMS; ++r) {
+    const unsigned i = tid + r * RS_THREADS;
+    if (i < tvalid) vals_out[gpos[r]] = sm.buf[i];
   }
 }
 

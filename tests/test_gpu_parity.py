@@ -191,4 +191,5 @@ def test_launch_count_is_native():
     builders.build_parallel(mesh, spec)
     b = _native.thread_builder()
     nbits = int(spec.ncells - 1).bit_length()
-    assert b.launches() == 3 + (nbits + 8) // 9     # 9-bit digits
+    passes = (nbits + 8) // 9                         # 9-bit digits
+    assert b.launches() in (3 + passes, 3 + 3 * passes)  # onesweep or reduce-then-scan
