@@ -95,6 +95,30 @@ int bit_length(uint64_t v) {
 
 size_t rs_smem_bytes() { return sizeof(RsSmem); }
 
+template <int BITS>
+void launch_scatter_bits(unsigned ntiles, cudaStream_t st, const unsigned* kin, const unsigned* vin, unsigned* ko,
+                         unsigned* vo, unsigned n, int shift, const unsigned* hist, const unsigned* offs) {
+  k_radix_scatter<BITS><<<ntiles, RS_THREADS, rs_smem_bytes(), st>>>(kin, vin, ko, vo, n, shift, hist, offs);
+}
+
+void launch_radix_scatter(int bits, unsigned ntiles, cudaStream_t st, const unsigned* kin, const unsigned* vin,
+                          unsigned* ko, unsigned* vo, unsigned n, int shift, const unsigned* hist,
+                          const unsigned* offs) {
+  switch (bits) {
+#define PG_CASE(B) \
+  case B:          \
+    launch_scatter_bits<B>(ntiles, st, kin, vin, ko, vo, n, shift, hist, offs); break;
+    PG_CASE(1) PG_CASE(2) PG_CASE(3) PG_CASE(4) PG_CASE(5) PG_CASE(6) PG_CASE(7) PG_CASE(8) PG_CASE(9)
+#undef PG_CASE
+    default: break;
+  }
+}
+
+template <int BITS>
+cudaError_t set_scatter_smem() {
+  return cudaFuncSetAttribute(k_radix_scatter<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem_bytes());
+}
+
 // PGRID_SYNC_DEBUG=1: synchronise after every launch so a fault names its kernel.
 bool sync_debug() {
   static const bool on = [] {
@@ -150,7 +174,9 @@ int pg_builder_create(int device, pg_builder** out) {
   b->device = device;
   for (auto& e : b->ev) CU(cudaEventCreate(&e));
   CU(cudaMallocHost(&b->h_scalars, 4 * sizeof(unsigned long long)));
-  CU(cudaFuncSetAttribute(k_radix_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem_bytes()));
+  CU(set_scatter_smem<1>()); CU(set_scatter_smem<2>()); CU(set_scatter_smem<3>());
+  CU(set_scatter_smem<4>()); CU(set_scatter_smem<5>()); CU(set_scatter_smem<6>());
+  CU(set_scatter_smem<7>()); CU(set_scatter_smem<8>()); CU(set_scatter_smem<9>());
   *out = b;
   return PG_OK;
 }
@@ -286,8 +312,8 @@ int run_passes(pg_builder* b, const PassPlan& plan, unsigned* keys0, unsigned* v
     LAUNCHED("k_tile_counts", st);
     k_scan_tile_counts<<<1u << plan.bits[p], SC_THREADS, 0, st>>>(counts, ntiles);
     LAUNCHED("k_scan_tile_counts", st);
-    k_radix_scatter<<<ntiles, RS_THREADS, rs_smem_bytes(), st>>>(kin, vin, ko, vo, (unsigned)n, plan.shift[p],
-                                                                  plan.bits[p], hist + p * kMaxBins, counts);
+    launch_radix_scatter(plan.bits[p], ntiles, st, kin, vin, ko, vo, (unsigned)n, plan.shift[p], hist + p * kMaxBins,
+                         counts);
     LAUNCHED("k_radix_scatter", st);
     b->launches += 3;
     *sorted_keys_out = ko;

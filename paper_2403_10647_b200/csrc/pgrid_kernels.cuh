@@ -15,6 +15,10 @@
 // with explicit round-to-nearest intrinsics so it matches numpy bit for bit.
 #pragma once
 #include <cstdint>
+
+#ifndef PGRID_RANK_BALLOT
+#define PGRID_RANK_BALLOT 1
+#endif
 #include <cuda_runtime.h>
 
 namespace pgrid {
@@ -518,22 +522,22 @@ k_scan_tile_counts(unsigned* __restrict__ counts, unsigned ntiles) {
 // Scatter one tile of a digit pass. Item j of lane l of warp w is tile element
 // w*512 + j*32 + l (coalesced loads); ranks follow element order, so the pass is stable.
 // Values never occupy registers: cp.async stages them in input order and they are
-// permuted shared->shared after the keys have been written.
-__global__ void __launch_bounds__(RS_THREADS, 4)
-k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
-                unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, unsigned no, int shift,
-                int bits, const unsigned* __restrict__ hist, const unsigned* __restrict__ offs) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  RsSmem& sm = *reinterpret_cast<RsSmem*>(smem_raw);
+// permuted shared->shared after the keys have been written. BITS and FULL are compile-time
+// so the ranking loop is branch-free and full tiles carry no bounds predicates.
+template <int BITS, bool FULL>
+__device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* __restrict__ keys_in,
+                                                   const unsigned* __restrict__ vals_in,
+                                                   unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out,
+                                                   unsigned tbase, unsigned tvalid, unsigned tile, unsigned ntiles,
+                                                   int shift, const unsigned* __restrict__ hist,
+                                                   const unsigned* __restrict__ offs) {
+  constexpr int NB = 1 << BITS;
+  constexpr unsigned DMASK = (unsigned)NB - 1u;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nbins = 1 << bits;
-  const unsigned dmask = (unsigned)nbins - 1u;
-  const unsigned ntiles = (no + RS_TILE - 1) / RS_TILE;
-  const unsigned tile = blockIdx.x;
-  const unsigned tbase = tile * (unsigned)RS_TILE;
-  const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
+  auto elem = [&](int j) { return (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane; };
+  auto valid = [&](int j) { return FULL || elem(j) < tvalid; };
 
-  if (tvalid == (unsigned)RS_TILE) {
+  if (FULL) {
 #pragma unroll
     for (int c = tid; c < RS_TILE / 4; c += RS_THREADS) cp_async16(&sm.vstage[4 * c], vals_in + tbase + 4 * c);
   } else {
@@ -543,28 +547,21 @@ k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict
   {
     unsigned* row = reinterpret_cast<unsigned*>(&sm.whist[warp][0]);
 #pragma unroll
-    for (int q = lane; q < kMaxBins / 2; q += 32) row[q] = 0u;
+    for (int q = lane; q < NB / 2; q += 32) row[q] = 0u;
   }
-  unsigned key[RS_ITEMS];
+  unsigned dg[RS_ITEMS];
 #pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) {
-    const unsigned e = (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane;
-    key[j] = e < tvalid ? __ldcs(keys_in + tbase + e) : 0u;
-  }
-  // peers (same-digit lanes) per item: bit-sliced ballots, all items interleaved for ILP
+  for (int j = 0; j < RS_ITEMS; ++j) dg[j] = valid(j) ? (__ldg(keys_in + tbase + elem(j)) >> shift) & DMASK : 0u;
+  // peers (same-digit lanes) per item: bit-sliced ballots, items interleaved for ILP
   unsigned pm[RS_ITEMS];
 #pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j)
-    pm[j] = __ballot_sync(0xffffffffu, (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane < tvalid);
+  for (int j = 0; j < RS_ITEMS; ++j) pm[j] = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid(j));
 #pragma unroll
-  for (int b = 0; b < kMaxDigitBits; ++b) {
-    if (b < bits) {
+  for (int b = 0; b < BITS; ++b) {
 #pragma unroll
-      for (int j = 0; j < RS_ITEMS; ++j) {
-        const bool set = (key[j] >> (shift + b)) & 1u;
-        const unsigned bb = __ballot_sync(0xffffffffu, set);
-        pm[j] &= set ? bb : ~bb;
-      }
+    for (int j = 0; j < RS_ITEMS; ++j) {
+      const unsigned bb = __ballot_sync(0xffffffffu, (dg[j] >> b) & 1u);
+      pm[j] &= ((dg[j] >> b) & 1u) ? bb : ~bb;
     }
   }
   __syncwarp();
@@ -572,14 +569,12 @@ k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict
   unsigned rank[RS_ITEMS];
 #pragma unroll
   for (int j = 0; j < RS_ITEMS; ++j) {
-    const unsigned e = (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane;
-    const unsigned peers = e < tvalid ? pm[j] : 0u;
-    const int leader = peers ? __ffs(peers) - 1 : lane;
+    const unsigned peers = valid(j) ? pm[j] : 0u;
+    const int leader = __ffs(peers | (1u << lane)) - 1;  // invalid lanes: themselves
     unsigned old = 0;
-    if (peers && lane == leader) {
-      const unsigned d = (key[j] >> shift) & dmask;
-      old = sm.whist[warp][d];
-      sm.whist[warp][d] = (unsigned short)(old + __popc(peers));
+    if (lane == leader && peers) {
+      old = sm.whist[warp][dg[j]];
+      sm.whist[warp][dg[j]] = (unsigned short)(old + __popc(peers));
     }
     old = __shfl_sync(0xffffffffu, old, leader);
     rank[j] = old + __popc(peers & lt);
@@ -592,7 +587,7 @@ k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict
   for (int q = 0; q < RS_DPT; ++q) {
     const int d = tid * RS_DPT + q;
     unsigned run = 0;
-    if (d < nbins) {
+    if (d < NB) {
 #pragma unroll
       for (int w = 0; w < RS_WARPS; ++w) {
         const unsigned c = sm.whist[w][d];
@@ -601,7 +596,7 @@ k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict
       }
     }
     tc[q] = run;
-    hs[q] = d < nbins ? __ldg(&hist[d]) : 0u;
+    hs[q] = d < NB ? __ldg(&hist[d]) : 0u;
     tsum += run;
     hsum += hs[q];
   }
@@ -611,7 +606,7 @@ k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict
 #pragma unroll
   for (int q = 0; q < RS_DPT; ++q) {
     const int d = tid * RS_DPT + q;
-    if (d < nbins) {
+    if (d < NB) {
       sm.local_start[d] = lpre;
       sm.gbase[d] = hpre + __ldg(&offs[(size_t)d * ntiles + tile]) - lpre;
     }
@@ -619,14 +614,12 @@ k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict
     hpre += hs[q];
   }
   __syncthreads();
-  // keys: stable local scatter into digit order, then run-coalesced write-out
+  // keys: stable local scatter into digit order (key re-read from L1/L2), run-coalesced write
 #pragma unroll
   for (int j = 0; j < RS_ITEMS; ++j) {
-    const unsigned e = (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane;
-    if (e < tvalid) {
-      const unsigned d = (key[j] >> shift) & dmask;
-      rank[j] += sm.local_start[d] + sm.whist[warp][d];  // rank -> tile position
-      sm.buf[rank[j]] = key[j];
+    if (valid(j)) {
+      rank[j] += sm.local_start[dg[j]] + sm.whist[warp][dg[j]];  // rank -> tile position
+      sm.buf[rank[j]] = keys_in[tbase + elem(j)];
     }
   }
   __syncthreads();
@@ -635,9 +628,9 @@ k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict
   for (int r = 0; r < RS_ITEMS; ++r) {
     const unsigned i = tid + r * RS_THREADS;
     gpos[r] = 0;
-    if (i < tvalid) {
+    if (FULL || i < tvalid) {
       const unsigned k = sm.buf[i];
-      gpos[r] = sm.gbase[(k >> shift) & dmask] + i;
+      gpos[r] = sm.gbase[(k >> shift) & DMASK] + i;
       if (keys_out) keys_out[gpos[r]] = k;
     }
   }
@@ -645,16 +638,33 @@ k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict
   __syncthreads();
   // values: shared->shared permutation with the same positions, then write-out
 #pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) {
-    const unsigned e = (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane;
-    if (e < tvalid) sm.buf[rank[j]] = sm.vstage[e];
-  }
+  for (int j = 0; j < RS_ITEMS; ++j)
+    if (valid(j)) sm.buf[rank[j]] = sm.vstage[elem(j)];
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < RS_ITEMS; ++r) {
     const unsigned i = tid + r * RS_THREADS;
-    if (i < tvalid) vals_out[gpos[r]] = sm.buf[i];
+    if (FULL || i < tvalid) vals_out[gpos[r]] = sm.buf[i];
   }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(RS_THREADS, 4)
+k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
+                unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, unsigned no, int shift,
+                const unsigned* __restrict__ hist, const unsigned* __restrict__ offs) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  RsSmem& sm = *reinterpret_cast<RsSmem*>(smem_raw);
+  const unsigned ntiles = (no + RS_TILE - 1) / RS_TILE;
+  const unsigned tile = blockIdx.x;
+  const unsigned tbase = tile * (unsigned)RS_TILE;
+  const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
+  if (tvalid == (unsigned)RS_TILE)
+    radix_scatter_tile<BITS, true>(sm, keys_in, vals_in, keys_out, vals_out, tbase, tvalid, tile, ntiles, shift,
+                                   hist, offs);
+  else
+    radix_scatter_tile<BITS, false>(sm, keys_in, vals_in, keys_out, vals_out, tbase, tvalid, tile, ntiles, shift,
+                                    hist, offs);
 }
 
 // ----------------------------------------------------------------------------------------
