@@ -97,17 +97,17 @@ size_t rs_smem_bytes() { return sizeof(RsSmem); }
 
 template <int BITS>
 void launch_scatter_bits(unsigned ntiles, cudaStream_t st, const unsigned* kin, const unsigned* vin, unsigned* ko,
-                         unsigned* vo, unsigned n, int shift, const unsigned* hist, const unsigned* offs) {
-  k_radix_scatter<BITS><<<ntiles, RS_THREADS, rs_smem_bytes(), st>>>(kin, vin, ko, vo, n, shift, hist, offs);
+                         unsigned* vo, unsigned n, int shift, const unsigned* hist, const unsigned* offs, unsigned ld) {
+  k_radix_scatter<BITS><<<ntiles, RS_THREADS, rs_smem_bytes(), st>>>(kin, vin, ko, vo, n, shift, hist, offs, ld);
 }
 
 void launch_radix_scatter(int bits, unsigned ntiles, cudaStream_t st, const unsigned* kin, const unsigned* vin,
                           unsigned* ko, unsigned* vo, unsigned n, int shift, const unsigned* hist,
-                          const unsigned* offs) {
+                          const unsigned* offs, unsigned ld) {
   switch (bits) {
 #define PG_CASE(B) \
   case B:          \
-    launch_scatter_bits<B>(ntiles, st, kin, vin, ko, vo, n, shift, hist, offs); break;
+    launch_scatter_bits<B>(ntiles, st, kin, vin, ko, vo, n, shift, hist, offs, ld); break;
     PG_CASE(1) PG_CASE(2) PG_CASE(3) PG_CASE(4) PG_CASE(5) PG_CASE(6) PG_CASE(7) PG_CASE(8) PG_CASE(9)
 #undef PG_CASE
     default: break;
@@ -116,7 +116,9 @@ void launch_radix_scatter(int bits, unsigned ntiles, cudaStream_t st, const unsi
 
 template <int BITS>
 cudaError_t set_scatter_smem() {
-  return cudaFuncSetAttribute(k_radix_scatter<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem_bytes());
+  cudaError_t e = cudaFuncSetAttribute(k_radix_scatter<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)rs_smem_bytes());
+  return e;
 }
 
 // PGRID_SYNC_DEBUG=1: synchronise after every launch so a fault names its kernel.
@@ -174,6 +176,7 @@ int pg_builder_create(int device, pg_builder** out) {
   b->device = device;
   for (auto& e : b->ev) CU(cudaEventCreate(&e));
   CU(cudaMallocHost(&b->h_scalars, 4 * sizeof(unsigned long long)));
+  CU(cudaFuncSetAttribute(k_pairs_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PeSmem)));
   CU(set_scatter_smem<1>()); CU(set_scatter_smem<2>()); CU(set_scatter_smem<3>());
   CU(set_scatter_smem<4>()); CU(set_scatter_smem<5>()); CU(set_scatter_smem<6>());
   CU(set_scatter_smem<7>()); CU(set_scatter_smem<8>()); CU(set_scatter_smem<9>());
@@ -295,11 +298,13 @@ namespace {
 
 // LSD passes over (keys0, vals0), ping-ponging with (keys1, vals1); the last pass writes its
 // values straight into vals_final (O). hist (plan.npasses x 512) must already be filled;
-// `counts` holds one [digit][tile] matrix.
-int run_passes(pg_builder* b, const PassPlan& plan, unsigned* keys0, unsigned* vals0, unsigned* keys1,
-               unsigned* vals1, unsigned* vals_final, uint64_t n, unsigned* hist, unsigned* counts,
+// `counts` holds one [digit][tile] matrix (row stride ld), already filled for pass 0 when
+// counts0_ready (K2 emits them).
+int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned* keys0, unsigned* vals0,
+               unsigned* keys1, unsigned* vals1, unsigned* vals_final, uint64_t n, unsigned* hist, unsigned* counts,
                cudaStream_t st, const unsigned** sorted_keys_out) {
   const unsigned ntiles = (unsigned)((n + RS_TILE - 1) / RS_TILE);
+  const unsigned ld = (ntiles + 3) & ~3u;
   unsigned* kbuf[2] = {keys0, keys1};
   unsigned* vbuf[2] = {vals0, vals1};
   for (int p = 0; p < plan.npasses; ++p) {
@@ -308,14 +313,17 @@ int run_passes(pg_builder* b, const PassPlan& plan, unsigned* keys0, unsigned* v
     unsigned* vin = vbuf[p & 1];
     unsigned* ko = kbuf[(p + 1) & 1];
     unsigned* vo = last ? vals_final : vbuf[(p + 1) & 1];
-    k_tile_counts<<<ntiles, RS_THREADS, 0, st>>>(kin, (unsigned)n, plan.shift[p], plan.bits[p], counts);
-    LAUNCHED("k_tile_counts", st);
-    k_scan_tile_counts<<<1u << plan.bits[p], SC_THREADS, 0, st>>>(counts, ntiles);
+    if (p > 0 || !counts0_ready) {
+      k_tile_counts<<<ntiles, RS_THREADS, 0, st>>>(kin, (unsigned)n, plan.shift[p], plan.bits[p], counts, ld);
+      LAUNCHED("k_tile_counts", st);
+      ++b->launches;
+    }
+    k_scan_tile_counts<<<1u << plan.bits[p], SC_THREADS, 0, st>>>(counts, ntiles, ld);
     LAUNCHED("k_scan_tile_counts", st);
     launch_radix_scatter(plan.bits[p], ntiles, st, kin, vin, ko, vo, (unsigned)n, plan.shift[p], hist + p * kMaxBins,
-                         counts);
+                         counts, ld);
     LAUNCHED("k_radix_scatter", st);
-    b->launches += 3;
+    b->launches += 2;
     *sorted_keys_out = ko;
   }
   return PG_OK;
@@ -346,44 +354,68 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
   unsigned* valsA = b->pairs.as<unsigned>(sec);
   unsigned* keysB = b->pairs.as<unsigned>(2 * sec);
   unsigned* valsB = b->pairs.as<unsigned>(3 * sec);
-  // sort scratch: [hist kMaxPasses x 512 (zeroed)][tile counts 512 x tiles]
+  // sort scratch: [hist kMaxPasses x 512 (zeroed)][pair-tile bounds][key-tile bounds][tile counts 512 x tiles]
   const unsigned rs_tiles = (unsigned)((no + RS_TILE - 1) / RS_TILE);
+  const unsigned k2_tiles = (unsigned)((no + K2_TILE - 1) / K2_TILE);
+  const unsigned g_tiles = (unsigned)((ncells + G_TILE - 1) / G_TILE);
   const size_t hist_bytes = align_up(kMaxPasses * kMaxBins * 4);
-  if ((rc = b->sort_sync.ensure(hist_bytes + (size_t)rs_tiles * kMaxBins * 4))) return rc;
+  const size_t pb_bytes = align_up((size_t)std::max(rs_tiles, k2_tiles) * 8 + 8);
+  const size_t kb_bytes = align_up((size_t)(g_tiles + 1) * 4);
+  if ((rc = b->sort_sync.ensure(hist_bytes + pb_bytes + kb_bytes + (size_t)((rs_tiles + 3) & ~3u) * kMaxBins * 4)))
+    return rc;
   unsigned* hist = b->sort_sync.as<unsigned>(0);
-  unsigned* counts = b->sort_sync.as<unsigned>(hist_bytes);
+  int2* pbounds = b->sort_sync.as<int2>(hist_bytes);
+  unsigned* kbounds = b->sort_sync.as<unsigned>(hist_bytes + pb_bytes);
+  unsigned* counts = b->sort_sync.as<unsigned>(hist_bytes + pb_bytes + kb_bytes);
+  const unsigned ld = (rs_tiles + 3) & ~3u;  // counts row stride
 
   CU(cudaEventRecord(b->ev[0], st));
   CU(cudaMemsetAsync(hist, 0, hist_bytes, st));
   const unsigned* sorted = keysA;
   if (no > 0) {
-    // K2: pairs (+ histograms). With no radix pass the pair order is final: vals -> O.
-    unsigned* v0 = plan.npasses == 0 ? dO : valsA;
-    const unsigned k2_tiles = (unsigned)((no + K2_TILE - 1) / K2_TILE);
-    k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->n, (unsigned)no, (unsigned)b->dims[0],
-                                                     (unsigned)b->dims[0] * (unsigned)b->dims[1], plan, keysA, v0,
-                                                     hist);
-    LAUNCHED("k_expand_pairs", st);
-    ++b->launches;
-    if (flags & PG_KEEP_STAGES) {
-      if ((rc = b->stage.ensure(2 * sec))) return rc;
-      CU(cudaMemcpyAsync(b->stage.as<unsigned>(0), keysA, no * 4, cudaMemcpyDeviceToDevice, st));
-      CU(cudaMemcpyAsync(b->stage.as<unsigned>(sec), v0, no * 4, cudaMemcpyDeviceToDevice, st));
-      b->stages_kept = true;
+    const unsigned dxu = (unsigned)b->dims[0], dxyu = (unsigned)b->dims[0] * (unsigned)b->dims[1];
+    if (plan.npasses == 0 || (flags & PG_KEEP_STAGES)) {
+      // pairs in generation order: final when there is no radix pass (vals -> O), and the
+      // record= stage dump otherwise
+      unsigned* v0 = plan.npasses == 0 ? dO : valsA;
+      k_pair_tile_bounds<<<(k2_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->n, (unsigned)no, K2_TILE, k2_tiles,
+                                                            pbounds);
+      LAUNCHED("k_pair_tile_bounds", st);
+      k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->n, (unsigned)no, dxu, dxyu, pbounds,
+                                                     keysA, v0);
+      LAUNCHED("k_expand_pairs", st);
+      b->launches += 2;
+      if (flags & PG_KEEP_STAGES) {
+        if ((rc = b->stage.ensure(2 * sec))) return rc;
+        CU(cudaMemcpyAsync(b->stage.as<unsigned>(0), keysA, no * 4, cudaMemcpyDeviceToDevice, st));
+        CU(cudaMemcpyAsync(b->stage.as<unsigned>(sec), v0, no * 4, cudaMemcpyDeviceToDevice, st));
+        b->stages_kept = true;
+      }
     }
-    CU(cudaEventRecord(b->ev[1], st));
     if (plan.npasses > 0) {
-      if ((rc = run_passes(b, plan, keysA, valsA, keysB, valsB, dO, no, hist, counts, st, &sorted)))
-        return rc;
+      // K2 on radix tiles: pairs in generation order + first-pass tile counts + histograms
+      k_pair_tile_bounds<<<(rs_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->n, (unsigned)no, RS_TILE, rs_tiles,
+                                                            pbounds);
+      LAUNCHED("k_pair_tile_bounds", st);
+      k_pairs_emit<<<rs_tiles, RS_THREADS, sizeof(PeSmem), st>>>(b->rec.as<uint4>(), b->n, (unsigned)no, dxu, dxyu,
+                                                                 plan, pbounds, keysA, valsA, counts, ld, hist);
+      LAUNCHED("k_pairs_emit", st);
+      b->launches += 2;
+      CU(cudaEventRecord(b->ev[1], st));
+      if ((rc = run_passes(b, plan, true, keysA, valsA, keysB, valsB, dO, no, hist, counts, st, &sorted))) return rc;
+    } else {
+      CU(cudaEventRecord(b->ev[1], st));
     }
   } else {
     CU(cudaEventRecord(b->ev[1], st));
   }
   CU(cudaEventRecord(b->ev[2], st));
-  const unsigned g_tiles = (unsigned)((ncells + G_TILE - 1) / G_TILE);
-  k_cell_offsets<<<g_tiles, G_THREADS, 0, st>>>(sorted, (unsigned)no, (unsigned)ncells, dG);
+  k_key_tile_bounds<<<(g_tiles + 1 + 7) / 8, 256, 0, st>>>(sorted, (unsigned)no, G_TILE, (unsigned)ncells, g_tiles + 1,
+                                                          kbounds);
+  LAUNCHED("k_key_tile_bounds", st);
+  k_cell_offsets<<<g_tiles, G_THREADS, 0, st>>>(sorted, (unsigned)no, (unsigned)ncells, kbounds, dG);
   LAUNCHED("k_cell_offsets", st);
-  ++b->launches;
+  b->launches += 2;
   b->sorted_keys = sorted;
   CU(cudaEventRecord(b->ev[3], st));
   if (flags & PG_HOST_OUTPUT) {
@@ -461,7 +493,7 @@ int pg_radix_sort_pairs(pg_builder* b, const uint32_t* keys, const uint32_t* val
   CU(cudaMemcpyAsync(vA, vals, (size_t)n * 4, in_kind, st));
   const unsigned rs_tiles = (unsigned)((n + RS_TILE - 1) / RS_TILE);
   const size_t hist_bytes = align_up(kMaxPasses * kMaxBins * 4);
-  if ((rc = b->sort_sync.ensure(hist_bytes + (size_t)rs_tiles * kMaxBins * 4))) return rc;
+  if ((rc = b->sort_sync.ensure(hist_bytes + (size_t)((rs_tiles + 3) & ~3u) * kMaxBins * 4))) return rc;
   unsigned* hist = b->sort_sync.as<unsigned>(0);
   unsigned* counts = b->sort_sync.as<unsigned>(hist_bytes);
   CU(cudaMemsetAsync(hist, 0, hist_bytes, st));
@@ -474,7 +506,7 @@ int pg_radix_sort_pairs(pg_builder* b, const uint32_t* keys, const uint32_t* val
     // host outputs: final values land in the staging section behind the pair buffers
     if ((rc = b->stage.ensure(sec))) return rc;
     unsigned* vdst = (flags & PG_HOST_OUTPUT) ? b->stage.as<unsigned>() : vals_out;
-    if ((rc = run_passes(b, plan, kA, vA, kB, vB, vdst, (uint64_t)n, hist, counts, st, &sorted)))
+    if ((rc = run_passes(b, plan, false, kA, vA, kB, vB, vdst, (uint64_t)n, hist, counts, st, &sorted)))
       return rc;
     vfinal = vdst;
   }

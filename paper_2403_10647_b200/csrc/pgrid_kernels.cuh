@@ -241,112 +241,177 @@ constexpr int K2_TILE = K2_THREADS * K2_ITEMS;
 constexpr int kMaxDigitBits = 9;
 constexpr int kMaxBins = 1 << kMaxDigitBits;  // 512
 
-// Each CTA owns pairs [p0, p0 + K2_TILE). The owning triangle of every pair is recovered
-// the way Alg. 1 does it (marks at run starts + inclusive max-scan), but
-// tile-locally: the tile's first owner comes from a 32-ary search over the record offsets,
-// the run starts inside the tile are scattered into shared memory, and a block max-scan
-// fills the gaps. Within a thread's 8 consecutive pairs the cell coordinate is stepped
-// incrementally (x-fastest), so the two divisions of _make_cell_ids (builders.py:111-113)
-// run at most once per thread.
-__global__ void __launch_bounds__(K2_THREADS)
-k_expand_pairs(const uint4* __restrict__ rec, long long n, unsigned no, unsigned dx, unsigned dxy,
-               PassPlan plan, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
-               unsigned* __restrict__ hist) {
-  __shared__ __align__(16) int slot[K2_TILE];
-  __shared__ unsigned sh_hist[kMaxPasses * kMaxBins];
-  __shared__ int sh_warpmax[K2_THREADS / 32];
-  __shared__ long long sh_olo;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned p0 = blockIdx.x * (unsigned)K2_TILE;
-  const unsigned pend = min(p0 + (unsigned)K2_TILE, no);
+// Object cache for one expansion tile: box records of the tile's triangles olo, olo+1, ...
+// (structure of arrays in shared memory); triangles past OC_CAP are read from global.
+constexpr int OC_CAP = 2560;
+struct ObjCache {
+  unsigned lo_cell[OC_CAP];
+  unsigned mx[OC_CAP];
+  unsigned my[OC_CAP];
+};
 
-  for (int i = tid; i < K2_TILE; i += K2_THREADS) slot[i] = -1;
-  for (int i = tid; i < plan.npasses * kMaxBins; i += K2_THREADS) sh_hist[i] = 0;
-  if (warp == 0) {
-    // olo = (#triangles with offset <= p0) - 1: the owner of pair p0.
-    const unsigned long long c = warp_lower_bound((unsigned long long)n, (unsigned long long)p0 + 1,
-                                                  [&](unsigned long long i) { return (unsigned long long)__ldg(&rec[i].w); });
-    if (lane == 0) sh_olo = (long long)c - 1;
-  }
+// Pair expansion of one tile [p0, p0 + THREADS*ITEMS): thread t produces the cell ids
+// (key) and owning triangle ids (own) of its ITEMS consecutive pairs p0 + t*ITEMS + j.
+// The owner of every pair is recovered the way Alg. 1 does it (marks at run starts +
+// inclusive max-scan), but tile-locally: the tile's first owner comes from
+// a 32-ary search over the record offsets, the run starts inside the tile are scattered into
+// shared memory (their box records cached alongside), and a block max-scan fills the gaps.
+// Inside a thread's consecutive pairs the cell coordinate is stepped incrementally
+// (x-fastest); a new run always starts at relative offset 0, so the two divisions of
+// _make_cell_ids (builders.py:111-113) only ever run for a thread's first pair.
+template <int THREADS, int ITEMS>
+__device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long long n, unsigned p0, unsigned pend,
+                                            unsigned dx, unsigned dxy, const int2* __restrict__ bounds, int* slot,
+                                            int* warpmax, ObjCache* oc, unsigned (&key)[ITEMS], int (&own)[ITEMS]) {
+  constexpr int TILE = THREADS * ITEMS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // [olo, oend): owner of pair p0, and one past the last triangle whose run starts in the tile
+  // (k_pair_tile_bounds precomputed both with 32-ary searches over the offsets)
+  const int2 bnd = __ldg(&bounds[p0 / TILE]);
+  const long long olo = bnd.x, oend = bnd.y;
+  for (int i = tid; i < TILE; i += THREADS) slot[i] = -1;
   __syncthreads();
-  const long long olo = sh_olo;
-  if (tid == 0) slot[0] = (int)olo;
-  // run starts inside the tile: every triangle after olo whose offset is < pend
-  for (long long ob = olo + 1;; ob += K2_THREADS) {
-    const long long o = ob + tid;
-    bool in = false;
-    if (o < n) {
-      const unsigned off = __ldg(&rec[o].w);
-      if (off < pend) {
-        atomicMax(&slot[off - p0], (int)o);  // zero-count triangles share the next start; max wins
-        in = true;
-      }
+  if (tid == 0) {
+    slot[0] = (int)olo;
+    const uint4 r = __ldg(&rec[olo]);
+    oc->lo_cell[0] = r.x;
+    oc->mx[0] = r.y;
+    oc->my[0] = r.z;
+  }
+  // run starts inside the tile (independent loads, no barrier per chunk)
+#pragma unroll 4
+  for (long long o = olo + 1 + tid; o < oend; o += THREADS) {
+    const uint4 r = __ldg(&rec[o]);
+    atomicMax(&slot[r.w - p0], (int)o);  // zero-count triangles share the next start; max wins
+    const long long ci = o - olo;
+    if (ci < OC_CAP) {
+      oc->lo_cell[ci] = r.x;
+      oc->mx[ci] = r.y;
+      oc->my[ci] = r.z;
     }
-    if (!__syncthreads_and(in)) break;
   }
   __syncthreads();
-  // inclusive max-scan over the slots (blocked: thread t owns slots [8t, 8t+8))
-  int own[K2_ITEMS];
-  {
-    const int4 a = *reinterpret_cast<const int4*>(&slot[tid * K2_ITEMS]);
-    const int4 b = *reinterpret_cast<const int4*>(&slot[tid * K2_ITEMS + 4]);
-    own[0] = a.x; own[1] = a.y; own[2] = a.z; own[3] = a.w;
-    own[4] = b.x; own[5] = b.y; own[6] = b.z; own[7] = b.w;
+  // inclusive max-scan over the slots (blocked: thread t owns slots [ITEMS*t, ITEMS*t + ITEMS))
+#pragma unroll
+  for (int q = 0; q < ITEMS / 4; ++q) {
+    const int4 a = *reinterpret_cast<const int4*>(&slot[tid * ITEMS + 4 * q]);
+    own[4 * q] = a.x;
+    own[4 * q + 1] = a.y;
+    own[4 * q + 2] = a.z;
+    own[4 * q + 3] = a.w;
   }
 #pragma unroll
-  for (int j = 1; j < K2_ITEMS; ++j) own[j] = max(own[j], own[j - 1]);
-  int run = own[K2_ITEMS - 1];
+  for (int j = 1; j < ITEMS; ++j) own[j] = max(own[j], own[j - 1]);
+  int run = own[ITEMS - 1];
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const int o = __shfl_up_sync(0xffffffffu, run, d);
     if (lane >= d) run = max(run, o);
   }
-  if (lane == 31) sh_warpmax[warp] = run;
+  if (lane == 31) warpmax[warp] = run;
   __syncthreads();
   int carry = __shfl_up_sync(0xffffffffu, run, 1);
   if (lane == 0) carry = -1;
-  for (int w = 0; w < warp; ++w) carry = max(carry, sh_warpmax[w]);
+  for (int w = 0; w < warp; ++w) carry = max(carry, warpmax[w]);
 #pragma unroll
-  for (int j = 0; j < K2_ITEMS; ++j) own[j] = max(own[j], carry);
+  for (int j = 0; j < ITEMS; ++j) own[j] = max(own[j], carry);
 
-  // expansion
-  unsigned key[K2_ITEMS];
-  const unsigned pbase = p0 + (unsigned)tid * K2_ITEMS;
-  int prev = -1;
+  auto box = [&](int o, unsigned& lc, unsigned& bx, unsigned& by) {
+    const long long ci = (long long)o - olo;
+    if (ci < OC_CAP) {
+      lc = oc->lo_cell[ci];
+      bx = oc->mx[ci];
+      by = oc->my[ci];
+    } else {
+      const uint4 r = __ldg(&rec[o]);
+      lc = r.x;
+      bx = r.y;
+      by = r.z;
+    }
+  };
+  const unsigned pbase = p0 + (unsigned)tid * ITEMS;
   unsigned cell = 0, x = 0, y = 0, mx = 1, my = 1;
-#pragma unroll
-  for (int j = 0; j < K2_ITEMS; ++j) {
-    const unsigned p = pbase + j;
-    key[j] = 0;
-    if (p < pend) {
-      const int o = own[j];
-      if (o != prev) {
-        const uint4 r = __ldg(&rec[o]);
-        const unsigned rel = p - r.w;
-        mx = r.y;
-        my = r.z;
-        const unsigned mxy = mx * my;
-        const unsigned z = rel / mxy;
-        const unsigned rem = rel - z * mxy;
-        y = rem / mx;
-        x = rem - y * mx;
-        cell = r.x + x + dx * y + dxy * z;
-        prev = o;
-      } else {
-        ++x;
-        ++cell;
-        if (x == mx) {
-          x = 0;
-          cell += dx - mx;
-          if (++y == my) {
-            y = 0;
-            cell += dxy - dx * my;
-          }
-        }
-      }
-      key[j] = cell;
+  if (pbase < pend) {  // first pair: may sit anywhere inside its run
+    const unsigned rel = pbase - __ldg(&rec[own[0]].w);
+    unsigned lc;
+    box(own[0], lc, mx, my);
+    if (rel == 0) {
+      cell = lc;
+    } else {
+      const unsigned mxy = mx * my;
+      const unsigned z = rel / mxy;
+      const unsigned rem = rel - z * mxy;
+      y = rem / mx;
+      x = rem - y * mx;
+      cell = lc + x + dx * y + dxy * z;
     }
   }
+  key[0] = cell;
+#pragma unroll
+  for (int j = 1; j < ITEMS; ++j) {
+    if (own[j] != own[j - 1]) {  // a new run starts at its relative offset 0
+      box(own[j], cell, mx, my);
+      x = 0;
+      y = 0;
+    } else {
+      ++x;
+      ++cell;
+      if (x == mx) {
+        x = 0;
+        cell += dx - mx;
+        if (++y == my) {
+          y = 0;
+          cell += dxy - dx * my;
+        }
+      }
+    }
+    key[j] = cell;
+  }
+}
+
+// Tile bounds of the pair expansion, one warp per tile: x = owner of the tile's first pair
+// ((#triangles with offset <= p0) - 1), y = one past the last triangle whose run starts
+// inside the tile (#triangles with offset < pend). Hoisting these searches out of the
+// expansion kernels keeps their CTAs from idling on dependent round trips at launch.
+__global__ void __launch_bounds__(256)
+k_pair_tile_bounds(const uint4* __restrict__ rec, long long n, unsigned no, unsigned tile, unsigned ntiles,
+                   int2* __restrict__ bounds) {
+  const unsigned t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= ntiles) return;
+  const unsigned p0 = t * tile;
+  const unsigned pend = min(p0 + tile, no);
+  auto ld = [&](unsigned long long i) { return (unsigned long long)__ldg(&rec[i].w); };
+  const unsigned long long a = warp_lower_bound((unsigned long long)n, (unsigned long long)p0 + 1, ld);
+  const unsigned long long b = warp_lower_bound((unsigned long long)n, (unsigned long long)pend, ld);
+  if ((threadIdx.x & 31) == 0) bounds[t] = make_int2((int)a - 1, (int)b);
+}
+
+// lower_bound(sorted, t * step) for t in [0, nq), one warp per query (K4's key ranges).
+__global__ void __launch_bounds__(256)
+k_key_tile_bounds(const unsigned* __restrict__ sorted, unsigned no, unsigned step, unsigned ncells, unsigned nq,
+                  unsigned* __restrict__ out) {
+  const unsigned t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= nq) return;
+  const unsigned long long c = min((unsigned long long)t * step, (unsigned long long)ncells);
+  const unsigned long long v =
+      warp_lower_bound(no, c, [&](unsigned long long i) { return (unsigned long long)__ldg(sorted + i); });
+  if ((threadIdx.x & 31) == 0) out[t] = (unsigned)v;
+}
+
+// Pairs in generation (object-major) order -- used when no radix pass follows
+// (ncells == 1) and for the record= stage dumps.
+__global__ void __launch_bounds__(K2_THREADS)
+k_expand_pairs(const uint4* __restrict__ rec, long long n, unsigned no, unsigned dx, unsigned dxy,
+               const int2* __restrict__ bounds, unsigned* __restrict__ keys, unsigned* __restrict__ vals) {
+  __shared__ __align__(16) int slot[K2_TILE];
+  __shared__ int warpmax[K2_THREADS / 32];
+  __shared__ ObjCache oc;
+  const unsigned p0 = blockIdx.x * (unsigned)K2_TILE;
+  const unsigned pend = min(p0 + (unsigned)K2_TILE, no);
+  unsigned key[K2_ITEMS];
+  int own[K2_ITEMS];
+  expand_tile<K2_THREADS, K2_ITEMS>(rec, n, p0, pend, dx, dxy, bounds, slot, warpmax, &oc, key, own);
+  const unsigned pbase = p0 + threadIdx.x * K2_ITEMS;
   if (pbase + K2_ITEMS <= pend) {
     uint4* kd = reinterpret_cast<uint4*>(keys + pbase);
     uint4* vd = reinterpret_cast<uint4*>(vals + pbase);
@@ -361,18 +426,6 @@ k_expand_pairs(const uint4* __restrict__ rec, long long n, unsigned no, unsigned
         keys[pbase + j] = key[j];
         vals[pbase + j] = (unsigned)own[j];
       }
-  }
-  // digit histograms of every radix pass (consumed by the onesweep passes)
-  for (int ps = 0; ps < plan.npasses; ++ps) {
-    const unsigned mask = (1u << plan.bits[ps]) - 1u;
-#pragma unroll
-    for (int j = 0; j < K2_ITEMS; ++j)
-      if (pbase + j < pend) atomicAdd(&sh_hist[ps * kMaxBins + ((key[j] >> plan.shift[ps]) & mask)], 1u);
-  }
-  __syncthreads();
-  for (int i = tid; i < plan.npasses * kMaxBins; i += K2_THREADS) {
-    const unsigned c = sh_hist[i];
-    if (c) atomicAdd(&hist[i], c);
   }
 }
 
@@ -452,7 +505,8 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* wsum, 
 }
 
 __global__ void __launch_bounds__(RS_THREADS)
-k_tile_counts(const unsigned* __restrict__ keys, unsigned no, int shift, int bits, unsigned* __restrict__ counts) {
+k_tile_counts(const unsigned* __restrict__ keys, unsigned no, int shift, int bits, unsigned* __restrict__ counts,
+              unsigned ld) {
   __shared__ unsigned h[kMaxBins];
   const int tid = threadIdx.x;
   const unsigned ntiles = (no + RS_TILE - 1) / RS_TILE;
@@ -478,44 +532,52 @@ k_tile_counts(const unsigned* __restrict__ keys, unsigned no, int shift, int bit
     for (unsigned e = tid; e < tvalid; e += RS_THREADS) atomicAdd(&h[(__ldcs(keys + tbase + e) >> shift) & dmask], 1u);
   }
   __syncthreads();
-  for (int b = tid; b < (1 << bits); b += RS_THREADS) counts[(size_t)b * ntiles + tile] = h[b];
+  for (int b = tid; b < (1 << bits); b += RS_THREADS) counts[(size_t)b * ld + tile] = h[b];
 }
 
-constexpr int SC_THREADS = 256;
-constexpr int SC_ITEMS = 16;
+constexpr int SC_THREADS = 1024;
+constexpr int SC_ITEMS = 8;
 // One CTA per digit row: counts[row][0..ntiles) -> exclusive prefix over tiles, in place.
+// Rows are padded to a multiple of 4 (ld) so each thread moves its 8 entries as two 16-byte
+// accesses; one iteration covers 8192 tiles (33.5M pairs).
 __global__ void __launch_bounds__(SC_THREADS)
-k_scan_tile_counts(unsigned* __restrict__ counts, unsigned ntiles) {
-  __shared__ unsigned s[SC_THREADS * SC_ITEMS];
+k_scan_tile_counts(unsigned* __restrict__ counts, unsigned ntiles, unsigned ld) {
   __shared__ unsigned wsum[SC_THREADS / 32];
   const int tid = threadIdx.x;
-  unsigned* row = counts + (size_t)blockIdx.x * ntiles;
+  unsigned* row = counts + (size_t)blockIdx.x * ld;
   unsigned carry = 0;
   for (unsigned base = 0; base < ntiles; base += SC_THREADS * SC_ITEMS) {
+    const unsigned i0 = base + tid * SC_ITEMS;
+    unsigned v[SC_ITEMS];
+    if (i0 + SC_ITEMS <= ld) {
+      const uint4 a = *reinterpret_cast<const uint4*>(row + i0);
+      const uint4 b = *reinterpret_cast<const uint4*>(row + i0 + 4);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
 #pragma unroll
-    for (int k = 0; k < SC_ITEMS; ++k) {
-      const unsigned i = base + tid + k * SC_THREADS;
-      s[tid + k * SC_THREADS] = i < ntiles ? row[i] : 0u;
+      for (int q = 0; q < SC_ITEMS; ++q) v[q] = i0 + q < ld ? row[i0 + q] : 0u;
     }
-    __syncthreads();
-    unsigned v[SC_ITEMS], run = 0;
+#pragma unroll
+    for (int q = 0; q < SC_ITEMS; ++q)
+      if (i0 + q >= ntiles) v[q] = 0u;  // padding columns hold garbage
+    unsigned run = 0;
 #pragma unroll
     for (int q = 0; q < SC_ITEMS; ++q) {
+      const unsigned c = v[q];
       v[q] = run;
-      run += s[tid * SC_ITEMS + q];
+      run += c;
     }
     unsigned total;
-    const unsigned pre = block_excl_scan<SC_THREADS / 32>(run, wsum, total);
+    const unsigned pre = carry + block_excl_scan<SC_THREADS / 32>(run, wsum, total);
+    if (i0 + SC_ITEMS <= ld) {
+      *reinterpret_cast<uint4*>(row + i0) = make_uint4(pre + v[0], pre + v[1], pre + v[2], pre + v[3]);
+      *reinterpret_cast<uint4*>(row + i0 + 4) = make_uint4(pre + v[4], pre + v[5], pre + v[6], pre + v[7]);
+    } else {
 #pragma unroll
-    for (int q = 0; q < SC_ITEMS; ++q) s[tid * SC_ITEMS + q] = carry + pre + v[q];
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < SC_ITEMS; ++k) {
-      const unsigned i = base + tid + k * SC_THREADS;
-      if (i < ntiles) row[i] = s[tid + k * SC_THREADS];
+      for (int q = 0; q < SC_ITEMS; ++q)
+        if (i0 + q < ntiles) row[i0 + q] = pre + v[q];
     }
     carry += total;
-    __syncthreads();
   }
 }
 
@@ -524,11 +586,11 @@ k_scan_tile_counts(unsigned* __restrict__ counts, unsigned ntiles) {
 // Values never occupy registers: cp.async stages them in input order and they are
 // permuted shared->shared after the keys have been written. BITS and FULL are compile-time
 // so the ranking loop is branch-free and full tiles carry no bounds predicates.
-template <int BITS, bool FULL>
+template <int BITS, bool FULL, bool SRC_SMEM = false>
 __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* __restrict__ keys_in,
                                                    const unsigned* __restrict__ vals_in,
                                                    unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out,
-                                                   unsigned tbase, unsigned tvalid, unsigned tile, unsigned ntiles,
+                                                   unsigned tbase, unsigned tvalid, unsigned tile, unsigned ld,
                                                    int shift, const unsigned* __restrict__ hist,
                                                    const unsigned* __restrict__ offs) {
   constexpr int NB = 1 << BITS;
@@ -537,13 +599,18 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
   auto elem = [&](int j) { return (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane; };
   auto valid = [&](int j) { return FULL || elem(j) < tvalid; };
 
-  if (FULL) {
+  // SRC_SMEM: keys_in points at a shared-memory copy of the tile (element order) and
+  // sm.vstage already holds the values
+  if (!SRC_SMEM) {
+    if (FULL) {
 #pragma unroll
-    for (int c = tid; c < RS_TILE / 4; c += RS_THREADS) cp_async16(&sm.vstage[4 * c], vals_in + tbase + 4 * c);
-  } else {
-    for (unsigned e = tid; e < tvalid; e += RS_THREADS) cp_async4(&sm.vstage[e], vals_in + tbase + e);
+      for (int c = tid; c < RS_TILE / 4; c += RS_THREADS) cp_async16(&sm.vstage[4 * c], vals_in + tbase + 4 * c);
+    } else {
+      for (unsigned e = tid; e < tvalid; e += RS_THREADS) cp_async4(&sm.vstage[e], vals_in + tbase + e);
+    }
+    cp_async_commit();
   }
-  cp_async_commit();
+  const unsigned* ksrc = SRC_SMEM ? keys_in : keys_in + tbase;
   {
     unsigned* row = reinterpret_cast<unsigned*>(&sm.whist[warp][0]);
 #pragma unroll
@@ -551,7 +618,7 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
   }
   unsigned dg[RS_ITEMS];
 #pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) dg[j] = valid(j) ? (__ldg(keys_in + tbase + elem(j)) >> shift) & DMASK : 0u;
+  for (int j = 0; j < RS_ITEMS; ++j) dg[j] = valid(j) ? ((SRC_SMEM ? ksrc[elem(j)] : __ldg(ksrc + elem(j))) >> shift) & DMASK : 0u;
   // peers (same-digit lanes) per item: bit-sliced ballots, items interleaved for ILP
   unsigned pm[RS_ITEMS];
 #pragma unroll
@@ -608,7 +675,7 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
     const int d = tid * RS_DPT + q;
     if (d < NB) {
       sm.local_start[d] = lpre;
-      sm.gbase[d] = hpre + __ldg(&offs[(size_t)d * ntiles + tile]) - lpre;
+      sm.gbase[d] = hpre + __ldg(&offs[(size_t)d * ld + tile]) - lpre;
     }
     lpre += tc[q];
     hpre += hs[q];
@@ -619,7 +686,7 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
   for (int j = 0; j < RS_ITEMS; ++j) {
     if (valid(j)) {
       rank[j] += sm.local_start[dg[j]] + sm.whist[warp][dg[j]];  // rank -> tile position
-      sm.buf[rank[j]] = keys_in[tbase + elem(j)];
+      sm.buf[rank[j]] = ksrc[elem(j)];
     }
   }
   __syncthreads();
@@ -634,7 +701,7 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
       if (keys_out) keys_out[gpos[r]] = k;
     }
   }
-  cp_async_wait();
+  if (!SRC_SMEM) cp_async_wait();
   __syncthreads();
   // values: shared->shared permutation with the same positions, then write-out
 #pragma unroll
@@ -652,19 +719,96 @@ template <int BITS>
 __global__ void __launch_bounds__(RS_THREADS, 4)
 k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
                 unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, unsigned no, int shift,
-                const unsigned* __restrict__ hist, const unsigned* __restrict__ offs) {
+                const unsigned* __restrict__ hist, const unsigned* __restrict__ offs, unsigned ld) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RsSmem& sm = *reinterpret_cast<RsSmem*>(smem_raw);
-  const unsigned ntiles = (no + RS_TILE - 1) / RS_TILE;
   const unsigned tile = blockIdx.x;
   const unsigned tbase = tile * (unsigned)RS_TILE;
   const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
   if (tvalid == (unsigned)RS_TILE)
-    radix_scatter_tile<BITS, true>(sm, keys_in, vals_in, keys_out, vals_out, tbase, tvalid, tile, ntiles, shift,
-                                   hist, offs);
+    radix_scatter_tile<BITS, true>(sm, keys_in, vals_in, keys_out, vals_out, tbase, tvalid, tile, ld, shift, hist,
+                                   offs);
   else
-    radix_scatter_tile<BITS, false>(sm, keys_in, vals_in, keys_out, vals_out, tbase, tvalid, tile, ntiles, shift,
-                                    hist, offs);
+    radix_scatter_tile<BITS, false>(sm, keys_in, vals_in, keys_out, vals_out, tbase, tvalid, tile, ld, shift, hist,
+                                    offs);
+}
+
+// ----------------------------------------------------------------------------------------
+// K2: pair expansion on radix-sort tiles. Each CTA expands RS_TILE pairs, writes them in
+// generation (object-major) order with 16-byte stores, and counts the tile's first-pass
+// digits (the per-tile counts the first radix pass needs, so that pass skips its own
+// upsweep) plus the global digit histograms of every pass.
+// ----------------------------------------------------------------------------------------
+struct PeSmem {
+  int slot[RS_TILE];
+  unsigned h[kMaxPasses * kMaxBins];
+  ObjCache oc;
+  int warpmax[RS_WARPS];
+};
+
+__global__ void __launch_bounds__(RS_THREADS)
+k_pairs_emit(const uint4* __restrict__ rec, long long n, unsigned no, unsigned dx, unsigned dxy, PassPlan plan,
+             const int2* __restrict__ bounds, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
+             unsigned* __restrict__ counts0, unsigned ld, unsigned* __restrict__ hist) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PeSmem& sm = *reinterpret_cast<PeSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const unsigned p0 = blockIdx.x * (unsigned)RS_TILE;
+  const unsigned pend = min(p0 + (unsigned)RS_TILE, no);
+  for (int b = tid; b < kMaxPasses * kMaxBins; b += RS_THREADS) sm.h[b] = 0u;
+  unsigned key[RS_ITEMS];
+  int own[RS_ITEMS];
+  expand_tile<RS_THREADS, RS_ITEMS>(rec, n, p0, pend, dx, dxy, bounds, sm.slot, sm.warpmax, &sm.oc, key, own);
+  const unsigned pbase = p0 + (unsigned)tid * RS_ITEMS;
+  const int nvalid = pend > pbase ? (int)min((unsigned)RS_ITEMS, pend - pbase) : 0;
+  if (nvalid == RS_ITEMS) {
+    uint4* kd = reinterpret_cast<uint4*>(keys + pbase);
+    uint4* vd = reinterpret_cast<uint4*>(vals + pbase);
+#pragma unroll
+    for (int q = 0; q < RS_ITEMS / 4; ++q) {
+      kd[q] = make_uint4(key[4 * q], key[4 * q + 1], key[4 * q + 2], key[4 * q + 3]);
+      vd[q] = make_uint4(own[4 * q], own[4 * q + 1], own[4 * q + 2], own[4 * q + 3]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j)
+      if (j < nvalid) {
+        keys[pbase + j] = key[j];
+        vals[pbase + j] = (unsigned)own[j];
+      }
+  }
+  {  // first-pass digit: consecutive cells rarely share it -- one atomic per pair
+    const int sh = plan.shift[0];
+    const unsigned mask = (1u << plan.bits[0]) - 1u;
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j)
+      if (j < nvalid) atomicAdd(&sm.h[(key[j] >> sh) & mask], 1u);
+  }
+#pragma unroll
+  for (int ps = 1; ps < kMaxPasses; ++ps) {  // higher digits: run-length aggregated in registers
+    if (ps < plan.npasses) {
+      const int sh = plan.shift[ps];
+      const unsigned mask = (1u << plan.bits[ps]) - 1u;
+      unsigned cur = (key[0] >> sh) & mask, cnt = 0;
+#pragma unroll
+      for (int j = 0; j < RS_ITEMS; ++j) {
+        if (j < nvalid) {
+          const unsigned d = (key[j] >> sh) & mask;
+          if (d != cur) {
+            atomicAdd(&sm.h[ps * kMaxBins + cur], cnt);
+            cur = d;
+            cnt = 0;
+          }
+          ++cnt;
+        }
+      }
+      if (cnt) atomicAdd(&sm.h[ps * kMaxBins + cur], cnt);
+    }
+  }
+  __syncthreads();
+  for (int b = tid; b < (1 << plan.bits[0]); b += RS_THREADS) counts0[(size_t)b * ld + blockIdx.x] = sm.h[b];
+  for (int b = tid; b < plan.npasses * kMaxBins; b += RS_THREADS)
+    if (sm.h[b]) atomicAdd(&hist[b], sm.h[b]);
 }
 
 // ----------------------------------------------------------------------------------------
@@ -675,28 +819,20 @@ constexpr int G_ITEMS = 16;
 constexpr int G_TILE = G_THREADS * G_ITEMS;  // cells per CTA
 
 // G[c] = #pairs with cell < c = lower_bound(sorted, c). Each CTA owns cells [c0, c0+G_TILE):
-// two warp searches bound its key range [i0, i1); every first occurrence of a cell marks
+// its key range [i0, i1) comes from k_key_tile_bounds; every first occurrence of a cell marks
 // its run start; a block suffix-min fills empty cells with the next run start (or i1).
 // The last CTA also writes the sentinel G[ncells] = NO (builders.py:131-133).
 __global__ void __launch_bounds__(G_THREADS)
-k_cell_offsets(const unsigned* __restrict__ sorted, unsigned no, unsigned ncells, unsigned* __restrict__ G) {
+k_cell_offsets(const unsigned* __restrict__ sorted, unsigned no, unsigned ncells, const unsigned* __restrict__ kb,
+               unsigned* __restrict__ G) {
   __shared__ __align__(16) unsigned mark[G_TILE];
-  __shared__ unsigned sh_i0, sh_i1;
   __shared__ unsigned sh_wmin[G_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned c0 = blockIdx.x * (unsigned)G_TILE;
   const unsigned c1 = min(c0 + (unsigned)G_TILE, ncells);
-  auto ld = [&](unsigned long long i) { return (unsigned long long)__ldg(sorted + i); };
-  if (warp == 0) {
-    const unsigned v = (unsigned)warp_lower_bound(no, c0, ld);
-    if (lane == 0) sh_i0 = v;
-  } else if (warp == 1) {
-    const unsigned v = (unsigned)warp_lower_bound(no, c1, ld);
-    if (lane == 0) sh_i1 = v;
-  }
+  const unsigned i0 = __ldg(&kb[blockIdx.x]), i1 = __ldg(&kb[blockIdx.x + 1]);  // k_key_tile_bounds
   for (int i = tid; i < G_TILE; i += G_THREADS) mark[i] = 0xffffffffu;
   __syncthreads();
-  const unsigned i0 = sh_i0, i1 = sh_i1;
   for (unsigned i = i0 + tid; i < i1; i += G_THREADS) {
     const unsigned k = __ldg(sorted + i);
     if (i == 0 || __ldg(sorted + i - 1) != k) mark[k - c0] = i;
