@@ -151,7 +151,7 @@ struct pg_builder {
   // K1 outputs / scratch
   DevBuf rec, k1_sync;
   // pair buffers and sort scratch
-  DevBuf pairs, sort_sync, stage, gbuf, obuf;
+  DevBuf pairs, sort_sync, stage, stage0, gbuf, obuf;
   // state of the last pg_count
   bool counted = false;
   int64_t n = 0;
@@ -163,6 +163,7 @@ struct pg_builder {
   bool k1_timed = false;  // ev[5]..ev[6] bracket K1 of the last pg_count
   int launches = 0;
   const unsigned* sorted_keys = nullptr;
+  const unsigned* tile_pre = nullptr;  // K1 tile prefixes of the last pg_count
 };
 
 extern "C" {
@@ -176,6 +177,7 @@ int pg_builder_create(int device, pg_builder** out) {
   b->device = device;
   for (auto& e : b->ev) CU(cudaEventCreate(&e));
   CU(cudaMallocHost(&b->h_scalars, 4 * sizeof(unsigned long long)));
+  CU(cudaFuncSetAttribute(k_boxes_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem)));
   CU(cudaFuncSetAttribute(k_pairs_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PeSmem)));
   CU(set_scatter_smem<1>()); CU(set_scatter_smem<2>()); CU(set_scatter_smem<3>());
   CU(set_scatter_smem<4>()); CU(set_scatter_smem<5>()); CU(set_scatter_smem<6>());
@@ -190,7 +192,7 @@ void pg_builder_destroy(pg_builder* b) {
   for (auto& e : b->ev)
     if (e) cudaEventDestroy(e);
   if (b->h_scalars) cudaFreeHost(b->h_scalars);
-  for (DevBuf* d : {&b->in_v, &b->in_t, &b->rec, &b->k1_sync, &b->pairs, &b->sort_sync, &b->stage,
+  for (DevBuf* d : {&b->in_v, &b->in_t, &b->rec, &b->k1_sync, &b->pairs, &b->sort_sync, &b->stage, &b->stage0,
                     &b->gbuf, &b->obuf})
     d->release();
   delete b;
@@ -265,20 +267,25 @@ int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64
   const unsigned ntiles = (unsigned)((n + K1_TILE - 1) / K1_TILE);
   int rc;
   if ((rc = b->rec.ensure((size_t)n * sizeof(uint4)))) return rc;
-  // sync area: [status u64 x ntiles][tile counter][err][total u64]
-  const size_t sync_bytes = align_up((size_t)ntiles * 8) + 256;
-  if ((rc = b->k1_sync.ensure(sync_bytes))) return rc;
-  unsigned long long* status = b->k1_sync.as<unsigned long long>();
-  unsigned* ctr = b->k1_sync.as<unsigned>(align_up((size_t)ntiles * 8));
-  unsigned* err = ctr + 1;
-  unsigned long long* total = b->k1_sync.as<unsigned long long>(align_up((size_t)ntiles * 8) + 8);
-  CU(cudaMemsetAsync(b->k1_sync.p, 0, sync_bytes, st));
+  // K1 area: [tile_sum u64 x ntiles][tile_pre u32 x ntiles][err u32][pad][total u64]
+  const size_t ts_bytes = align_up((size_t)ntiles * 8), tp_bytes = align_up((size_t)ntiles * 4);
+  if ((rc = b->k1_sync.ensure(ts_bytes + tp_bytes + 256))) return rc;
+  unsigned long long* tile_sum = b->k1_sync.as<unsigned long long>();
+  unsigned* tile_pre = b->k1_sync.as<unsigned>(ts_bytes);
+  unsigned* err = b->k1_sync.as<unsigned>(ts_bytes + tp_bytes);
+  unsigned long long* total = b->k1_sync.as<unsigned long long>(ts_bytes + tp_bytes + 8);
+  b->tile_pre = tile_pre;
+  CU(cudaMemsetAsync(err, 0, 16, st));
   CU(cudaEventRecord(b->ev[5], st));
-  k_boxes_count_scan<<<ntiles, K1_THREADS, 0, st>>>(dV, reinterpret_cast<const int*>(dT), n, ds,
-                                                     b->rec.as<uint4>(), status, ctr, total, err);
-  LAUNCHED("k_boxes_count_scan", st);
+  // TMA bulk staging needs 16-byte aligned sources
+  const int bulk_ok = ((reinterpret_cast<uintptr_t>(dV) | reinterpret_cast<uintptr_t>(dT)) & 15) == 0;
+  k_boxes_count<<<ntiles, K1_THREADS, sizeof(K1Smem), st>>>(dV, nv, reinterpret_cast<const int*>(dT), n, ds, bulk_ok,
+                                                            b->rec.as<uint4>(), tile_sum, err);
+  LAUNCHED("k_boxes_count", st);
+  k_scan_tile_sums<<<1, TS_THREADS, 0, st>>>(tile_sum, ntiles, tile_pre, total);
+  LAUNCHED("k_scan_tile_sums", st);
   CU(cudaEventRecord(b->ev[6], st));
-  b->launches = 1;
+  b->launches = 2;
   b->k1_timed = true;
   CU(cudaMemcpyAsync(&b->h_scalars[0], total, 8, cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(&b->h_scalars[1], err, 4, cudaMemcpyDeviceToHost, st));
@@ -378,11 +385,11 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
       // pairs in generation order: final when there is no radix pass (vals -> O), and the
       // record= stage dump otherwise
       unsigned* v0 = plan.npasses == 0 ? dO : valsA;
-      k_pair_tile_bounds<<<(k2_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->n, (unsigned)no, K2_TILE, k2_tiles,
-                                                            pbounds);
+      k_pair_tile_bounds<<<(k2_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no,
+                                                            K2_TILE, k2_tiles, pbounds);
       LAUNCHED("k_pair_tile_bounds", st);
-      k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->n, (unsigned)no, dxu, dxyu, pbounds,
-                                                     keysA, v0);
+      k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no, dxu, dxyu,
+                                                     pbounds, keysA, v0);
       LAUNCHED("k_expand_pairs", st);
       b->launches += 2;
       if (flags & PG_KEEP_STAGES) {
@@ -394,11 +401,12 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
     }
     if (plan.npasses > 0) {
       // K2 on radix tiles: pairs in generation order + first-pass tile counts + histograms
-      k_pair_tile_bounds<<<(rs_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->n, (unsigned)no, RS_TILE, rs_tiles,
-                                                            pbounds);
+      k_pair_tile_bounds<<<(rs_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no,
+                                                            RS_TILE, rs_tiles, pbounds);
       LAUNCHED("k_pair_tile_bounds", st);
-      k_pairs_emit<<<rs_tiles, RS_THREADS, sizeof(PeSmem), st>>>(b->rec.as<uint4>(), b->n, (unsigned)no, dxu, dxyu,
-                                                                 plan, pbounds, keysA, valsA, counts, ld, hist);
+      k_pairs_emit<<<rs_tiles, RS_THREADS, sizeof(PeSmem), st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no,
+                                                                 dxu, dxyu, plan, pbounds, keysA, valsA, counts, ld,
+                                                                 hist);
       LAUNCHED("k_pairs_emit", st);
       b->launches += 2;
       CU(cudaEventRecord(b->ev[1], st));
@@ -450,7 +458,14 @@ int pg_stage(pg_builder* b, int stage, void* dst, uint32_t flags, void* stream_)
   const size_t sec = align_up(std::max<size_t>((size_t)b->no * 4, 16));
   switch (stage) {
     case 0:
-      if (b->n) CU(cudaMemcpyAsync(dst, b->rec.p, (size_t)b->n * 16, kind, st));
+      if (b->n) {
+        int rc;
+        if ((rc = b->stage0.ensure((size_t)b->n * 16))) return rc;
+        k_abs_offsets<<<(unsigned)std::min<int64_t>((b->n + 255) / 256, 148 * 16), 256, 0, st>>>(
+            b->rec.as<uint4>(), b->tile_pre, b->n, b->stage0.as<uint4>());
+        LAUNCHED("k_abs_offsets", st);
+        CU(cudaMemcpyAsync(dst, b->stage0.p, (size_t)b->n * 16, kind, st));
+      }
       break;
     case 1:
     case 2:

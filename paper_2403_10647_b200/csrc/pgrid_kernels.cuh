@@ -107,129 +107,218 @@ __device__ __forceinline__ unsigned long long warp_lower_bound(unsigned long lon
 // K1: boxes + counts + decoupled-look-back exclusive scan
 // ----------------------------------------------------------------------------------------
 constexpr int K1_THREADS = 256;
-constexpr int K1_ITEMS = 4;
-constexpr int K1_TILE = K1_THREADS * K1_ITEMS;
+constexpr int K1_ROUNDS = 2;                       // triangles per thread (striped rounds)
+constexpr int K1_TILE = K1_THREADS * K1_ROUNDS;    // 512 triangles per CTA
 constexpr unsigned long long LB_AGG = 1ull << 62;
 constexpr unsigned long long LB_PREFIX = 2ull << 62;
 constexpr unsigned long long LB_VALUE = (1ull << 62) - 1;
 
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+// TMA bulk copy global -> shared (no tensor map): 16-byte aligned, size a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+struct K1Smem {
+  double v[K1_TILE * 9];   // the tile's 3*K1_TILE vertices when the mesh is a soup (36 KB)
+  int t[K1_TILE * 3];      // the tile's triangle indices (6 KB)
+  unsigned long long bar;
+  unsigned tile;
+};
+
 // Per-triangle record written by K1 and read by K2: {lo_cell, mx, my, pair offset}.
 // mx/my are the box extents in x/y; count = mx*my*mz is implied by the offsets.
 // Dropped triangles (keep == false, gridcore.py:159) are {0, 1, 1, off} with count 0.
-__global__ void __launch_bounds__(K1_THREADS)
-k_boxes_count_scan(const double* __restrict__ V, const int* __restrict__ T, long long n, DevSpec s,
-                   uint4* __restrict__ rec, unsigned long long* __restrict__ status,
-                   unsigned* __restrict__ tile_ctr, unsigned long long* __restrict__ total,
-                   unsigned* __restrict__ err) {
-  __shared__ unsigned sh_tile;
-  __shared__ unsigned long long sh_warp[K1_THREADS / 32];
-  __shared__ unsigned long long sh_excl;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) sh_tile = atomicAdd(tile_ctr, 1u);
-  __syncthreads();
-  const unsigned tile = sh_tile;
-  const unsigned ntiles = (unsigned)((n + K1_TILE - 1) / K1_TILE);
-  const long long first = (long long)tile * K1_TILE + (long long)tid * K1_ITEMS;
+//
+// Data movement: one elected thread streams the tile's 6 KB of indices and -- speculatively,
+// as if the mesh were an unshared-vertex soup (geometry.py:206-207) -- its 36 KB of vertex
+// rows into shared memory with TMA bulk copies on an mbarrier. If every index of the tile
+// is 3*i+k the boxes are computed from shared memory; otherwise (indexed meshes) the
+// vertices are gathered from global memory. Both paths compute the same IEEE f64 values.
+__device__ __forceinline__ void tri_box(const double* a, const double* b, const double* c, const DevSpec& s,
+                                        unsigned dx, unsigned dxy, uint3& box, unsigned& cnt, bool& bad) {
+  bool keep = true;
+  unsigned lo[3], hi[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double x0 = a[k], x1 = b[k], x2 = c[k];
+    // np.min/np.max propagate NaN, which fails both comparisons (gridcore.py:156-159);
+    // fmin/fmax do not, so NaN is folded into keep explicitly.
+    const bool nan = isnan(x0) | isnan(x1) | isnan(x2);
+    const double mn = fmin(fmin(x0, x1), x2);
+    const double mx = fmax(fmax(x0, x1), x2);
+    keep &= !nan && (mx >= s.lo[k]) && (mn <= s.hi[k]);
+    // one IEEE subtract, one IEEE divide, floor (gridcore.py:161-162)
+    lo[k] = clip_axis(np_floor_i64(__ddiv_rn(__dsub_rn(mn, s.lo[k]), s.cell[k])), s.dims[k]);
+    hi[k] = clip_axis(np_floor_i64(__ddiv_rn(__dsub_rn(mx, s.lo[k]), s.cell[k])), s.dims[k]);
+  }
+  if (keep && (hi[0] < lo[0] || hi[1] < lo[1] || hi[2] < lo[2])) {
+    // +inf / >2^63 upper corners cast to INT64_MIN and clip to 0 below lo: the reference
+    // then fails its non-negative / coincident-mark checks (primitives.py:22-25, 71-72).
+    bad = true;
+    keep = false;
+  }
+  box = make_uint3(0u, 1u, 1u);
+  cnt = 0;
+  if (keep) {
+    const unsigned ex = hi[0] - lo[0] + 1, ey = hi[1] - lo[1] + 1, ez = hi[2] - lo[2] + 1;
+    box = make_uint3(lo[0] + dx * lo[1] + dxy * lo[2], ex, ey);
+    cnt = ex * ey * ez;  // <= ncells <= 2^30
+  }
+}
 
-  uint3 box[K1_ITEMS];
-  unsigned cnt[K1_ITEMS];
+// K1a: boxes + counts of one 512-triangle tile; rec.w = the pair offset relative to the tile
+// start, tile_sum[tile] = the tile's pair count (u64). The cross-tile exclusive scan is
+// k_scan_tile_sums (reduce-then-scan: a decoupled look-back here serialises at roughly
+// window/round-trip tiles per microsecond on B200).
+__global__ void __launch_bounds__(K1_THREADS)
+k_boxes_count(const double* __restrict__ V, long long nv, const int* __restrict__ T, long long n, DevSpec s,
+              int bulk_ok, uint4* __restrict__ rec, unsigned long long* __restrict__ tile_sum,
+              unsigned* __restrict__ err) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  K1Smem& sm = *reinterpret_cast<K1Smem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned tile = blockIdx.x;
+  const long long tbase = (long long)tile * K1_TILE;
+  const int tcount = (int)min((long long)K1_TILE, n - tbase);
+  const bool full = tcount == K1_TILE;
+  // speculative soup staging is in range only if the tile's vertex rows exist
+  const bool spec_v = bulk_ok && full && 3 * (tbase + K1_TILE) <= nv;
+  if (bulk_ok && full) {
+    if (tid == 0) {
+      mbar_init(&sm.bar, 1);
+      const unsigned tb = K1_TILE * 3 * sizeof(int), vb = spec_v ? K1_TILE * 9 * sizeof(double) : 0u;
+      mbar_expect_tx(&sm.bar, tb + vb);
+      bulk_g2s(sm.t, T + 3 * tbase, tb, &sm.bar);
+      if (spec_v) bulk_g2s(sm.v, V + 9 * tbase, vb, &sm.bar);
+    }
+    __syncthreads();  // barrier initialised before anyone waits on it
+    mbar_wait(&sm.bar, 0);
+  } else {
+    for (int q = tid; q < 3 * tcount; q += K1_THREADS) sm.t[q] = __ldg(T + 3 * tbase + q);
+    __syncthreads();
+  }
+  // soup test over the whole tile: index 3*i+k == 3*(tbase+i)+k
+  bool mine = true;
+  for (int q = tid; q < 3 * tcount; q += K1_THREADS) mine &= sm.t[q] == (int)(3 * tbase + q);
+  const bool soup = __syncthreads_and(mine) && spec_v;
+
   const unsigned dx = (unsigned)s.dims[0], dxy = (unsigned)s.dims[0] * (unsigned)s.dims[1];
+  uint3 box[K1_ROUNDS];
+  unsigned cnt[K1_ROUNDS];
+  bool bad = false;
 #pragma unroll
-  for (int j = 0; j < K1_ITEMS; ++j) {
-    const long long i = first + j;
-    box[j] = make_uint3(0u, 1u, 1u);
-    cnt[j] = 0;
-    if (i < n) {
-      const int t0 = __ldg(T + 3 * i), t1 = __ldg(T + 3 * i + 1), t2 = __ldg(T + 3 * i + 2);
-      bool keep = true;
-      unsigned lo[3], hi[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const double a = __ldg(V + 3 * (long long)t0 + k);
-        const double b = __ldg(V + 3 * (long long)t1 + k);
-        const double c = __ldg(V + 3 * (long long)t2 + k);
-        // np.min/np.max propagate NaN, which fails both comparisons (gridcore.py:156-159);
-        // fmin/fmax do not, so NaN is folded into keep explicitly.
-        const bool nan = isnan(a) | isnan(b) | isnan(c);
-        const double mn = fmin(fmin(a, b), c);
-        const double mx = fmax(fmax(a, b), c);
-        keep &= !nan && (mx >= s.lo[k]) && (mn <= s.hi[k]);
-        const double ql = __ddiv_rn(__dsub_rn(mn, s.lo[k]), s.cell[k]);
-        const double qh = __ddiv_rn(__dsub_rn(mx, s.lo[k]), s.cell[k]);
-        lo[k] = clip_axis(np_floor_i64(ql), s.dims[k]);
-        hi[k] = clip_axis(np_floor_i64(qh), s.dims[k]);
-      }
-      if (keep && (hi[0] < lo[0] || hi[1] < lo[1] || hi[2] < lo[2])) {
-        // +inf / >2^63 upper corners cast to INT64_MIN and clip to 0 below lo: the reference
-        // then fails its non-negative / coincident-mark checks (primitives.py:22-25, 71-72).
-        atomicOr(err, 1u);
-        keep = false;
-      }
-      if (keep) {
-        const unsigned ex = hi[0] - lo[0] + 1, ey = hi[1] - lo[1] + 1, ez = hi[2] - lo[2] + 1;
-        box[j] = make_uint3(lo[0] + dx * lo[1] + dxy * lo[2], ex, ey);
-        cnt[j] = ex * ey * ez;  // <= ncells <= 2^30
+  for (int r = 0; r < K1_ROUNDS; ++r) {
+    const int i = r * K1_THREADS + tid;  // striped: coalesced record stores
+    box[r] = make_uint3(0u, 1u, 1u);
+    cnt[r] = 0;
+    if (i < tcount) {
+      if (soup) {
+        const double* p = sm.v + 9 * i;
+        tri_box(p, p + 3, p + 6, s, dx, dxy, box[r], cnt[r], bad);
+      } else {
+        tri_box(V + 3 * (long long)sm.t[3 * i], V + 3 * (long long)sm.t[3 * i + 1], V + 3 * (long long)sm.t[3 * i + 2],
+                s, dx, dxy, box[r], cnt[r], bad);
       }
     }
   }
-  // block-wide exclusive scan of the counts (blocked arrangement keeps triangle order)
-  unsigned long long tsum = 0;
+  if (bad) atomicOr(err, 1u);
+  // block-wide exclusive scan in triangle order (round-major, then thread)
+  __shared__ unsigned long long rtot[K1_ROUNDS * (K1_THREADS / 32)];
+  unsigned long long incl[K1_ROUNDS];
 #pragma unroll
-  for (int j = 0; j < K1_ITEMS; ++j) tsum += cnt[j];
-  unsigned long long incl = tsum;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += o;
-  }
-  if (lane == 31) sh_warp[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    unsigned long long w = lane < K1_THREADS / 32 ? sh_warp[lane] : 0ull;
-    unsigned long long wi = w;
+  for (int r = 0; r < K1_ROUNDS; ++r) {
+    unsigned long long v = cnt[r];
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const unsigned long long o = __shfl_up_sync(0xffffffffu, wi, d);
-      if (lane >= d) wi += o;
+      const unsigned long long o = __shfl_up_sync(0xffffffffu, v, d);
+      if (lane >= d) v += o;
     }
-    const unsigned long long aggregate = __shfl_sync(0xffffffffu, wi, K1_THREADS / 32 - 1);
-    if (lane < K1_THREADS / 32) sh_warp[lane] = wi - w;  // exclusive warp prefix
-    // decoupled look-back (one warp, 32 predecessors per round)
-    unsigned long long excl = 0;
-    if (tile == 0) {
-      if (lane == 0) st_relaxed_u64(status, LB_PREFIX | aggregate);
-    } else {
-      if (lane == 0) st_relaxed_u64(status + tile, LB_AGG | aggregate);
-      long long pred = (long long)tile - 1 - lane;
-      while (true) {
-        unsigned long long v = pred >= 0 ? ld_relaxed_u64(status + pred) : LB_PREFIX;
-        while (__any_sync(0xffffffffu, (v >> 62) == 0)) {
-          if ((v >> 62) == 0) v = ld_relaxed_u64(status + pred);
-        }
-        const unsigned pmask = __ballot_sync(0xffffffffu, (v >> 62) == 2);
-        const int stop = pmask ? __ffs(pmask) - 1 : 31;
-        unsigned long long contrib = lane <= stop ? (v & LB_VALUE) : 0ull;
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, d);
-        excl += contrib;
-        if (pmask) break;
-        pred -= 32;
-      }
-      if (lane == 0) st_relaxed_u64(status + tile, LB_PREFIX | (excl + aggregate));
-    }
-    if (lane == 0) {
-      sh_excl = excl;
-      if (tile == ntiles - 1) *total = excl + aggregate;
-    }
+    incl[r] = v;
+    if (lane == 31) rtot[r * (K1_THREADS / 32) + warp] = v;
   }
   __syncthreads();
-  unsigned long long off = sh_excl + sh_warp[warp] + (incl - tsum);
+  if (warp == 0) {
+    constexpr int NE = K1_ROUNDS * (K1_THREADS / 32);
+    const unsigned long long e = lane < NE ? rtot[lane] : 0ull;
+    unsigned long long ei = e;
 #pragma unroll
-  for (int j = 0; j < K1_ITEMS; ++j) {
-    const long long i = first + j;
-    if (i < n) rec[i] = make_uint4(box[j].x, box[j].y, box[j].z, (unsigned)off);
-    off += cnt[j];
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long o = __shfl_up_sync(0xffffffffu, ei, d);
+      if (lane >= d) ei += o;
+    }
+    if (lane < NE) rtot[lane] = ei - e;
+    if (lane == NE - 1) tile_sum[tile] = ei;
   }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < K1_ROUNDS; ++r) {
+    const int i = r * K1_THREADS + tid;
+    if (i < tcount) {
+      const unsigned long long off = rtot[r * (K1_THREADS / 32) + warp] + incl[r] - cnt[r];
+      rec[tbase + i] = make_uint4(box[r].x, box[r].y, box[r].z, (unsigned)off);
+    }
+  }
+}
+
+// K1b: exclusive scan of the per-tile pair counts (one CTA) -> tile_pre (u32; only used once
+// NO <= 2^30 is established) and the total NO (u64, exact).
+constexpr int TS_THREADS = 1024;
+__global__ void __launch_bounds__(TS_THREADS)
+k_scan_tile_sums(const unsigned long long* __restrict__ tile_sum, unsigned ntiles, unsigned* __restrict__ tile_pre,
+                 unsigned long long* __restrict__ total) {
+  __shared__ unsigned long long wsum[TS_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned per = (ntiles + TS_THREADS - 1) / TS_THREADS;
+  const unsigned i0 = tid * per, i1 = min(i0 + per, ntiles);
+  unsigned long long run = 0;
+  for (unsigned i = i0; i < i1; ++i) run += tile_sum[i];
+  unsigned long long inc = run;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  unsigned long long add = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < TS_THREADS / 32; ++w) {
+    add += w < warp ? wsum[w] : 0ull;
+    tot += wsum[w];
+  }
+  unsigned long long acc = add + inc - run;
+  for (unsigned i = i0; i < i1; ++i) {
+    tile_pre[i] = (unsigned)acc;
+    acc += tile_sum[i];
+  }
+  if (tid == 0) *total = tot;
+}
+
+// absolute pair offset of triangle o (K1 tiles of K1_TILE triangles)
+__device__ __forceinline__ unsigned tri_offset(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre,
+                                               long long o) {
+  return __ldg(&tile_pre[o / K1_TILE]) + __ldg(&rec[o].w);
 }
 
 // ----------------------------------------------------------------------------------------
@@ -261,8 +350,9 @@ struct ObjCache {
 // _make_cell_ids (builders.py:111-113) only ever run for a thread's first pair.
 template <int THREADS, int ITEMS>
 __device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long long n, unsigned p0, unsigned pend,
-                                            unsigned dx, unsigned dxy, const int2* __restrict__ bounds, int* slot,
-                                            int* warpmax, ObjCache* oc, unsigned (&key)[ITEMS], int (&own)[ITEMS]) {
+                                            unsigned dx, unsigned dxy, const unsigned* __restrict__ tile_pre,
+                                            const int2* __restrict__ bounds, int* slot, int* warpmax, ObjCache* oc,
+                                            unsigned (&key)[ITEMS], int (&own)[ITEMS]) {
   constexpr int TILE = THREADS * ITEMS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // [olo, oend): owner of pair p0, and one past the last triangle whose run starts in the tile
@@ -282,7 +372,8 @@ __device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long 
 #pragma unroll 4
   for (long long o = olo + 1 + tid; o < oend; o += THREADS) {
     const uint4 r = __ldg(&rec[o]);
-    atomicMax(&slot[r.w - p0], (int)o);  // zero-count triangles share the next start; max wins
+    const unsigned off = __ldg(&tile_pre[o / K1_TILE]) + r.w;
+    atomicMax(&slot[off - p0], (int)o);  // zero-count triangles share the next start; max wins
     const long long ci = o - olo;
     if (ci < OC_CAP) {
       oc->lo_cell[ci] = r.x;
@@ -332,7 +423,7 @@ __device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long 
   const unsigned pbase = p0 + (unsigned)tid * ITEMS;
   unsigned cell = 0, x = 0, y = 0, mx = 1, my = 1;
   if (pbase < pend) {  // first pair: may sit anywhere inside its run
-    const unsigned rel = pbase - __ldg(&rec[own[0]].w);
+    const unsigned rel = pbase - tri_offset(rec, tile_pre, own[0]);
     unsigned lc;
     box(own[0], lc, mx, my);
     if (rel == 0) {
@@ -369,18 +460,28 @@ __device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long 
   }
 }
 
+// record= stage 0: records with absolute pair offsets
+__global__ void k_abs_offsets(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n,
+                              uint4* __restrict__ out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    uint4 r = rec[i];
+    r.w += tile_pre[i / K1_TILE];
+    out[i] = r;
+  }
+}
+
 // Tile bounds of the pair expansion, one warp per tile: x = owner of the tile's first pair
 // ((#triangles with offset <= p0) - 1), y = one past the last triangle whose run starts
 // inside the tile (#triangles with offset < pend). Hoisting these searches out of the
 // expansion kernels keeps their CTAs from idling on dependent round trips at launch.
 __global__ void __launch_bounds__(256)
-k_pair_tile_bounds(const uint4* __restrict__ rec, long long n, unsigned no, unsigned tile, unsigned ntiles,
-                   int2* __restrict__ bounds) {
+k_pair_tile_bounds(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, unsigned no,
+                   unsigned tile, unsigned ntiles, int2* __restrict__ bounds) {
   const unsigned t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= ntiles) return;
   const unsigned p0 = t * tile;
   const unsigned pend = min(p0 + tile, no);
-  auto ld = [&](unsigned long long i) { return (unsigned long long)__ldg(&rec[i].w); };
+  auto ld = [&](unsigned long long i) { return (unsigned long long)tri_offset(rec, tile_pre, i); };
   const unsigned long long a = warp_lower_bound((unsigned long long)n, (unsigned long long)p0 + 1, ld);
   const unsigned long long b = warp_lower_bound((unsigned long long)n, (unsigned long long)pend, ld);
   if ((threadIdx.x & 31) == 0) bounds[t] = make_int2((int)a - 1, (int)b);
@@ -401,8 +502,9 @@ k_key_tile_bounds(const unsigned* __restrict__ sorted, unsigned no, unsigned ste
 // Pairs in generation (object-major) order -- used when no radix pass follows
 // (ncells == 1) and for the record= stage dumps.
 __global__ void __launch_bounds__(K2_THREADS)
-k_expand_pairs(const uint4* __restrict__ rec, long long n, unsigned no, unsigned dx, unsigned dxy,
-               const int2* __restrict__ bounds, unsigned* __restrict__ keys, unsigned* __restrict__ vals) {
+k_expand_pairs(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, unsigned no,
+               unsigned dx, unsigned dxy, const int2* __restrict__ bounds, unsigned* __restrict__ keys,
+               unsigned* __restrict__ vals) {
   __shared__ __align__(16) int slot[K2_TILE];
   __shared__ int warpmax[K2_THREADS / 32];
   __shared__ ObjCache oc;
@@ -410,7 +512,7 @@ k_expand_pairs(const uint4* __restrict__ rec, long long n, unsigned no, unsigned
   const unsigned pend = min(p0 + (unsigned)K2_TILE, no);
   unsigned key[K2_ITEMS];
   int own[K2_ITEMS];
-  expand_tile<K2_THREADS, K2_ITEMS>(rec, n, p0, pend, dx, dxy, bounds, slot, warpmax, &oc, key, own);
+  expand_tile<K2_THREADS, K2_ITEMS>(rec, n, p0, pend, dx, dxy, tile_pre, bounds, slot, warpmax, &oc, key, own);
   const unsigned pbase = p0 + threadIdx.x * K2_ITEMS;
   if (pbase + K2_ITEMS <= pend) {
     uint4* kd = reinterpret_cast<uint4*>(keys + pbase);
@@ -747,8 +849,8 @@ struct PeSmem {
 };
 
 __global__ void __launch_bounds__(RS_THREADS)
-k_pairs_emit(const uint4* __restrict__ rec, long long n, unsigned no, unsigned dx, unsigned dxy, PassPlan plan,
-             const int2* __restrict__ bounds, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
+k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, unsigned no,
+             unsigned dx, unsigned dxy, PassPlan plan, const int2* __restrict__ bounds, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
              unsigned* __restrict__ counts0, unsigned ld, unsigned* __restrict__ hist) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PeSmem& sm = *reinterpret_cast<PeSmem*>(smem_raw);
@@ -758,7 +860,7 @@ k_pairs_emit(const uint4* __restrict__ rec, long long n, unsigned no, unsigned d
   for (int b = tid; b < kMaxPasses * kMaxBins; b += RS_THREADS) sm.h[b] = 0u;
   unsigned key[RS_ITEMS];
   int own[RS_ITEMS];
-  expand_tile<RS_THREADS, RS_ITEMS>(rec, n, p0, pend, dx, dxy, bounds, sm.slot, sm.warpmax, &sm.oc, key, own);
+  expand_tile<RS_THREADS, RS_ITEMS>(rec, n, p0, pend, dx, dxy, tile_pre, bounds, sm.slot, sm.warpmax, &sm.oc, key, own);
   const unsigned pbase = p0 + (unsigned)tid * RS_ITEMS;
   const int nvalid = pend > pbase ? (int)min((unsigned)RS_ITEMS, pend - pbase) : 0;
   if (nvalid == RS_ITEMS) {

@@ -192,5 +192,5 @@ def test_launch_count_is_native():
     b = _native.thread_builder()
     nbits = int(spec.ncells - 1).bit_length()
     passes = (nbits + 8) // 9                         # 9-bit digits
-    # K1, tile bounds, K4 + its bounds, and count/scan/scatter per pass (pass 0 fused with K2)
-    assert b.launches() == 4 + 3 * passes
+    # K1 (+ tile scan), tile bounds, K4 + its bounds, and count/scan/scatter per pass (pass 0 counted by K2)
+    assert b.launches() == 5 + 3 * passes
