@@ -325,7 +325,7 @@ int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned
       LAUNCHED("k_tile_counts", st);
       ++b->launches;
     }
-    k_scan_tile_counts<<<1u << plan.bits[p], SC_THREADS, 0, st>>>(counts, ntiles, ld);
+    k_scan_tile_counts<<<1u << plan.bits[p], SC_THREADS, 0, st>>>(counts, ntiles, ld, hist + p * kMaxBins);
     LAUNCHED("k_scan_tile_counts", st);
     launch_radix_scatter(plan.bits[p], ntiles, st, kin, vin, ko, vo, (unsigned)n, plan.shift[p], hist + p * kMaxBins,
                          counts, ld);
@@ -400,13 +400,12 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
       }
     }
     if (plan.npasses > 0) {
-      // K2 on radix tiles: pairs in generation order + first-pass tile counts + histograms
+      // K2 on radix tiles: pairs in generation order + first-pass tile counts
       k_pair_tile_bounds<<<(rs_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no,
                                                             RS_TILE, rs_tiles, pbounds);
       LAUNCHED("k_pair_tile_bounds", st);
       k_pairs_emit<<<rs_tiles, RS_THREADS, sizeof(PeSmem), st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no,
-                                                                 dxu, dxyu, plan, pbounds, keysA, valsA, counts, ld,
-                                                                 hist);
+                                                                 dxu, dxyu, plan, pbounds, keysA, valsA, counts, ld);
       LAUNCHED("k_pairs_emit", st);
       b->launches += 2;
       CU(cudaEventRecord(b->ev[1], st));
@@ -442,7 +441,7 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
     if (b->k1_timed) CU(cudaEventElapsedTime(&t_k1, b->ev[5], b->ev[6]));
     phase_ms[0] = t_k1;  // count: K1 device time (callers add their H2D / readback around it)
     phase_ms[1] = 0.f;  // scan: fused into count (K1)
-    phase_ms[2] = t01;  // pairgen: K2 (+ histograms)
+    phase_ms[2] = t01;  // pairgen: tile bounds + K2 (+ first-pass tile counts)
     phase_ms[3] = t12;  // sort: onesweep passes
     phase_ms[4] = 0.f;  // rle: fused into finalize (K4)
     phase_ms[5] = t23 + t34;  // finalize: K4 (+ D2H of G/O for host outputs)
@@ -515,9 +514,6 @@ int pg_radix_sort_pairs(pg_builder* b, const uint32_t* keys, const uint32_t* val
   const unsigned* sorted = kA;
   unsigned* vfinal = vA;
   if (plan.npasses > 0) {
-    k_digit_hist<<<std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(kA, n, plan, hist);
-    LAUNCHED("k_digit_hist", st);
-    ++b->launches;
     // host outputs: final values land in the staging section behind the pair buffers
     if ((rc = b->stage.ensure(sec))) return rc;
     unsigned* vdst = (flags & PG_HOST_OUTPUT) ? b->stage.as<unsigned>() : vals_out;

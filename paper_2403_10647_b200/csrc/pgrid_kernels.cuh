@@ -284,33 +284,38 @@ k_boxes_count(const double* __restrict__ V, long long nv, const int* __restrict_
 // K1b: exclusive scan of the per-tile pair counts (one CTA) -> tile_pre (u32; only used once
 // NO <= 2^30 is established) and the total NO (u64, exact).
 constexpr int TS_THREADS = 1024;
+constexpr int TS_WARPS = TS_THREADS / 32;
 __global__ void __launch_bounds__(TS_THREADS)
 k_scan_tile_sums(const unsigned long long* __restrict__ tile_sum, unsigned ntiles, unsigned* __restrict__ tile_pre,
                  unsigned long long* __restrict__ total) {
-  __shared__ unsigned long long wsum[TS_THREADS / 32];
+  __shared__ unsigned long long wsum[TS_WARPS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned per = (ntiles + TS_THREADS - 1) / TS_THREADS;
-  const unsigned i0 = tid * per, i1 = min(i0 + per, ntiles);
-  unsigned long long run = 0;
-  for (unsigned i = i0; i < i1; ++i) run += tile_sum[i];
-  unsigned long long inc = run;
+  // warp w owns the contiguous segment [w*seg, (w+1)*seg), read in coalesced 32-wide chunks
+  const unsigned seg = ((ntiles + TS_WARPS - 1) / TS_WARPS + 31) & ~31u;
+  const unsigned s0 = min((unsigned)warp * seg, ntiles), s1 = min(s0 + seg, ntiles);
+  unsigned long long part = 0;
+#pragma unroll 4
+  for (unsigned i = s0 + lane; i < s1; i += 32) part += tile_sum[i];
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const unsigned long long o = __shfl_up_sync(0xffffffffu, inc, d);
-    if (lane >= d) inc += o;
-  }
-  if (lane == 31) wsum[warp] = inc;
+  for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
+  if (lane == 0) wsum[warp] = part;
   __syncthreads();
-  unsigned long long add = 0, tot = 0;
-#pragma unroll
-  for (int w = 0; w < TS_THREADS / 32; ++w) {
-    add += w < warp ? wsum[w] : 0ull;
+  unsigned long long carry = 0, tot = 0;
+  for (int w = 0; w < TS_WARPS; ++w) {
+    carry += w < warp ? wsum[w] : 0ull;
     tot += wsum[w];
   }
-  unsigned long long acc = add + inc - run;
-  for (unsigned i = i0; i < i1; ++i) {
-    tile_pre[i] = (unsigned)acc;
-    acc += tile_sum[i];
+  for (unsigned c = s0; c < s1; c += 32) {
+    const unsigned i = c + lane;
+    const unsigned long long v = i < s1 ? tile_sum[i] : 0ull;
+    unsigned long long inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long o = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += o;
+    }
+    if (i < s1) tile_pre[i] = (unsigned)(carry + inc - v);
+    carry += __shfl_sync(0xffffffffu, inc, 31);
   }
   if (tid == 0) *total = tot;
 }
@@ -643,7 +648,7 @@ constexpr int SC_ITEMS = 8;
 // Rows are padded to a multiple of 4 (ld) so each thread moves its 8 entries as two 16-byte
 // accesses; one iteration covers 8192 tiles (33.5M pairs).
 __global__ void __launch_bounds__(SC_THREADS)
-k_scan_tile_counts(unsigned* __restrict__ counts, unsigned ntiles, unsigned ld) {
+k_scan_tile_counts(unsigned* __restrict__ counts, unsigned ntiles, unsigned ld, unsigned* __restrict__ row_total) {
   __shared__ unsigned wsum[SC_THREADS / 32];
   const int tid = threadIdx.x;
   unsigned* row = counts + (size_t)blockIdx.x * ld;
@@ -681,6 +686,7 @@ k_scan_tile_counts(unsigned* __restrict__ counts, unsigned ntiles, unsigned ld) 
     }
     carry += total;
   }
+  if (tid == 0) row_total[blockIdx.x] = carry;  // the global count of this digit (its histogram bin)
 }
 
 // Scatter one tile of a digit pass. Item j of lane l of warp w is tile element
@@ -839,11 +845,11 @@ k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict
 // K2: pair expansion on radix-sort tiles. Each CTA expands RS_TILE pairs, writes them in
 // generation (object-major) order with 16-byte stores, and counts the tile's first-pass
 // digits (the per-tile counts the first radix pass needs, so that pass skips its own
-// upsweep) plus the global digit histograms of every pass.
+// upsweep; the row scan turns them into the global histogram too).
 // ----------------------------------------------------------------------------------------
 struct PeSmem {
   int slot[RS_TILE];
-  unsigned h[kMaxPasses * kMaxBins];
+  unsigned h[kMaxBins];
   ObjCache oc;
   int warpmax[RS_WARPS];
 };
@@ -851,13 +857,13 @@ struct PeSmem {
 __global__ void __launch_bounds__(RS_THREADS)
 k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, unsigned no,
              unsigned dx, unsigned dxy, PassPlan plan, const int2* __restrict__ bounds, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
-             unsigned* __restrict__ counts0, unsigned ld, unsigned* __restrict__ hist) {
+             unsigned* __restrict__ counts0, unsigned ld) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PeSmem& sm = *reinterpret_cast<PeSmem*>(smem_raw);
   const int tid = threadIdx.x;
   const unsigned p0 = blockIdx.x * (unsigned)RS_TILE;
   const unsigned pend = min(p0 + (unsigned)RS_TILE, no);
-  for (int b = tid; b < kMaxPasses * kMaxBins; b += RS_THREADS) sm.h[b] = 0u;
+  for (int b = tid; b < kMaxBins; b += RS_THREADS) sm.h[b] = 0u;
   unsigned key[RS_ITEMS];
   int own[RS_ITEMS];
   expand_tile<RS_THREADS, RS_ITEMS>(rec, n, p0, pend, dx, dxy, tile_pre, bounds, sm.slot, sm.warpmax, &sm.oc, key, own);
@@ -886,31 +892,8 @@ k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pr
     for (int j = 0; j < RS_ITEMS; ++j)
       if (j < nvalid) atomicAdd(&sm.h[(key[j] >> sh) & mask], 1u);
   }
-#pragma unroll
-  for (int ps = 1; ps < kMaxPasses; ++ps) {  // higher digits: run-length aggregated in registers
-    if (ps < plan.npasses) {
-      const int sh = plan.shift[ps];
-      const unsigned mask = (1u << plan.bits[ps]) - 1u;
-      unsigned cur = (key[0] >> sh) & mask, cnt = 0;
-#pragma unroll
-      for (int j = 0; j < RS_ITEMS; ++j) {
-        if (j < nvalid) {
-          const unsigned d = (key[j] >> sh) & mask;
-          if (d != cur) {
-            atomicAdd(&sm.h[ps * kMaxBins + cur], cnt);
-            cur = d;
-            cnt = 0;
-          }
-          ++cnt;
-        }
-      }
-      if (cnt) atomicAdd(&sm.h[ps * kMaxBins + cur], cnt);
-    }
-  }
   __syncthreads();
   for (int b = tid; b < (1 << plan.bits[0]); b += RS_THREADS) counts0[(size_t)b * ld + blockIdx.x] = sm.h[b];
-  for (int b = tid; b < plan.npasses * kMaxBins; b += RS_THREADS)
-    if (sm.h[b]) atomicAdd(&hist[b], sm.h[b]);
 }
 
 // ----------------------------------------------------------------------------------------
@@ -933,11 +916,27 @@ k_cell_offsets(const unsigned* __restrict__ sorted, unsigned no, unsigned ncells
   const unsigned c0 = blockIdx.x * (unsigned)G_TILE;
   const unsigned c1 = min(c0 + (unsigned)G_TILE, ncells);
   const unsigned i0 = __ldg(&kb[blockIdx.x]), i1 = __ldg(&kb[blockIdx.x + 1]);  // k_key_tile_bounds
-  for (int i = tid; i < G_TILE; i += G_THREADS) mark[i] = 0xffffffffu;
+#pragma unroll
+  for (int q = 0; q < G_TILE / 4 / G_THREADS; ++q)
+    reinterpret_cast<uint4*>(mark)[tid + q * G_THREADS] = make_uint4(~0u, ~0u, ~0u, ~0u);
   __syncthreads();
-  for (unsigned i = i0 + tid; i < i1; i += G_THREADS) {
-    const unsigned k = __ldg(sorted + i);
-    if (i == 0 || __ldg(sorted + i - 1) != k) mark[k - c0] = i;
+  // first occurrences: 4 independent coalesced loads per thread per chunk; the predecessor
+  // key comes from the neighbouring lane (lane 0 loads it)
+  for (unsigned base = i0; base < i1; base += 4 * G_THREADS) {
+    unsigned k[4], pk[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const unsigned i = base + j * G_THREADS + tid;
+      k[j] = i < i1 ? __ldg(sorted + i) : 0xffffffffu;
+      pk[j] = (lane == 0 && i < i1 && i > 0) ? __ldg(sorted + i - 1) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const unsigned i = base + j * G_THREADS + tid;
+      const unsigned up = __shfl_up_sync(0xffffffffu, k[j], 1);
+      const unsigned prev = lane == 0 ? pk[j] : up;
+      if (i < i1 && (i == 0 || prev != k[j])) mark[k[j] - c0] = i;
+    }
   }
   __syncthreads();
   // block suffix-min (thread t owns cells [16t, 16t+16))
