@@ -57,9 +57,10 @@ typedef struct pg_builder pg_builder;
 int  pg_builder_create(int device, pg_builder **out);
 void pg_builder_destroy(pg_builder *b);
 
-/* Phase 1 of build_parallel: triangle AABB -> clamped cell box -> CountCells, fused with
- * the decoupled-look-back ExclusiveSum (builders.py:90-101, gridcore.py:145-167).
- * V: f64[nv*3] row-major vertices; T: i32[n*3] triangle vertex indices (geometry.py:33-45).
+/* Phase 1 of build_parallel: triangle AABB -> clamped cell box -> CountCells with the tile-
+ * local part of the ExclusiveSum, then the cross-tile scan (builders.py:90-101,
+ * gridcore.py:145-167). V: f64[nv*3] row-major vertices; T: i32[n*3] triangle vertex
+ * indices (geometry.py:33-45), validated on the device (InvariantError when out of range).
  * Returns NO (number of <cell, object> pairs) in *no_out after one device->host readback.
  * SizeError conditions are detected here (NO > 2^32-1, NO > 2^30, ncells > 2^30, n > 2^30). */
 int pg_count(pg_builder *b, const double *V, int64_t nv, const int32_t *T, int64_t n,
@@ -89,6 +90,9 @@ int pg_radix_sort_pairs(pg_builder *b, const uint32_t *keys, const uint32_t *val
 /* Page-lock host memory so PG_HOST_* copies run at full PCIe rate (optional). */
 int pg_host_register(void *ptr, uint64_t bytes);
 int pg_host_unregister(void *ptr);
+/* Page-locked host allocations (the Python side pools them for G/O outputs). */
+int pg_host_alloc(uint64_t bytes, void **out);
+int pg_host_free(void *ptr);
 
 /* Number of device kernel launches issued by the last pg_count + pg_finish pair. */
 int pg_last_launch_count(pg_builder *b);

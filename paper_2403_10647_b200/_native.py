@@ -29,8 +29,8 @@ NPHASES = 6
 
 # every symbol include/pgrid.h declares (checked by tests/test_boundary.py)
 EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
-           "pg_radix_sort_pairs", "pg_host_register", "pg_host_unregister",
-           "pg_last_launch_count", "pg_last_error")
+           "pg_radix_sort_pairs", "pg_host_register", "pg_host_unregister", "pg_host_alloc",
+           "pg_host_free", "pg_last_launch_count", "pg_last_error")
 
 
 class PgSpec(ctypes.Structure):
@@ -78,11 +78,13 @@ def load():
         lib.pg_radix_sort_pairs.argtypes = [vp, vp, vp, vp, vp, i64, ctypes.c_int, u32, vp]
         lib.pg_host_register.argtypes = [vp, u64]
         lib.pg_host_unregister.argtypes = [vp]
+        lib.pg_host_alloc.argtypes = [u64, ctypes.POINTER(vp)]
+        lib.pg_host_free.argtypes = [vp]
         lib.pg_last_launch_count.argtypes = [vp]
         lib.pg_last_error.restype = ctypes.c_char_p
         for name in ("pg_builder_create", "pg_count", "pg_finish", "pg_stage",
                      "pg_radix_sort_pairs", "pg_host_register", "pg_host_unregister",
-                     "pg_last_launch_count"):
+                     "pg_host_alloc", "pg_host_free", "pg_last_launch_count"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -175,3 +177,60 @@ def host_register(a):
 
 def host_unregister(a):
     check(load().pg_host_unregister(ptr(a)))
+
+
+class _PinnedBlock:
+    """One page-locked allocation; returns itself to the pool when the last array view of it
+    is garbage-collected."""
+
+    __slots__ = ("ptr", "nbytes", "pool", "__weakref__")
+
+    def __init__(self, ptr, nbytes, pool):
+        self.ptr, self.nbytes, self.pool = ptr, nbytes, pool
+
+    def __del__(self):
+        try:
+            self.pool._release(self)
+        except Exception:
+            pass
+
+
+class PinnedPool:
+    """Caching allocator of page-locked host memory for device->host outputs (G and O).
+
+    Outputs in pageable numpy memory copy at ~5 GB/s; page-locked ones at PCIe rate. Blocks
+    are recycled once the caller drops every array that views them, so steady-state builds
+    allocate nothing. Arrays handed out are ordinary numpy arrays."""
+
+    def __init__(self):
+        self._free = {}   # nbytes -> [ptr]
+        self._lock = threading.Lock()
+
+    @staticmethod
+    def _bucket(nbytes):
+        return max(4096, 1 << (int(nbytes) - 1).bit_length())
+
+    def empty(self, count, dtype=np.uint32):
+        dtype = np.dtype(dtype)
+        nbytes = int(count) * dtype.itemsize
+        if nbytes == 0:
+            return np.empty(count, dtype)
+        size = self._bucket(nbytes)
+        with self._lock:
+            lst = self._free.get(size)
+            ptr = lst.pop() if lst else None
+        if ptr is None:
+            out = ctypes.c_void_p()
+            check(load().pg_host_alloc(size, ctypes.byref(out)))
+            ptr = out.value
+        block = _PinnedBlock(ptr, size, self)
+        buf = (ctypes.c_uint8 * size).from_address(ptr)
+        buf._pg_block = block   # keeps the block alive while any view exists
+        return np.frombuffer(buf, dtype=dtype, count=int(count))
+
+    def _release(self, block):
+        with self._lock:
+            self._free.setdefault(block.nbytes, []).append(block.ptr)
+
+
+pinned_pool = PinnedPool()

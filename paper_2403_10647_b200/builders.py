@@ -16,7 +16,6 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native
-from .errors import InvariantError
 from .gridcore import CompactGrid
 
 PHASES = ("count", "scan", "pairgen", "sort", "rle", "finalize")   # builders.py:19
@@ -41,10 +40,9 @@ class BuildReport:
 
 
 def _mesh_arrays(mesh):
+    # index range validity (geometry.py:41-43) is checked on the device by K1
     V = np.ascontiguousarray(mesh.vertices, dtype=np.float64).reshape(-1, 3)
     T = np.ascontiguousarray(mesh.triangles, dtype=np.int32).reshape(-1, 3)
-    if T.size and (T.min() < 0 or T.max() >= len(V)):
-        raise InvariantError("triangle index out of range")
     return V, T
 
 
@@ -93,8 +91,9 @@ def build_parallel(mesh, spec, workers=None, record=None, device=0):
     no = b.count(V, len(V), T, n, spec, flags=_native.PG_HOST_INPUT)
     ms["count"] = (time.perf_counter() - t0) * 1e3
     ncells = int(spec.dims[0]) * int(spec.dims[1]) * int(spec.dims[2])
-    G = np.empty(ncells + 1, np.uint32)
-    O = np.empty(no, np.uint32)
+    # page-locked outputs (recycled once the caller drops them): D2H at PCIe rate
+    G = _native.pinned_pool.empty(ncells + 1, np.uint32)
+    O = _native.pinned_pool.empty(no, np.uint32)
     flags = _native.PG_HOST_OUTPUT | (_native.PG_KEEP_STAGES if record is not None else 0)
     phases = b.finish(G, O, flags=flags)
     for name, v in zip(PHASES, phases):

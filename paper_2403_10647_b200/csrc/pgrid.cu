@@ -204,6 +204,19 @@ int pg_host_register(void* ptr, uint64_t bytes) {
   return PG_OK;
 }
 
+int pg_host_alloc(uint64_t bytes, void** out) {
+  if (!out) return fail(PG_INVARIANT_ERROR, "null out pointer");
+  *out = nullptr;
+  if (!bytes) return PG_OK;
+  CU(cudaHostAlloc(out, bytes, cudaHostAllocDefault));
+  return PG_OK;
+}
+
+int pg_host_free(void* ptr) {
+  if (ptr) CU(cudaFreeHost(ptr));
+  return PG_OK;
+}
+
 int pg_host_unregister(void* ptr) {
   if (!ptr) return PG_OK;
   CU(cudaHostUnregister(ptr));
@@ -293,7 +306,8 @@ int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64
   const uint64_t no = b->h_scalars[0];
   const unsigned errf = (unsigned)(b->h_scalars[1] & 0xffffffffu);
   *no_out = no;
-  if (errf) return fail(PG_INVARIANT_ERROR, "triangle cell box with hi < lo (non-finite or huge upper corner)");
+  if (errf & 2u) return fail(PG_INVARIANT_ERROR, "triangle index out of range");
+  if (errf & 1u) return fail(PG_INVARIANT_ERROR, "triangle cell box with hi < lo (non-finite or huge upper corner)");
   if ((int64_t)no > kMaxIds) return fail(PG_SIZE_ERROR, "%llu cell/object pairs exceed 32-bit id space", (unsigned long long)no);
   if ((int64_t)no > kMaxScan) return fail(PG_SIZE_ERROR, "array of %llu elements exceeds the scan size limit", (unsigned long long)no);
   b->no = no;

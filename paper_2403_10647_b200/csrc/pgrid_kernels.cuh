@@ -218,10 +218,19 @@ k_boxes_count(const double* __restrict__ V, long long nv, const int* __restrict_
     for (int q = tid; q < 3 * tcount; q += K1_THREADS) sm.t[q] = __ldg(T + 3 * tbase + q);
     __syncthreads();
   }
-  // soup test over the whole tile: index 3*i+k == 3*(tbase+i)+k
-  bool mine = true;
-  for (int q = tid; q < 3 * tcount; q += K1_THREADS) mine &= sm.t[q] == (int)(3 * tbase + q);
+  // soup test over the whole tile (index 3*i+k == 3*(tbase+i)+k) and index validation
+  // (geometry.py:41-43: every index in [0, nv), else InvariantError)
+  bool mine = true, inrange = true;
+  for (int q = tid; q < 3 * tcount; q += K1_THREADS) {
+    const int v = sm.t[q];
+    mine &= v == (int)(3 * tbase + q);
+    inrange &= v >= 0 && (long long)v < nv;
+  }
   const bool soup = __syncthreads_and(mine) && spec_v;
+  if (!__syncthreads_and(inrange)) {
+    if (tid == 0) atomicOr(err, 2u);
+    return;  // never gather through an out-of-range index
+  }
 
   const unsigned dx = (unsigned)s.dims[0], dxy = (unsigned)s.dims[0] * (unsigned)s.dims[1];
   uint3 box[K1_ROUNDS];

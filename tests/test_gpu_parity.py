@@ -194,3 +194,31 @@ def test_launch_count_is_native():
     passes = (nbits + 8) // 9                         # 9-bit digits
     # K1 (+ tile scan), tile bounds, K4 + its bounds, and count/scan/scatter per pass (pass 0 counted by K2)
     assert b.launches() == 5 + 3 * passes
+
+
+def test_index_out_of_range_detected_on_device():
+    """geometry.py:41-43 raises InvariantError for bad indices; duck-typed meshes skip that
+    constructor, so K1 validates every index on the device."""
+    class RawMesh:
+        pass
+    m = RawMesh()
+    m.vertices = np.random.default_rng(1).random((30, 3))
+    m.triangles = np.array([[0, 1, 2], [3, 4, 30]], np.int32)
+    m.ntriangles = 2
+    spec = GridSpec(Aabb([0, 0, 0], [1, 1, 1]), (4, 4, 4))
+    with pytest.raises(InvariantError):
+        builders.build_parallel(m, spec)
+    m.triangles = np.array([[0, 1, -1]], np.int32)
+    with pytest.raises(InvariantError):
+        builders.build_parallel(m, spec)
+
+
+def test_pinned_outputs_are_recycled_and_independent():
+    mesh = gen_scene("uniform", 5000, 3)
+    spec = spec_for_mesh(mesh)
+    g1, _ = builders.build_parallel(mesh, spec)
+    keep = (g1.G.copy(), g1.O.copy())
+    g2, _ = builders.build_parallel(mesh, spec)       # g1 still alive: distinct buffers
+    assert np.array_equal(g1.G, keep[0]) and np.array_equal(g1.O, keep[1])
+    assert np.array_equal(g2.G, keep[0]) and np.array_equal(g2.O, keep[1])
+    assert g1.G.ctypes.data != g2.G.ctypes.data
