@@ -87,6 +87,23 @@ int pg_radix_sort_pairs(pg_builder *b, const uint32_t *keys, const uint32_t *val
                         uint32_t *keys_out, uint32_t *vals_out, int64_t n, int key_bits,
                         uint32_t flags, void *stream);
 
+/* Sharded (multi-GPU) building blocks, device pointers only:
+ *   pg_pairs      -- after pg_count on a triangle shard: its <cell, triangle> pairs in
+ *                    generation (object-major) order; triangle ids += val_offset (shard base)
+ *   pg_partition  -- stable partition of pairs into cell slabs: slab = slab_of_bucket[key >>
+ *                    bucket_shift] (nslabs <= 16); keys leave rebased by slab_base[slab];
+ *                    slab_counts (host) receives the pairs per slab
+ *   pg_sort_cells -- the Alg. 1 tail over arbitrary pairs with keys in [0, ncells): stable
+ *                    radix sort + RLE/scatter/scan into G[ncells+1], O[n]
+ *                    (builders.py:120-141) */
+int pg_pairs(pg_builder *b, uint32_t *keys, uint32_t *vals, uint32_t val_offset, void *stream);
+int pg_partition(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int64_t n,
+                 const uint32_t *slab_of_bucket, int bucket_shift, int nslabs,
+                 const uint32_t *slab_base, uint32_t *keys_out, uint32_t *vals_out,
+                 uint64_t *slab_counts, void *stream);
+int pg_sort_cells(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int64_t n,
+                  int64_t ncells, uint32_t *G, uint32_t *O, void *stream);
+
 /* Page-lock host memory so PG_HOST_* copies run at full PCIe rate (optional). */
 int pg_host_register(void *ptr, uint64_t bytes);
 int pg_host_unregister(void *ptr);

@@ -29,8 +29,9 @@ NPHASES = 6
 
 # every symbol include/pgrid.h declares (checked by tests/test_boundary.py)
 EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
-           "pg_radix_sort_pairs", "pg_host_register", "pg_host_unregister", "pg_host_alloc",
-           "pg_host_free", "pg_last_launch_count", "pg_last_error")
+           "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_host_register",
+           "pg_host_unregister", "pg_host_alloc", "pg_host_free", "pg_last_launch_count",
+           "pg_last_error")
 
 
 class PgSpec(ctypes.Structure):
@@ -76,6 +77,10 @@ def load():
         lib.pg_finish.argtypes = [vp, vp, vp, u32, vp, ctypes.POINTER(ctypes.c_float)]
         lib.pg_stage.argtypes = [vp, ctypes.c_int, vp, u32, vp]
         lib.pg_radix_sort_pairs.argtypes = [vp, vp, vp, vp, vp, i64, ctypes.c_int, u32, vp]
+        lib.pg_pairs.argtypes = [vp, vp, vp, u32, vp]
+        lib.pg_partition.argtypes = [vp, vp, vp, i64, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp,
+                                     ctypes.POINTER(u64), vp]
+        lib.pg_sort_cells.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp]
         lib.pg_host_register.argtypes = [vp, u64]
         lib.pg_host_unregister.argtypes = [vp]
         lib.pg_host_alloc.argtypes = [u64, ctypes.POINTER(vp)]
@@ -83,8 +88,9 @@ def load():
         lib.pg_last_launch_count.argtypes = [vp]
         lib.pg_last_error.restype = ctypes.c_char_p
         for name in ("pg_builder_create", "pg_count", "pg_finish", "pg_stage",
-                     "pg_radix_sort_pairs", "pg_host_register", "pg_host_unregister",
-                     "pg_host_alloc", "pg_host_free", "pg_last_launch_count"):
+                     "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells",
+                     "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
+                     "pg_last_launch_count"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -157,6 +163,22 @@ class Builder:
 
     def launches(self):
         return int(self._lib.pg_last_launch_count(self._h))
+
+    # sharded-build building blocks (device pointers)
+    def pairs(self, keys, vals, val_offset=0, stream=None):
+        check(self._lib.pg_pairs(self._h, ptr(keys), ptr(vals), int(val_offset), stream))
+
+    def partition(self, keys, vals, n, slab_of_bucket, bucket_shift, nslabs, slab_base, keys_out,
+                  vals_out, stream=None):
+        counts = (ctypes.c_uint64 * nslabs)()
+        check(self._lib.pg_partition(self._h, ptr(keys), ptr(vals), int(n), ptr(slab_of_bucket),
+                                     int(bucket_shift), int(nslabs), ptr(slab_base), ptr(keys_out),
+                                     ptr(vals_out), counts, stream))
+        return [int(c) for c in counts]
+
+    def sort_cells(self, keys, vals, n, ncells, G, O, stream=None):
+        check(self._lib.pg_sort_cells(self._h, ptr(keys), ptr(vals), int(n), int(ncells), ptr(G),
+                                      ptr(O), stream))
 
 
 _tls = threading.local()

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/pgrid.h"
 #include "pgrid_kernels.cuh"
@@ -95,19 +96,34 @@ int bit_length(uint64_t v) {
 
 size_t rs_smem_bytes() { return sizeof(RsSmem); }
 
-template <int BITS>
+template <int BITS, bool TABLE>
 void launch_scatter_bits(unsigned ntiles, cudaStream_t st, const unsigned* kin, const unsigned* vin, unsigned* ko,
-                         unsigned* vo, unsigned n, int shift, const unsigned* hist, const unsigned* offs, unsigned ld) {
-  k_radix_scatter<BITS><<<ntiles, RS_THREADS, rs_smem_bytes(), st>>>(kin, vin, ko, vo, n, shift, hist, offs, ld);
+                         unsigned* vo, unsigned n, int shift, const unsigned* hist, const unsigned* offs, unsigned ld,
+                         const unsigned* dtable, const unsigned* kbase) {
+  k_radix_scatter<BITS, TABLE><<<ntiles, RS_THREADS, rs_smem_bytes(), st>>>(kin, vin, ko, vo, n, shift, hist, offs,
+                                                                           ld, dtable, kbase);
 }
 
+// bit-field digits of 1..9 bits, or (dtable != null) slab-table digits of 1..4 bits
 void launch_radix_scatter(int bits, unsigned ntiles, cudaStream_t st, const unsigned* kin, const unsigned* vin,
                           unsigned* ko, unsigned* vo, unsigned n, int shift, const unsigned* hist,
-                          const unsigned* offs, unsigned ld) {
+                          const unsigned* offs, unsigned ld, const unsigned* dtable = nullptr,
+                          const unsigned* kbase = nullptr) {
+  if (dtable) {
+    switch (bits) {
+#define PG_CASE(B) \
+  case B:          \
+    launch_scatter_bits<B, true>(ntiles, st, kin, vin, ko, vo, n, shift, hist, offs, ld, dtable, kbase); break;
+      PG_CASE(1) PG_CASE(2) PG_CASE(3) PG_CASE(4)
+#undef PG_CASE
+      default: break;
+    }
+    return;
+  }
   switch (bits) {
 #define PG_CASE(B) \
   case B:          \
-    launch_scatter_bits<B>(ntiles, st, kin, vin, ko, vo, n, shift, hist, offs, ld); break;
+    launch_scatter_bits<B, false>(ntiles, st, kin, vin, ko, vo, n, shift, hist, offs, ld, nullptr, nullptr); break;
     PG_CASE(1) PG_CASE(2) PG_CASE(3) PG_CASE(4) PG_CASE(5) PG_CASE(6) PG_CASE(7) PG_CASE(8) PG_CASE(9)
 #undef PG_CASE
     default: break;
@@ -116,9 +132,11 @@ void launch_radix_scatter(int bits, unsigned ntiles, cudaStream_t st, const unsi
 
 template <int BITS>
 cudaError_t set_scatter_smem() {
-  cudaError_t e = cudaFuncSetAttribute(k_radix_scatter<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(k_radix_scatter<BITS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)rs_smem_bytes());
-  return e;
+  if (e != cudaSuccess || BITS > 4) return e;
+  return cudaFuncSetAttribute(k_radix_scatter<(BITS > 4 ? 1 : BITS), true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)rs_smem_bytes());
 }
 
 // PGRID_SYNC_DEBUG=1: synchronise after every launch so a fault names its kernel.
@@ -335,7 +353,8 @@ int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned
     unsigned* ko = kbuf[(p + 1) & 1];
     unsigned* vo = last ? vals_final : vbuf[(p + 1) & 1];
     if (p > 0 || !counts0_ready) {
-      k_tile_counts<<<ntiles, RS_THREADS, 0, st>>>(kin, (unsigned)n, plan.shift[p], plan.bits[p], counts, ld);
+      const DigitFn dig{plan.shift[p], (1u << plan.bits[p]) - 1u, nullptr};
+      k_tile_counts<<<ntiles, RS_THREADS, 0, st>>>(kin, (unsigned)n, dig, 1 << plan.bits[p], counts, ld);
       LAUNCHED("k_tile_counts", st);
       ++b->launches;
     }
@@ -403,7 +422,7 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
                                                             K2_TILE, k2_tiles, pbounds);
       LAUNCHED("k_pair_tile_bounds", st);
       k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no, dxu, dxyu,
-                                                     pbounds, keysA, v0);
+                                                     pbounds, keysA, v0, 0u);
       LAUNCHED("k_expand_pairs", st);
       b->launches += 2;
       if (flags & PG_KEEP_STAGES) {
@@ -539,6 +558,109 @@ int pg_radix_sort_pairs(pg_builder* b, const uint32_t* keys, const uint32_t* val
   CU(cudaMemcpyAsync(keys_out, sorted, (size_t)n * 4, out_kind, st));
   if (vfinal != vals_out) CU(cudaMemcpyAsync(vals_out, vfinal, (size_t)n * 4, out_kind, st));
   CU(cudaStreamSynchronize(st));
+  return PG_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// Building blocks of the sharded (multi-GPU) build: pairs of the counted shard, a stable
+// partition of pairs into cell slabs, and the sort + G tail over one slab.
+// ---------------------------------------------------------------------------------------
+int pg_pairs(pg_builder* b, uint32_t* keys, uint32_t* vals, uint32_t val_offset, void* stream_) {
+  if (!b || !b->counted) return fail(PG_STATE_ERROR, "pg_pairs without a successful pg_count");
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  const uint64_t no = b->no;
+  if (no == 0) return PG_OK;
+  const unsigned k2_tiles = (unsigned)((no + K2_TILE - 1) / K2_TILE);
+  int rc;
+  if ((rc = b->sort_sync.ensure(align_up((size_t)k2_tiles * 8 + 8)))) return rc;
+  int2* pbounds = b->sort_sync.as<int2>(0);
+  const unsigned dxu = (unsigned)b->dims[0], dxyu = (unsigned)b->dims[0] * (unsigned)b->dims[1];
+  k_pair_tile_bounds<<<(k2_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no, K2_TILE,
+                                                        k2_tiles, pbounds);
+  LAUNCHED("k_pair_tile_bounds", st);
+  k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no, dxu, dxyu,
+                                                 pbounds, keys, vals, val_offset);
+  LAUNCHED("k_expand_pairs", st);
+  return PG_OK;
+}
+
+int pg_partition(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int64_t n, const uint32_t* slab_of_bucket,
+                 int bucket_shift, int nslabs, const uint32_t* slab_base, uint32_t* keys_out, uint32_t* vals_out,
+                 uint64_t* slab_counts, void* stream_) {
+  if (!b) return fail(PG_INVARIANT_ERROR, "null builder");
+  if (nslabs < 1 || nslabs > 16) return fail(PG_INVARIANT_ERROR, "nslabs must be in [1, 16]");
+  if (n < 0 || n > kMaxScan) return fail(PG_SIZE_ERROR, "partition of %lld pairs exceeds the size limit", (long long)n);
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  if (n == 0) {
+    for (int s = 0; s < nslabs; ++s) slab_counts[s] = 0;
+    return PG_OK;
+  }
+  const int bits = std::max(1, bit_length((uint64_t)(nslabs - 1)));
+  const unsigned ntiles = (unsigned)((n + RS_TILE - 1) / RS_TILE);
+  const unsigned ld = (ntiles + 3) & ~3u;
+  int rc;
+  const size_t hist_bytes = align_up(kMaxBins * 4);
+  if ((rc = b->sort_sync.ensure(hist_bytes + (size_t)ld * kMaxBins * 4))) return rc;
+  unsigned* hist = b->sort_sync.as<unsigned>(0);
+  unsigned* counts = b->sort_sync.as<unsigned>(hist_bytes);
+  CU(cudaMemsetAsync(hist, 0, hist_bytes, st));
+  const DigitFn dig{bucket_shift, 0u, slab_of_bucket};
+  k_tile_counts<<<ntiles, RS_THREADS, 0, st>>>(keys, (unsigned)n, dig, 1 << bits, counts, ld);
+  LAUNCHED("k_tile_counts", st);
+  k_scan_tile_counts<<<1u << bits, SC_THREADS, 0, st>>>(counts, ntiles, ld, hist);
+  LAUNCHED("k_scan_tile_counts", st);
+  launch_radix_scatter(bits, ntiles, st, keys, vals, keys_out, vals_out, (unsigned)n, bucket_shift, hist, counts, ld,
+                       slab_of_bucket, slab_base);
+  LAUNCHED("k_radix_scatter", st);
+  std::vector<unsigned> h(nslabs);
+  CU(cudaMemcpyAsync(h.data(), hist, sizeof(unsigned) * nslabs, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  for (int s = 0; s < nslabs; ++s) slab_counts[s] = h[s];
+  return PG_OK;
+}
+
+int pg_sort_cells(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int64_t n, int64_t ncells, uint32_t* G,
+                  uint32_t* O, void* stream_) {
+  if (!b) return fail(PG_INVARIANT_ERROR, "null builder");
+  if (ncells < 1 || ncells > kMaxScan) return fail(PG_SIZE_ERROR, "ncells out of range");
+  if (n < 0 || n > kMaxScan) return fail(PG_SIZE_ERROR, "sort of %lld pairs exceeds the size limit", (long long)n);
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  const PassPlan plan = make_plan(bit_length((uint64_t)(ncells - 1)), kMaxDigitBits);
+  const size_t sec = align_up(std::max<size_t>((size_t)n * 4, 16));
+  int rc;
+  if ((rc = b->pairs.ensure(4 * sec))) return rc;
+  unsigned* kA = b->pairs.as<unsigned>(0);
+  unsigned* vA = b->pairs.as<unsigned>(sec);
+  unsigned* kB = b->pairs.as<unsigned>(2 * sec);
+  unsigned* vB = b->pairs.as<unsigned>(3 * sec);
+  const unsigned rs_tiles = (unsigned)((n + RS_TILE - 1) / RS_TILE);
+  const unsigned g_tiles = (unsigned)((ncells + G_TILE - 1) / G_TILE);
+  const size_t hist_bytes = align_up(kMaxPasses * kMaxBins * 4);
+  const size_t kb_bytes = align_up((size_t)(g_tiles + 1) * 4);
+  if ((rc = b->sort_sync.ensure(hist_bytes + kb_bytes + (size_t)((rs_tiles + 3) & ~3u) * kMaxBins * 4))) return rc;
+  unsigned* hist = b->sort_sync.as<unsigned>(0);
+  unsigned* kbounds = b->sort_sync.as<unsigned>(hist_bytes);
+  unsigned* counts = b->sort_sync.as<unsigned>(hist_bytes + kb_bytes);
+  const unsigned* sorted = keys;
+  if (n > 0) {
+    CU(cudaMemcpyAsync(kA, keys, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    if (plan.npasses == 0) {
+      CU(cudaMemcpyAsync(O, vals, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+      sorted = kA;
+    } else {
+      CU(cudaMemcpyAsync(vA, vals, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+      CU(cudaMemsetAsync(hist, 0, hist_bytes, st));
+      if ((rc = run_passes(b, plan, false, kA, vA, kB, vB, O, (uint64_t)n, hist, counts, st, &sorted))) return rc;
+    }
+  }
+  k_key_tile_bounds<<<(g_tiles + 1 + 7) / 8, 256, 0, st>>>(sorted, (unsigned)n, G_TILE, (unsigned)ncells, g_tiles + 1,
+                                                          kbounds);
+  LAUNCHED("k_key_tile_bounds", st);
+  k_cell_offsets<<<g_tiles, G_THREADS, 0, st>>>(sorted, (unsigned)n, (unsigned)ncells, kbounds, G);
+  LAUNCHED("k_cell_offsets", st);
   return PG_OK;
 }
 

@@ -518,7 +518,7 @@ k_key_tile_bounds(const unsigned* __restrict__ sorted, unsigned no, unsigned ste
 __global__ void __launch_bounds__(K2_THREADS)
 k_expand_pairs(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, unsigned no,
                unsigned dx, unsigned dxy, const int2* __restrict__ bounds, unsigned* __restrict__ keys,
-               unsigned* __restrict__ vals) {
+               unsigned* __restrict__ vals, unsigned val_offset) {
   __shared__ __align__(16) int slot[K2_TILE];
   __shared__ int warpmax[K2_THREADS / 32];
   __shared__ ObjCache oc;
@@ -533,14 +533,14 @@ k_expand_pairs(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_
     uint4* vd = reinterpret_cast<uint4*>(vals + pbase);
     kd[0] = make_uint4(key[0], key[1], key[2], key[3]);
     kd[1] = make_uint4(key[4], key[5], key[6], key[7]);
-    vd[0] = make_uint4(own[0], own[1], own[2], own[3]);
-    vd[1] = make_uint4(own[4], own[5], own[6], own[7]);
+    vd[0] = make_uint4(own[0] + val_offset, own[1] + val_offset, own[2] + val_offset, own[3] + val_offset);
+    vd[1] = make_uint4(own[4] + val_offset, own[5] + val_offset, own[6] + val_offset, own[7] + val_offset);
   } else {
 #pragma unroll
     for (int j = 0; j < K2_ITEMS; ++j)
       if (pbase + j < pend) {
         keys[pbase + j] = key[j];
-        vals[pbase + j] = (unsigned)own[j];
+        vals[pbase + j] = (unsigned)own[j] + val_offset;
       }
   }
 }
@@ -620,16 +620,24 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* wsum, 
   return add + inc - v;
 }
 
+// Digit of a key: a bit field, or (slab partitioning) a table lookup of a coarse bucket.
+struct DigitFn {
+  int shift;
+  unsigned mask;
+  const unsigned* __restrict__ table;  // non-null: digit = table[key >> shift]
+  __device__ __forceinline__ unsigned operator()(unsigned k) const {
+    return table ? __ldg(&table[k >> shift]) : (k >> shift) & mask;
+  }
+};
+
 __global__ void __launch_bounds__(RS_THREADS)
-k_tile_counts(const unsigned* __restrict__ keys, unsigned no, int shift, int bits, unsigned* __restrict__ counts,
+k_tile_counts(const unsigned* __restrict__ keys, unsigned no, DigitFn dig, int nbins, unsigned* __restrict__ counts,
               unsigned ld) {
   __shared__ unsigned h[kMaxBins];
   const int tid = threadIdx.x;
-  const unsigned ntiles = (no + RS_TILE - 1) / RS_TILE;
   const unsigned tile = blockIdx.x;
   const unsigned tbase = tile * (unsigned)RS_TILE;
   const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
-  const unsigned dmask = (1u << bits) - 1u;
   for (int b = tid; b < kMaxBins; b += RS_THREADS) h[b] = 0u;
   __syncthreads();
   if (tvalid == (unsigned)RS_TILE) {
@@ -639,16 +647,16 @@ k_tile_counts(const unsigned* __restrict__ keys, unsigned no, int shift, int bit
     for (int r = 0; r < RS_TILE / 4 / RS_THREADS; ++r) k[r] = __ldcs(src + tid + r * RS_THREADS);
 #pragma unroll
     for (int r = 0; r < RS_TILE / 4 / RS_THREADS; ++r) {
-      atomicAdd(&h[(k[r].x >> shift) & dmask], 1u);
-      atomicAdd(&h[(k[r].y >> shift) & dmask], 1u);
-      atomicAdd(&h[(k[r].z >> shift) & dmask], 1u);
-      atomicAdd(&h[(k[r].w >> shift) & dmask], 1u);
+      atomicAdd(&h[dig(k[r].x)], 1u);
+      atomicAdd(&h[dig(k[r].y)], 1u);
+      atomicAdd(&h[dig(k[r].z)], 1u);
+      atomicAdd(&h[dig(k[r].w)], 1u);
     }
   } else {
-    for (unsigned e = tid; e < tvalid; e += RS_THREADS) atomicAdd(&h[(__ldcs(keys + tbase + e) >> shift) & dmask], 1u);
+    for (unsigned e = tid; e < tvalid; e += RS_THREADS) atomicAdd(&h[dig(__ldcs(keys + tbase + e))], 1u);
   }
   __syncthreads();
-  for (int b = tid; b < (1 << bits); b += RS_THREADS) counts[(size_t)b * ld + tile] = h[b];
+  for (int b = tid; b < nbins; b += RS_THREADS) counts[(size_t)b * ld + tile] = h[b];
 }
 
 constexpr int SC_THREADS = 1024;
@@ -703,15 +711,20 @@ k_scan_tile_counts(unsigned* __restrict__ counts, unsigned ntiles, unsigned ld, 
 // Values never occupy registers: cp.async stages them in input order and they are
 // permuted shared->shared after the keys have been written. BITS and FULL are compile-time
 // so the ranking loop is branch-free and full tiles carry no bounds predicates.
-template <int BITS, bool FULL, bool SRC_SMEM = false>
+template <int BITS, bool FULL, bool TABLE = false, bool SRC_SMEM = false>
 __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* __restrict__ keys_in,
                                                    const unsigned* __restrict__ vals_in,
                                                    unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out,
                                                    unsigned tbase, unsigned tvalid, unsigned tile, unsigned ld,
                                                    int shift, const unsigned* __restrict__ hist,
-                                                   const unsigned* __restrict__ offs) {
+                                                   const unsigned* __restrict__ offs,
+                                                   const unsigned* __restrict__ dtable = nullptr,
+                                                   const unsigned* __restrict__ kbase = nullptr) {
   constexpr int NB = 1 << BITS;
   constexpr unsigned DMASK = (unsigned)NB - 1u;
+  // digit of a key: bit field, or slab id = dtable[key >> shift] (keys then leave rebased
+  // by kbase[slab], i.e. relative to their slab's first cell)
+  auto digit = [&](unsigned k) -> unsigned { return TABLE ? __ldg(&dtable[k >> shift]) : (k >> shift) & DMASK; };
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   auto elem = [&](int j) { return (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane; };
   auto valid = [&](int j) { return FULL || elem(j) < tvalid; };
@@ -735,7 +748,7 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
   }
   unsigned dg[RS_ITEMS];
 #pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) dg[j] = valid(j) ? ((SRC_SMEM ? ksrc[elem(j)] : __ldg(ksrc + elem(j))) >> shift) & DMASK : 0u;
+  for (int j = 0; j < RS_ITEMS; ++j) dg[j] = valid(j) ? digit(SRC_SMEM ? ksrc[elem(j)] : __ldg(ksrc + elem(j))) : 0u;
   // peers (same-digit lanes) per item: bit-sliced ballots, items interleaved for ILP
   unsigned pm[RS_ITEMS];
 #pragma unroll
@@ -814,8 +827,9 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
     gpos[r] = 0;
     if (FULL || i < tvalid) {
       const unsigned k = sm.buf[i];
-      gpos[r] = sm.gbase[(k >> shift) & DMASK] + i;
-      if (keys_out) keys_out[gpos[r]] = k;
+      const unsigned d = digit(k);
+      gpos[r] = sm.gbase[d] + i;
+      if (keys_out) keys_out[gpos[r]] = TABLE ? k - __ldg(&kbase[d]) : k;
     }
   }
   if (!SRC_SMEM) cp_async_wait();
@@ -832,22 +846,23 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
   }
 }
 
-template <int BITS>
+template <int BITS, bool TABLE>
 __global__ void __launch_bounds__(RS_THREADS, 4)
 k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
                 unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, unsigned no, int shift,
-                const unsigned* __restrict__ hist, const unsigned* __restrict__ offs, unsigned ld) {
+                const unsigned* __restrict__ hist, const unsigned* __restrict__ offs, unsigned ld,
+                const unsigned* __restrict__ dtable, const unsigned* __restrict__ kbase) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RsSmem& sm = *reinterpret_cast<RsSmem*>(smem_raw);
   const unsigned tile = blockIdx.x;
   const unsigned tbase = tile * (unsigned)RS_TILE;
   const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
   if (tvalid == (unsigned)RS_TILE)
-    radix_scatter_tile<BITS, true>(sm, keys_in, vals_in, keys_out, vals_out, tbase, tvalid, tile, ld, shift, hist,
-                                   offs);
+    radix_scatter_tile<BITS, true, TABLE>(sm, keys_in, vals_in, keys_out, vals_out, tbase, tvalid, tile, ld, shift,
+                                          hist, offs, dtable, kbase);
   else
-    radix_scatter_tile<BITS, false>(sm, keys_in, vals_in, keys_out, vals_out, tbase, tvalid, tile, ld, shift, hist,
-                                    offs);
+    radix_scatter_tile<BITS, false, TABLE>(sm, keys_in, vals_in, keys_out, vals_out, tbase, tvalid, tile, ld, shift,
+                                           hist, offs, dtable, kbase);
 }
 
 // ----------------------------------------------------------------------------------------

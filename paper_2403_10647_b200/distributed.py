@@ -1,0 +1,278 @@
+"""Sharded build across GPUs: triangle shards -> cell slabs -> one all-to-all.
+
+Every rank r of P owns the contiguous triangle shard [r*N/P, (r+1)*N/P) and runs the count
+and pair-expansion kernels on it. A coarse cell-id histogram (all-reduce) cuts the cell range
+into P slabs of about NO/P pairs. Each rank stably partitions its pairs by slab and one
+variable-size all-to-all routes them to the slab owners. all_to_all delivers the chunks in
+source-rank order and the shards are ascending triangle ranges, so a rank's received pairs
+are in global object-major order: the local stable radix sort by cell then reproduces the
+reference's order exactly (`builders.py:123-125`, ascending object ids per cell). Each
+slab's G is rebased by the exclusive scan of the slab pair totals; the global G and O are
+the slab-ordered concatenations.
+
+The orchestration is written against two small interfaces so the same code runs
+  * on GPUs: `CudaOps` (libpgrid kernels on this rank's device) + `TorchComm` (NCCL), and
+  * in tests: any ops object with the same methods + `TorchComm` over gloo, or
+    `run_emulated` (every rank's phases executed in sequence in one process).
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+
+COARSE_BITS = 12       # slab cuts at 2^12-bucket granularity of the cell-id range
+MAX_SLABS = 16         # pg_partition's digit table limit
+
+
+@dataclass
+class SlabPlan:
+    shift: int                 # bucket = cell >> shift
+    nbuckets: int
+    cuts: np.ndarray           # int64[P+1] bucket boundaries of the slabs
+    cell_lo: np.ndarray        # int64[P] first cell of each slab
+    cell_hi: np.ndarray        # int64[P] one past the last cell
+    pair_base: np.ndarray      # int64[P+1] exclusive scan of the slab pair totals
+    table: np.ndarray          # uint32[nbuckets] slab id of every bucket
+
+
+def coarse_shift(ncells):
+    key_bits = int(ncells - 1).bit_length()
+    return max(0, key_bits - COARSE_BITS)
+
+
+def plan_slabs(hist, ncells, nslabs):
+    """Balanced slab cuts from the global coarse histogram (identical on every rank)."""
+    hist = np.asarray(hist, dtype=np.int64)
+    shift = coarse_shift(ncells)
+    nb = len(hist)
+    total = int(hist.sum())
+    cum = np.concatenate([[0], np.cumsum(hist)])          # pairs before bucket b
+    cuts = np.zeros(nslabs + 1, dtype=np.int64)
+    for s in range(1, nslabs):
+        # first bucket whose start has at least s/P of the pairs before it
+        cuts[s] = max(cuts[s - 1], int(np.searchsorted(cum, (s * total + nslabs - 1) // nslabs)))
+        cuts[s] = min(cuts[s], nb)
+    cuts[nslabs] = nb
+    cell_lo = np.minimum(cuts[:-1] << shift, ncells)
+    cell_hi = np.minimum(cuts[1:] << shift, ncells)
+    pair_base = cum[cuts]
+    table = np.zeros(nb, dtype=np.uint32)
+    for s in range(nslabs):
+        table[cuts[s]:cuts[s + 1]] = s
+    return SlabPlan(shift, nb, cuts, cell_lo, cell_hi, pair_base, table)
+
+
+def shard_range(n, rank, world):
+    return (n * rank) // world, (n * (rank + 1)) // world
+
+
+def assemble(slabs, ncells):
+    """Global (G, O) from the slab results [(pair_base, G_rel, O)] in slab order."""
+    G = np.empty(ncells + 1, dtype=np.uint32)
+    parts = []
+    pos = 0
+    for base, g_rel, o in slabs:
+        k = len(g_rel) - 1
+        G[pos:pos + k] = np.asarray(g_rel[:-1], dtype=np.int64) + base
+        pos += k
+        parts.append(np.asarray(o, dtype=np.uint32))
+    O = np.concatenate(parts) if parts else np.zeros(0, np.uint32)
+    G[ncells] = len(O)
+    assert pos == ncells
+    return G, O
+
+
+class ShardState:
+    """Per-rank state of one sharded build, advanced phase by phase."""
+
+    def __init__(self, ops, V, T, tri_base, spec, rank, world):
+        self.ops, self.rank, self.world = ops, rank, world
+        self.spec = spec
+        self.ncells = int(spec.dims[0]) * int(spec.dims[1]) * int(spec.dims[2])
+        self.V, self.T, self.tri_base = V, T, tri_base
+
+    def phase_count(self):
+        """K1 + K2 on the shard; returns the local coarse histogram."""
+        self.no = self.ops.count(self.V, self.T, self.spec)
+        self.keys, self.vals = self.ops.pairs(self.no, self.tri_base)
+        self.shift = coarse_shift(self.ncells)
+        nb = ((self.ncells - 1) >> self.shift) + 1
+        return self.ops.coarse_hist(self.keys, self.shift, nb)
+
+    def phase_partition(self, plan):
+        """Stable partition by slab; returns the per-slab send counts."""
+        self.plan = plan
+        base = plan.cell_lo.astype(np.uint32)
+        self.kout, self.vout, counts = self.ops.partition(self.keys, self.vals, plan.table, plan.shift,
+                                                          self.world, base)
+        self.send_counts = counts
+        return counts
+
+    def phase_sort(self, krecv, vrecv):
+        """Local stable sort of the received slab + its G (relative), O."""
+        lo, hi = int(self.plan.cell_lo[self.rank]), int(self.plan.cell_hi[self.rank])
+        n = self.ops.length(krecv)
+        if hi == lo:
+            return int(self.plan.pair_base[self.rank]), np.zeros(1, np.uint32), np.zeros(0, np.uint32)
+        G, O = self.ops.sort_cells(krecv, vrecv, n, hi - lo)
+        return int(self.plan.pair_base[self.rank]), G, O
+
+
+def build_sharded(ops, comm, V, T, tri_base, spec, gather=True):
+    """One rank's part of the sharded build (run on every rank of `comm`).
+
+    Returns (G, O) on rank 0 when gather=True (None elsewhere); with gather=False each rank
+    returns its slab as (cell_lo, cell_hi, pair_base, G_rel, O)."""
+    rank, world = comm.rank, comm.world
+    if world > MAX_SLABS:
+        raise ValueError(f"at most {MAX_SLABS} ranks")
+    st = ShardState(ops, V, T, tri_base, spec, rank, world)
+    hist = comm.allreduce_sum(np.asarray(st.phase_count(), dtype=np.int64))
+    plan = plan_slabs(hist, st.ncells, world)
+    send = st.phase_partition(plan)
+    recv = comm.alltoall_counts(send)
+    krecv, vrecv = comm.alltoall_pairs(st.kout, st.vout, send, recv, ops)
+    base, G_rel, O = st.phase_sort(krecv, vrecv)
+    if not gather:
+        return int(plan.cell_lo[rank]), int(plan.cell_hi[rank]), base, ops.to_numpy(G_rel), ops.to_numpy(O)
+    slabs = comm.gather_to_root((base, ops.to_numpy(G_rel), ops.to_numpy(O)))
+    if rank != 0:
+        return None
+    return assemble(slabs, st.ncells)
+
+
+class TorchComm:
+    """Collectives over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None, device=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = device
+
+    def _t(self, arr):
+        import torch
+        t = torch.as_tensor(np.asarray(arr))
+        return t.to(self.device) if self.device is not None else t
+
+    def allreduce_sum(self, arr):
+        t = self._t(arr)
+        self.dist.all_reduce(t, group=self.group)
+        return t.cpu().numpy()
+
+    def alltoall_counts(self, send):
+        import torch
+        s = self._t(np.asarray(send, dtype=np.int64))
+        r = torch.empty_like(s)
+        self.dist.all_to_all_single(r, s, group=self.group)
+        return [int(x) for x in r.cpu().numpy()]
+
+    def alltoall_pairs(self, keys, vals, send, recv, ops):
+        kr = ops.empty_pairs(sum(recv))
+        vr = ops.empty_pairs(sum(recv))
+        self.dist.all_to_all_single(kr, ops.as_tensor(keys), recv, send, group=self.group)
+        self.dist.all_to_all_single(vr, ops.as_tensor(vals), recv, send, group=self.group)
+        return kr, vr
+
+    def gather_to_root(self, obj):
+        out = [None] * self.world if self.rank == 0 else None
+        self.dist.gather_object(obj, out, dst=0, group=self.group)
+        return out
+
+
+def run_emulated(make_ops, V, T, spec, world):
+    """Every rank's phases executed in sequence in one process (no inter-rank waiting):
+    exercises the kernels and the orchestration of the sharded build on a single device."""
+    n = len(T)
+    states = []
+    for r in range(world):
+        lo, hi = shard_range(n, r, world)
+        states.append(ShardState(make_ops(), V, T[lo:hi], lo, spec, r, world))
+    hist = np.sum([np.asarray(s.phase_count(), dtype=np.int64) for s in states], axis=0)
+    plan = plan_slabs(hist, states[0].ncells, world)
+    sends = [s.phase_partition(plan) for s in states]
+    slabs = []
+    for r, s in enumerate(states):
+        ops = s.ops
+        ks, vs = [], []
+        for q, src in enumerate(states):       # source-rank order, like all_to_all
+            off = int(np.sum(sends[q][:r]))
+            ks.append(ops.slice(src.kout, off, sends[q][r]))
+            vs.append(ops.slice(src.vout, off, sends[q][r]))
+        krecv, vrecv = ops.concat(ks), ops.concat(vs)
+        base, G_rel, O = s.phase_sort(krecv, vrecv)
+        slabs.append((base, ops.to_numpy(G_rel), ops.to_numpy(O)))
+    return assemble(slabs, states[0].ncells)
+
+
+class CudaOps:
+    """Per-rank device steps on this rank's GPU: libpgrid kernels on torch-allocated memory."""
+
+    def __init__(self, device=0, stream=None):
+        import torch
+
+        from . import _native
+        self.torch = torch
+        self.dev = torch.device("cuda", device)
+        self.b = _native.Builder(device)
+        self.stream = stream
+
+    def _sp(self):
+        s = self.stream or self.torch.cuda.current_stream(self.dev)
+        return s.cuda_stream
+
+    def as_tensor(self, x):
+        return x
+
+    def empty_pairs(self, n):
+        return self.torch.empty(n, dtype=self.torch.int32, device=self.dev)
+
+    def length(self, x):
+        return int(x.numel())
+
+    def slice(self, x, off, n):
+        return x[off:off + n]
+
+    def concat(self, xs):
+        return self.torch.cat(xs) if xs else self.empty_pairs(0)
+
+    def to_numpy(self, x):
+        return x.cpu().numpy().view(np.uint32) if hasattr(x, "cpu") else np.asarray(x, np.uint32)
+
+    def count(self, V, T, spec):
+        torch = self.torch
+        if not isinstance(V, torch.Tensor):
+            V = torch.from_numpy(np.ascontiguousarray(V)).to(self.dev)
+        if not isinstance(T, torch.Tensor):
+            T = torch.from_numpy(np.ascontiguousarray(T)).to(self.dev)
+        self._V, self._T = V, T          # keep alive for the stream
+        return self.b.count(V, V.shape[0], T, T.shape[0], spec, 0, self._sp())
+
+    def pairs(self, no, tri_base):
+        k, v = self.empty_pairs(no), self.empty_pairs(no)
+        self.b.pairs(k, v, tri_base, self._sp())
+        return k, v
+
+    def coarse_hist(self, keys, shift, nbuckets):
+        if keys.numel() == 0:
+            return np.zeros(nbuckets, np.int64)
+        # slab planning only (not on the pair data path): a 4096-bin histogram
+        h = self.torch.bincount((keys >> shift).long(), minlength=nbuckets)
+        return h.cpu().numpy().astype(np.int64)
+
+    def partition(self, keys, vals, table, shift, nslabs, base):
+        torch = self.torch
+        n = int(keys.numel())
+        dt = torch.from_numpy(np.asarray(table, np.uint32).view(np.int32)).to(self.dev)
+        db = torch.from_numpy(np.asarray(base, np.uint32).view(np.int32)).to(self.dev)
+        ko, vo = self.empty_pairs(n), self.empty_pairs(n)
+        counts = self.b.partition(keys, vals, n, dt, shift, nslabs, db, ko, vo, self._sp())
+        return ko, vo, counts
+
+    def sort_cells(self, keys, vals, n, ncells):
+        G = self.torch.empty(ncells + 1, dtype=self.torch.int32, device=self.dev)
+        O = self.empty_pairs(n)
+        self.b.sort_cells(keys, vals, n, ncells, G, O, self._sp())
+        return G, O
