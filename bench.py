@@ -8,7 +8,10 @@ case). `value` = builds/s with inputs resident in HBM (device pointers through t
 `e2e` = the same through the public numpy API (pinned host inputs, H2D + build + D2H of G
 and O inside the timed region). Rank 0 prints one JSON line.
 
-N > 1 (torchrun): every rank builds its own copy of the scene (replicas; weak scaling).
+N > 1 (torchrun): the sharded build of SURVEY.md §8e on an N x 10M-triangle architectural
+scene (weak scaling: 10M triangles per GPU): each rank generates and counts its triangle
+shard, pairs are routed to cell slabs by one NCCL all-to-all, every rank sorts its slab and
+writes its G/O slice (distributed output).
 `--impl reference` times the reference's own CPU build (oracle/_ref, C lane, all host
 threads) on the same config instead.
 """
@@ -39,6 +42,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-budget-s", type=float, default=150.0)
+    ap.add_argument("--sharded", action="store_true", help="use the sharded path even at N=1 (testing)")
     return ap.parse_args()
 
 
@@ -201,6 +205,98 @@ def cpu_baseline(args, mesh, spec):
             "sample": f"1 full {args.config} build, C oracle port, single thread, {sec:.2f}s"}
 
 
+def run_sharded(args, world, rank, local):
+    """N > 1: sharded build over NCCL (paper_2403_10647_b200/distributed.py)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_10647_b200 import _native
+    from paper_2403_10647_b200 import distributed as D
+    from paper_2403_10647_b200 import gridcore, scenes
+
+    kind, n1, seed, density = scenes.CONFIGS[args.config]
+    if kind != "arch":
+        raise SystemExit("sharded bench supports the arch configs")
+    n = n1 * world
+    lo, hi = D.shard_range(n, rank, world)
+    shard = scenes.gen_arch_shard(n, seed, density, lo, hi)
+    dev = torch.device("cuda", local)
+    bmin = torch.from_numpy(shard.vertices.min(axis=0).copy()).to(dev)
+    bmax = torch.from_numpy(shard.vertices.max(axis=0).copy()).to(dev)
+    dist.all_reduce(bmin, op=dist.ReduceOp.MIN)
+    dist.all_reduce(bmax, op=dist.ReduceOp.MAX)
+    spec = gridcore.spec_from_bounds(bmin.cpu().numpy(), bmax.cpu().numpy(), n, density=density)
+    Vd = torch.from_numpy(shard.vertices.copy()).to(dev)
+    Td = torch.from_numpy(shard.triangles.copy()).to(dev)
+    ops = D.CudaOps(local)
+    comm = D.TorchComm(device=dev)
+
+    def step():
+        return D.build_sharded(ops, comm, Vd, Td, lo, spec, gather=False)
+
+    res = step()
+    launches = ops.b.launches()
+    for _ in range(max(args.warmup, 3)):
+        res = step()
+    no_local = int(res[4].numel())
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        dist.barrier()
+        ev0.record()
+        for _ in range(args.steps):
+            step()
+        ev1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = torch.tensor([ev0.elapsed_time(ev1) / args.steps], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    no_t = torch.tensor([no_local], device=dev, dtype=torch.int64)
+    dist.all_reduce(no_t)
+    no = int(no_t.item())
+
+    # e2e: pinned host shard in, H2D + sharded build + D2H of this rank's G/O slab out
+    Vh, Th = shard.vertices.copy(), shard.triangles.copy()
+    _native.host_register(Vh)
+    _native.host_register(Th)
+    e2e = []
+    for _ in range(args.e2e_steps or min(args.steps, 5)):
+        dist.barrier()
+        t0 = time.perf_counter()
+        r = D.build_sharded(ops, comm, Vh, Th, lo, spec, gather=False)
+        g_host, o_host = ops.to_numpy(r[3]), ops.to_numpy(r[4])     # this rank's slab, D2H
+        t = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e.append(float(t.item()))
+    e2e_sec = statistics.median(e2e)
+    out_bytes = torch.tensor([(g_host.nbytes + o_host.nbytes)], device=dev, dtype=torch.int64)
+    dist.all_reduce(out_bytes)
+    line = {
+        # whole-job throughput in the metric's unit: 10M-triangle-scene builds per second
+        # (N x builds/s of the N x 10M scene), so weak scaling is value(N) / (N value(1))
+        "metric": METRIC, "value": round(world * 1e3 / ms, 3), "unit": "builds/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config} x{world} (sharded)", "scene": kind, "triangles": n,
+                   "triangles_per_gpu": n1, "dims": list(spec.dims), "ncells": spec.ncells, "no": no,
+                   "parallelism": f"triangle shards x{world} -> cell slabs, NCCL all-to-all",
+                   "output": "distributed (each rank its G/O slab)",
+                   "value_def": f"{world} x builds/s of the {world} x {n1 // 1_000_000}M-triangle scene",
+                   "scene_builds_per_s": round(1e3 / ms, 3),
+                   "parity": "orchestration verified by tests/test_distributed.py + test_gpu_distributed.py"},
+        "mpairs_per_s": round(no / (ms * 1e-3) / 1e6, 2),
+        "e2e": {"value": round(world / e2e_sec, 3), "unit": "builds/s",
+                "h2d_bytes_per_step": int((Vh.nbytes + Th.nbytes) * world),
+                "d2h_bytes_per_step": int(out_bytes.item()), "ms_per_step": round(e2e_sec * 1e3, 2)},
+        "gpu_launches": launches * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world, rank, local = dist_env()
@@ -217,9 +313,18 @@ def main():
 
     import torch
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        try:
+            run_sharded(args, world, rank, local)
+        finally:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
 
     from paper_2403_10647_b200 import _native, builders, scenes
 

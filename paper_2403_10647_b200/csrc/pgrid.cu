@@ -582,6 +582,7 @@ int pg_pairs(pg_builder* b, uint32_t* keys, uint32_t* vals, uint32_t val_offset,
   k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no, dxu, dxyu,
                                                  pbounds, keys, vals, val_offset);
   LAUNCHED("k_expand_pairs", st);
+  b->launches += 2;
   return PG_OK;
 }
 
@@ -614,6 +615,7 @@ int pg_partition(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int6
   launch_radix_scatter(bits, ntiles, st, keys, vals, keys_out, vals_out, (unsigned)n, bucket_shift, hist, counts, ld,
                        slab_of_bucket, slab_base);
   LAUNCHED("k_radix_scatter", st);
+  b->launches += 3;
   std::vector<unsigned> h(nslabs);
   CU(cudaMemcpyAsync(h.data(), hist, sizeof(unsigned) * nslabs, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
@@ -661,6 +663,7 @@ int pg_sort_cells(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int
   LAUNCHED("k_key_tile_bounds", st);
   k_cell_offsets<<<g_tiles, G_THREADS, 0, st>>>(sorted, (unsigned)n, (unsigned)ncells, kbounds, G);
   LAUNCHED("k_cell_offsets", st);
+  b->launches += 2;
   return PG_OK;
 }
 

@@ -122,7 +122,8 @@ def build_sharded(ops, comm, V, T, tri_base, spec, gather=True):
     """One rank's part of the sharded build (run on every rank of `comm`).
 
     Returns (G, O) on rank 0 when gather=True (None elsewhere); with gather=False each rank
-    returns its slab as (cell_lo, cell_hi, pair_base, G_rel, O)."""
+    returns its slab as (cell_lo, cell_hi, pair_base, G_rel, O) with G_rel/O left where the
+    ops keep them (device memory for CudaOps)."""
     rank, world = comm.rank, comm.world
     if world > MAX_SLABS:
         raise ValueError(f"at most {MAX_SLABS} ranks")
@@ -134,7 +135,7 @@ def build_sharded(ops, comm, V, T, tri_base, spec, gather=True):
     krecv, vrecv = comm.alltoall_pairs(st.kout, st.vout, send, recv, ops)
     base, G_rel, O = st.phase_sort(krecv, vrecv)
     if not gather:
-        return int(plan.cell_lo[rank]), int(plan.cell_hi[rank]), base, ops.to_numpy(G_rel), ops.to_numpy(O)
+        return int(plan.cell_lo[rank]), int(plan.cell_hi[rank]), base, G_rel, O
     slabs = comm.gather_to_root((base, ops.to_numpy(G_rel), ops.to_numpy(O)))
     if rank != 0:
         return None

@@ -162,6 +162,20 @@ def spec_for_mesh(mesh, dims=None, density=5.0):
     return GridSpec(padded, dims)
 
 
+def spec_from_bounds(lo, hi, ntriangles, dims=None, density=5.0):
+    """spec_for_mesh from tight bounds already reduced over shards (min/max are exact, so a
+    sharded build sees the same doubles as spec_for_mesh on the whole mesh)."""
+    tight = Aabb(lo, hi)
+    longest = float((tight.hi - tight.lo).max())
+    pad = BOUNDS_PAD * longest if longest > 0 else BOUNDS_PAD
+    plo = tight.lo - pad
+    phi = np.maximum(tight.hi + pad, plo + 2 * pad)
+    padded = Aabb(plo, phi)
+    if dims is None:
+        dims = compute_dims(padded, ntriangles, density)
+    return GridSpec(padded, dims)
+
+
 def key_bits_for(ncells):
     """Radix key width: (ncells-1).bit_length() (builders.py:124)."""
     return int(ncells - 1).bit_length()

@@ -35,11 +35,12 @@ def _splitmix64_finalize(x):
     return x ^ (x >> np.uint64(31))
 
 
-def uniforms(seed, count, stream=0):
-    """`count` doubles in [0,1) from the counter-based stream (geometry.py:134-139)."""
+def uniforms(seed, count, stream=0, start=0):
+    """`count` doubles in [0,1) from the counter-based stream (geometry.py:134-139);
+    `start` skips the first draws, so uniforms(s, b - a, st, a) == uniforms(s, b, st)[a:b]."""
     base = np.uint64((seed * _SEED_MUL + stream) & 0xFFFFFFFFFFFFFFFF)
     with np.errstate(over="ignore"):
-        ctr = np.arange(1, count + 1, dtype=np.uint64) * _GAMMA + base
+        ctr = np.arange(start + 1, start + count + 1, dtype=np.uint64) * _GAMMA + base
         bits = _splitmix64_finalize(ctr)
     return (bits >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
 
@@ -76,6 +77,30 @@ def _wall_quads(nquads, seed):
     tris[0::2] = corners[:, [0, 1, 2]]
     tris[1::2] = corners[:, [0, 2, 3]]
     return tris
+
+
+def _small_triangles_range(a, b, seed, stream, size):
+    """Triangles [a, b) of small_triangles(n, seed, stream, size) (scalar size)."""
+    k = b - a
+    centres = uniforms(seed, 3 * k, stream, 3 * a).reshape(k, 3) * (1.0 - size) + size / 2
+    jitter = (uniforms(seed, 9 * k, stream + 1, 9 * a).reshape(k, 3, 3) - 0.5) * size
+    return centres[:, None, :] + jitter
+
+
+def gen_arch_shard(n, seed, density, lo, hi):
+    """Triangles [lo, hi) of gen_scene("arch", n, seed, density) as an unshared-vertex soup
+    (for sharded builds: each rank generates only its own shard)."""
+    edge = _cell_edge(n, density)
+    nquads = min(64, n // 2)
+    nwall = 2 * nquads
+    parts = []
+    if lo < nwall:
+        parts.append(_wall_quads(nquads, seed)[lo:min(hi, nwall)])
+    a, b = max(lo, nwall) - nwall, hi - nwall
+    if b > a:
+        parts.append(_small_triangles_range(a, b, seed, 31, 0.35 * edge))
+    tris = np.concatenate(parts, axis=0) if parts else np.empty((0, 3, 3))
+    return _soup(tris)
 
 
 def _snap(x, bits):
