@@ -178,6 +178,7 @@ struct pg_builder {
   int dims[3] = {1, 1, 1};
   int key_bits = 0;
   bool stages_kept = false;
+  size_t stage_sec = 0;  // offset of the kept values inside `stage`
   bool k1_timed = false;  // ev[5]..ev[6] bracket K1 of the last pg_count
   int launches = 0;
   const unsigned* sorted_keys = nullptr;
@@ -354,7 +355,8 @@ int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned
     unsigned* vo = last ? vals_final : vbuf[(p + 1) & 1];
     if (p > 0 || !counts0_ready) {
       const DigitFn dig{plan.shift[p], (1u << plan.bits[p]) - 1u, nullptr};
-      k_tile_counts<<<ntiles, RS_THREADS, 0, st>>>(kin, (unsigned)n, dig, 1 << plan.bits[p], counts, ld);
+      k_tile_counts<<<(ntiles + TC_TILES - 1) / TC_TILES, RS_THREADS, 0, st>>>(kin, (unsigned)n, dig,
+                                                                              1 << plan.bits[p], counts, ld);
       LAUNCHED("k_tile_counts", st);
       ++b->launches;
     }
@@ -387,8 +389,10 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
     dG = b->gbuf.as<unsigned>();
     dO = b->obuf.as<unsigned>();
   }
-  // pairs: keysA | valsA | keysB | valsB (16 B aligned sections)
-  const size_t sec = align_up(std::max<size_t>((size_t)no * 4, 16));
+  // pairs: keysA | valsA | keysB | valsB (16 B aligned sections); keysB also holds K2's
+  // tile-major first-pass counts before pass 0 runs
+  const size_t sec = align_up(std::max<size_t>(std::max<size_t>((size_t)no * 4, 16),
+                                               (size_t)((no + RS_TILE - 1) / RS_TILE) * kMaxBins * 4));
   if ((rc = b->pairs.ensure(4 * sec))) return rc;
   unsigned* keysA = b->pairs.as<unsigned>(0);
   unsigned* valsA = b->pairs.as<unsigned>(sec);
@@ -429,6 +433,7 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
         if ((rc = b->stage.ensure(2 * sec))) return rc;
         CU(cudaMemcpyAsync(b->stage.as<unsigned>(0), keysA, no * 4, cudaMemcpyDeviceToDevice, st));
         CU(cudaMemcpyAsync(b->stage.as<unsigned>(sec), v0, no * 4, cudaMemcpyDeviceToDevice, st));
+        b->stage_sec = sec;
         b->stages_kept = true;
       }
     }
@@ -437,10 +442,16 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
       k_pair_tile_bounds<<<(rs_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no,
                                                             RS_TILE, rs_tiles, pbounds);
       LAUNCHED("k_pair_tile_bounds", st);
+      // K2 writes its first-pass tile counts tile-major into the B key buffer (free until
+      // pass 0 scatters into it), then they are transposed into the digit-major matrix
+      unsigned* tm = keysB;
       k_pairs_emit<<<rs_tiles, RS_THREADS, sizeof(PeSmem), st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no,
-                                                                 dxu, dxyu, plan, pbounds, keysA, valsA, counts, ld);
+                                                                 dxu, dxyu, plan, pbounds, keysA, valsA, tm);
       LAUNCHED("k_pairs_emit", st);
-      b->launches += 2;
+      k_transpose_counts<<<dim3((rs_tiles + 31) / 32, ((1u << plan.bits[0]) + 31) / 32), 256, 0, st>>>(
+          tm, rs_tiles, 1 << plan.bits[0], counts, ld);
+      LAUNCHED("k_transpose_counts", st);
+      b->launches += 3;
       CU(cudaEventRecord(b->ev[1], st));
       if ((rc = run_passes(b, plan, true, keysA, valsA, keysB, valsB, dO, no, hist, counts, st, &sorted))) return rc;
     } else {
@@ -487,7 +498,7 @@ int pg_stage(pg_builder* b, int stage, void* dst, uint32_t flags, void* stream_)
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   CU(cudaSetDevice(b->device));
   const cudaMemcpyKind kind = (flags & PG_HOST_OUTPUT) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-  const size_t sec = align_up(std::max<size_t>((size_t)b->no * 4, 16));
+  const size_t sec = b->stage_sec;
   switch (stage) {
     case 0:
       if (b->n) {
@@ -608,7 +619,8 @@ int pg_partition(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int6
   unsigned* counts = b->sort_sync.as<unsigned>(hist_bytes);
   CU(cudaMemsetAsync(hist, 0, hist_bytes, st));
   const DigitFn dig{bucket_shift, 0u, slab_of_bucket};
-  k_tile_counts<<<ntiles, RS_THREADS, 0, st>>>(keys, (unsigned)n, dig, 1 << bits, counts, ld);
+  k_tile_counts<<<(ntiles + TC_TILES - 1) / TC_TILES, RS_THREADS, 0, st>>>(keys, (unsigned)n, dig, 1 << bits, counts,
+                                                                          ld);
   LAUNCHED("k_tile_counts", st);
   k_scan_tile_counts<<<1u << bits, SC_THREADS, 0, st>>>(counts, ntiles, ld, hist);
   LAUNCHED("k_scan_tile_counts", st);

@@ -630,40 +630,70 @@ struct DigitFn {
   }
 };
 
+// Upsweep of a radix pass: per-tile digit counts, TC_TILES tiles per CTA so every digit row
+// of the digit-major matrix receives TC_TILES consecutive entries (a full 32-byte sector).
+constexpr int TC_TILES = 8;
 __global__ void __launch_bounds__(RS_THREADS)
 k_tile_counts(const unsigned* __restrict__ keys, unsigned no, DigitFn dig, int nbins, unsigned* __restrict__ counts,
               unsigned ld) {
-  __shared__ unsigned h[kMaxBins];
+  __shared__ unsigned h[TC_TILES][kMaxBins];
   const int tid = threadIdx.x;
-  const unsigned tile = blockIdx.x;
-  const unsigned tbase = tile * (unsigned)RS_TILE;
-  const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
-  for (int b = tid; b < kMaxBins; b += RS_THREADS) h[b] = 0u;
+  const unsigned ntiles = (no + RS_TILE - 1) / RS_TILE;
+  const unsigned t0 = blockIdx.x * TC_TILES;
+  for (int b = tid; b < TC_TILES * kMaxBins; b += RS_THREADS) (&h[0][0])[b] = 0u;
   __syncthreads();
-  if (tvalid == (unsigned)RS_TILE) {
-    const uint4* src = reinterpret_cast<const uint4*>(keys + tbase);
-    uint4 k[RS_TILE / 4 / RS_THREADS];
+  for (int q = 0; q < TC_TILES; ++q) {
+    const unsigned tile = t0 + q;
+    if (tile >= ntiles) break;
+    const unsigned tbase = tile * (unsigned)RS_TILE;
+    const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
+    if (tvalid == (unsigned)RS_TILE) {
+      const uint4* src = reinterpret_cast<const uint4*>(keys + tbase);
+      uint4 k[RS_TILE / 4 / RS_THREADS];
 #pragma unroll
-    for (int r = 0; r < RS_TILE / 4 / RS_THREADS; ++r) k[r] = __ldcs(src + tid + r * RS_THREADS);
+      for (int r = 0; r < RS_TILE / 4 / RS_THREADS; ++r) k[r] = __ldcs(src + tid + r * RS_THREADS);
 #pragma unroll
-    for (int r = 0; r < RS_TILE / 4 / RS_THREADS; ++r) {
-      atomicAdd(&h[dig(k[r].x)], 1u);
-      atomicAdd(&h[dig(k[r].y)], 1u);
-      atomicAdd(&h[dig(k[r].z)], 1u);
-      atomicAdd(&h[dig(k[r].w)], 1u);
+      for (int r = 0; r < RS_TILE / 4 / RS_THREADS; ++r) {
+        atomicAdd(&h[q][dig(k[r].x)], 1u);
+        atomicAdd(&h[q][dig(k[r].y)], 1u);
+        atomicAdd(&h[q][dig(k[r].z)], 1u);
+        atomicAdd(&h[q][dig(k[r].w)], 1u);
+      }
+    } else {
+      for (unsigned e = tid; e < tvalid; e += RS_THREADS) atomicAdd(&h[q][dig(__ldcs(keys + tbase + e))], 1u);
     }
-  } else {
-    for (unsigned e = tid; e < tvalid; e += RS_THREADS) atomicAdd(&h[dig(__ldcs(keys + tbase + e))], 1u);
   }
   __syncthreads();
-  for (int b = tid; b < nbins; b += RS_THREADS) counts[(size_t)b * ld + tile] = h[b];
+  for (int i = tid; i < nbins * TC_TILES; i += RS_THREADS) {
+    const int b = i / TC_TILES, q = i % TC_TILES;
+    if (t0 + q < ntiles) counts[(size_t)b * ld + t0 + q] = h[q][b];
+  }
+}
+
+// K2 writes its first-pass counts tile-major (one coalesced row per CTA); transpose them to
+// the digit-major layout the row scan and the scatter use.
+__global__ void __launch_bounds__(256)
+k_transpose_counts(const unsigned* __restrict__ tm, unsigned ntiles, int nbins, unsigned* __restrict__ dm, unsigned ld) {
+  __shared__ unsigned blk[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const unsigned t0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
+  for (int r = ty; r < 32; r += 8) {
+    const unsigned t = t0 + r, d = d0 + tx;
+    blk[r][tx] = (t < ntiles && d < (unsigned)nbins) ? tm[(size_t)t * kMaxBins + d] : 0u;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const unsigned d = d0 + r, t = t0 + tx;
+    if (t < ntiles && d < (unsigned)nbins) dm[(size_t)d * ld + t] = blk[tx][r];
+  }
 }
 
 constexpr int SC_THREADS = 1024;
 constexpr int SC_ITEMS = 8;
 // One CTA per digit row: counts[row][0..ntiles) -> exclusive prefix over tiles, in place.
 // Rows are padded to a multiple of 4 (ld) so each thread moves its 8 entries as two 16-byte
-// accesses; one iteration covers 8192 tiles (33.5M pairs).
+// accesses; one iteration covers 8192 tiles (33.5M pairs). The row total is the digit's
+// global count (its histogram bin).
 __global__ void __launch_bounds__(SC_THREADS)
 k_scan_tile_counts(unsigned* __restrict__ counts, unsigned ntiles, unsigned ld, unsigned* __restrict__ row_total) {
   __shared__ unsigned wsum[SC_THREADS / 32];
@@ -703,7 +733,7 @@ k_scan_tile_counts(unsigned* __restrict__ counts, unsigned ntiles, unsigned ld, 
     }
     carry += total;
   }
-  if (tid == 0) row_total[blockIdx.x] = carry;  // the global count of this digit (its histogram bin)
+  if (tid == 0) row_total[blockIdx.x] = carry;
 }
 
 // Scatter one tile of a digit pass. Item j of lane l of warp w is tile element
@@ -881,7 +911,7 @@ struct PeSmem {
 __global__ void __launch_bounds__(RS_THREADS)
 k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, unsigned no,
              unsigned dx, unsigned dxy, PassPlan plan, const int2* __restrict__ bounds, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
-             unsigned* __restrict__ counts0, unsigned ld) {
+             unsigned* __restrict__ counts0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PeSmem& sm = *reinterpret_cast<PeSmem*>(smem_raw);
   const int tid = threadIdx.x;
@@ -917,7 +947,8 @@ k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pr
       if (j < nvalid) atomicAdd(&sm.h[(key[j] >> sh) & mask], 1u);
   }
   __syncthreads();
-  for (int b = tid; b < (1 << plan.bits[0]); b += RS_THREADS) counts0[(size_t)b * ld + blockIdx.x] = sm.h[b];
+  // tile-major row (coalesced); k_transpose_counts makes it digit-major
+  for (int b = tid; b < (1 << plan.bits[0]); b += RS_THREADS) counts0[(size_t)blockIdx.x * kMaxBins + b] = sm.h[b];
 }
 
 // ----------------------------------------------------------------------------------------
