@@ -13,7 +13,7 @@ import numpy as np
 
 from .errors import DeviceError, GridError, InvariantError, SizeError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libpgrid.so")
+LIB_PATH = os.environ.get("PGRID_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libpgrid.so")
 
 PG_OK = 0
 PG_SIZE_ERROR = 1

@@ -134,6 +134,7 @@ template <int BITS>
 cudaError_t set_scatter_smem() {
   cudaError_t e = cudaFuncSetAttribute(k_radix_scatter<BITS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)rs_smem_bytes());
+
   if (e != cudaSuccess || BITS > 4) return e;
   return cudaFuncSetAttribute(k_radix_scatter<(BITS > 4 ? 1 : BITS), true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)rs_smem_bytes());

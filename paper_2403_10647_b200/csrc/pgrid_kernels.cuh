@@ -574,7 +574,8 @@ constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_ITEMS = 16;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 pairs per tile
-constexpr int RS_DPT = kMaxBins / RS_THREADS;   // digits per thread in the per-digit phases (2)
+constexpr int RS_DPT = kMaxBins / RS_THREADS;
+constexpr int RS_MIN_CTAS = 4;  // 64 registers, 45 KB smem: 4 CTAs (32 warps) per SM   // digits per thread in the per-digit phases (2)
 
 struct RsSmem {
   unsigned buf[RS_TILE];                     // tile in digit order: keys, then values
@@ -877,7 +878,7 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
 }
 
 template <int BITS, bool TABLE>
-__global__ void __launch_bounds__(RS_THREADS, 4)
+__global__ void __launch_bounds__(RS_THREADS, RS_MIN_CTAS)
 k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
                 unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, unsigned no, int shift,
                 const unsigned* __restrict__ hist, const unsigned* __restrict__ offs, unsigned ld,
