@@ -77,7 +77,7 @@ def load():
         lib.pg_finish.argtypes = [vp, vp, vp, u32, vp, ctypes.POINTER(ctypes.c_float)]
         lib.pg_stage.argtypes = [vp, ctypes.c_int, vp, u32, vp]
         lib.pg_radix_sort_pairs.argtypes = [vp, vp, vp, vp, vp, i64, ctypes.c_int, u32, vp]
-        lib.pg_pairs.argtypes = [vp, vp, vp, u32, vp]
+        lib.pg_pairs.argtypes = [vp, vp, vp, u32, ctypes.c_int, ctypes.c_int, ctypes.POINTER(u64), vp]
         lib.pg_partition.argtypes = [vp, vp, vp, i64, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp,
                                      ctypes.POINTER(u64), vp]
         lib.pg_sort_cells.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp]
@@ -165,8 +165,13 @@ class Builder:
         return int(self._lib.pg_last_launch_count(self._h))
 
     # sharded-build building blocks (device pointers)
-    def pairs(self, keys, vals, val_offset=0, stream=None):
-        check(self._lib.pg_pairs(self._h, ptr(keys), ptr(vals), int(val_offset), stream))
+    def pairs(self, keys, vals, val_offset=0, coarse_shift=0, coarse_bins=0, stream=None):
+        """Generation-order pairs; with coarse_bins > 0 also returns the histogram of
+        cell >> coarse_shift (slab planning)."""
+        hist = (ctypes.c_uint64 * coarse_bins)() if coarse_bins else None
+        check(self._lib.pg_pairs(self._h, ptr(keys), ptr(vals), int(val_offset), int(coarse_shift),
+                                 int(coarse_bins), hist, stream))
+        return np.ctypeslib.as_array(hist).astype(np.int64) if coarse_bins else None
 
     def partition(self, keys, vals, n, slab_of_bucket, bucket_shift, nslabs, slab_base, keys_out,
                   vals_out, stream=None):

@@ -343,13 +343,20 @@ namespace {
 // counts0_ready (K2 emits them).
 int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned* keys0, unsigned* vals0,
                unsigned* keys1, unsigned* vals1, unsigned* vals_final, uint64_t n, unsigned* hist, unsigned* counts,
-               cudaStream_t st, const unsigned** sorted_keys_out) {
+               cudaStream_t st, const unsigned** sorted_keys_out, unsigned* keys2 = nullptr,
+               unsigned* vals2 = nullptr) {
   const unsigned ntiles = (unsigned)((n + RS_TILE - 1) / RS_TILE);
   const unsigned ld = (ntiles + 3) & ~3u;
+  // pass p reads buffer p%2 and writes (p+1)%2; with keys2/vals2 the input (buffer 0) is
+  // read-only and passes >= 2 use buffer 2 in its place
   unsigned* kbuf[2] = {keys0, keys1};
   unsigned* vbuf[2] = {vals0, vals1};
   for (int p = 0; p < plan.npasses; ++p) {
     const bool last = p == plan.npasses - 1;
+    if (p == 1 && keys2) {
+      kbuf[0] = keys2;
+      vbuf[0] = vals2;
+    }
     unsigned* kin = kbuf[p & 1];
     unsigned* vin = vbuf[p & 1];
     unsigned* ko = kbuf[(p + 1) & 1];
@@ -427,7 +434,7 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
                                                             K2_TILE, k2_tiles, pbounds);
       LAUNCHED("k_pair_tile_bounds", st);
       k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no, dxu, dxyu,
-                                                     pbounds, keysA, v0, 0u);
+                                                     pbounds, keysA, v0, 0u, nullptr, 0, 0);
       LAUNCHED("k_expand_pairs", st);
       b->launches += 2;
       if (flags & PG_KEEP_STAGES) {
@@ -577,24 +584,38 @@ int pg_radix_sort_pairs(pg_builder* b, const uint32_t* keys, const uint32_t* val
 // Building blocks of the sharded (multi-GPU) build: pairs of the counted shard, a stable
 // partition of pairs into cell slabs, and the sort + G tail over one slab.
 // ---------------------------------------------------------------------------------------
-int pg_pairs(pg_builder* b, uint32_t* keys, uint32_t* vals, uint32_t val_offset, void* stream_) {
+int pg_pairs(pg_builder* b, uint32_t* keys, uint32_t* vals, uint32_t val_offset, int coarse_shift, int coarse_bins,
+             uint64_t* coarse_hist, void* stream_) {
   if (!b || !b->counted) return fail(PG_STATE_ERROR, "pg_pairs without a successful pg_count");
+  if (coarse_hist && (coarse_bins < 1 || coarse_bins > 3 * OC_CAP))
+    return fail(PG_INVARIANT_ERROR, "coarse_bins must be in [1, %d]", 3 * OC_CAP);
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   CU(cudaSetDevice(b->device));
   const uint64_t no = b->no;
-  if (no == 0) return PG_OK;
   const unsigned k2_tiles = (unsigned)((no + K2_TILE - 1) / K2_TILE);
   int rc;
-  if ((rc = b->sort_sync.ensure(align_up((size_t)k2_tiles * 8 + 8)))) return rc;
+  const size_t pb_bytes = align_up((size_t)k2_tiles * 8 + 8);
+  if ((rc = b->sort_sync.ensure(pb_bytes + (size_t)std::max(coarse_bins, 1) * 4))) return rc;
   int2* pbounds = b->sort_sync.as<int2>(0);
-  const unsigned dxu = (unsigned)b->dims[0], dxyu = (unsigned)b->dims[0] * (unsigned)b->dims[1];
-  k_pair_tile_bounds<<<(k2_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no, K2_TILE,
-                                                        k2_tiles, pbounds);
-  LAUNCHED("k_pair_tile_bounds", st);
-  k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no, dxu, dxyu,
-                                                 pbounds, keys, vals, val_offset);
-  LAUNCHED("k_expand_pairs", st);
-  b->launches += 2;
+  unsigned* dcoarse = coarse_hist ? b->sort_sync.as<unsigned>(pb_bytes) : nullptr;
+  if (dcoarse) CU(cudaMemsetAsync(dcoarse, 0, (size_t)coarse_bins * 4, st));
+  if (no > 0) {
+    const unsigned dxu = (unsigned)b->dims[0], dxyu = (unsigned)b->dims[0] * (unsigned)b->dims[1];
+    k_pair_tile_bounds<<<(k2_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no,
+                                                          K2_TILE, k2_tiles, pbounds);
+    LAUNCHED("k_pair_tile_bounds", st);
+    k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no, dxu, dxyu,
+                                                   pbounds, keys, vals, val_offset, dcoarse, coarse_shift,
+                                                   coarse_bins);
+    LAUNCHED("k_expand_pairs", st);
+    b->launches += 2;
+  }
+  if (coarse_hist) {
+    std::vector<unsigned> h(coarse_bins);
+    CU(cudaMemcpyAsync(h.data(), dcoarse, (size_t)coarse_bins * 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (int i = 0; i < coarse_bins; ++i) coarse_hist[i] = h[i];
+  }
   return PG_OK;
 }
 
@@ -661,14 +682,14 @@ int pg_sort_cells(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int
   unsigned* counts = b->sort_sync.as<unsigned>(hist_bytes + kb_bytes);
   const unsigned* sorted = keys;
   if (n > 0) {
-    CU(cudaMemcpyAsync(kA, keys, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
     if (plan.npasses == 0) {
       CU(cudaMemcpyAsync(O, vals, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
-      sorted = kA;
     } else {
-      CU(cudaMemcpyAsync(vA, vals, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
       CU(cudaMemsetAsync(hist, 0, hist_bytes, st));
-      if ((rc = run_passes(b, plan, false, kA, vA, kB, vB, O, (uint64_t)n, hist, counts, st, &sorted))) return rc;
+      // pass 0 reads the caller's (const) pairs; later passes ping-pong in the workspace
+      if ((rc = run_passes(b, plan, false, const_cast<unsigned*>(keys), const_cast<unsigned*>(vals), kB, vB, O,
+                           (uint64_t)n, hist, counts, st, &sorted, kA, vA)))
+        return rc;
     }
   }
   k_key_tile_bounds<<<(g_tiles + 1 + 7) / 8, 256, 0, st>>>(sorted, (unsigned)n, G_TILE, (unsigned)ncells, g_tiles + 1,

@@ -346,7 +346,7 @@ constexpr int kMaxBins = 1 << kMaxDigitBits;  // 512
 
 // Object cache for one expansion tile: box records of the tile's triangles olo, olo+1, ...
 // (structure of arrays in shared memory); triangles past OC_CAP are read from global.
-constexpr int OC_CAP = 2560;
+constexpr int OC_CAP = 2560;  // (3*OC_CAP words also host K2's <= 4096-bin coarse histogram)
 struct ObjCache {
   unsigned lo_cell[OC_CAP];
   unsigned mx[OC_CAP];
@@ -518,7 +518,8 @@ k_key_tile_bounds(const unsigned* __restrict__ sorted, unsigned no, unsigned ste
 __global__ void __launch_bounds__(K2_THREADS)
 k_expand_pairs(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, unsigned no,
                unsigned dx, unsigned dxy, const int2* __restrict__ bounds, unsigned* __restrict__ keys,
-               unsigned* __restrict__ vals, unsigned val_offset) {
+               unsigned* __restrict__ vals, unsigned val_offset, unsigned* __restrict__ coarse, int coarse_shift,
+               int coarse_bins) {
   __shared__ __align__(16) int slot[K2_TILE];
   __shared__ int warpmax[K2_THREADS / 32];
   __shared__ ObjCache oc;
@@ -528,6 +529,28 @@ k_expand_pairs(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_
   int own[K2_ITEMS];
   expand_tile<K2_THREADS, K2_ITEMS>(rec, n, p0, pend, dx, dxy, tile_pre, bounds, slot, warpmax, &oc, key, own);
   const unsigned pbase = p0 + threadIdx.x * K2_ITEMS;
+  if (coarse) {  // coarse cell-bucket histogram for slab planning (sharded builds)
+    unsigned* hc = reinterpret_cast<unsigned*>(oc.lo_cell);  // object cache is dead now
+    __syncthreads();
+    for (int b = threadIdx.x; b < coarse_bins; b += K2_THREADS) hc[b] = 0u;
+    __syncthreads();
+    unsigned cur = 0xffffffffu, cnt = 0;
+#pragma unroll
+    for (int j = 0; j < K2_ITEMS; ++j)
+      if (pbase + j < pend) {
+        const unsigned b = key[j] >> coarse_shift;
+        if (b != cur) {
+          if (cnt) atomicAdd(&hc[cur], cnt);
+          cur = b;
+          cnt = 0;
+        }
+        ++cnt;
+      }
+    if (cnt) atomicAdd(&hc[cur], cnt);
+    __syncthreads();
+    for (int b = threadIdx.x; b < coarse_bins; b += K2_THREADS)
+      if (hc[b]) atomicAdd(&coarse[b], hc[b]);
+  }
   if (pbase + K2_ITEMS <= pend) {
     uint4* kd = reinterpret_cast<uint4*>(keys + pbase);
     uint4* vd = reinterpret_cast<uint4*>(vals + pbase);

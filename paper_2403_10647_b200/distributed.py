@@ -92,12 +92,12 @@ class ShardState:
         self.V, self.T, self.tri_base = V, T, tri_base
 
     def phase_count(self):
-        """K1 + K2 on the shard; returns the local coarse histogram."""
+        """K1 + K2 on the shard; returns the local coarse histogram (computed by K2)."""
         self.no = self.ops.count(self.V, self.T, self.spec)
-        self.keys, self.vals = self.ops.pairs(self.no, self.tri_base)
         self.shift = coarse_shift(self.ncells)
         nb = ((self.ncells - 1) >> self.shift) + 1
-        return self.ops.coarse_hist(self.keys, self.shift, nb)
+        self.keys, self.vals, hist = self.ops.pairs(self.no, self.tri_base, self.shift, nb)
+        return hist
 
     def phase_partition(self, plan):
         """Stable partition by slab; returns the per-slab send counts."""
@@ -171,8 +171,10 @@ class TorchComm:
         return [int(x) for x in r.cpu().numpy()]
 
     def alltoall_pairs(self, keys, vals, send, recv, ops):
-        kr = ops.empty_pairs(sum(recv))
-        vr = ops.empty_pairs(sum(recv))
+        if hasattr(ops, "recv_buffers"):
+            kr, vr = ops.recv_buffers(sum(recv))
+        else:
+            kr, vr = ops.empty_pairs(sum(recv)), ops.empty_pairs(sum(recv))
         self.dist.all_to_all_single(kr, ops.as_tensor(keys), recv, send, group=self.group)
         self.dist.all_to_all_single(vr, ops.as_tensor(vals), recv, send, group=self.group)
         return kr, vr
@@ -209,7 +211,10 @@ def run_emulated(make_ops, V, T, spec, world):
 
 
 class CudaOps:
-    """Per-rank device steps on this rank's GPU: libpgrid kernels on torch-allocated memory."""
+    """Per-rank device steps on this rank's GPU: libpgrid kernels on torch-allocated memory.
+
+    Buffers are grow-only and reused across builds (named slots), so a steady-state sharded
+    build allocates nothing -- cudaMalloc inside the step would serialise the device."""
 
     def __init__(self, device=0, stream=None):
         import torch
@@ -219,16 +224,29 @@ class CudaOps:
         self.dev = torch.device("cuda", device)
         self.b = _native.Builder(device)
         self.stream = stream
+        self._bufs = {}
 
     def _sp(self):
         s = self.stream or self.torch.cuda.current_stream(self.dev)
         return s.cuda_stream
 
+    def _buf(self, name, n):
+        t = self._bufs.get(name)
+        if t is None or t.numel() < n:
+            t = self.torch.empty(max(int(n * 1.25), 16), dtype=self.torch.int32, device=self.dev)
+            self._bufs[name] = t
+        return t[:n]
+
     def as_tensor(self, x):
         return x
 
-    def empty_pairs(self, n):
-        return self.torch.empty(n, dtype=self.torch.int32, device=self.dev)
+    def empty_pairs(self, n, name=None):
+        if name is None:
+            return self.torch.empty(n, dtype=self.torch.int32, device=self.dev)
+        return self._buf(name, n)
+
+    def recv_buffers(self, n):
+        return self._buf("recv_k", n), self._buf("recv_v", n)
 
     def length(self, x):
         return int(x.numel())
@@ -251,29 +269,23 @@ class CudaOps:
         self._V, self._T = V, T          # keep alive for the stream
         return self.b.count(V, V.shape[0], T, T.shape[0], spec, 0, self._sp())
 
-    def pairs(self, no, tri_base):
-        k, v = self.empty_pairs(no), self.empty_pairs(no)
-        self.b.pairs(k, v, tri_base, self._sp())
-        return k, v
-
-    def coarse_hist(self, keys, shift, nbuckets):
-        if keys.numel() == 0:
-            return np.zeros(nbuckets, np.int64)
-        # slab planning only (not on the pair data path): a 4096-bin histogram
-        h = self.torch.bincount((keys >> shift).long(), minlength=nbuckets)
-        return h.cpu().numpy().astype(np.int64)
+    def pairs(self, no, tri_base, shift, nbuckets):
+        k, v = self._buf("pair_k", no), self._buf("pair_v", no)
+        hist = self.b.pairs(k, v, tri_base, shift, nbuckets, self._sp())
+        return k, v, hist
 
     def partition(self, keys, vals, table, shift, nslabs, base):
         torch = self.torch
         n = int(keys.numel())
-        dt = torch.from_numpy(np.asarray(table, np.uint32).view(np.int32)).to(self.dev)
-        db = torch.from_numpy(np.asarray(base, np.uint32).view(np.int32)).to(self.dev)
-        ko, vo = self.empty_pairs(n), self.empty_pairs(n)
+        dt = torch.from_numpy(np.asarray(table, np.uint32).view(np.int32)).to(self.dev, non_blocking=False)
+        db = torch.from_numpy(np.asarray(base, np.uint32).view(np.int32)).to(self.dev, non_blocking=False)
+        self._tables = (dt, db)
+        ko, vo = self._buf("part_k", n), self._buf("part_v", n)
         counts = self.b.partition(keys, vals, n, dt, shift, nslabs, db, ko, vo, self._sp())
         return ko, vo, counts
 
     def sort_cells(self, keys, vals, n, ncells):
-        G = self.torch.empty(ncells + 1, dtype=self.torch.int32, device=self.dev)
-        O = self.empty_pairs(n)
+        G = self._buf("G", ncells + 1)
+        O = self._buf("O", n)
         self.b.sort_cells(keys, vals, n, ncells, G, O, self._sp())
         return G, O

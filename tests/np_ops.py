@@ -37,7 +37,7 @@ class NumpyOps:
         self._cnt = np.where(keep, m[:, 0] * m[:, 1] * m[:, 2], 0)
         return int(self._cnt.sum())
 
-    def pairs(self, no, tri_base):
+    def pairs(self, no, tri_base, shift, nbuckets):
         keys = np.empty(no, np.uint32)
         vals = np.empty(no, np.uint32)
         dx, dy = self._dims[0], self._dims[1]
@@ -50,10 +50,8 @@ class NumpyOps:
             keys[p:p + len(cells)] = cells
             vals[p:p + len(cells)] = tri_base + i
             p += len(cells)
-        return keys, vals
-
-    def coarse_hist(self, keys, shift, nbuckets):
-        return np.bincount(np.asarray(keys, np.int64) >> shift, minlength=nbuckets).astype(np.int64)
+        hist = np.bincount(keys.astype(np.int64) >> shift, minlength=nbuckets).astype(np.int64)
+        return keys, vals, hist
 
     def partition(self, keys, vals, table, shift, nslabs, base):
         keys = np.asarray(keys, np.uint32)
