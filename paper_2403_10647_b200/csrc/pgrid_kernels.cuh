@@ -603,8 +603,7 @@ constexpr int RS_MIN_CTAS = 4;  // 64 registers, 45 KB smem: 4 CTAs (32 warps) p
 struct RsSmem {
   unsigned buf[RS_TILE];                     // tile in digit order: keys, then values
   unsigned vstage[RS_TILE];                  // values in input order (cp.async staging)
-  unsigned short whist[RS_WARPS][kMaxBins];  // per-warp digit counts -> exclusive warp offsets
-  unsigned local_start[kMaxBins];            // tile-local exclusive digit prefix
+  unsigned short whist[RS_WARPS][kMaxBins];  // per-warp digit counts -> tile offset of (warp, digit)
   unsigned gbase[kMaxBins];                  // global position of buf[0] for each digit
   unsigned wsum[RS_WARPS];
 };
@@ -858,7 +857,9 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
   for (int q = 0; q < RS_DPT; ++q) {
     const int d = tid * RS_DPT + q;
     if (d < NB) {
-      sm.local_start[d] = lpre;
+      // fold the tile-local digit start into every warp's offset: one lookup per item below
+#pragma unroll
+      for (int w = 0; w < RS_WARPS; ++w) sm.whist[w][d] = (unsigned short)(sm.whist[w][d] + lpre);
       sm.gbase[d] = hpre + __ldg(&offs[(size_t)d * ld + tile]) - lpre;
     }
     lpre += tc[q];
@@ -869,7 +870,7 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
 #pragma unroll
   for (int j = 0; j < RS_ITEMS; ++j) {
     if (valid(j)) {
-      rank[j] += sm.local_start[dg[j]] + sm.whist[warp][dg[j]];  // rank -> tile position
+      rank[j] += sm.whist[warp][dg[j]];  // rank -> tile position
       sm.buf[rank[j]] = ksrc[elem(j)];
     }
   }
