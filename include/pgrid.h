@@ -33,6 +33,7 @@ extern "C" {
 #define PG_INVARIANT_ERROR 2   /* precondition violated (primitives.py:22-25, gridcore.py:44-52) */
 #define PG_CUDA_ERROR 3        /* CUDA runtime failure */
 #define PG_STATE_ERROR 4       /* call sequence violated (finish before count, ...) */
+#define PG_CAPACITY_ERROR 5    /* pg_build_wait: NO exceeded the O capacity given to pg_build_async */
 
 /* Flags. */
 #define PG_HOST_INPUT 1u       /* V/T (or sort inputs) are host pointers: copied H2D in-call */
@@ -72,6 +73,14 @@ int pg_count(pg_builder *b, const double *V, int64_t nv, const int32_t *T, int64
  * phase_ms may be NULL. */
 int pg_finish(pg_builder *b, uint32_t *G, uint32_t *O, uint32_t flags, void *stream,
               float *phase_ms);
+
+/* Sync-free build on device-resident V/T/G/O (no host round trip between K1 and the sort):
+ * enqueues the whole of Alg. 1 on `stream` with every buffer sized for o_capacity pairs;
+ * identical repeated calls replay a captured CUDA graph. pg_build_wait synchronises and
+ * returns NO (PG_CAPACITY_ERROR if NO > o_capacity: enlarge O and call again). */
+int pg_build_async(pg_builder *b, const double *V, int64_t nv, const int32_t *T, int64_t n,
+                   const pg_spec *spec, uint32_t *G, uint32_t *O, uint64_t o_capacity, void *stream);
+int pg_build_wait(pg_builder *b, uint64_t *no_out);
 
 /* Record support (builders.py:138-140, 161-163): copy one stage of the last build into dst.
  *   stage 0: per-triangle record u32[n][4] = {lo_cell, mx, my, pair offset} (count==0 <=> dropped)

@@ -20,6 +20,7 @@ PG_SIZE_ERROR = 1
 PG_INVARIANT_ERROR = 2
 PG_CUDA_ERROR = 3
 PG_STATE_ERROR = 4
+PG_CAPACITY_ERROR = 5
 
 PG_HOST_INPUT = 1
 PG_HOST_OUTPUT = 2
@@ -29,7 +30,8 @@ NPHASES = 6
 
 # every symbol include/pgrid.h declares (checked by tests/test_boundary.py)
 EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
-           "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_host_register",
+           "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_build_async",
+           "pg_build_wait", "pg_host_register",
            "pg_host_unregister", "pg_host_alloc", "pg_host_free", "pg_last_launch_count",
            "pg_last_error")
 
@@ -81,6 +83,8 @@ def load():
         lib.pg_partition.argtypes = [vp, vp, vp, i64, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp,
                                      ctypes.POINTER(u64), vp]
         lib.pg_sort_cells.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp]
+        lib.pg_build_async.argtypes = [vp, vp, i64, vp, i64, ctypes.POINTER(PgSpec), vp, vp, u64, vp]
+        lib.pg_build_wait.argtypes = [vp, ctypes.POINTER(u64)]
         lib.pg_host_register.argtypes = [vp, u64]
         lib.pg_host_unregister.argtypes = [vp]
         lib.pg_host_alloc.argtypes = [u64, ctypes.POINTER(vp)]
@@ -89,7 +93,7 @@ def load():
         lib.pg_last_error.restype = ctypes.c_char_p
         for name in ("pg_builder_create", "pg_count", "pg_finish", "pg_stage",
                      "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells",
-                     "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
+                     "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
                      "pg_last_launch_count"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
@@ -163,6 +167,21 @@ class Builder:
 
     def launches(self):
         return int(self._lib.pg_last_launch_count(self._h))
+
+    def build_async(self, V, nv, T, n, spec, G, O, capacity, stream=None, pgspec=None):
+        """Sync-free device build (CUDA-graph replay for repeated identical calls)."""
+        s = pgspec or PgSpec.from_spec(spec)
+        check(self._lib.pg_build_async(self._h, ptr(V), int(nv), ptr(T), int(n), ctypes.byref(s), ptr(G),
+                                       ptr(O), int(capacity), stream))
+
+    def build_wait(self):
+        """Synchronise the last build_async; returns NO (-NO if it exceeded the capacity)."""
+        no = ctypes.c_uint64(0)
+        rc = self._lib.pg_build_wait(self._h, ctypes.byref(no))
+        if rc == PG_CAPACITY_ERROR:
+            return -int(no.value)
+        check(rc)
+        return int(no.value)
 
     # sharded-build building blocks (device pointers)
     def pairs(self, keys, vals, val_offset=0, coarse_shift=0, coarse_bins=0, stream=None):

@@ -98,7 +98,7 @@ size_t rs_smem_bytes() { return sizeof(RsSmem); }
 
 template <int BITS, bool TABLE>
 void launch_scatter_bits(unsigned ntiles, cudaStream_t st, const unsigned* kin, const unsigned* vin, unsigned* ko,
-                         unsigned* vo, unsigned n, int shift, const unsigned* hist, const unsigned* offs, unsigned ld,
+                         unsigned* vo, Count n, int shift, const unsigned* hist, const unsigned* offs, unsigned ld,
                          const unsigned* dtable, const unsigned* kbase) {
   k_radix_scatter<BITS, TABLE><<<ntiles, RS_THREADS, rs_smem_bytes(), st>>>(kin, vin, ko, vo, n, shift, hist, offs,
                                                                            ld, dtable, kbase);
@@ -106,7 +106,7 @@ void launch_scatter_bits(unsigned ntiles, cudaStream_t st, const unsigned* kin, 
 
 // bit-field digits of 1..9 bits, or (dtable != null) slab-table digits of 1..4 bits
 void launch_radix_scatter(int bits, unsigned ntiles, cudaStream_t st, const unsigned* kin, const unsigned* vin,
-                          unsigned* ko, unsigned* vo, unsigned n, int shift, const unsigned* hist,
+                          unsigned* ko, unsigned* vo, Count n, int shift, const unsigned* hist,
                           const unsigned* offs, unsigned ld, const unsigned* dtable = nullptr,
                           const unsigned* kbase = nullptr) {
   if (dtable) {
@@ -184,6 +184,14 @@ struct pg_builder {
   int launches = 0;
   const unsigned* sorted_keys = nullptr;
   const unsigned* tile_pre = nullptr;  // K1 tile prefixes of the last pg_count
+  unsigned long long* d_total = nullptr;  // device NO of the last count
+  // sync-free build (pg_build_async): private stream, events, and the captured CUDA graph
+  cudaStream_t gst = nullptr;
+  cudaEvent_t g_in = nullptr, g_out = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<unsigned char> gkey;
+  uint64_t g_cap = 0;
+  int glaunches = 0;
 };
 
 extern "C" {
@@ -212,6 +220,10 @@ void pg_builder_destroy(pg_builder* b) {
   for (auto& e : b->ev)
     if (e) cudaEventDestroy(e);
   if (b->h_scalars) cudaFreeHost(b->h_scalars);
+  if (b->gexec) cudaGraphExecDestroy(b->gexec);
+  if (b->g_in) cudaEventDestroy(b->g_in);
+  if (b->g_out) cudaEventDestroy(b->g_out);
+  if (b->gst) cudaStreamDestroy(b->gst);
   for (DevBuf* d : {&b->in_v, &b->in_t, &b->rec, &b->k1_sync, &b->pairs, &b->sort_sync, &b->stage, &b->stage0,
                     &b->gbuf, &b->obuf})
     d->release();
@@ -245,11 +257,10 @@ int pg_host_unregister(void* ptr) {
 
 int pg_last_launch_count(pg_builder* b) { return b ? b->launches : 0; }
 
-int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64_t n, const pg_spec* spec,
-             uint32_t flags, void* stream_, uint64_t* no_out) {
-  if (!b || !spec || !no_out) return fail(PG_INVARIANT_ERROR, "null argument");
-  cudaStream_t st = static_cast<cudaStream_t>(stream_);
-  CU(cudaSetDevice(b->device));
+namespace {
+
+// Validation + builder state for a build of (n triangles, spec); fills the device spec.
+int count_setup(pg_builder* b, int64_t nv, int64_t n, const pg_spec* spec, DevSpec& ds) {
   b->counted = false;
   b->stages_kept = false;
   b->k1_timed = false;
@@ -264,11 +275,9 @@ int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64
   }
   // The reference raises SizeError once the G scan sees more than 2^30 cells
   // (primitives.py:29-31 via builders.py:130); every successful build has ncells <= 2^30.
-  if (ncells > kMaxScan) return fail(PG_SIZE_ERROR, "array of %lld elements exceeds the scan size limit", (long long)ncells);
+  if (ncells > kMaxScan)
+    return fail(PG_SIZE_ERROR, "array of %lld elements exceeds the scan size limit", (long long)ncells);
   if (n > kMaxScan) return fail(PG_SIZE_ERROR, "%lld triangles exceed the scan size limit", (long long)n);
-  if (n > 0 && (!V || !T)) return fail(PG_INVARIANT_ERROR, "null mesh arrays");
-
-  DevSpec ds;
   for (int k = 0; k < 3; ++k) {
     ds.lo[k] = spec->lo[k];
     ds.hi[k] = spec->hi[k];
@@ -279,24 +288,13 @@ int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64
   b->n = n;
   b->ncells = ncells;
   b->key_bits = bit_length((uint64_t)(ncells - 1));  // builders.py:124
+  return PG_OK;
+}
 
-  if (n == 0) {
-    b->no = 0;
-    *no_out = 0;
-    b->counted = true;
-    return PG_OK;
-  }
-  const double* dV = V;
-  const int32_t* dT = T;
-  if (flags & PG_HOST_INPUT) {
-    int rc;
-    if ((rc = b->in_v.ensure((size_t)nv * 3 * sizeof(double)))) return rc;
-    if ((rc = b->in_t.ensure((size_t)n * 3 * sizeof(int32_t)))) return rc;
-    CU(cudaMemcpyAsync(b->in_v.p, V, (size_t)nv * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(b->in_t.p, T, (size_t)n * 3 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    dV = b->in_v.as<double>();
-    dT = b->in_t.as<int32_t>();
-  }
+// K1 + cross-tile scan on device-resident V/T (n >= 1); NO and the error flags are copied
+// to the pinned b->h_scalars asynchronously (read them after the stream is synchronised).
+int count_enqueue(pg_builder* b, const double* dV, int64_t nv, const int32_t* dT, int64_t n, const DevSpec& ds,
+                  cudaStream_t st) {
   const unsigned ntiles = (unsigned)((n + K1_TILE - 1) / K1_TILE);
   int rc;
   if ((rc = b->rec.ensure((size_t)n * sizeof(uint4)))) return rc;
@@ -308,6 +306,7 @@ int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64
   unsigned* err = b->k1_sync.as<unsigned>(ts_bytes + tp_bytes);
   unsigned long long* total = b->k1_sync.as<unsigned long long>(ts_bytes + tp_bytes + 8);
   b->tile_pre = tile_pre;
+  b->d_total = total;
   CU(cudaMemsetAsync(err, 0, 16, st));
   CU(cudaEventRecord(b->ev[5], st));
   // TMA bulk staging needs 16-byte aligned sources
@@ -322,17 +321,61 @@ int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64
   b->k1_timed = true;
   CU(cudaMemcpyAsync(&b->h_scalars[0], total, 8, cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(&b->h_scalars[1], err, 4, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
+  return PG_OK;
+}
+
+// Error checks on the NO / flags that count_enqueue copied back (stream synchronised).
+int count_check(pg_builder* b, uint64_t* no_out) {
   const uint64_t no = b->h_scalars[0];
   const unsigned errf = (unsigned)(b->h_scalars[1] & 0xffffffffu);
-  *no_out = no;
+  if (no_out) *no_out = no;
   if (errf & 2u) return fail(PG_INVARIANT_ERROR, "triangle index out of range");
   if (errf & 1u) return fail(PG_INVARIANT_ERROR, "triangle cell box with hi < lo (non-finite or huge upper corner)");
-  if ((int64_t)no > kMaxIds) return fail(PG_SIZE_ERROR, "%llu cell/object pairs exceed 32-bit id space", (unsigned long long)no);
-  if ((int64_t)no > kMaxScan) return fail(PG_SIZE_ERROR, "array of %llu elements exceeds the scan size limit", (unsigned long long)no);
+  if ((int64_t)no > kMaxIds)
+    return fail(PG_SIZE_ERROR, "%llu cell/object pairs exceed 32-bit id space", (unsigned long long)no);
+  if ((int64_t)no > kMaxScan)
+    return fail(PG_SIZE_ERROR, "array of %llu elements exceeds the scan size limit", (unsigned long long)no);
   b->no = no;
   b->counted = true;
   return PG_OK;
+}
+
+void drop_graph(pg_builder* b) {
+  if (b->gexec) cudaGraphExecDestroy(b->gexec);
+  b->gexec = nullptr;
+}
+
+}  // namespace
+
+int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64_t n, const pg_spec* spec,
+             uint32_t flags, void* stream_, uint64_t* no_out) {
+  if (!b || !spec || !no_out) return fail(PG_INVARIANT_ERROR, "null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  drop_graph(b);
+  DevSpec ds;
+  int rc;
+  if ((rc = count_setup(b, nv, n, spec, ds))) return rc;
+  if (n == 0) {
+    b->no = 0;
+    *no_out = 0;
+    b->counted = true;
+    return PG_OK;
+  }
+  if (!V || !T) return fail(PG_INVARIANT_ERROR, "null mesh arrays");
+  const double* dV = V;
+  const int32_t* dT = T;
+  if (flags & PG_HOST_INPUT) {
+    if ((rc = b->in_v.ensure((size_t)nv * 3 * sizeof(double)))) return rc;
+    if ((rc = b->in_t.ensure((size_t)n * 3 * sizeof(int32_t)))) return rc;
+    CU(cudaMemcpyAsync(b->in_v.p, V, (size_t)nv * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(b->in_t.p, T, (size_t)n * 3 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    dV = b->in_v.as<double>();
+    dT = b->in_t.as<int32_t>();
+  }
+  if ((rc = count_enqueue(b, dV, nv, dT, n, ds, st))) return rc;
+  CU(cudaStreamSynchronize(st));
+  return count_check(b, no_out);
 }
 
 namespace {
@@ -342,10 +385,11 @@ namespace {
 // `counts` holds one [digit][tile] matrix (row stride ld), already filled for pass 0 when
 // counts0_ready (K2 emits them).
 int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned* keys0, unsigned* vals0,
-               unsigned* keys1, unsigned* vals1, unsigned* vals_final, uint64_t n, unsigned* hist, unsigned* counts,
-               cudaStream_t st, const unsigned** sorted_keys_out, unsigned* keys2 = nullptr,
+               unsigned* keys1, unsigned* vals1, unsigned* vals_final, Count cno, uint64_t cap, unsigned* hist,
+               unsigned* counts, cudaStream_t st, const unsigned** sorted_keys_out, unsigned* keys2 = nullptr,
                unsigned* vals2 = nullptr) {
-  const unsigned ntiles = (unsigned)((n + RS_TILE - 1) / RS_TILE);
+  // grids are sized for `cap` pairs; the kernels read the actual count from `cno`
+  const unsigned ntiles = (unsigned)((cap + RS_TILE - 1) / RS_TILE);
   const unsigned ld = (ntiles + 3) & ~3u;
   // pass p reads buffer p%2 and writes (p+1)%2; with keys2/vals2 the input (buffer 0) is
   // read-only and passes >= 2 use buffer 2 in its place
@@ -363,15 +407,15 @@ int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned
     unsigned* vo = last ? vals_final : vbuf[(p + 1) & 1];
     if (p > 0 || !counts0_ready) {
       const DigitFn dig{plan.shift[p], (1u << plan.bits[p]) - 1u, nullptr};
-      k_tile_counts<<<(ntiles + TC_TILES - 1) / TC_TILES, RS_THREADS, 0, st>>>(kin, (unsigned)n, dig,
-                                                                              1 << plan.bits[p], counts, ld);
+      k_tile_counts<<<(ntiles + TC_TILES - 1) / TC_TILES, RS_THREADS, 0, st>>>(kin, cno, dig, 1 << plan.bits[p],
+                                                                              counts, ld);
       LAUNCHED("k_tile_counts", st);
       ++b->launches;
     }
-    k_scan_tile_counts<<<1u << plan.bits[p], SC_THREADS, 0, st>>>(counts, ntiles, ld, hist + p * kMaxBins);
+    k_scan_tile_counts<<<1u << plan.bits[p], SC_THREADS, 0, st>>>(counts, cno, ld, hist + p * kMaxBins);
     LAUNCHED("k_scan_tile_counts", st);
-    launch_radix_scatter(plan.bits[p], ntiles, st, kin, vin, ko, vo, (unsigned)n, plan.shift[p], hist + p * kMaxBins,
-                         counts, ld);
+    launch_radix_scatter(plan.bits[p], ntiles, st, kin, vin, ko, vo, cno, plan.shift[p], hist + p * kMaxBins, counts,
+                         ld);
     LAUNCHED("k_radix_scatter", st);
     b->launches += 2;
     *sorted_keys_out = ko;
@@ -381,11 +425,11 @@ int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned
 
 }  // namespace
 
-int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* stream_, float* phase_ms) {
-  if (!b || !b->counted) return fail(PG_STATE_ERROR, "pg_finish without a successful pg_count");
-  cudaStream_t st = static_cast<cudaStream_t>(stream_);
-  CU(cudaSetDevice(b->device));
-  const uint64_t no = b->no;
+// Pair expansion -> radix passes -> G for the last counted mesh. `cno` carries the pair
+// count (host value, or device pointer for the sync-free build); every buffer and grid is
+// sized for `no` = its capacity bound.
+int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStream_t st, float* phase_ms, Count cno,
+                uint64_t no) {
   const int64_t ncells = b->ncells;
   const PassPlan plan = make_plan(b->key_bits, kMaxDigitBits);
   int rc;
@@ -430,11 +474,11 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
       // pairs in generation order: final when there is no radix pass (vals -> O), and the
       // record= stage dump otherwise
       unsigned* v0 = plan.npasses == 0 ? dO : valsA;
-      k_pair_tile_bounds<<<(k2_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no,
-                                                            K2_TILE, k2_tiles, pbounds);
+      k_pair_tile_bounds<<<(k2_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, cno, K2_TILE,
+                                                            pbounds);
       LAUNCHED("k_pair_tile_bounds", st);
-      k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no, dxu, dxyu,
-                                                     pbounds, keysA, v0, 0u, nullptr, 0, 0);
+      k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, cno, dxu, dxyu, pbounds,
+                                                     keysA, v0, 0u, nullptr, 0, 0);
       LAUNCHED("k_expand_pairs", st);
       b->launches += 2;
       if (flags & PG_KEEP_STAGES) {
@@ -447,21 +491,22 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
     }
     if (plan.npasses > 0) {
       // K2 on radix tiles: pairs in generation order + first-pass tile counts
-      k_pair_tile_bounds<<<(rs_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no,
-                                                            RS_TILE, rs_tiles, pbounds);
+      k_pair_tile_bounds<<<(rs_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, cno, RS_TILE,
+                                                            pbounds);
       LAUNCHED("k_pair_tile_bounds", st);
       // K2 writes its first-pass tile counts tile-major into the B key buffer (free until
       // pass 0 scatters into it), then they are transposed into the digit-major matrix
       unsigned* tm = keysB;
-      k_pairs_emit<<<rs_tiles, RS_THREADS, sizeof(PeSmem), st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no,
-                                                                 dxu, dxyu, plan, pbounds, keysA, valsA, tm);
+      k_pairs_emit<<<rs_tiles, RS_THREADS, sizeof(PeSmem), st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, cno, dxu,
+                                                                 dxyu, plan, pbounds, keysA, valsA, tm);
       LAUNCHED("k_pairs_emit", st);
       k_transpose_counts<<<dim3((rs_tiles + 31) / 32, ((1u << plan.bits[0]) + 31) / 32), 256, 0, st>>>(
-          tm, rs_tiles, 1 << plan.bits[0], counts, ld);
+          tm, cno, 1 << plan.bits[0], counts, ld);
       LAUNCHED("k_transpose_counts", st);
       b->launches += 3;
       CU(cudaEventRecord(b->ev[1], st));
-      if ((rc = run_passes(b, plan, true, keysA, valsA, keysB, valsB, dO, no, hist, counts, st, &sorted))) return rc;
+      if ((rc = run_passes(b, plan, true, keysA, valsA, keysB, valsB, dO, cno, no, hist, counts, st, &sorted)))
+        return rc;
     } else {
       CU(cudaEventRecord(b->ev[1], st));
     }
@@ -469,10 +514,10 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
     CU(cudaEventRecord(b->ev[1], st));
   }
   CU(cudaEventRecord(b->ev[2], st));
-  k_key_tile_bounds<<<(g_tiles + 1 + 7) / 8, 256, 0, st>>>(sorted, (unsigned)no, G_TILE, (unsigned)ncells, g_tiles + 1,
+  k_key_tile_bounds<<<(g_tiles + 1 + 7) / 8, 256, 0, st>>>(sorted, cno, G_TILE, (unsigned)ncells, g_tiles + 1,
                                                           kbounds);
   LAUNCHED("k_key_tile_bounds", st);
-  k_cell_offsets<<<g_tiles, G_THREADS, 0, st>>>(sorted, (unsigned)no, (unsigned)ncells, kbounds, dG);
+  k_cell_offsets<<<g_tiles, G_THREADS, 0, st>>>(sorted, cno, (unsigned)ncells, kbounds, dG);
   LAUNCHED("k_cell_offsets", st);
   b->launches += 2;
   b->sorted_keys = sorted;
@@ -498,6 +543,92 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
     phase_ms[4] = 0.f;  // rle: fused into finalize (K4)
     phase_ms[5] = t23 + t34;  // finalize: K4 (+ D2H of G/O for host outputs)
   }
+  return PG_OK;
+}
+
+int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* stream_, float* phase_ms) {
+  if (!b || !b->counted) return fail(PG_STATE_ERROR, "pg_finish without a successful pg_count");
+  CU(cudaSetDevice(b->device));
+  drop_graph(b);
+  return finish_impl(b, G, O, flags, static_cast<cudaStream_t>(stream_), phase_ms, Count{nullptr, (unsigned)b->no},
+                     b->no);
+}
+
+// Sync-free build on device-resident data: the whole of Alg. 1 is enqueued without reading
+// NO back (kernels after K1 take it from device memory; buffers and grids are sized for
+// o_capacity). The first call with a given argument set runs eagerly (allocating the
+// workspace) and then captures the same enqueue sequence into a CUDA graph; later calls
+// with identical arguments replay the graph. Ordering with `stream` is kept with events.
+// pg_build_wait() synchronises and reports NO and any error; PG_CAPACITY_ERROR means NO
+// exceeded o_capacity (G/O are then invalid: grow O and rebuild).
+int pg_build_async(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64_t n, const pg_spec* spec,
+                   uint32_t* G, uint32_t* O, uint64_t o_capacity, void* stream_) {
+  if (!b || !spec || !G) return fail(PG_INVARIANT_ERROR, "null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  if (!b->gst) {
+    CU(cudaStreamCreateWithFlags(&b->gst, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&b->g_in, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&b->g_out, cudaEventDisableTiming));
+  }
+  const uint64_t cap = std::max<uint64_t>(std::min<uint64_t>(o_capacity, (uint64_t)kMaxScan), 1);
+  // graph key: every argument the enqueue sequence depends on
+  std::vector<unsigned char> key(sizeof(pg_spec) + 8 * sizeof(uint64_t));
+  {
+    const uint64_t k[8] = {(uint64_t)(uintptr_t)V, (uint64_t)nv, (uint64_t)(uintptr_t)T, (uint64_t)n,
+                           (uint64_t)(uintptr_t)G, (uint64_t)(uintptr_t)O, cap, 0};
+    memcpy(key.data(), spec, sizeof(pg_spec));
+    memcpy(key.data() + sizeof(pg_spec), k, sizeof k);
+  }
+  CU(cudaEventRecord(b->g_in, st));
+  CU(cudaStreamWaitEvent(b->gst, b->g_in, 0));
+  if (b->gexec && key == b->gkey) {
+    CU(cudaGraphLaunch(b->gexec, b->gst));
+    b->launches = b->glaunches;
+  } else {
+    drop_graph(b);
+    DevSpec ds;
+    int rc;
+    if ((rc = count_setup(b, nv, n, spec, ds))) return rc;
+    if (n == 0 || !V || !T) return fail(PG_INVARIANT_ERROR, "pg_build_async needs a non-empty device mesh");
+    auto enqueue = [&](cudaStream_t s2) -> int {
+      int r;
+      if ((r = count_enqueue(b, V, nv, T, n, ds, s2))) return r;
+      return finish_impl(b, G, O, 0, s2, nullptr, Count{b->d_total, (unsigned)cap}, cap);
+    };
+    if ((rc = enqueue(b->gst))) return rc;  // eager run: sizes the workspace
+    b->glaunches = b->launches;
+    if (!sync_debug()) {
+      cudaGraph_t graph = nullptr;
+      CU(cudaStreamBeginCapture(b->gst, cudaStreamCaptureModeThreadLocal));
+      rc = enqueue(b->gst);
+      cudaError_t ec = cudaStreamEndCapture(b->gst, &graph);
+      if (rc) return rc;
+      if (ec != cudaSuccess) return fail(PG_CUDA_ERROR, "graph capture failed: %s", cudaGetErrorString(ec));
+      cudaError_t ei = cudaGraphInstantiate(&b->gexec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ei != cudaSuccess) {
+        b->gexec = nullptr;
+        return fail(PG_CUDA_ERROR, "graph instantiate failed: %s", cudaGetErrorString(ei));
+      }
+      b->gkey = key;
+    }
+  }
+  b->g_cap = cap;
+  CU(cudaEventRecord(b->g_out, b->gst));
+  CU(cudaStreamWaitEvent(st, b->g_out, 0));
+  return PG_OK;
+}
+
+int pg_build_wait(pg_builder* b, uint64_t* no_out) {
+  if (!b || !b->gst) return fail(PG_STATE_ERROR, "no asynchronous build in flight");
+  CU(cudaSetDevice(b->device));
+  CU(cudaStreamSynchronize(b->gst));
+  int rc = count_check(b, no_out);
+  if (rc) return rc;
+  if (b->no > b->g_cap)
+    return fail(PG_CAPACITY_ERROR, "NO = %llu exceeds the O capacity %llu", (unsigned long long)b->no,
+                (unsigned long long)b->g_cap);
   return PG_OK;
 }
 
@@ -541,6 +672,7 @@ int pg_radix_sort_pairs(pg_builder* b, const uint32_t* keys, const uint32_t* val
   if (n > kMaxScan) return fail(PG_SIZE_ERROR, "sort of %lld pairs exceeds the size limit", (long long)n);
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   CU(cudaSetDevice(b->device));
+  drop_graph(b);
   b->counted = false;
   b->launches = 0;
   if (n == 0) return PG_OK;
@@ -569,7 +701,8 @@ int pg_radix_sort_pairs(pg_builder* b, const uint32_t* keys, const uint32_t* val
     // host outputs: final values land in the staging section behind the pair buffers
     if ((rc = b->stage.ensure(sec))) return rc;
     unsigned* vdst = (flags & PG_HOST_OUTPUT) ? b->stage.as<unsigned>() : vals_out;
-    if ((rc = run_passes(b, plan, false, kA, vA, kB, vB, vdst, (uint64_t)n, hist, counts, st, &sorted)))
+    if ((rc = run_passes(b, plan, false, kA, vA, kB, vB, vdst, Count{nullptr, (unsigned)n}, (uint64_t)n, hist, counts,
+                         st, &sorted)))
       return rc;
     vfinal = vdst;
   }
@@ -591,6 +724,7 @@ int pg_pairs(pg_builder* b, uint32_t* keys, uint32_t* vals, uint32_t val_offset,
     return fail(PG_INVARIANT_ERROR, "coarse_bins must be in [1, %d]", 3 * OC_CAP);
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   CU(cudaSetDevice(b->device));
+  drop_graph(b);
   const uint64_t no = b->no;
   const unsigned k2_tiles = (unsigned)((no + K2_TILE - 1) / K2_TILE);
   int rc;
@@ -601,10 +735,11 @@ int pg_pairs(pg_builder* b, uint32_t* keys, uint32_t* vals, uint32_t val_offset,
   if (dcoarse) CU(cudaMemsetAsync(dcoarse, 0, (size_t)coarse_bins * 4, st));
   if (no > 0) {
     const unsigned dxu = (unsigned)b->dims[0], dxyu = (unsigned)b->dims[0] * (unsigned)b->dims[1];
-    k_pair_tile_bounds<<<(k2_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no,
-                                                          K2_TILE, k2_tiles, pbounds);
+    k_pair_tile_bounds<<<(k2_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n,
+                                                          Count{nullptr, (unsigned)no}, K2_TILE, pbounds);
     LAUNCHED("k_pair_tile_bounds", st);
-    k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no, dxu, dxyu,
+    k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, Count{nullptr, (unsigned)no},
+                                                   dxu, dxyu,
                                                    pbounds, keys, vals, val_offset, dcoarse, coarse_shift,
                                                    coarse_bins);
     LAUNCHED("k_expand_pairs", st);
@@ -627,6 +762,7 @@ int pg_partition(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int6
   if (n < 0 || n > kMaxScan) return fail(PG_SIZE_ERROR, "partition of %lld pairs exceeds the size limit", (long long)n);
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   CU(cudaSetDevice(b->device));
+  drop_graph(b);
   if (n == 0) {
     for (int s = 0; s < nslabs; ++s) slab_counts[s] = 0;
     return PG_OK;
@@ -641,12 +777,12 @@ int pg_partition(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int6
   unsigned* counts = b->sort_sync.as<unsigned>(hist_bytes);
   CU(cudaMemsetAsync(hist, 0, hist_bytes, st));
   const DigitFn dig{bucket_shift, 0u, slab_of_bucket};
-  k_tile_counts<<<(ntiles + TC_TILES - 1) / TC_TILES, RS_THREADS, 0, st>>>(keys, (unsigned)n, dig, 1 << bits, counts,
-                                                                          ld);
+  const Count cn{nullptr, (unsigned)n};
+  k_tile_counts<<<(ntiles + TC_TILES - 1) / TC_TILES, RS_THREADS, 0, st>>>(keys, cn, dig, 1 << bits, counts, ld);
   LAUNCHED("k_tile_counts", st);
-  k_scan_tile_counts<<<1u << bits, SC_THREADS, 0, st>>>(counts, ntiles, ld, hist);
+  k_scan_tile_counts<<<1u << bits, SC_THREADS, 0, st>>>(counts, cn, ld, hist);
   LAUNCHED("k_scan_tile_counts", st);
-  launch_radix_scatter(bits, ntiles, st, keys, vals, keys_out, vals_out, (unsigned)n, bucket_shift, hist, counts, ld,
+  launch_radix_scatter(bits, ntiles, st, keys, vals, keys_out, vals_out, cn, bucket_shift, hist, counts, ld,
                        slab_of_bucket, slab_base);
   LAUNCHED("k_radix_scatter", st);
   b->launches += 3;
@@ -664,6 +800,7 @@ int pg_sort_cells(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int
   if (n < 0 || n > kMaxScan) return fail(PG_SIZE_ERROR, "sort of %lld pairs exceeds the size limit", (long long)n);
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   CU(cudaSetDevice(b->device));
+  drop_graph(b);
   const PassPlan plan = make_plan(bit_length((uint64_t)(ncells - 1)), kMaxDigitBits);
   const size_t sec = align_up(std::max<size_t>((size_t)n * 4, 16));
   int rc;
@@ -688,14 +825,14 @@ int pg_sort_cells(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int
       CU(cudaMemsetAsync(hist, 0, hist_bytes, st));
       // pass 0 reads the caller's (const) pairs; later passes ping-pong in the workspace
       if ((rc = run_passes(b, plan, false, const_cast<unsigned*>(keys), const_cast<unsigned*>(vals), kB, vB, O,
-                           (uint64_t)n, hist, counts, st, &sorted, kA, vA)))
+                           Count{nullptr, (unsigned)n}, (uint64_t)n, hist, counts, st, &sorted, kA, vA)))
         return rc;
     }
   }
-  k_key_tile_bounds<<<(g_tiles + 1 + 7) / 8, 256, 0, st>>>(sorted, (unsigned)n, G_TILE, (unsigned)ncells, g_tiles + 1,
-                                                          kbounds);
+  k_key_tile_bounds<<<(g_tiles + 1 + 7) / 8, 256, 0, st>>>(sorted, Count{nullptr, (unsigned)n}, G_TILE,
+                                                          (unsigned)ncells, g_tiles + 1, kbounds);
   LAUNCHED("k_key_tile_bounds", st);
-  k_cell_offsets<<<g_tiles, G_THREADS, 0, st>>>(sorted, (unsigned)n, (unsigned)ncells, kbounds, G);
+  k_cell_offsets<<<g_tiles, G_THREADS, 0, st>>>(sorted, Count{nullptr, (unsigned)n}, (unsigned)ncells, kbounds, G);
   LAUNCHED("k_cell_offsets", st);
   b->launches += 2;
   return PG_OK;

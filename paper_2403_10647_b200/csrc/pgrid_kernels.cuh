@@ -41,6 +41,20 @@ struct PassPlan {
   int bits[kMaxPasses];
 };
 
+// A pair count known either on the host (dev == nullptr: val) or only on the device (the
+// sync-free build: min(*dev, val), val = the capacity the buffers were sized for). Kernels
+// downstream of K1 take their NO this way so a whole build can be enqueued -- and captured
+// in a CUDA graph -- without reading NO back first.
+struct Count {
+  const unsigned long long* dev;
+  unsigned val;
+  __device__ __forceinline__ unsigned get() const {
+    if (!dev) return val;
+    const unsigned long long v = *dev;
+    return v < (unsigned long long)val ? (unsigned)v : val;
+  }
+};
+
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -489,8 +503,10 @@ __global__ void k_abs_offsets(const uint4* __restrict__ rec, const unsigned* __r
 // inside the tile (#triangles with offset < pend). Hoisting these searches out of the
 // expansion kernels keeps their CTAs from idling on dependent round trips at launch.
 __global__ void __launch_bounds__(256)
-k_pair_tile_bounds(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, unsigned no,
-                   unsigned tile, unsigned ntiles, int2* __restrict__ bounds) {
+k_pair_tile_bounds(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno,
+                   unsigned tile, int2* __restrict__ bounds) {
+  const unsigned no = cno.get();
+  const unsigned ntiles = (no + tile - 1) / tile;
   const unsigned t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= ntiles) return;
   const unsigned p0 = t * tile;
@@ -503,8 +519,9 @@ k_pair_tile_bounds(const uint4* __restrict__ rec, const unsigned* __restrict__ t
 
 // lower_bound(sorted, t * step) for t in [0, nq), one warp per query (K4's key ranges).
 __global__ void __launch_bounds__(256)
-k_key_tile_bounds(const unsigned* __restrict__ sorted, unsigned no, unsigned step, unsigned ncells, unsigned nq,
+k_key_tile_bounds(const unsigned* __restrict__ sorted, Count cno, unsigned step, unsigned ncells, unsigned nq,
                   unsigned* __restrict__ out) {
+  const unsigned no = cno.get();
   const unsigned t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= nq) return;
   const unsigned long long c = min((unsigned long long)t * step, (unsigned long long)ncells);
@@ -516,14 +533,16 @@ k_key_tile_bounds(const unsigned* __restrict__ sorted, unsigned no, unsigned ste
 // Pairs in generation (object-major) order -- used when no radix pass follows
 // (ncells == 1) and for the record= stage dumps.
 __global__ void __launch_bounds__(K2_THREADS)
-k_expand_pairs(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, unsigned no,
+k_expand_pairs(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno,
                unsigned dx, unsigned dxy, const int2* __restrict__ bounds, unsigned* __restrict__ keys,
                unsigned* __restrict__ vals, unsigned val_offset, unsigned* __restrict__ coarse, int coarse_shift,
                int coarse_bins) {
   __shared__ __align__(16) int slot[K2_TILE];
   __shared__ int warpmax[K2_THREADS / 32];
   __shared__ ObjCache oc;
+  const unsigned no = cno.get();
   const unsigned p0 = blockIdx.x * (unsigned)K2_TILE;
+  if (p0 >= no) return;
   const unsigned pend = min(p0 + (unsigned)K2_TILE, no);
   unsigned key[K2_ITEMS];
   int own[K2_ITEMS];
@@ -657,9 +676,10 @@ struct DigitFn {
 // of the digit-major matrix receives TC_TILES consecutive entries (a full 32-byte sector).
 constexpr int TC_TILES = 8;
 __global__ void __launch_bounds__(RS_THREADS)
-k_tile_counts(const unsigned* __restrict__ keys, unsigned no, DigitFn dig, int nbins, unsigned* __restrict__ counts,
+k_tile_counts(const unsigned* __restrict__ keys, Count cno, DigitFn dig, int nbins, unsigned* __restrict__ counts,
               unsigned ld) {
   __shared__ unsigned h[TC_TILES][kMaxBins];
+  const unsigned no = cno.get();
   const int tid = threadIdx.x;
   const unsigned ntiles = (no + RS_TILE - 1) / RS_TILE;
   const unsigned t0 = blockIdx.x * TC_TILES;
@@ -696,8 +716,9 @@ k_tile_counts(const unsigned* __restrict__ keys, unsigned no, DigitFn dig, int n
 // K2 writes its first-pass counts tile-major (one coalesced row per CTA); transpose them to
 // the digit-major layout the row scan and the scatter use.
 __global__ void __launch_bounds__(256)
-k_transpose_counts(const unsigned* __restrict__ tm, unsigned ntiles, int nbins, unsigned* __restrict__ dm, unsigned ld) {
+k_transpose_counts(const unsigned* __restrict__ tm, Count cno, int nbins, unsigned* __restrict__ dm, unsigned ld) {
   __shared__ unsigned blk[32][33];
+  const unsigned ntiles = (cno.get() + RS_TILE - 1) / RS_TILE;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   const unsigned t0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
   for (int r = ty; r < 32; r += 8) {
@@ -718,8 +739,9 @@ constexpr int SC_ITEMS = 8;
 // accesses; one iteration covers 8192 tiles (33.5M pairs). The row total is the digit's
 // global count (its histogram bin).
 __global__ void __launch_bounds__(SC_THREADS)
-k_scan_tile_counts(unsigned* __restrict__ counts, unsigned ntiles, unsigned ld, unsigned* __restrict__ row_total) {
+k_scan_tile_counts(unsigned* __restrict__ counts, Count cno, unsigned ld, unsigned* __restrict__ row_total) {
   __shared__ unsigned wsum[SC_THREADS / 32];
+  const unsigned ntiles = (cno.get() + RS_TILE - 1) / RS_TILE;
   const int tid = threadIdx.x;
   unsigned* row = counts + (size_t)blockIdx.x * ld;
   unsigned carry = 0;
@@ -904,13 +926,15 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
 template <int BITS, bool TABLE>
 __global__ void __launch_bounds__(RS_THREADS, RS_MIN_CTAS)
 k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
-                unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, unsigned no, int shift,
+                unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, Count cno, int shift,
                 const unsigned* __restrict__ hist, const unsigned* __restrict__ offs, unsigned ld,
                 const unsigned* __restrict__ dtable, const unsigned* __restrict__ kbase) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RsSmem& sm = *reinterpret_cast<RsSmem*>(smem_raw);
+  const unsigned no = cno.get();
   const unsigned tile = blockIdx.x;
   const unsigned tbase = tile * (unsigned)RS_TILE;
+  if (tbase >= no) return;
   const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
   if (tvalid == (unsigned)RS_TILE)
     radix_scatter_tile<BITS, true, TABLE>(sm, keys_in, vals_in, keys_out, vals_out, tbase, tvalid, tile, ld, shift,
@@ -934,13 +958,15 @@ struct PeSmem {
 };
 
 __global__ void __launch_bounds__(RS_THREADS)
-k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, unsigned no,
+k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno,
              unsigned dx, unsigned dxy, PassPlan plan, const int2* __restrict__ bounds, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
              unsigned* __restrict__ counts0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PeSmem& sm = *reinterpret_cast<PeSmem*>(smem_raw);
   const int tid = threadIdx.x;
+  const unsigned no = cno.get();
   const unsigned p0 = blockIdx.x * (unsigned)RS_TILE;
+  if (p0 >= no) return;
   const unsigned pend = min(p0 + (unsigned)RS_TILE, no);
   for (int b = tid; b < kMaxBins; b += RS_THREADS) sm.h[b] = 0u;
   unsigned key[RS_ITEMS];
@@ -988,8 +1014,9 @@ constexpr int G_TILE = G_THREADS * G_ITEMS;  // cells per CTA
 // its run start; a block suffix-min fills empty cells with the next run start (or i1).
 // The last CTA also writes the sentinel G[ncells] = NO (builders.py:131-133).
 __global__ void __launch_bounds__(G_THREADS)
-k_cell_offsets(const unsigned* __restrict__ sorted, unsigned no, unsigned ncells, const unsigned* __restrict__ kb,
+k_cell_offsets(const unsigned* __restrict__ sorted, Count cno, unsigned ncells, const unsigned* __restrict__ kb,
                unsigned* __restrict__ G) {
+  const unsigned no = cno.get();
   __shared__ __align__(16) unsigned mark[G_TILE];
   __shared__ unsigned sh_wmin[G_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

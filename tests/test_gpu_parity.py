@@ -223,3 +223,24 @@ def test_pinned_outputs_are_recycled_and_independent():
     assert np.array_equal(g1.G, keep[0]) and np.array_equal(g1.O, keep[1])
     assert np.array_equal(g2.G, keep[0]) and np.array_equal(g2.O, keep[1])
     assert g1.G.ctypes.data != g2.G.ctypes.data
+
+
+def test_sync_free_graph_build_matches_and_reports_capacity(hashes):
+    """pg_build_async: eager run, then CUDA-graph replays; identical G/O; capacity errors."""
+    import torch
+    h = hashes["cfg1"]
+    mesh, spec = scene_from_recipe(h["recipe"])
+    b = _native.Builder(0)
+    Vd = torch.from_numpy(mesh.vertices.copy()).cuda()
+    Td = torch.from_numpy(mesh.triangles.copy()).cuda()
+    Gd = torch.empty(spec.ncells + 1, dtype=torch.int32, device="cuda")
+    Od = torch.empty(h["no"] + 100, dtype=torch.int32, device="cuda")
+    for _ in range(3):      # eager + capture, then replays
+        Gd.fill_(-1)
+        b.build_async(Vd, len(mesh.vertices), Td, len(mesh.triangles), spec, Gd, Od, h["no"] + 100)
+        assert b.build_wait() == h["no"]
+        assert sha(Gd.cpu().numpy().view(np.uint32)) == h["G_sha256"]
+        assert sha(Od[:h["no"]].cpu().numpy().view(np.uint32)) == h["O_sha256"]
+    small = torch.empty(1000, dtype=torch.int32, device="cuda")
+    b.build_async(Vd, len(mesh.vertices), Td, len(mesh.triangles), spec, Gd, small, 1000)
+    assert b.build_wait() == -h["no"]          # capacity exceeded is reported, not silent
