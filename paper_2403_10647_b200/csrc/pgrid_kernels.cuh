@@ -1046,41 +1046,45 @@ k_cell_offsets(const unsigned* __restrict__ sorted, Count cno, unsigned ncells, 
     }
   }
   __syncthreads();
-  // block suffix-min (thread t owns cells [16t, 16t+16))
-  unsigned v[G_ITEMS];
+  // block suffix-min, group by group from the right: in group g thread t owns the four cells
+  // g*1024 + 4t .. +3, so the mark loads are conflict-free and the G stores fully coalesced
+  unsigned carry = i1;  // min over all cells right of the current group
 #pragma unroll
-  for (int q = 0; q < G_ITEMS / 4; ++q) {
-    const uint4 a = *reinterpret_cast<const uint4*>(&mark[tid * G_ITEMS + 4 * q]);
-    v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
-  }
-  unsigned tmin = i1;
+  for (int g = G_ITEMS / 4 - 1; g >= 0; --g) {
+    const uint4 a = reinterpret_cast<const uint4*>(mark)[g * G_THREADS + tid];
+    unsigned v0 = a.x, v1 = a.y, v2 = a.z, v3 = a.w;
+    unsigned suf = min(min(v0, v1), min(v2, v3));  // inclusive suffix-min over lanes >= lane
 #pragma unroll
-  for (int q = 0; q < G_ITEMS; ++q) tmin = min(tmin, v[q]);
-  unsigned suf = tmin;  // inclusive suffix-min over lanes >= lane
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned o = __shfl_down_sync(0xffffffffu, suf, d);
+      if (lane + d < 32) suf = min(suf, o);
+    }
+    if (lane == 0) sh_wmin[warp] = suf;
+    __syncthreads();
+    unsigned right = __shfl_down_sync(0xffffffffu, suf, 1);
+    if (lane == 31) right = 0xffffffffu;
+    unsigned gmin = 0xffffffffu;
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const unsigned o = __shfl_down_sync(0xffffffffu, suf, d);
-    if (lane + d < 32) suf = min(suf, o);
-  }
-  if (lane == 0) sh_wmin[warp] = suf;
-  __syncthreads();
-  unsigned carry = __shfl_down_sync(0xffffffffu, suf, 1);
-  if (lane == 31) carry = i1;
-  for (int w = warp + 1; w < G_THREADS / 32; ++w) carry = min(carry, sh_wmin[w]);
-#pragma unroll
-  for (int q = G_ITEMS - 1; q >= 0; --q) {
-    carry = min(carry, v[q]);
-    v[q] = carry;
-  }
-  const unsigned cb = c0 + (unsigned)tid * G_ITEMS;
-  if (cb + G_ITEMS <= c1) {
-    uint4* dst = reinterpret_cast<uint4*>(G + cb);
-#pragma unroll
-    for (int q = 0; q < G_ITEMS / 4; ++q) dst[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-  } else {
-#pragma unroll
-    for (int q = 0; q < G_ITEMS; ++q)
-      if (cb + q < c1) G[cb + q] = v[q];
+    for (int w = 0; w < G_THREADS / 32; ++w) {
+      const unsigned x = sh_wmin[w];
+      if (w > warp) right = min(right, x);
+      gmin = min(gmin, x);
+    }
+    right = min(right, carry);
+    v3 = min(v3, right);
+    v2 = min(v2, v3);
+    v1 = min(v1, v2);
+    v0 = min(v0, v1);
+    const unsigned cb = c0 + (unsigned)(g * G_THREADS + tid) * 4;
+    if (cb + 4 <= c1) {
+      *reinterpret_cast<uint4*>(G + cb) = make_uint4(v0, v1, v2, v3);
+    } else {
+      if (cb < c1) G[cb] = v0;
+      if (cb + 1 < c1) G[cb + 1] = v1;
+      if (cb + 2 < c1) G[cb + 2] = v2;
+    }
+    carry = min(carry, gmin);
+    __syncthreads();  // sh_wmin is reused by the next group
   }
   if (blockIdx.x == gridDim.x - 1 && tid == 0) G[ncells] = no;
 }
