@@ -951,11 +951,12 @@ k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict
 // upsweep; the row scan turns them into the global histogram too).
 // ----------------------------------------------------------------------------------------
 struct PeSmem {
-  int slot[RS_TILE];
+  __align__(16) int slot[RS_TILE];  // expansion slots, then the transposed keys
   unsigned h[kMaxBins];
-  ObjCache oc;
+  __align__(16) ObjCache oc;        // object cache, then the transposed values
   int warpmax[RS_WARPS];
 };
+static_assert(sizeof(ObjCache) >= RS_TILE * 4, "the object cache doubles as the value transpose buffer");
 
 __global__ void __launch_bounds__(RS_THREADS)
 k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno,
@@ -974,21 +975,39 @@ k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pr
   expand_tile<RS_THREADS, RS_ITEMS>(rec, n, p0, pend, dx, dxy, tile_pre, bounds, sm.slot, sm.warpmax, &sm.oc, key, own);
   const unsigned pbase = p0 + (unsigned)tid * RS_ITEMS;
   const int nvalid = pend > pbase ? (int)min((unsigned)RS_ITEMS, pend - pbase) : 0;
-  if (nvalid == RS_ITEMS) {
-    uint4* kd = reinterpret_cast<uint4*>(keys + pbase);
-    uint4* vd = reinterpret_cast<uint4*>(vals + pbase);
+  // transpose through shared memory (the expansion's slots and object cache are dead): a
+  // thread's 16 consecutive pairs leave as 16-byte chunks striped over the CTA, so every
+  // warp store is 512 contiguous bytes; chunk index c is XOR-swizzled against bank conflicts
+  __syncthreads();
+  {
+    uint4* ks = reinterpret_cast<uint4*>(sm.slot);
+    uint4* vs = reinterpret_cast<uint4*>(sm.oc.lo_cell);
+    auto swz = [](unsigned c) { return c ^ ((c >> 3) & 7u); };
 #pragma unroll
     for (int q = 0; q < RS_ITEMS / 4; ++q) {
-      kd[q] = make_uint4(key[4 * q], key[4 * q + 1], key[4 * q + 2], key[4 * q + 3]);
-      vd[q] = make_uint4(own[4 * q], own[4 * q + 1], own[4 * q + 2], own[4 * q + 3]);
+      const unsigned c = (unsigned)tid * (RS_ITEMS / 4) + q;
+      ks[swz(c)] = make_uint4(key[4 * q], key[4 * q + 1], key[4 * q + 2], key[4 * q + 3]);
+      vs[swz(c)] = make_uint4(own[4 * q], own[4 * q + 1], own[4 * q + 2], own[4 * q + 3]);
     }
-  } else {
+    __syncthreads();
 #pragma unroll
-    for (int j = 0; j < RS_ITEMS; ++j)
-      if (j < nvalid) {
-        keys[pbase + j] = key[j];
-        vals[pbase + j] = (unsigned)own[j];
+    for (int q = 0; q < RS_ITEMS / 4; ++q) {
+      const unsigned c = (unsigned)tid + q * RS_THREADS;
+      const unsigned e = p0 + 4 * c;
+      const uint4 kk = ks[swz(c)], vv = vs[swz(c)];
+      if (e + 4 <= pend) {
+        reinterpret_cast<uint4*>(keys + e)[0] = kk;
+        reinterpret_cast<uint4*>(vals + e)[0] = vv;
+      } else {
+        const unsigned kx[4] = {kk.x, kk.y, kk.z, kk.w}, vx[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (e + r < pend) {
+            keys[e + r] = kx[r];
+            vals[e + r] = vx[r];
+          }
       }
+    }
   }
   {  // first-pass digit: consecutive cells rarely share it -- one atomic per pair
     const int sh = plan.shift[0];
