@@ -387,10 +387,13 @@ __device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long 
   // (k_pair_tile_bounds precomputed both with 32-ary searches over the offsets)
   const int2 bnd = __ldg(&bounds[p0 / TILE]);
   const long long olo = bnd.x, oend = bnd.y;
+  // slots live in 16-byte chunks whose index is XOR-swizzled (slot_at) so the per-thread
+  // chunk reads of the max-scan below are bank-conflict free
+  auto slot_at = [](unsigned e) { return ((((e >> 2) ^ ((e >> 5) & 7u)) << 2) | (e & 3u)); };
   for (int i = tid; i < TILE; i += THREADS) slot[i] = -1;
   __syncthreads();
   if (tid == 0) {
-    slot[0] = (int)olo;
+    slot[0] = (int)olo;  // slot_at(0) == 0
     const uint4 r = __ldg(&rec[olo]);
     oc->lo_cell[0] = r.x;
     oc->mx[0] = r.y;
@@ -401,7 +404,7 @@ __device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long 
   for (long long o = olo + 1 + tid; o < oend; o += THREADS) {
     const uint4 r = __ldg(&rec[o]);
     const unsigned off = __ldg(&tile_pre[o / K1_TILE]) + r.w;
-    atomicMax(&slot[off - p0], (int)o);  // zero-count triangles share the next start; max wins
+    atomicMax(&slot[slot_at(off - p0)], (int)o);  // zero-count triangles share the next start; max wins
     const long long ci = o - olo;
     if (ci < OC_CAP) {
       oc->lo_cell[ci] = r.x;
@@ -413,7 +416,7 @@ __device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long 
   // inclusive max-scan over the slots (blocked: thread t owns slots [ITEMS*t, ITEMS*t + ITEMS))
 #pragma unroll
   for (int q = 0; q < ITEMS / 4; ++q) {
-    const int4 a = *reinterpret_cast<const int4*>(&slot[tid * ITEMS + 4 * q]);
+    const int4 a = *reinterpret_cast<const int4*>(&slot[slot_at((unsigned)(tid * ITEMS + 4 * q))]);
     own[4 * q] = a.x;
     own[4 * q + 1] = a.y;
     own[4 * q + 2] = a.z;
