@@ -87,6 +87,17 @@ def _small_triangles_range(a, b, seed, stream, size):
     return centres[:, None, :] + jitter
 
 
+def gen_uniform_chunked(n, seed, chunk=10_000_000):
+    """gen_scene("uniform", n, seed) built chunk by chunk (bounded temporaries for 100M+
+    triangles); bit-identical to the one-shot generator."""
+    size = min(0.05, 0.6 * n ** (-1.0 / 3.0))
+    V = np.empty((3 * n, 3), dtype=np.float64)
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
+        V[3 * a:3 * b] = _small_triangles_range(a, b, seed, 10, size).reshape(-1, 3)
+    return TriangleMesh(V, np.arange(3 * n, dtype=np.int32).reshape(n, 3))
+
+
 def gen_arch_shard(n, seed, density, lo, hi):
     """Triangles [lo, hi) of gen_scene("arch", n, seed, density) as an unshared-vertex soup
     (for sharded builds: each rank generates only its own shard)."""

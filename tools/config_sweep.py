@@ -22,6 +22,7 @@ hashes = json.load(open(os.path.join(ROOT, "tests", "golden", "hashes.json")))["
 runs = [("cfg1", "uniform", 100_000, 5.0), ("cfg2", "lognormal", 1_000_000, 5.0), ("cfg3", "arch", 10_000_000, 4.0),
         ("cfg3u", "uniform", 10_000_000, 5.0)]
 runs += [(f"cfg4_d{d}", "uniform", 10_000_000, float(d)) for d in (1, 2, 4, 8, 16, 32, 64)]
+runs += [("cfg5_1gpu", "uniform", 100_000_000, 5.0)]   # config 5's scene on one B200
 if a.only:
     runs = [r for r in runs if r[0] in a.only.split(",")]
 b = _native.Builder(0)
@@ -31,7 +32,8 @@ for name, kind, n, dens in runs:
     key = (kind, n)
     if key not in cache:
         cache.clear()
-        m = scenes.gen_scene(kind, n, 7, dens if kind in ("lognormal", "arch") else 5.0)
+        m = (scenes.gen_uniform_chunked(n, 7) if n > 20_000_000 else
+             scenes.gen_scene(kind, n, 7, dens if kind in ("lognormal", "arch") else 5.0))
         cache[key] = (m, torch.from_numpy(m.vertices.copy()).cuda(), torch.from_numpy(m.triangles.copy()).cuda())
     mesh, Vd, Td = cache[key]
     spec = spec_for_mesh(mesh, density=dens)
