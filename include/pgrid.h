@@ -100,19 +100,20 @@ int pg_radix_sort_pairs(pg_builder *b, const uint32_t *keys, const uint32_t *val
  *   pg_pairs      -- after pg_count on a triangle shard: its <cell, triangle> pairs in
  *                    generation (object-major) order; triangle ids += val_offset (shard base);
  *                    optionally the histogram of cell >> coarse_shift (coarse_bins <= 7680
- *                    bins, host u64) used to plan the slabs
+ *                    u32 bins, device) used to plan the slabs
  *   pg_partition  -- stable partition of pairs into cell slabs: slab = slab_of_bucket[key >>
  *                    bucket_shift] (nslabs <= 16); keys leave rebased by slab_base[slab];
- *                    slab_counts (host) receives the pairs per slab
+ *                    slab_counts (device, 2^ceil(log2 nslabs) u32) receives the pairs per slab
+ * None of the three synchronises the host: sizes stay on the device for the collectives.
  *   pg_sort_cells -- the Alg. 1 tail over arbitrary pairs with keys in [0, ncells): stable
  *                    radix sort + RLE/scatter/scan into G[ncells+1], O[n]
  *                    (builders.py:120-141) */
 int pg_pairs(pg_builder *b, uint32_t *keys, uint32_t *vals, uint32_t val_offset, int coarse_shift,
-             int coarse_bins, uint64_t *coarse_hist, void *stream);
+             int coarse_bins, uint32_t *coarse_hist, void *stream);
 int pg_partition(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int64_t n,
                  const uint32_t *slab_of_bucket, int bucket_shift, int nslabs,
                  const uint32_t *slab_base, uint32_t *keys_out, uint32_t *vals_out,
-                 uint64_t *slab_counts, void *stream);
+                 uint32_t *slab_counts, void *stream);
 int pg_sort_cells(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int64_t n,
                   int64_t ncells, uint32_t *G, uint32_t *O, void *stream);
 

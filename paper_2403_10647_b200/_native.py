@@ -79,9 +79,8 @@ def load():
         lib.pg_finish.argtypes = [vp, vp, vp, u32, vp, ctypes.POINTER(ctypes.c_float)]
         lib.pg_stage.argtypes = [vp, ctypes.c_int, vp, u32, vp]
         lib.pg_radix_sort_pairs.argtypes = [vp, vp, vp, vp, vp, i64, ctypes.c_int, u32, vp]
-        lib.pg_pairs.argtypes = [vp, vp, vp, u32, ctypes.c_int, ctypes.c_int, ctypes.POINTER(u64), vp]
-        lib.pg_partition.argtypes = [vp, vp, vp, i64, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp,
-                                     ctypes.POINTER(u64), vp]
+        lib.pg_pairs.argtypes = [vp, vp, vp, u32, ctypes.c_int, ctypes.c_int, vp, vp]
+        lib.pg_partition.argtypes = [vp, vp, vp, i64, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp]
         lib.pg_sort_cells.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp]
         lib.pg_build_async.argtypes = [vp, vp, i64, vp, i64, ctypes.POINTER(PgSpec), vp, vp, u64, vp]
         lib.pg_build_wait.argtypes = [vp, ctypes.POINTER(u64)]
@@ -184,21 +183,19 @@ class Builder:
         return int(no.value)
 
     # sharded-build building blocks (device pointers)
-    def pairs(self, keys, vals, val_offset=0, coarse_shift=0, coarse_bins=0, stream=None):
-        """Generation-order pairs; with coarse_bins > 0 also returns the histogram of
-        cell >> coarse_shift (slab planning)."""
-        hist = (ctypes.c_uint64 * coarse_bins)() if coarse_bins else None
+    def pairs(self, keys, vals, val_offset=0, coarse_shift=0, coarse_bins=0, coarse_hist=None, stream=None):
+        """Generation-order pairs of the counted shard; with coarse_hist (device u32[coarse_bins])
+        also the histogram of cell >> coarse_shift. No host synchronisation."""
         check(self._lib.pg_pairs(self._h, ptr(keys), ptr(vals), int(val_offset), int(coarse_shift),
-                                 int(coarse_bins), hist, stream))
-        return np.ctypeslib.as_array(hist).astype(np.int64) if coarse_bins else None
+                                 int(coarse_bins), ptr(coarse_hist), stream))
 
     def partition(self, keys, vals, n, slab_of_bucket, bucket_shift, nslabs, slab_base, keys_out,
-                  vals_out, stream=None):
-        counts = (ctypes.c_uint64 * nslabs)()
+                  vals_out, slab_counts, stream=None):
+        """Stable slab partition; slab_counts (device u32[2^ceil(log2 nslabs)]) receives the
+        per-slab pair counts. No host synchronisation."""
         check(self._lib.pg_partition(self._h, ptr(keys), ptr(vals), int(n), ptr(slab_of_bucket),
                                      int(bucket_shift), int(nslabs), ptr(slab_base), ptr(keys_out),
-                                     ptr(vals_out), counts, stream))
-        return [int(c) for c in counts]
+                                     ptr(vals_out), ptr(slab_counts), stream))
 
     def sort_cells(self, keys, vals, n, ncells, G, O, stream=None):
         check(self._lib.pg_sort_cells(self._h, ptr(keys), ptr(vals), int(n), int(ncells), ptr(G),

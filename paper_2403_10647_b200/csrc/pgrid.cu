@@ -718,7 +718,7 @@ int pg_radix_sort_pairs(pg_builder* b, const uint32_t* keys, const uint32_t* val
 // partition of pairs into cell slabs, and the sort + G tail over one slab.
 // ---------------------------------------------------------------------------------------
 int pg_pairs(pg_builder* b, uint32_t* keys, uint32_t* vals, uint32_t val_offset, int coarse_shift, int coarse_bins,
-             uint64_t* coarse_hist, void* stream_) {
+             uint32_t* coarse_hist, void* stream_) {
   if (!b || !b->counted) return fail(PG_STATE_ERROR, "pg_pairs without a successful pg_count");
   if (coarse_hist && (coarse_bins < 1 || coarse_bins > 3 * OC_CAP))
     return fail(PG_INVARIANT_ERROR, "coarse_bins must be in [1, %d]", 3 * OC_CAP);
@@ -729,9 +729,9 @@ int pg_pairs(pg_builder* b, uint32_t* keys, uint32_t* vals, uint32_t val_offset,
   const unsigned k2_tiles = (unsigned)((no + K2_TILE - 1) / K2_TILE);
   int rc;
   const size_t pb_bytes = align_up((size_t)k2_tiles * 8 + 8);
-  if ((rc = b->sort_sync.ensure(pb_bytes + (size_t)std::max(coarse_bins, 1) * 4))) return rc;
+  if ((rc = b->sort_sync.ensure(pb_bytes))) return rc;
   int2* pbounds = b->sort_sync.as<int2>(0);
-  unsigned* dcoarse = coarse_hist ? b->sort_sync.as<unsigned>(pb_bytes) : nullptr;
+  unsigned* dcoarse = coarse_hist;  // device, accumulated (zeroed here), no host round trip
   if (dcoarse) CU(cudaMemsetAsync(dcoarse, 0, (size_t)coarse_bins * 4, st));
   if (no > 0) {
     const unsigned dxu = (unsigned)b->dims[0], dxyu = (unsigned)b->dims[0] * (unsigned)b->dims[1];
@@ -745,18 +745,12 @@ int pg_pairs(pg_builder* b, uint32_t* keys, uint32_t* vals, uint32_t val_offset,
     LAUNCHED("k_expand_pairs", st);
     b->launches += 2;
   }
-  if (coarse_hist) {
-    std::vector<unsigned> h(coarse_bins);
-    CU(cudaMemcpyAsync(h.data(), dcoarse, (size_t)coarse_bins * 4, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    for (int i = 0; i < coarse_bins; ++i) coarse_hist[i] = h[i];
-  }
   return PG_OK;
 }
 
 int pg_partition(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int64_t n, const uint32_t* slab_of_bucket,
                  int bucket_shift, int nslabs, const uint32_t* slab_base, uint32_t* keys_out, uint32_t* vals_out,
-                 uint64_t* slab_counts, void* stream_) {
+                 uint32_t* slab_counts, void* stream_) {
   if (!b) return fail(PG_INVARIANT_ERROR, "null builder");
   if (nslabs < 1 || nslabs > 16) return fail(PG_INVARIANT_ERROR, "nslabs must be in [1, 16]");
   if (n < 0 || n > kMaxScan) return fail(PG_SIZE_ERROR, "partition of %lld pairs exceeds the size limit", (long long)n);
@@ -764,32 +758,27 @@ int pg_partition(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int6
   CU(cudaSetDevice(b->device));
   drop_graph(b);
   if (n == 0) {
-    for (int s = 0; s < nslabs; ++s) slab_counts[s] = 0;
+    CU(cudaMemsetAsync(slab_counts, 0, (size_t)nslabs * 4, st));
     return PG_OK;
   }
   const int bits = std::max(1, bit_length((uint64_t)(nslabs - 1)));
   const unsigned ntiles = (unsigned)((n + RS_TILE - 1) / RS_TILE);
   const unsigned ld = (ntiles + 3) & ~3u;
   int rc;
-  const size_t hist_bytes = align_up(kMaxBins * 4);
-  if ((rc = b->sort_sync.ensure(hist_bytes + (size_t)ld * kMaxBins * 4))) return rc;
-  unsigned* hist = b->sort_sync.as<unsigned>(0);
-  unsigned* counts = b->sort_sync.as<unsigned>(hist_bytes);
-  CU(cudaMemsetAsync(hist, 0, hist_bytes, st));
+  if ((rc = b->sort_sync.ensure((size_t)ld * kMaxBins * 4))) return rc;
+  unsigned* counts = b->sort_sync.as<unsigned>(0);
+  // slab_counts (device) receives the row totals = pairs per slab, and serves as the pass's
+  // digit histogram; it must hold 2^bits entries
   const DigitFn dig{bucket_shift, 0u, slab_of_bucket};
   const Count cn{nullptr, (unsigned)n};
   k_tile_counts<<<(ntiles + TC_TILES - 1) / TC_TILES, RS_THREADS, 0, st>>>(keys, cn, dig, 1 << bits, counts, ld);
   LAUNCHED("k_tile_counts", st);
-  k_scan_tile_counts<<<1u << bits, SC_THREADS, 0, st>>>(counts, cn, ld, hist);
+  k_scan_tile_counts<<<1u << bits, SC_THREADS, 0, st>>>(counts, cn, ld, slab_counts);
   LAUNCHED("k_scan_tile_counts", st);
-  launch_radix_scatter(bits, ntiles, st, keys, vals, keys_out, vals_out, cn, bucket_shift, hist, counts, ld,
+  launch_radix_scatter(bits, ntiles, st, keys, vals, keys_out, vals_out, cn, bucket_shift, slab_counts, counts, ld,
                        slab_of_bucket, slab_base);
   LAUNCHED("k_radix_scatter", st);
   b->launches += 3;
-  std::vector<unsigned> h(nslabs);
-  CU(cudaMemcpyAsync(h.data(), hist, sizeof(unsigned) * nslabs, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  for (int s = 0; s < nslabs; ++s) slab_counts[s] = h[s];
   return PG_OK;
 }
 

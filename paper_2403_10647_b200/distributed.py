@@ -128,10 +128,9 @@ def build_sharded(ops, comm, V, T, tri_base, spec, gather=True):
     if world > MAX_SLABS:
         raise ValueError(f"at most {MAX_SLABS} ranks")
     st = ShardState(ops, V, T, tri_base, spec, rank, world)
-    hist = comm.allreduce_sum(np.asarray(st.phase_count(), dtype=np.int64))
+    hist = comm.allreduce_sum(st.phase_count())
     plan = plan_slabs(hist, st.ncells, world)
-    send = st.phase_partition(plan)
-    recv = comm.alltoall_counts(send)
+    send, recv = comm.alltoall_counts(st.phase_partition(plan))
     krecv, vrecv = comm.alltoall_pairs(st.kout, st.vout, send, recv, ops)
     base, G_rel, O = st.phase_sort(krecv, vrecv)
     if not gather:
@@ -159,16 +158,22 @@ class TorchComm:
         return t.to(self.device) if self.device is not None else t
 
     def allreduce_sum(self, arr):
-        t = self._t(arr)
+        """Sum over ranks; device tensors are reduced where they are (one host copy after)."""
+        import torch
+        t = arr if isinstance(arr, torch.Tensor) else self._t(arr)
+        t = t.to(torch.int64)
         self.dist.all_reduce(t, group=self.group)
         return t.cpu().numpy()
 
     def alltoall_counts(self, send):
+        """Exchange per-slab pair counts; returns (send, recv) as host lists (one host copy)."""
         import torch
-        s = self._t(np.asarray(send, dtype=np.int64))
+        s = (send if isinstance(send, torch.Tensor) else self._t(np.asarray(send, dtype=np.int64)))
+        s = s[:self.world].to(torch.int64)
         r = torch.empty_like(s)
         self.dist.all_to_all_single(r, s, group=self.group)
-        return [int(x) for x in r.cpu().numpy()]
+        both = torch.stack([s, r]).cpu().numpy()
+        return [int(x) for x in both[0]], [int(x) for x in both[1]]
 
     def alltoall_pairs(self, keys, vals, send, recv, ops):
         if hasattr(ops, "recv_buffers"):
@@ -193,9 +198,9 @@ def run_emulated(make_ops, V, T, spec, world):
     for r in range(world):
         lo, hi = shard_range(n, r, world)
         states.append(ShardState(make_ops(), V, T[lo:hi], lo, spec, r, world))
-    hist = np.sum([np.asarray(s.phase_count(), dtype=np.int64) for s in states], axis=0)
+    hist = np.sum([s.ops.to_numpy(s.phase_count()).astype(np.int64) for s in states], axis=0)
     plan = plan_slabs(hist, states[0].ncells, world)
-    sends = [s.phase_partition(plan) for s in states]
+    sends = [[int(x) for x in s.ops.to_numpy(s.phase_partition(plan))[:world]] for s in states]
     slabs = []
     for r, s in enumerate(states):
         ops = s.ops
@@ -271,17 +276,19 @@ class CudaOps:
 
     def pairs(self, no, tri_base, shift, nbuckets):
         k, v = self._buf("pair_k", no), self._buf("pair_v", no)
-        hist = self.b.pairs(k, v, tri_base, shift, nbuckets, self._sp())
-        return k, v, hist
+        hist = self._buf("coarse", nbuckets)
+        self.b.pairs(k, v, tri_base, shift, nbuckets, hist, self._sp())
+        return k, v, hist.view(self.torch.int32)
 
     def partition(self, keys, vals, table, shift, nslabs, base):
         torch = self.torch
         n = int(keys.numel())
-        dt = torch.from_numpy(np.asarray(table, np.uint32).view(np.int32)).to(self.dev, non_blocking=False)
-        db = torch.from_numpy(np.asarray(base, np.uint32).view(np.int32)).to(self.dev, non_blocking=False)
+        dt = torch.from_numpy(np.asarray(table, np.uint32).view(np.int32)).to(self.dev)
+        db = torch.from_numpy(np.asarray(base, np.uint32).view(np.int32)).to(self.dev)
         self._tables = (dt, db)
         ko, vo = self._buf("part_k", n), self._buf("part_v", n)
-        counts = self.b.partition(keys, vals, n, dt, shift, nslabs, db, ko, vo, self._sp())
+        counts = self._buf("slab_counts", 16)
+        self.b.partition(keys, vals, n, dt, shift, nslabs, db, ko, vo, counts, self._sp())
         return ko, vo, counts
 
     def sort_cells(self, keys, vals, n, ncells):

@@ -58,7 +58,7 @@ class NumpyOps:
         slab = np.asarray(table, np.int64)[keys.astype(np.int64) >> shift]
         order = np.argsort(slab, kind="stable")
         ko = (keys[order].astype(np.int64) - np.asarray(base, np.int64)[slab[order]]).astype(np.uint32)
-        counts = np.bincount(slab, minlength=nslabs).tolist()
+        counts = np.bincount(slab, minlength=nslabs).astype(np.int64)
         return ko, np.asarray(vals, np.uint32)[order], counts
 
     def sort_cells(self, keys, vals, n, ncells):

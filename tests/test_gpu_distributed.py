@@ -44,7 +44,7 @@ def test_partition_kernel_is_stable_and_rebased():
     ko, vo, counts = ops.partition(kt, vt, plan.table, plan.shift, 5, plan.cell_lo.astype(np.uint32))
     slab = plan.table[keys >> shift].astype(np.int64)
     order = np.argsort(slab, kind="stable")
-    assert counts == np.bincount(slab, minlength=5).tolist()
+    assert ops.to_numpy(counts)[:5].tolist() == np.bincount(slab, minlength=5).tolist()
     assert np.array_equal(ops.to_numpy(vo), vals[order])
     assert np.array_equal(ops.to_numpy(ko), (keys[order] - plan.cell_lo[slab[order]]).astype(np.uint32))
 

@@ -27,10 +27,10 @@ for it in range(6):
     st.no = ops.count(Vd, Td, spec); t = tick("count", t)
     st.shift = D.coarse_shift(st.ncells); nb = ((st.ncells - 1) >> st.shift) + 1
     st.keys, st.vals, h = ops.pairs(st.no, 0, st.shift, nb); t = tick("pairs+hist", t)
-    h = comm.allreduce_sum(np.asarray(h, np.int64)); t = tick("allreduce", t)
+    h = comm.allreduce_sum(h); t = tick("allreduce", t)
     plan = D.plan_slabs(h, st.ncells, 1); t = tick("plan", t)
-    send = st.phase_partition(plan); t = tick("partition", t)
-    recv = comm.alltoall_counts(send); t = tick("a2a_counts", t)
+    sc = st.phase_partition(plan); t = tick("partition", t)
+    send, recv = comm.alltoall_counts(sc); t = tick("a2a_counts", t)
     kr, vr = comm.alltoall_pairs(st.kout, st.vout, send, recv, ops); t = tick("a2a_pairs", t)
     r = st.phase_sort(kr, vr); t = tick("sort_cells", t)
 torch.cuda.synchronize()
