@@ -619,8 +619,8 @@ constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_ITEMS = 16;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 pairs per tile
-constexpr int RS_DPT = kMaxBins / RS_THREADS;
-constexpr int RS_MIN_CTAS = 4;  // 64 registers, 45 KB smem: 4 CTAs (32 warps) per SM   // digits per thread in the per-digit phases (2)
+constexpr int RS_DPT = kMaxBins / RS_THREADS;  // digits per thread in the per-digit phases
+constexpr int RS_MIN_CTAS = 4;  // 64 registers, 45 KB smem: 4 CTAs (32 warps) per SM
 
 struct RsSmem {
   unsigned buf[RS_TILE];                     // tile in digit order: keys, then values
