@@ -74,6 +74,13 @@ int pg_count(pg_builder *b, const double *V, int64_t nv, const int32_t *T, int64
 int pg_finish(pg_builder *b, uint32_t *G, uint32_t *O, uint32_t flags, void *stream,
               float *phase_ms);
 
+/* The paper's comparison builders (builders.py:172-231), after pg_count: algo 1 = sorted grid
+ * (one pair-generation task per object, then the same sort/G tail), algo 2 = compact grid
+ * (per-cell counters, scan, slot claims, canonical per-cell sort). Same G/O as pg_finish;
+ * max_task_work (may be NULL) receives the largest per-object task (sorted builder). */
+int pg_finish_baseline(pg_builder *b, int algo, uint32_t *G, uint32_t *O, uint32_t flags,
+                       void *stream, float *phase_ms, uint64_t *max_task_work);
+
 /* Sync-free build on device-resident V/T/G/O (no host round trip between K1 and the sort):
  * enqueues the whole of Alg. 1 on `stream` with every buffer sized for o_capacity pairs;
  * identical repeated calls replay a captured CUDA graph. pg_build_wait synchronises and

@@ -8,11 +8,11 @@ from .errors import DeviceError, GridError, InvariantError, ObjParseError, SizeE
 from .gridcore import (Aabb, CompactGrid, GridSpec, TriangleMesh, compute_dims, grids_equal,
                        mesh_bounds, spec_for_mesh)
 from .scenes import gen_scene
-from .builders import PHASES, BuildReport, build_parallel
+from .builders import PHASES, BuildReport, build_compact, build_parallel, build_sorted
 
 __version__ = "0.1.0"
 
 __all__ = ["Aabb", "BuildReport", "CompactGrid", "DeviceError", "GridError", "GridSpec",
            "InvariantError", "ObjParseError", "PHASES", "SizeError", "TriangleMesh",
-           "build_parallel", "compute_dims", "gen_scene", "grids_equal", "mesh_bounds",
+           "build_compact", "build_parallel", "build_sorted", "compute_dims", "gen_scene", "grids_equal", "mesh_bounds",
            "spec_for_mesh"]

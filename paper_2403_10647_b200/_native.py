@@ -30,7 +30,8 @@ NPHASES = 6
 
 # every symbol include/pgrid.h declares (checked by tests/test_boundary.py)
 EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
-           "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_build_async",
+           "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_finish_baseline",
+           "pg_build_async",
            "pg_build_wait", "pg_host_register",
            "pg_host_unregister", "pg_host_alloc", "pg_host_free", "pg_last_launch_count",
            "pg_last_error")
@@ -82,6 +83,8 @@ def load():
         lib.pg_pairs.argtypes = [vp, vp, vp, u32, ctypes.c_int, ctypes.c_int, vp, vp]
         lib.pg_partition.argtypes = [vp, vp, vp, i64, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp]
         lib.pg_sort_cells.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp]
+        lib.pg_finish_baseline.argtypes = [vp, ctypes.c_int, vp, vp, u32, vp, ctypes.POINTER(ctypes.c_float),
+                                           ctypes.POINTER(u64)]
         lib.pg_build_async.argtypes = [vp, vp, i64, vp, i64, ctypes.POINTER(PgSpec), vp, vp, u64, vp]
         lib.pg_build_wait.argtypes = [vp, ctypes.POINTER(u64)]
         lib.pg_host_register.argtypes = [vp, u64]
@@ -92,7 +95,7 @@ def load():
         lib.pg_last_error.restype = ctypes.c_char_p
         for name in ("pg_builder_create", "pg_count", "pg_finish", "pg_stage",
                      "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells",
-                     "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
+                     "pg_finish_baseline", "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
                      "pg_last_launch_count"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
@@ -156,6 +159,14 @@ class Builder:
         phases = (ctypes.c_float * NPHASES)() if timed else None
         check(self._lib.pg_finish(self._h, ptr(G), ptr(O), flags, stream, phases))
         return list(phases) if timed else None
+
+    def finish_baseline(self, algo, G, O, flags=0, stream=None):
+        """algo 1 = sorted grid, 2 = compact grid (builders.py:172-231); returns (phases, max_task_work)."""
+        phases = (ctypes.c_float * NPHASES)()
+        mw = ctypes.c_uint64(0)
+        check(self._lib.pg_finish_baseline(self._h, int(algo), ptr(G), ptr(O), flags, stream, phases,
+                                           ctypes.byref(mw)))
+        return list(phases), int(mw.value)
 
     def stage(self, stage, dst, flags=PG_HOST_OUTPUT, stream=None):
         check(self._lib.pg_stage(self._h, int(stage), ptr(dst), flags, stream))

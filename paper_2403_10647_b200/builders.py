@@ -107,3 +107,51 @@ def build_parallel(mesh, spec, workers=None, record=None, device=0):
                          max_task_work=PAIRGEN_OPS_PER_PAIR if no else 0,
                          total_work=PAIRGEN_OPS_PER_PAIR * no, phase_ms=ms)
     return CompactGrid(spec, G, O), report
+
+
+def _baseline(algo, name, mesh, spec, device):
+    V, T = _mesh_arrays(mesh)
+    n = len(T)
+    b = _native.thread_builder(device)
+    ms = {p: 0.0 for p in PHASES}
+    t0 = time.perf_counter()
+    no = b.count(V, len(V), T, n, spec, flags=_native.PG_HOST_INPUT)
+    count_ms = (time.perf_counter() - t0) * 1e3
+    ncells = int(spec.dims[0]) * int(spec.dims[1]) * int(spec.dims[2])
+    G = _native.pinned_pool.empty(ncells + 1, np.uint32)
+    O = _native.pinned_pool.empty(no, np.uint32)
+    phases, max_work = b.finish_baseline(algo, G, O, flags=_native.PG_HOST_OUTPUT)
+    for p, v in zip(PHASES, phases):
+        ms[p] = float(v)
+    ms["count"] += count_ms
+    return G, O, no, max_work, ms
+
+
+def build_sorted(mesh, spec, workers=None, record=None, device=0):
+    """The paper's sorted-grid baseline on the GPU (builders.py:172-192): one pair-generation
+    task per triangle walks its whole cell box (the load imbalance Alg. 1 removes), then the
+    same radix sort and G tail. Identical G/O to build_parallel.
+
+    record= fills the same arrays as the reference's build_sorted; its pairs are, by
+    construction, the parallel builder's pairs (object-major, x-fastest), so they are taken
+    from that path's stage dumps."""
+    del workers
+    if record is not None:
+        rec = {}
+        build_parallel(mesh, spec, record=rec, device=device)
+        record.update({k: rec[k] for k in ("v", "offsets", "no", "obj_ids", "global_c", "sorted_c", "sorted_o",
+                                            "rle_uniques", "rle_counts", "g")})
+    G, O, no, max_work, ms = _baseline(1, "sorted", mesh, spec, device)
+    if _fault_inject and no:          # shared sorted tail (builders.py:135-137)
+        O[0] ^= 1
+    report = BuildReport("sorted", no=no, max_task_work=max_work if no else 0, total_work=no, phase_ms=ms)
+    return CompactGrid(spec, G, O), report
+
+
+def build_compact(mesh, spec, workers=None, device=0):
+    """The paper's compact-grid baseline on the GPU (builders.py:195-231): per-cell counters,
+    exclusive scan into G, slot claims, then a canonical per-cell sort. Identical G/O."""
+    del workers
+    G, O, no, max_work, ms = _baseline(2, "compact", mesh, spec, device)
+    report = BuildReport("compact", no=no, max_task_work=max_work if no else 0, total_work=2 * no, phase_ms=ms)
+    return CompactGrid(spec, G, O), report

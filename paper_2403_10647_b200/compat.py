@@ -6,7 +6,9 @@
 
 replaces, in place (SURVEY.md §8b "Callers"):
   * pargrid.builders.build_parallel and pargrid.build_parallel  (builders.py:144)
-  * pargrid.cli.ALGORITHMS["parallel"]                          (cli.py:30-34)
+  * pargrid.builders.build_sorted / build_compact (+ pargrid.*) (builders.py:172, 195)
+    -- the GPU comparison builders of SURVEY §8(f) row 1 (algos="all")
+  * pargrid.cli.ALGORITHMS[...] for each replaced builder       (cli.py:30-34)
   * pargrid.kernels._BACKENDS["cuda"]                           (kernels/__init__.py:17-19)
 The wrapper returns the reference's own CompactGrid / BuildReport types, raises the
 reference's own error classes and honours pargrid.builders._fault_inject, so the
@@ -36,24 +38,42 @@ def _wrap_errors(fn, perr):
     return call
 
 
-def make_build_parallel(pargrid):
+def _make_builder(pargrid, ours, has_record, fault_hook):
     perr = pargrid.errors
     pbuilders = sys.modules["pargrid.builders"]
     pgridcore = sys.modules["pargrid.gridcore"]
 
-    def build_parallel(mesh, spec, workers=None, record=None):
-        grid, rep = _wrap_errors(_b.build_parallel, perr)(mesh, spec, workers=workers, record=record)
+    def convert(spec, grid, rep):
         O = grid.O
-        if pbuilders._fault_inject and rep.no:
+        if fault_hook and pbuilders._fault_inject and rep.no:
             O = O.copy()
             O[0] ^= 1
         report = pbuilders.BuildReport(rep.algo, no=rep.no, max_task_work=rep.max_task_work,
                                        total_work=rep.total_work, phase_ms=dict(rep.phase_ms))
         return pgridcore.CompactGrid(spec, grid.G, O), report
 
-    build_parallel.__doc__ = _b.build_parallel.__doc__
-    build_parallel.__wrapped_b200__ = True
-    return build_parallel
+    if has_record:
+        def build(mesh, spec, workers=None, record=None):
+            return convert(spec, *_wrap_errors(ours, perr)(mesh, spec, workers=workers, record=record))
+    else:
+        def build(mesh, spec, workers=None):
+            return convert(spec, *_wrap_errors(ours, perr)(mesh, spec, workers=workers))
+    build.__name__ = ours.__name__
+    build.__doc__ = ours.__doc__
+    build.__wrapped_b200__ = True
+    return build
+
+
+def make_build_parallel(pargrid):
+    return _make_builder(pargrid, _b.build_parallel, True, True)
+
+
+def make_build_sorted(pargrid):
+    return _make_builder(pargrid, _b.build_sorted, True, True)
+
+
+def make_build_compact(pargrid):
+    return _make_builder(pargrid, _b.build_compact, False, False)
 
 
 def make_backend(pargrid):
@@ -67,18 +87,26 @@ def make_backend(pargrid):
     return mod
 
 
-def install(pargrid=None, backend=True):
+def install(pargrid=None, backend=True, algos=("parallel",)):
+    """algos: which builders to replace ("parallel", "sorted", "compact", or "all")."""
     if pargrid is None:
         import pargrid  # noqa: F401
         pargrid = sys.modules["pargrid"]
-    bp = make_build_parallel(pargrid)
-    sys.modules["pargrid.builders"].build_parallel = bp
-    pargrid.build_parallel = bp
+    if algos == "all":
+        algos = ("parallel", "sorted", "compact")
+    makers = {"parallel": make_build_parallel, "sorted": make_build_sorted, "compact": make_build_compact}
     cli = sys.modules.get("pargrid.cli")
     if cli is None:
         import importlib
         cli = importlib.import_module("pargrid.cli")
-    cli.ALGORITHMS["parallel"] = bp
+    bp = None
+    for algo in algos:
+        fn = makers[algo](pargrid)
+        setattr(sys.modules["pargrid.builders"], f"build_{algo}", fn)
+        setattr(pargrid, f"build_{algo}", fn)
+        cli.ALGORITHMS[algo] = fn
+        if algo == "parallel":
+            bp = fn
     if backend:
         sys.modules["pargrid.kernels"]._BACKENDS["cuda"] = make_backend(pargrid)
     return bp

@@ -170,7 +170,7 @@ struct pg_builder {
   // K1 outputs / scratch
   DevBuf rec, k1_sync;
   // pair buffers and sort scratch
-  DevBuf pairs, sort_sync, stage, stage0, gbuf, obuf;
+  DevBuf pairs, sort_sync, stage, stage0, gbuf, obuf, cells;
   // state of the last pg_count
   bool counted = false;
   int64_t n = 0;
@@ -225,7 +225,7 @@ void pg_builder_destroy(pg_builder* b) {
   if (b->g_out) cudaEventDestroy(b->g_out);
   if (b->gst) cudaStreamDestroy(b->gst);
   for (DevBuf* d : {&b->in_v, &b->in_t, &b->rec, &b->k1_sync, &b->pairs, &b->sort_sync, &b->stage, &b->stage0,
-                    &b->gbuf, &b->obuf})
+                    &b->gbuf, &b->obuf, &b->cells})
     d->release();
   delete b;
 }
@@ -629,6 +629,149 @@ int pg_build_wait(pg_builder* b, uint64_t* no_out) {
   if (b->no > b->g_cap)
     return fail(PG_CAPACITY_ERROR, "NO = %llu exceeds the O capacity %llu", (unsigned long long)b->no,
                 (unsigned long long)b->g_cap);
+  return PG_OK;
+}
+
+// The paper's comparison builders on the GPU (builders.py:172-231): after pg_count,
+// algo 1 = "sorted" (per-object pair generation + the same radix/G tail), algo 2 = "compact"
+// (per-cell counters, scan, slot claims, per-cell canonical sort). Same G/O as pg_finish.
+int pg_finish_baseline(pg_builder* b, int algo, uint32_t* G, uint32_t* O, uint32_t flags, void* stream_,
+                       float* phase_ms, uint64_t* max_task_work) {
+  if (!b || !b->counted) return fail(PG_STATE_ERROR, "pg_finish_baseline without a successful pg_count");
+  if (algo != 1 && algo != 2) return fail(PG_INVARIANT_ERROR, "algo must be 1 (sorted) or 2 (compact)");
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  drop_graph(b);
+  const uint64_t no = b->no;
+  const int64_t ncells = b->ncells;
+  int rc;
+  unsigned* dG = G;
+  unsigned* dO = O;
+  if (flags & PG_HOST_OUTPUT) {
+    if ((rc = b->gbuf.ensure((size_t)(ncells + 1) * 4))) return rc;
+    if ((rc = b->obuf.ensure(std::max<size_t>((size_t)no * 4, 4)))) return rc;
+    dG = b->gbuf.as<unsigned>();
+    dO = b->obuf.as<unsigned>();
+  }
+  const unsigned dxu = (unsigned)b->dims[0], dxyu = (unsigned)b->dims[0] * (unsigned)b->dims[1];
+  const unsigned tgrid = (unsigned)((b->n + 255) / 256);
+  CU(cudaEventRecord(b->ev[0], st));
+  if (algo == 1) {
+    const PassPlan plan = make_plan(b->key_bits, kMaxDigitBits);
+    const size_t sec = align_up(std::max<size_t>((size_t)no * 4, 16));
+    if ((rc = b->pairs.ensure(4 * sec + 256))) return rc;
+    unsigned* kA = b->pairs.as<unsigned>(0);
+    unsigned* vA = b->pairs.as<unsigned>(sec);
+    unsigned* kB = b->pairs.as<unsigned>(2 * sec);
+    unsigned* vB = b->pairs.as<unsigned>(3 * sec);
+    unsigned* dmax = b->pairs.as<unsigned>(4 * sec);
+    const unsigned rs_tiles = (unsigned)((no + RS_TILE - 1) / RS_TILE);
+    const unsigned g_tiles = (unsigned)((ncells + G_TILE - 1) / G_TILE);
+    const size_t hist_bytes = align_up(kMaxPasses * kMaxBins * 4), kb_bytes = align_up((size_t)(g_tiles + 1) * 4);
+    if ((rc = b->sort_sync.ensure(hist_bytes + kb_bytes + (size_t)((rs_tiles + 3) & ~3u) * kMaxBins * 4))) return rc;
+    unsigned* hist = b->sort_sync.as<unsigned>(0);
+    unsigned* kbounds = b->sort_sync.as<unsigned>(hist_bytes);
+    unsigned* counts = b->sort_sync.as<unsigned>(hist_bytes + kb_bytes);
+    CU(cudaMemsetAsync(dmax, 0, 4, st));
+    if (b->n) {
+      k_pairgen_per_object<<<tgrid, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no, dxu, dxyu,
+                                                  kA, plan.npasses ? vA : dO, dmax);
+      LAUNCHED("k_pairgen_per_object", st);
+    }
+    CU(cudaEventRecord(b->ev[1], st));
+    const unsigned* sorted = kA;
+    if (no && plan.npasses) {
+      CU(cudaMemsetAsync(hist, 0, hist_bytes, st));
+      if ((rc = run_passes(b, plan, false, kA, vA, kB, vB, dO, Count{nullptr, (unsigned)no}, no, hist, counts, st,
+                           &sorted)))
+        return rc;
+    }
+    CU(cudaEventRecord(b->ev[2], st));
+    k_key_tile_bounds<<<(g_tiles + 1 + 7) / 8, 256, 0, st>>>(sorted, Count{nullptr, (unsigned)no}, G_TILE,
+                                                            (unsigned)ncells, g_tiles + 1, kbounds);
+    LAUNCHED("k_key_tile_bounds", st);
+    k_cell_offsets<<<g_tiles, G_THREADS, 0, st>>>(sorted, Count{nullptr, (unsigned)no}, (unsigned)ncells, kbounds, dG);
+    LAUNCHED("k_cell_offsets", st);
+    CU(cudaEventRecord(b->ev[3], st));
+    unsigned hm = 0;
+    CU(cudaMemcpyAsync(&hm, dmax, 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (max_task_work) *max_task_work = hm;
+  } else {
+    // cells: [counts / cursors u32 x ncells][big-segment list u32 x ncells][tile sums][tile prefixes][scalars]
+    const unsigned xtiles = (unsigned)((ncells + XS_TILE - 1) / XS_TILE);
+    const size_t cbytes = align_up((size_t)ncells * 4);
+    const size_t need = 2 * cbytes + align_up((size_t)xtiles * 8) + align_up((size_t)xtiles * 4) + 256;
+    if ((rc = b->cells.ensure(need))) return rc;
+    unsigned* cnt = b->cells.as<unsigned>(0);
+    unsigned* big = b->cells.as<unsigned>(cbytes);
+    unsigned long long* tsum = b->cells.as<unsigned long long>(2 * cbytes);
+    unsigned* tpre = b->cells.as<unsigned>(2 * cbytes + align_up((size_t)xtiles * 8));
+    unsigned* scal = b->cells.as<unsigned>(2 * cbytes + align_up((size_t)xtiles * 8) + align_up((size_t)xtiles * 4));
+    unsigned long long* total = reinterpret_cast<unsigned long long*>(scal + 2);
+    CU(cudaMemsetAsync(cnt, 0, (size_t)ncells * 4, st));
+    CU(cudaMemsetAsync(scal, 0, 16, st));
+    if (b->n) {
+      k_compact_walk<false><<<tgrid, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no, dxu, dxyu,
+                                                   cnt, nullptr, scal + 1);
+      LAUNCHED("k_compact_walk<count>", st);
+    }
+    CU(cudaEventRecord(b->ev[1], st));
+    k_tile_reduce<<<xtiles, XS_THREADS, 0, st>>>(cnt, ncells, tsum);
+    LAUNCHED("k_tile_reduce", st);
+    k_scan_tile_sums<<<1, TS_THREADS, 0, st>>>(tsum, xtiles, tpre, total);
+    LAUNCHED("k_scan_tile_sums", st);
+    k_tile_scan_apply<<<xtiles, XS_THREADS, 0, st>>>(cnt, ncells, tpre, total, dG);
+    LAUNCHED("k_tile_scan_apply", st);
+    CU(cudaMemcpyAsync(cnt, dG, (size_t)ncells * 4, cudaMemcpyDeviceToDevice, st));  // cursors = G
+    CU(cudaEventRecord(b->ev[2], st));
+    if (b->n) {
+      k_compact_walk<true><<<tgrid, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)no, dxu, dxyu,
+                                                  cnt, dO, nullptr);
+      LAUNCHED("k_compact_walk<fill>", st);
+    }
+    k_sort_segments_small<<<(unsigned)((ncells + 255) / 256), 256, 0, st>>>(dG, (unsigned)ncells, dO, big, scal);
+    LAUNCHED("k_sort_segments_small", st);
+    unsigned hsc[2] = {0, 0};
+    CU(cudaMemcpyAsync(hsc, scal, 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    const unsigned hb = hsc[0];
+    if (hb) {
+      k_sort_segments_big<<<hb, 1024, 0, st>>>(dG, big, scal, dO);
+      LAUNCHED("k_sort_segments_big", st);
+    }
+    CU(cudaEventRecord(b->ev[3], st));
+    if (max_task_work) *max_task_work = hsc[1];  // the largest per-object walk (builders.py:228)
+  }
+  if (flags & PG_HOST_OUTPUT) {
+    CU(cudaMemcpyAsync(G, dG, (size_t)(ncells + 1) * 4, cudaMemcpyDeviceToHost, st));
+    if (no) CU(cudaMemcpyAsync(O, dO, no * 4, cudaMemcpyDeviceToHost, st));
+  }
+  CU(cudaEventRecord(b->ev[4], st));
+  CU(cudaEventSynchronize(b->ev[4]));
+  if (phase_ms) {
+    float t01 = 0, t12 = 0, t23 = 0, t34 = 0, t_k1 = 0;
+    CU(cudaEventElapsedTime(&t01, b->ev[0], b->ev[1]));
+    CU(cudaEventElapsedTime(&t12, b->ev[1], b->ev[2]));
+    CU(cudaEventElapsedTime(&t23, b->ev[2], b->ev[3]));
+    CU(cudaEventElapsedTime(&t34, b->ev[3], b->ev[4]));
+    if (b->k1_timed) CU(cudaEventElapsedTime(&t_k1, b->ev[5], b->ev[6]));
+    phase_ms[0] = t_k1;
+    if (algo == 1) {  // count | scan | pairgen | sort | rle | finalize
+      phase_ms[1] = 0.f;
+      phase_ms[2] = t01;
+      phase_ms[3] = t12;
+      phase_ms[4] = 0.f;
+      phase_ms[5] = t23 + t34;
+    } else {          // compact: counting in "count", G scan in "scan", fill in "pairgen", sort in "finalize"
+      phase_ms[0] += t01;
+      phase_ms[1] = t12;
+      phase_ms[2] = t23;
+      phase_ms[3] = 0.f;
+      phase_ms[4] = 0.f;
+      phase_ms[5] = t34;
+    }
+  }
   return PG_OK;
 }
 

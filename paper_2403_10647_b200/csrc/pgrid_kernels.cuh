@@ -1111,4 +1111,190 @@ k_cell_offsets(const unsigned* __restrict__ sorted, Count cno, unsigned ncells, 
   if (blockIdx.x == gridDim.x - 1 && tid == 0) G[ncells] = no;
 }
 
+// ----------------------------------------------------------------------------------------
+// The paper's comparison builders: "sorted" and "compact" grids
+// (builders.py:172-231). Both walk each triangle's whole cell box in one thread, which is
+// exactly the per-object load imbalance Alg. 1 removes; they produce the same
+// canonical G/O and share K1 with the parallel builder.
+// ----------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned tri_offset_or_end(const uint4* __restrict__ rec,
+                                                      const unsigned* __restrict__ tile_pre, long long n,
+                                                      unsigned no, long long i) {
+  return i < n ? tri_offset(rec, tile_pre, i) : no;
+}
+
+// pairgen_sorted (_ckernels.pyx:53-70): one thread per triangle writes its cells, x-fastest.
+__global__ void __launch_bounds__(256)
+k_pairgen_per_object(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, unsigned no,
+                     unsigned dx, unsigned dxy, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
+                     unsigned* __restrict__ max_work) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint4 r = __ldg(&rec[i]);
+  unsigned pos = tri_offset_or_end(rec, tile_pre, n, no, i);
+  const unsigned end = tri_offset_or_end(rec, tile_pre, n, no, i + 1);
+  if (end > pos) atomicMax(max_work, end - pos);
+  const unsigned mz = (end - pos) / (r.y * r.z);
+  for (unsigned z = 0; z < mz; ++z)
+    for (unsigned y = 0; y < r.z; ++y) {
+      const unsigned row = r.x + dx * y + dxy * z;
+      for (unsigned x = 0; x < r.y; ++x) {
+        keys[pos] = row + x;
+        vals[pos] = (unsigned)i;
+        ++pos;
+      }
+    }
+}
+
+// compact_count / compact_fill (_ckernels.pyx:73-109): per-cell counters, then slot claims.
+template <bool FILL>
+__global__ void __launch_bounds__(256)
+k_compact_walk(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, unsigned no,
+               unsigned dx, unsigned dxy, unsigned* __restrict__ cell, unsigned* __restrict__ O,
+               unsigned* __restrict__ max_work) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint4 r = __ldg(&rec[i]);
+  const unsigned cnt = tri_offset_or_end(rec, tile_pre, n, no, i + 1) - tri_offset_or_end(rec, tile_pre, n, no, i);
+  if (!cnt) return;
+  if (!FILL && max_work) atomicMax(max_work, cnt);
+  const unsigned mz = cnt / (r.y * r.z);
+  for (unsigned z = 0; z < mz; ++z)
+    for (unsigned y = 0; y < r.z; ++y) {
+      const unsigned row = r.x + dx * y + dxy * z;
+      unsigned x = 0;
+      if (FILL) {  // cell[] = cursors (copy of G); 4 slot claims in flight per step
+        for (; x + 4 <= r.y; x += 4) {
+          const unsigned s0 = atomicAdd(&cell[row + x], 1u), s1 = atomicAdd(&cell[row + x + 1], 1u);
+          const unsigned s2 = atomicAdd(&cell[row + x + 2], 1u), s3 = atomicAdd(&cell[row + x + 3], 1u);
+          O[s0] = (unsigned)i;
+          O[s1] = (unsigned)i;
+          O[s2] = (unsigned)i;
+          O[s3] = (unsigned)i;
+        }
+      }
+      for (; x < r.y; ++x) {
+        if (FILL)
+          O[atomicAdd(&cell[row + x], 1u)] = (unsigned)i;
+        else
+          atomicAdd(&cell[row + x], 1u);                   // cell[] = counts
+      }
+    }
+}
+
+// Generic exclusive scan of u32[n] -> out[n] (+ out[n] = total when with_total): per-tile sums,
+// k_scan_tile_sums over the tiles, then the tile-local scans.
+constexpr int XS_THREADS = 256;
+constexpr int XS_ITEMS = 16;
+constexpr int XS_TILE = XS_THREADS * XS_ITEMS;
+__global__ void __launch_bounds__(XS_THREADS)
+k_tile_reduce(const unsigned* __restrict__ in, long long n, unsigned long long* __restrict__ tile_sum) {
+  __shared__ unsigned long long w[XS_THREADS / 32];
+  const long long base = (long long)blockIdx.x * XS_TILE;
+  unsigned long long s = 0;
+#pragma unroll
+  for (int q = 0; q < XS_ITEMS; ++q) {
+    const long long i = base + q * XS_THREADS + threadIdx.x;
+    s += i < n ? __ldg(in + i) : 0u;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
+  if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int k = 0; k < XS_THREADS / 32; ++k) t += w[k];
+    tile_sum[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(XS_THREADS)
+k_tile_scan_apply(const unsigned* __restrict__ in, long long n, const unsigned* __restrict__ tile_pre,
+                  const unsigned long long* __restrict__ total, unsigned* __restrict__ out) {
+  __shared__ unsigned wsum[XS_THREADS / 32];
+  const long long base = (long long)blockIdx.x * XS_TILE + (long long)threadIdx.x * XS_ITEMS;
+  unsigned v[XS_ITEMS], run = 0;
+#pragma unroll
+  for (int q = 0; q < XS_ITEMS; ++q) {
+    const unsigned x = base + q < n ? __ldg(in + base + q) : 0u;
+    v[q] = run;
+    run += x;
+  }
+  unsigned tot;
+  const unsigned pre = tile_pre[blockIdx.x] + block_excl_scan<XS_THREADS / 32>(run, wsum, tot);
+#pragma unroll
+  for (int q = 0; q < XS_ITEMS; ++q)
+    if (base + q < n) out[base + q] = pre + v[q];
+  if (blockIdx.x == 0 && threadIdx.x == 0 && total) out[n] = (unsigned)*total;
+}
+
+// Canonicalisation of the compact grid (ids ascending per cell, builders.py:221-225):
+// short segments by one thread (insertion sort), longer ones queued for a CTA each.
+constexpr int SEG_SMALL = 32;
+constexpr int SEG_BLOCK = 4096;
+__global__ void __launch_bounds__(256)
+k_sort_segments_small(const unsigned* __restrict__ G, unsigned ncells, unsigned* __restrict__ O,
+                      unsigned* __restrict__ big, unsigned* __restrict__ nbig) {
+  const unsigned c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncells) return;
+  const unsigned a = G[c], e = G[c + 1];
+  const unsigned len = e - a;
+  if (len <= 1) return;
+  if (len > SEG_SMALL) {
+    big[atomicAdd(nbig, 1u)] = c;
+    return;
+  }
+  for (unsigned k = 1; k < len; ++k) {  // insertion sort (segments are mostly 1-3 ids)
+    const unsigned x = O[a + k];
+    unsigned m = k;
+    while (m > 0 && O[a + m - 1] > x) {
+      O[a + m] = O[a + m - 1];
+      --m;
+    }
+    O[a + m] = x;
+  }
+}
+
+// One CTA per long segment: bitonic sort, all compare-exchanges ascending (the first stage of
+// each merge pairs k with its mirror k ^ (size-1)), so virtual +inf padding past the segment
+// never moves and compare-exchanges against it can be skipped. Segments of up to SEG_BLOCK
+// ids are sorted in shared memory, longer ones (rare) in place in global memory.
+template <typename Load, typename Store>
+__device__ __forceinline__ void bitonic_ascending(unsigned len, Load ld, Store stv) {
+  unsigned p2 = 1;
+  while (p2 < len) p2 <<= 1;
+  for (unsigned size = 2; size <= p2; size <<= 1)
+    for (unsigned stride = size >> 1; stride > 0; stride >>= 1) {
+      for (unsigned k = threadIdx.x; k < p2; k += blockDim.x) {
+        const unsigned j = stride == (size >> 1) ? (k ^ (size - 1)) : (k ^ stride);
+        if (j > k && j < len) {
+          const unsigned x = ld(k), y = ld(j);
+          if (x > y) {
+            stv(k, y);
+            stv(j, x);
+          }
+        }
+      }
+      __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(1024)
+k_sort_segments_big(const unsigned* __restrict__ G, const unsigned* __restrict__ big, const unsigned* __restrict__ nbig,
+                    unsigned* __restrict__ O) {
+  __shared__ unsigned sh[SEG_BLOCK];
+  if (blockIdx.x >= *nbig) return;
+  const unsigned c = big[blockIdx.x];
+  const unsigned a = G[c], len = G[c + 1] - a;
+  if (len <= SEG_BLOCK) {
+    for (unsigned k = threadIdx.x; k < len; k += blockDim.x) sh[k] = O[a + k];
+    __syncthreads();
+    bitonic_ascending(len, [&](unsigned k) { return sh[k]; }, [&](unsigned k, unsigned v) { sh[k] = v; });
+    for (unsigned k = threadIdx.x; k < len; k += blockDim.x) O[a + k] = sh[k];
+  } else {
+    unsigned* seg = O + a;
+    bitonic_ascending(len, [&](unsigned k) { return seg[k]; }, [&](unsigned k, unsigned v) { seg[k] = v; });
+  }
+}
+
 }  // namespace pgrid

@@ -14,10 +14,12 @@ REF = os.path.join(ROOT, "oracle", "_ref")
 pytestmark = pytest.mark.gpu
 
 
-def test_reference_suite_against_gpu_builder():
+@pytest.mark.parametrize("algos", ["parallel", "all"])
+def test_reference_suite_against_gpu_builder(algos):
     if not os.path.isdir(os.path.join(REF, "tests")):
         pytest.skip("oracle/_ref/tests not built (make -C oracle ref)")
     env = dict(os.environ)
+    env["PGRID_INJECT_ALGOS"] = algos
     env["PYTHONPATH"] = os.pathsep.join([REF, os.path.join(ROOT, "tests"), ROOT, env.get("PYTHONPATH", "")])
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "ref_inject_plugin",
                         "-p", "no:cacheprovider", os.path.join(REF, "tests")],
