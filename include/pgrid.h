@@ -39,6 +39,8 @@ extern "C" {
 #define PG_HOST_INPUT 1u       /* V/T (or sort inputs) are host pointers: copied H2D in-call */
 #define PG_HOST_OUTPUT 2u      /* G/O (or sort outputs) are host pointers: copied D2H in-call */
 #define PG_KEEP_STAGES 4u      /* keep the unsorted pairs for pg_stage (record= support) */
+#define PG_HOST_RAYS 8u        /* pg_dda_cast: rays are host pointers (grid stays on device) */
+#define PG_CHECK 16u           /* pg_dda_cast: synchronise and report device-side errors */
 
 /* Grid specification: the exact host doubles of GridSpec (gridcore.py:36-57). */
 typedef struct {
@@ -80,6 +82,21 @@ int pg_finish(pg_builder *b, uint32_t *G, uint32_t *O, uint32_t flags, void *str
  * max_task_work (may be NULL) receives the largest per-object task (sorted builder). */
 int pg_finish_baseline(pg_builder *b, int algo, uint32_t *G, uint32_t *O, uint32_t flags,
                        void *stream, float *phase_ms, uint64_t *max_task_work);
+
+/* Ray casting over a built grid (traverse.py:114-131 ->
+ * kernels.dda_cast, kernels/__init__.py:66-67 -> _ckernels.pyx:146-260).
+ * pg_dda_prepare stages the mesh once (per-triangle v0/e1/e2 records; PG_HOST_INPUT: V/T are
+ * host pointers; index range checked -> PG_INVARIANT_ERROR). pg_dda_cast then walks the
+ * grid (G u32[ncells+1], O u32[no]) for nrays rays (origins/dirs f64[nrays][3], t_max
+ * f64[nrays]) and writes ids i64 (-1 on a miss) and ts f64 (+inf on a miss), bit-identical
+ * to the reference's compiled lane. Flags: PG_HOST_INPUT (grid and rays on the host),
+ * PG_HOST_RAYS (rays only), PG_HOST_OUTPUT (ids/ts on the host), PG_CHECK (synchronise and
+ * fail on an O entry outside the prepared mesh). */
+int pg_dda_prepare(pg_builder *b, const double *V, int64_t nv, const int32_t *T, int64_t n,
+                   uint32_t flags, void *stream);
+int pg_dda_cast(pg_builder *b, const uint32_t *G, const uint32_t *O, int64_t no, const pg_spec *spec,
+                const double *origins, const double *dirs, const double *t_max, int64_t nrays,
+                int64_t *ids, double *ts, uint32_t flags, void *stream);
 
 /* Sync-free build on device-resident V/T/G/O (no host round trip between K1 and the sort):
  * enqueues the whole of Alg. 1 on `stream` with every buffer sized for o_capacity pairs;

@@ -46,6 +46,8 @@ def lib():
         _lib.orc_build_parallel.argtypes = [p, p, ctypes.c_int64, p, p, p, p, p, p, p]
         _lib.orc_radix_sort_pairs.argtypes = [p, p, ctypes.c_int64, ctypes.c_int, p, p]
         _lib.orc_cell_boxes.argtypes = [p, p, ctypes.c_int64, p, p, p, p]
+        _lib.orc_dda_cast.argtypes = [p, p, p, p, p, p, p, p, ctypes.c_int64, p, p]
+        _lib.orc_brute_cast.argtypes = [p, p, ctypes.c_int64, p, p, p, ctypes.c_int64, p, p]
     return _lib
 
 
@@ -120,6 +122,37 @@ def build_parallel(vertices, triangles, spec, stages=False):
         return G, O
     return G, O, {"no": NO, "global_c": st[0], "obj_ids": st[1],
                   "sorted_c": st[2], "sorted_o": st[3]}
+
+
+def _rays(origins, dirs, t_max):
+    o = np.ascontiguousarray(origins, dtype=np.float64).reshape(-1, 3)
+    d = np.ascontiguousarray(dirs, dtype=np.float64).reshape(-1, 3)
+    t = np.ascontiguousarray(t_max, dtype=np.float64).reshape(-1)
+    return o, d, t
+
+
+def dda_cast(G, O, vertices, triangles, spec, origins, dirs, t_max):
+    """_ckernels.pyx:146-260 restated in C: (ids i64 with -1 on miss, ts f64)."""
+    V, T = _arrays(vertices, triangles)
+    G = np.ascontiguousarray(G, dtype=np.uint32)
+    O = np.ascontiguousarray(O, dtype=np.uint32)
+    o, d, t = _rays(origins, dirs, t_max)
+    ids = np.empty(len(o), np.int64)
+    ts = np.empty(len(o), np.float64)
+    s = spec_of(spec)
+    lib().orc_dda_cast(_ptr(G), _ptr(O), _ptr(V), _ptr(T), ctypes.byref(s), _ptr(o), _ptr(d), _ptr(t),
+                       len(o), _ptr(ids), _ptr(ts))
+    return ids, ts
+
+
+def brute_cast(vertices, triangles, origins, dirs, t_max):
+    """traverse.py:134-170 (all-triangles nearest hit) restated in C."""
+    V, T = _arrays(vertices, triangles)
+    o, d, t = _rays(origins, dirs, t_max)
+    ids = np.empty(len(o), np.int64)
+    ts = np.empty(len(o), np.float64)
+    lib().orc_brute_cast(_ptr(V), _ptr(T), len(T), _ptr(o), _ptr(d), _ptr(t), len(o), _ptr(ids), _ptr(ts))
+    return ids, ts
 
 
 def reference_module():

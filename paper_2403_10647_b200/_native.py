@@ -25,13 +25,15 @@ PG_CAPACITY_ERROR = 5
 PG_HOST_INPUT = 1
 PG_HOST_OUTPUT = 2
 PG_KEEP_STAGES = 4
+PG_HOST_RAYS = 8
+PG_CHECK = 16
 
 NPHASES = 6
 
 # every symbol include/pgrid.h declares (checked by tests/test_boundary.py)
 EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
            "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_finish_baseline",
-           "pg_build_async",
+           "pg_dda_prepare", "pg_dda_cast", "pg_build_async",
            "pg_build_wait", "pg_host_register",
            "pg_host_unregister", "pg_host_alloc", "pg_host_free", "pg_last_launch_count",
            "pg_last_error")
@@ -85,6 +87,8 @@ def load():
         lib.pg_sort_cells.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp]
         lib.pg_finish_baseline.argtypes = [vp, ctypes.c_int, vp, vp, u32, vp, ctypes.POINTER(ctypes.c_float),
                                            ctypes.POINTER(u64)]
+        lib.pg_dda_prepare.argtypes = [vp, vp, i64, vp, i64, u32, vp]
+        lib.pg_dda_cast.argtypes = [vp, vp, vp, i64, ctypes.POINTER(PgSpec), vp, vp, vp, i64, vp, vp, u32, vp]
         lib.pg_build_async.argtypes = [vp, vp, i64, vp, i64, ctypes.POINTER(PgSpec), vp, vp, u64, vp]
         lib.pg_build_wait.argtypes = [vp, ctypes.POINTER(u64)]
         lib.pg_host_register.argtypes = [vp, u64]
@@ -95,7 +99,7 @@ def load():
         lib.pg_last_error.restype = ctypes.c_char_p
         for name in ("pg_builder_create", "pg_count", "pg_finish", "pg_stage",
                      "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells",
-                     "pg_finish_baseline", "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
+                     "pg_finish_baseline", "pg_dda_prepare", "pg_dda_cast", "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
                      "pg_last_launch_count"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
@@ -167,6 +171,14 @@ class Builder:
         check(self._lib.pg_finish_baseline(self._h, int(algo), ptr(G), ptr(O), flags, stream, phases,
                                            ctypes.byref(mw)))
         return list(phases), int(mw.value)
+
+    def dda_prepare(self, V, nv, T, n, flags=0, stream=None):
+        check(self._lib.pg_dda_prepare(self._h, ptr(V), int(nv), ptr(T), int(n), flags, stream))
+
+    def dda_cast(self, G, O, no, spec, origins, dirs, t_max, nrays, ids, ts, flags=0, stream=None, pgspec=None):
+        s = pgspec or PgSpec.from_spec(spec)
+        check(self._lib.pg_dda_cast(self._h, ptr(G), ptr(O), int(no), ctypes.byref(s), ptr(origins), ptr(dirs),
+                                    ptr(t_max), int(nrays), ptr(ids), ptr(ts), flags, stream))
 
     def stage(self, stage, dst, flags=PG_HOST_OUTPUT, stream=None):
         check(self._lib.pg_stage(self._h, int(stage), ptr(dst), flags, stream))

@@ -10,6 +10,7 @@ replaces, in place (SURVEY.md §8b "Callers"):
     -- the GPU comparison builders of SURVEY §8(f) row 1 (algos="all")
   * pargrid.cli.ALGORITHMS[...] for each replaced builder       (cli.py:30-34)
   * pargrid.kernels._BACKENDS["cuda"]                           (kernels/__init__.py:17-19)
+    -- radix_sort_pairs and dda_cast on the GPU
 The wrapper returns the reference's own CompactGrid / BuildReport types, raises the
 reference's own error classes and honours pargrid.builders._fault_inject, so the
 reference's test-suite runs unchanged against the GPU path (tests/test_reference_suite.py).
@@ -82,7 +83,8 @@ def make_backend(pargrid):
     mod = types.ModuleType("pargrid_cuda_lane")
     mod.BACKEND_NAME = _k.BACKEND_NAME
     mod.radix_sort_pairs = _k.radix_sort_pairs
-    for name in ("pairgen_sorted", "compact_count", "compact_fill", "dda_cast"):
+    mod.dda_cast = _k.dda_cast
+    for name in ("pairgen_sorted", "compact_count", "compact_fill"):
         setattr(mod, name, getattr(lane, name))
     return mod
 

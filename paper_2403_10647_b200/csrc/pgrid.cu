@@ -15,6 +15,7 @@
 
 #include "../../include/pgrid.h"
 #include "pgrid_kernels.cuh"
+#include "pgrid_dda.cuh"
 
 using namespace pgrid;
 
@@ -192,6 +193,9 @@ struct pg_builder {
   std::vector<unsigned char> gkey;
   uint64_t g_cap = 0;
   int glaunches = 0;
+  // ray casting (pg_dda_prepare / pg_dda_cast): prepared triangles + staging
+  DevBuf tris, dda_err, dda_grid, dda_rays, dda_out;
+  int64_t dda_ntri = -1;
 };
 
 extern "C" {
@@ -967,6 +971,120 @@ int pg_sort_cells(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int
   k_cell_offsets<<<g_tiles, G_THREADS, 0, st>>>(sorted, Count{nullptr, (unsigned)n}, (unsigned)ncells, kbounds, G);
   LAUNCHED("k_cell_offsets", st);
   b->launches += 2;
+  return PG_OK;
+}
+
+int pg_dda_prepare(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64_t n, uint32_t flags,
+                   void* stream_) {
+  if (!b) return fail(PG_INVARIANT_ERROR, "null builder");
+  if (nv < 0 || n < 0) return fail(PG_INVARIANT_ERROR, "negative mesh size");
+  if (n > 0 && (!V || !T)) return fail(PG_INVARIANT_ERROR, "null mesh arrays");
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  int rc;
+  b->dda_ntri = -1;
+  if ((rc = b->tris.ensure(std::max<size_t>((size_t)n * sizeof(TriRec), 16)))) return rc;
+  if ((rc = b->dda_err.ensure(16))) return rc;
+  if (n == 0) {
+    b->dda_ntri = 0;
+    return PG_OK;
+  }
+  const double* dV = V;
+  const int32_t* dT = T;
+  if (flags & PG_HOST_INPUT) {
+    if ((rc = b->in_v.ensure(std::max<size_t>((size_t)nv * 24, 16)))) return rc;
+    if ((rc = b->in_t.ensure((size_t)n * 12))) return rc;
+    if (nv) CU(cudaMemcpyAsync(b->in_v.p, V, (size_t)nv * 24, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(b->in_t.p, T, (size_t)n * 12, cudaMemcpyHostToDevice, st));
+    dV = b->in_v.as<double>();
+    dT = b->in_t.as<int32_t>();
+  }
+  unsigned* err = b->dda_err.as<unsigned>();
+  CU(cudaMemsetAsync(err, 0, 4, st));
+  k_dda_prepare<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dV, nv, dT, n, b->tris.as<TriRec>(), err);
+  LAUNCHED("k_dda_prepare", st);
+  unsigned herr = 0;
+  CU(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (herr & 2u) return fail(PG_INVARIANT_ERROR, "triangle index out of range");
+  b->dda_ntri = n;
+  return PG_OK;
+}
+
+int pg_dda_cast(pg_builder* b, const uint32_t* G, const uint32_t* O, int64_t no, const pg_spec* spec,
+                const double* origins, const double* dirs, const double* t_max, int64_t nrays, int64_t* ids,
+                double* ts, uint32_t flags, void* stream_) {
+  if (!b || !spec) return fail(PG_INVARIANT_ERROR, "null argument");
+  if (b->dda_ntri < 0) return fail(PG_STATE_ERROR, "pg_dda_cast before a successful pg_dda_prepare");
+  if (nrays < 0 || no < 0) return fail(PG_INVARIANT_ERROR, "negative size");
+  int64_t ncells = 1;
+  for (int k = 0; k < 3; ++k) {
+    if (spec->dims[k] < 1) return fail(PG_INVARIANT_ERROR, "dims must be positive");
+    ncells *= spec->dims[k];
+    if (ncells > kMaxIds) return fail(PG_SIZE_ERROR, "%lld cells exceed 32-bit id space", (long long)ncells);
+  }
+  if (nrays == 0) return PG_OK;
+  if (!G || (no && !O) || !origins || !dirs || !t_max || !ids || !ts)
+    return fail(PG_INVARIANT_ERROR, "null array");
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  int rc;
+  const unsigned* dG = G;
+  const unsigned* dO = O;
+  if (flags & PG_HOST_INPUT) {
+    const size_t gb = align_up((size_t)(ncells + 1) * 4);
+    if ((rc = b->dda_grid.ensure(gb + std::max<size_t>((size_t)no * 4, 16)))) return rc;
+    CU(cudaMemcpyAsync(b->dda_grid.p, G, (size_t)(ncells + 1) * 4, cudaMemcpyHostToDevice, st));
+    if (no) CU(cudaMemcpyAsync(b->dda_grid.as<char>(gb), O, (size_t)no * 4, cudaMemcpyHostToDevice, st));
+    dG = b->dda_grid.as<unsigned>();
+    dO = b->dda_grid.as<unsigned>(gb);
+  }
+  const double* dor = origins;
+  const double* ddi = dirs;
+  const double* dtm = t_max;
+  if (flags & (PG_HOST_INPUT | PG_HOST_RAYS)) {
+    const size_t rb = (size_t)nrays * 24;
+    if ((rc = b->dda_rays.ensure(2 * align_up(rb) + (size_t)nrays * 8))) return rc;
+    CU(cudaMemcpyAsync(b->dda_rays.p, origins, rb, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(b->dda_rays.as<char>(align_up(rb)), dirs, rb, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(b->dda_rays.as<char>(2 * align_up(rb)), t_max, (size_t)nrays * 8, cudaMemcpyHostToDevice, st));
+    dor = b->dda_rays.as<double>();
+    ddi = b->dda_rays.as<double>(align_up(rb));
+    dtm = b->dda_rays.as<double>(2 * align_up(rb));
+  }
+  long long* dids = reinterpret_cast<long long*>(ids);
+  double* dts = ts;
+  if (flags & PG_HOST_OUTPUT) {
+    if ((rc = b->dda_out.ensure(2 * align_up((size_t)nrays * 8)))) return rc;
+    dids = b->dda_out.as<long long>();
+    dts = b->dda_out.as<double>(align_up((size_t)nrays * 8));
+  }
+  DdaGrid gs;
+  for (int k = 0; k < 3; ++k) {
+    gs.lo[k] = spec->lo[k];
+    gs.hi[k] = spec->hi[k];
+    gs.cs[k] = spec->cell[k];
+    gs.nd[k] = spec->dims[k];
+  }
+  gs.ntri = b->dda_ntri;
+  unsigned* err = b->dda_err.as<unsigned>();
+  CU(cudaMemsetAsync(err, 0, 4, st));
+  k_dda_cast<<<(unsigned)((nrays + 127) / 128), 128, 0, st>>>(dG, dO, b->tris.as<TriRec>(), gs, dor, ddi, dtm, nrays,
+                                                               dids, dts, err);
+  LAUNCHED("k_dda_cast", st);
+  b->launches = 1;
+  if (flags & PG_HOST_OUTPUT) {
+    CU(cudaMemcpyAsync(ids, dids, (size_t)nrays * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(ts, dts, (size_t)nrays * 8, cudaMemcpyDeviceToHost, st));
+  }
+  if (flags & PG_CHECK) {
+    unsigned herr = 0;
+    CU(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (herr & 4u) return fail(PG_INVARIANT_ERROR, "O holds an object id outside the prepared mesh");
+  } else if (flags & PG_HOST_OUTPUT) {
+    CU(cudaStreamSynchronize(st));
+  }
   return PG_OK;
 }
 

@@ -28,3 +28,12 @@ def kat():
 def hashes():
     with open(os.path.join(GOLDEN, "hashes.json")) as fh:
         return json.load(fh)["scenes"]
+
+
+@pytest.fixture(scope="session")
+def rays():
+    """Golden ray-casting fixtures (tests/golden/make_golden_rays.py): (arrays, case meta)."""
+    with np.load(os.path.join(GOLDEN, "rays.npz")) as z:
+        arrays = {k: z[k] for k in z.files}
+    with open(os.path.join(GOLDEN, "rays.json")) as fh:
+        return arrays, json.load(fh)["cases"]

@@ -27,3 +27,19 @@ def scene_from_recipe(recipe):
     if "dims" in recipe:
         return mesh, spec_for_mesh(mesh, dims=tuple(recipe["dims"]))
     return mesh, spec_for_mesh(mesh, density=recipe["density"])
+
+
+RAY_CASES = ("unit",) + tuple(f"validate_{i}" for i in range(10)) + \
+    ("inside_walls", "inside_uniform", "inside_skewed", "cfg1", "cfg2", "arch1m")
+
+
+def ray_case(rays, name):
+    """(mesh, spec, origins, dirs, t_max) of a golden ray case (make_golden_rays.py)."""
+    arrays, meta = rays
+    recipe = meta[name]["recipe"]
+    if recipe["kind"] == "unit_triangle":
+        mesh = TriangleMesh([[0, 0, 0], [1, 0, 0], [0, 1, 0]], [[0, 1, 2]])
+        spec = spec_for_mesh(mesh, dims=tuple(recipe["dims"]))
+    else:
+        mesh, spec = scene_from_recipe(recipe)
+    return (mesh, spec, arrays[f"{name}/origins"], arrays[f"{name}/dirs"], arrays[f"{name}/t_max"])
