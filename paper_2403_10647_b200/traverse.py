@@ -102,8 +102,8 @@ class RayCaster:
         else:
             self.spec = grid.spec
             dev = torch.device("cuda", device)
-            self.G = torch.from_numpy(np.ascontiguousarray(grid.G, np.uint32).view(np.int32)).to(dev)
-            self.O = torch.from_numpy(np.ascontiguousarray(grid.O, np.uint32).view(np.int32)).to(dev)
+            self.G = torch.from_numpy(np.array(grid.G, np.uint32).view(np.int32)).to(dev)
+            self.O = torch.from_numpy(np.array(grid.O, np.uint32).view(np.int32)).to(dev)
         self.no = int(self.O.numel())
         self._pg = _native.PgSpec.from_spec(self.spec)
         V, T = mesh if isinstance(mesh, tuple) else _mesh(mesh)
