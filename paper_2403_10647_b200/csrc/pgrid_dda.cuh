@@ -78,6 +78,10 @@ __device__ __forceinline__ double ray_tri(double ox, double oy, double oz, doubl
   return t > 0.0 ? t : 0.0;
 }
 
+#ifndef DDA_MIN_CTAS
+#define DDA_MIN_CTAS 6  // 80 registers: 24 warps per SM (measured best of 4, 6, 8) to hide the dependent G -> O -> triangle loads
+#endif
+
 struct DdaGrid {
   double lo[3], hi[3], cs[3];
   long long nd[3];
@@ -87,7 +91,7 @@ struct DdaGrid {
 // _ckernels.pyx:146-260, one thread per ray. The traversal of a ray whose loop never ends
 // in the reference (zero / NaN direction with an unbounded segment) is cut after
 // sum(dims) + 3 cells; every terminating ray visits fewer cells than that.
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, DDA_MIN_CTAS)
 k_dda_cast(const unsigned* __restrict__ G, const unsigned* __restrict__ O, const TriRec* __restrict__ tris,
            DdaGrid gs, const double* __restrict__ orig, const double* __restrict__ dirv,
            const double* __restrict__ tmax, long long nrays, long long* __restrict__ ids, double* __restrict__ ts,
@@ -144,12 +148,32 @@ k_dda_cast(const unsigned* __restrict__ G, const unsigned* __restrict__ O, const
     }
     double t_entry = t0;
     const long long cap = gs.nd[0] + gs.nd[1] + gs.nd[2] + 3;
+    const long long stride[3] = {1, gs.nd[0], gs.nd[0] * gs.nd[1]};
+    long long cid = cell[0] + gs.nd[0] * (cell[1] + gs.nd[1] * cell[2]);
+    unsigned s0 = __ldg(G + cid), s1 = __ldg(G + cid + 1);
     for (long long it = 0; it < cap; ++it) {
       double t_exit = tnext[0];
       if (tnext[1] < t_exit) t_exit = tnext[1];
       if (tnext[2] < t_exit) t_exit = tnext[2];
-      const long long cid = cell[0] + gs.nd[0] * (cell[1] + gs.nd[1] * cell[2]);
-      const unsigned s0 = __ldg(G + cid), s1 = __ldg(G + cid + 1);
+      // the step taken after this cell depends on tnext only: choose it now and fetch the
+      // next cell's G range while this cell's candidates are tested
+      int axis;
+      if (tnext[0] <= tnext[1] && tnext[0] <= tnext[2])
+        axis = 0;
+      else if (tnext[1] <= tnext[2])
+        axis = 1;
+      else
+        axis = 2;
+      const int stp = axis == 0 ? step[0] : axis == 1 ? step[1] : step[2];
+      const long long nc = (axis == 0 ? cell[0] : axis == 1 ? cell[1] : cell[2]) + stp;
+      const long long lim = axis == 0 ? gs.nd[0] : axis == 1 ? gs.nd[1] : gs.nd[2];
+      const bool inside = nc >= 0 && nc < lim;
+      const long long ncid = cid + (long long)stp * (axis == 0 ? stride[0] : axis == 1 ? stride[1] : stride[2]);
+      unsigned n0 = 0, n1 = 0;
+      if (inside) {
+        n0 = __ldg(G + ncid);
+        n1 = __ldg(G + ncid + 1);
+      }
       const double lo_t = __dsub_rn(t_entry, kTEps), hi_t = __dadd_rn(t_exit, kTEps);
       for (unsigned slot = s0; slot < s1; ++slot) {
         const unsigned tri = __ldg(O + slot);
@@ -168,24 +192,16 @@ k_dda_cast(const unsigned* __restrict__ G, const unsigned* __restrict__ O, const
         }
       }
       if (best_id >= 0 && t_exit > __dadd_rn(best_t, kTEps)) break;
-      int axis;
-      if (tnext[0] <= tnext[1] && tnext[0] <= tnext[2])
-        axis = 0;
-      else if (tnext[1] <= tnext[2])
-        axis = 1;
-      else
-        axis = 2;
-      // registers, not local memory: select the axis explicitly
-      const long long nc = (axis == 0 ? cell[0] : axis == 1 ? cell[1] : cell[2]) +
-                           (axis == 0 ? step[0] : axis == 1 ? step[1] : step[2]);
-      const long long lim = axis == 0 ? gs.nd[0] : axis == 1 ? gs.nd[1] : gs.nd[2];
-      if (nc < 0 || nc >= lim) break;
+      if (!inside) break;
       if (axis == 0) cell[0] = nc; else if (axis == 1) cell[1] = nc; else cell[2] = nc;
+      cid = ncid;
       t_entry = t_exit;
       if (axis == 0) tnext[0] = __dadd_rn(tnext[0], tdelta[0]);
       else if (axis == 1) tnext[1] = __dadd_rn(tnext[1], tdelta[1]);
       else tnext[2] = __dadd_rn(tnext[2], tdelta[2]);
       if (t_entry > __dadd_rn(t1, kTEps)) break;
+      s0 = n0;
+      s1 = n1;
     }
   }
   ids[r] = best_id;

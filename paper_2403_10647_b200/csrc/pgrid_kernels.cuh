@@ -932,7 +932,7 @@ k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict
                 unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, Count cno, int shift,
                 const unsigned* __restrict__ hist, const unsigned* __restrict__ offs, unsigned ld,
                 const unsigned* __restrict__ dtable, const unsigned* __restrict__ kbase) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   RsSmem& sm = *reinterpret_cast<RsSmem*>(smem_raw);
   const unsigned no = cno.get();
   const unsigned tile = blockIdx.x;
@@ -965,7 +965,7 @@ __global__ void __launch_bounds__(RS_THREADS)
 k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno,
              unsigned dx, unsigned dxy, PassPlan plan, const int2* __restrict__ bounds, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
              unsigned* __restrict__ counts0) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   PeSmem& sm = *reinterpret_cast<PeSmem*>(smem_raw);
   const int tid = threadIdx.x;
   const unsigned no = cno.get();
