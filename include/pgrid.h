@@ -98,6 +98,12 @@ int pg_dda_cast(pg_builder *b, const uint32_t *G, const uint32_t *O, int64_t no,
                 const double *origins, const double *dirs, const double *t_max, int64_t nrays,
                 int64_t *ids, double *ts, uint32_t flags, void *stream);
 
+/* Grid statistics (stats.py:42-64) for the mesh of the last pg_count
+ * (the grid's spec) and its grid G (u32[ncells+1]; PG_HOST_INPUT: host pointer):
+ * out[0] = non-empty cells, out[1] = in-grid objects, out[2] = max cells per in-grid
+ * object, out[3] = NO. The float attributes are derived from these on the host. */
+int pg_grid_stats(pg_builder *b, const uint32_t *G, uint32_t flags, void *stream, uint64_t *out);
+
 /* Sync-free build on device-resident V/T/G/O (no host round trip between K1 and the sort):
  * enqueues the whole of Alg. 1 on `stream` with every buffer sized for o_capacity pairs;
  * identical repeated calls replay a captured CUDA graph. pg_build_wait synchronises and

@@ -9,6 +9,8 @@ replaces, in place (SURVEY.md §8b "Callers"):
   * pargrid.builders.build_sorted / build_compact (+ pargrid.*) (builders.py:172, 195)
     -- the GPU comparison builders of SURVEY §8(f) row 1 (algos="all")
   * pargrid.cli.ALGORITHMS[...] for each replaced builder       (cli.py:30-34)
+  * pargrid.stats.compute_stats and pargrid.compute_stats       (stats.py:43; GPU reductions,
+    with consumers=True)
   * pargrid.kernels._BACKENDS["cuda"]                           (kernels/__init__.py:17-19)
     -- radix_sort_pairs and dda_cast on the GPU
 The wrapper returns the reference's own CompactGrid / BuildReport types, raises the
@@ -22,6 +24,7 @@ import types
 from . import builders as _b
 from . import errors as _e
 from . import kernels as _k
+from . import stats as _s
 
 
 def _wrap_errors(fn, perr):
@@ -77,6 +80,19 @@ def make_build_compact(pargrid):
     return _make_builder(pargrid, _b.build_compact, False, False)
 
 
+def make_compute_stats(pargrid):
+    perr = pargrid.errors
+    pstats = sys.modules["pargrid.stats"]
+
+    def compute_stats(grid, mesh):
+        st = _wrap_errors(_s.compute_stats, perr)(grid, mesh)
+        return pstats.GridStats(**{f: getattr(st, f) for f in st.__dataclass_fields__})
+
+    compute_stats.__doc__ = _s.compute_stats.__doc__
+    compute_stats.__wrapped_b200__ = True
+    return compute_stats
+
+
 def make_backend(pargrid):
     kernels = sys.modules["pargrid.kernels"]
     lane = kernels._BACKENDS.get("c") or kernels._BACKENDS["python"]
@@ -89,8 +105,9 @@ def make_backend(pargrid):
     return mod
 
 
-def install(pargrid=None, backend=True, algos=("parallel",)):
-    """algos: which builders to replace ("parallel", "sorted", "compact", or "all")."""
+def install(pargrid=None, backend=True, algos=("parallel",), consumers=False):
+    """algos: which builders to replace ("parallel", "sorted", "compact", or "all");
+    consumers: also replace compute_stats (ray casting goes through the "cuda" lane)."""
     if pargrid is None:
         import pargrid  # noqa: F401
         pargrid = sys.modules["pargrid"]
@@ -109,6 +126,13 @@ def install(pargrid=None, backend=True, algos=("parallel",)):
         cli.ALGORITHMS[algo] = fn
         if algo == "parallel":
             bp = fn
+    if consumers:
+        import importlib
+        pstats = importlib.import_module("pargrid.stats")
+        cs = make_compute_stats(pargrid)
+        pstats.compute_stats = cs
+        pargrid.compute_stats = cs
+        cli.compute_stats = cs
     if backend:
         sys.modules["pargrid.kernels"]._BACKENDS["cuda"] = make_backend(pargrid)
     return bp

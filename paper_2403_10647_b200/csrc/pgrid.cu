@@ -1088,4 +1088,42 @@ int pg_dda_cast(pg_builder* b, const uint32_t* G, const uint32_t* O, int64_t no,
   return PG_OK;
 }
 
+int pg_grid_stats(pg_builder* b, const uint32_t* G, uint32_t flags, void* stream_, uint64_t* out) {
+  if (!b || !out) return fail(PG_INVARIANT_ERROR, "null argument");
+  if (!b->counted) return fail(PG_STATE_ERROR, "pg_grid_stats before pg_count");
+  if (!G) return fail(PG_INVARIANT_ERROR, "null G");
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  int rc;
+  const int64_t ncells = b->ncells;
+  const unsigned* dG = G;
+  if (flags & PG_HOST_INPUT) {
+    if ((rc = b->gbuf.ensure((size_t)(ncells + 1) * 4))) return rc;
+    CU(cudaMemcpyAsync(b->gbuf.p, G, (size_t)(ncells + 1) * 4, cudaMemcpyHostToDevice, st));
+    dG = b->gbuf.as<unsigned>();
+  }
+  if ((rc = b->dda_err.ensure(64))) return rc;
+  unsigned long long* acc = b->dda_err.as<unsigned long long>();
+  CU(cudaMemsetAsync(acc, 0, 3 * sizeof(unsigned long long), st));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
+  const long long cblocks = std::min<long long>((ncells + 255) / 256, 8LL * sms);
+  k_stats_cells<<<(unsigned)std::max<long long>(cblocks, 1), 256, 0, st>>>(dG, ncells, acc);
+  LAUNCHED("k_stats_cells", st);
+  b->launches = 1;
+  if (b->n > 0) {
+    const long long oblocks = std::min<long long>((b->n + 255) / 256, 8LL * sms);
+    k_stats_objects<<<(unsigned)oblocks, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, (unsigned)b->no, acc);
+    LAUNCHED("k_stats_objects", st);
+    ++b->launches;
+  }
+  CU(cudaMemcpyAsync(b->h_scalars, acc, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  out[0] = b->h_scalars[0];  // nonempty cells
+  out[1] = b->h_scalars[1];  // in-grid objects
+  out[2] = b->h_scalars[2];  // max cells per in-grid object
+  out[3] = b->no;            // NO of the counted mesh
+  return PG_OK;
+}
+
 }  // extern "C"

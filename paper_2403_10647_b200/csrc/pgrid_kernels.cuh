@@ -1297,4 +1297,49 @@ k_sort_segments_big(const unsigned* __restrict__ G, const unsigned* __restrict__
   }
 }
 
+
+// ----------------------------------------------------------------------------------------
+// Grid statistics (stats.py:42-64): the integer inputs of GridStats.
+//   stats[0] += #cells with G[c+1] != G[c]     stats[1] += #in-grid objects (count > 0)
+//   stats[2] = max cells per in-grid object
+// ----------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v, unsigned long long* sh) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  unsigned long long t = 0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+  return t;
+}
+
+__global__ void __launch_bounds__(256)
+k_stats_cells(const unsigned* __restrict__ G, long long ncells, unsigned long long* __restrict__ stats) {
+  __shared__ unsigned long long sh[8];
+  unsigned long long c = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < ncells; i += (long long)gridDim.x * blockDim.x)
+    c += __ldg(G + i + 1) != __ldg(G + i);
+  c = block_sum_u64(c, sh);
+  if (threadIdx.x == 0 && c) atomicAdd(stats, c);
+}
+
+__global__ void __launch_bounds__(256)
+k_stats_objects(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, unsigned no,
+                unsigned long long* __restrict__ stats) {
+  __shared__ unsigned long long sh[8];
+  unsigned long long kept = 0;
+  unsigned mx = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned cnt = tri_offset_or_end(rec, tile_pre, n, no, i + 1) - tri_offset_or_end(rec, tile_pre, n, no, i);
+    kept += cnt != 0;
+    mx = max(mx, cnt);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(stats + 2, (unsigned long long)mx);
+  kept = block_sum_u64(kept, sh);
+  if (threadIdx.x == 0 && kept) atomicAdd(stats + 1, kept);
+}
+
 }  // namespace pgrid

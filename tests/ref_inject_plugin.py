@@ -10,4 +10,5 @@ def pytest_configure(config):
 
     from paper_2403_10647_b200 import compat
     algos = os.environ.get("PGRID_INJECT_ALGOS", "parallel")
-    compat.install(pargrid, algos="all" if algos == "all" else tuple(algos.split(",")))
+    compat.install(pargrid, algos="all" if algos == "all" else tuple(algos.split(",")),
+                   consumers=algos == "all")
