@@ -98,6 +98,13 @@ int pg_dda_cast(pg_builder *b, const uint32_t *G, const uint32_t *O, int64_t no,
                 const double *origins, const double *dirs, const double *t_max, int64_t nrays,
                 int64_t *ids, double *ts, uint32_t flags, void *stream);
 
+/* Tight mesh bounds on the device (geometry.py:55-59 mesh_bounds, the
+ * reduction inside gridcore.spec_for_mesh, gridcore.py:185-198): per-axis min / max over all
+ * nv vertices (PG_HOST_INPUT: V is a host pointer). NaN -> PG_INVARIANT_ERROR (Aabb,
+ * geometry.py:20-25); nv == 0 -> PG_INVARIANT_ERROR. Padding and dims stay on the host. */
+int pg_mesh_bounds(pg_builder *b, const double *V, int64_t nv, uint32_t flags, void *stream,
+                   double *lo, double *hi);
+
 /* Grid statistics (stats.py:42-64) for the mesh of the last pg_count
  * (the grid's spec) and its grid G (u32[ncells+1]; PG_HOST_INPUT: host pointer):
  * out[0] = non-empty cells, out[1] = in-grid objects, out[2] = max cells per in-grid

@@ -33,7 +33,7 @@ NPHASES = 6
 # every symbol include/pgrid.h declares (checked by tests/test_boundary.py)
 EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
            "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_finish_baseline",
-           "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_build_async",
+           "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_build_async",
            "pg_build_wait", "pg_host_register",
            "pg_host_unregister", "pg_host_alloc", "pg_host_free", "pg_last_launch_count",
            "pg_last_error")
@@ -90,6 +90,8 @@ def load():
         lib.pg_dda_prepare.argtypes = [vp, vp, i64, vp, i64, u32, vp]
         lib.pg_dda_cast.argtypes = [vp, vp, vp, i64, ctypes.POINTER(PgSpec), vp, vp, vp, i64, vp, vp, u32, vp]
         lib.pg_grid_stats.argtypes = [vp, vp, u32, vp, ctypes.POINTER(u64)]
+        lib.pg_mesh_bounds.argtypes = [vp, vp, i64, u32, vp, ctypes.POINTER(ctypes.c_double),
+                                       ctypes.POINTER(ctypes.c_double)]
         lib.pg_build_async.argtypes = [vp, vp, i64, vp, i64, ctypes.POINTER(PgSpec), vp, vp, u64, vp]
         lib.pg_build_wait.argtypes = [vp, ctypes.POINTER(u64)]
         lib.pg_host_register.argtypes = [vp, u64]
@@ -100,7 +102,7 @@ def load():
         lib.pg_last_error.restype = ctypes.c_char_p
         for name in ("pg_builder_create", "pg_count", "pg_finish", "pg_stage",
                      "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells",
-                     "pg_finish_baseline", "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
+                     "pg_finish_baseline", "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
                      "pg_last_launch_count"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
@@ -180,6 +182,13 @@ class Builder:
         s = pgspec or PgSpec.from_spec(spec)
         check(self._lib.pg_dda_cast(self._h, ptr(G), ptr(O), int(no), ctypes.byref(s), ptr(origins), ptr(dirs),
                                     ptr(t_max), int(nrays), ptr(ids), ptr(ts), flags, stream))
+
+    def mesh_bounds(self, V, nv, flags=0, stream=None):
+        """Tight per-axis (lo, hi) of all nv vertices, reduced on the device."""
+        lo = (ctypes.c_double * 3)()
+        hi = (ctypes.c_double * 3)()
+        check(self._lib.pg_mesh_bounds(self._h, ptr(V), int(nv), flags, stream, lo, hi))
+        return np.array(lo[:], np.float64), np.array(hi[:], np.float64)
 
     def grid_stats(self, G, flags=0, stream=None):
         """(nonempty cells, in-grid objects, max cells per object, NO) of the last count."""

@@ -155,3 +155,42 @@ def build_compact(mesh, spec, workers=None, device=0):
     G, O, no, max_work, ms = _baseline(2, "compact", mesh, spec, device)
     report = BuildReport("compact", no=no, max_task_work=max_work if no else 0, total_work=2 * no, phase_ms=ms)
     return CompactGrid(spec, G, O), report
+
+
+def device_spec_for_mesh(V, nv, ntriangles, dims=None, density=5.0, device=0, stream=None):
+    """gridcore.spec_for_mesh (gridcore.py:185-198) with the bounds reduction on the device:
+    V may be a host array or a device tensor of nv x 3 doubles. The min / max are exact, so
+    padding and dims (host arithmetic on six doubles) give the reference's spec bit for bit."""
+    from .gridcore import spec_from_bounds
+    b = _native.thread_builder(device)
+    on_host = isinstance(V, np.ndarray)
+    lo, hi = b.mesh_bounds(V, nv, flags=_native.PG_HOST_INPUT if on_host else 0, stream=stream)
+    return spec_from_bounds(lo, hi, ntriangles, dims=dims, density=density)
+
+
+def build_from_mesh(mesh, dims=None, density=5.0, device=0):
+    """spec_for_mesh + build_parallel with one host->device copy of the mesh: bounds reduced on
+    the device (pg_mesh_bounds), spec padded on the host, then Alg. 1 on the resident arrays.
+    Returns (grid, report); grid.spec is the reference's spec_for_mesh(mesh, dims, density)."""
+    import torch
+    V, T = _mesh_arrays(mesh)
+    n = len(T)
+    dev = torch.device("cuda", device)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    Vd = torch.from_numpy(V).to(dev, non_blocking=False)
+    Td = torch.from_numpy(T).to(dev, non_blocking=False)
+    spec = device_spec_for_mesh(Vd, len(V), n, dims=dims, density=density, device=device, stream=st)
+    b = _native.thread_builder(device)
+    ms = {p: 0.0 for p in PHASES}
+    t0 = time.perf_counter()
+    no = b.count(Vd, len(V), Td, n, spec, flags=0, stream=st)
+    ms["count"] = (time.perf_counter() - t0) * 1e3
+    G = _native.pinned_pool.empty(spec.ncells + 1, np.uint32)
+    O = _native.pinned_pool.empty(no, np.uint32)
+    phases = b.finish(G, O, flags=_native.PG_HOST_OUTPUT, stream=st)
+    for name, v in zip(PHASES, phases):
+        if name != "count":
+            ms[name] = float(v)
+    report = BuildReport("parallel", no=no, max_task_work=PAIRGEN_OPS_PER_PAIR if no else 0,
+                         total_work=PAIRGEN_OPS_PER_PAIR * no, phase_ms=ms)
+    return CompactGrid(spec, G, O), report

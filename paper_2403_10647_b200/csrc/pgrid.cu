@@ -1126,4 +1126,45 @@ int pg_grid_stats(pg_builder* b, const uint32_t* G, uint32_t flags, void* stream
   return PG_OK;
 }
 
+int pg_mesh_bounds(pg_builder* b, const double* V, int64_t nv, uint32_t flags, void* stream_, double* lo,
+                   double* hi) {
+  if (!b || !lo || !hi) return fail(PG_INVARIANT_ERROR, "null argument");
+  if (nv <= 0) return fail(PG_INVARIANT_ERROR, "cannot bound an empty mesh");
+  if (!V) return fail(PG_INVARIANT_ERROR, "null vertex array");
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  int rc;
+  const double* dV = V;
+  if (flags & PG_HOST_INPUT) {
+    if ((rc = b->in_v.ensure((size_t)nv * 24))) return rc;
+    CU(cudaMemcpyAsync(b->in_v.p, V, (size_t)nv * 24, cudaMemcpyHostToDevice, st));
+    dV = b->in_v.as<double>();
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
+  const long long nflat = nv * 3;
+  const int nblocks = (int)std::max<long long>(1, std::min<long long>(8LL * sms, (nflat + MB_THREADS - 1) / MB_THREADS));
+  if ((rc = b->dda_err.ensure(align_up(16) + (size_t)nblocks * 48 + 48))) return rc;
+  unsigned* flag = b->dda_err.as<unsigned>();
+  double* part = b->dda_err.as<double>(align_up(16));
+  double* out = part + (size_t)nblocks * 6;
+  CU(cudaMemsetAsync(flag, 0, 4, st));
+  k_mesh_bounds<<<nblocks, MB_THREADS, 0, st>>>(dV, nflat, part, flag);
+  LAUNCHED("k_mesh_bounds", st);
+  k_mesh_bounds_final<<<1, 32, 0, st>>>(part, nblocks, out);
+  LAUNCHED("k_mesh_bounds_final", st);
+  b->launches = 2;
+  double h[6];
+  unsigned hf = 0;
+  CU(cudaMemcpyAsync(h, out, 48, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(&hf, flag, 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (hf & 1u) return fail(PG_INVARIANT_ERROR, "Aabb corners must not be NaN");
+  for (int k = 0; k < 3; ++k) {
+    lo[k] = h[k];
+    hi[k] = h[3 + k];
+  }
+  return PG_OK;
+}
+
 }  // extern "C"

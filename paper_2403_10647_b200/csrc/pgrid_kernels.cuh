@@ -14,6 +14,8 @@
 // All integer work is exact; the only floating point is the f64 sub/div/floor of K1, done
 // with explicit round-to-nearest intrinsics so it matches numpy bit for bit.
 #pragma once
+
+#include <math_constants.h>
 #include <cstdint>
 
 #ifndef PGRID_RANK_BALLOT
@@ -1340,6 +1342,54 @@ k_stats_objects(const uint4* __restrict__ rec, const unsigned* __restrict__ tile
   if ((threadIdx.x & 31) == 0 && mx) atomicMax(stats + 2, (unsigned long long)mx);
   kept = block_sum_u64(kept, sh);
   if (threadIdx.x == 0 && kept) atomicAdd(stats + 1, kept);
+}
+
+
+// ----------------------------------------------------------------------------------------
+// Mesh bounds (geometry.py:55-59 mesh_bounds over ALL vertices, referenced
+// or not): per-axis min / max of V (nv x 3 doubles). np.min / np.max propagate NaN, which
+// the reference then rejects (Aabb, geometry.py:20-25): a NaN sets flag bit 1 instead.
+// Threads stride the flat array by a multiple of 3, so each thread stays on one axis.
+// ----------------------------------------------------------------------------------------
+constexpr int MB_THREADS = 192;
+__global__ void __launch_bounds__(MB_THREADS)
+k_mesh_bounds(const double* __restrict__ V, long long nflat, double* __restrict__ part, unsigned* __restrict__ flag) {
+  __shared__ double smin[MB_THREADS], smax[MB_THREADS];
+  const long long stride = (long long)gridDim.x * MB_THREADS;
+  double mn = CUDART_INF, mx = -CUDART_INF;
+  bool nan = false;
+  for (long long i = (long long)blockIdx.x * MB_THREADS + threadIdx.x; i < nflat; i += stride) {
+    const double v = __ldg(V + i);
+    nan |= v != v;
+    mn = v < mn ? v : mn;
+    mx = v > mx ? v : mx;
+  }
+  if (__any_sync(0xffffffffu, nan) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+  smin[threadIdx.x] = mn;
+  smax[threadIdx.x] = mx;
+  __syncthreads();
+  if (threadIdx.x < 3) {  // thread k reduces axis (k + block offset) % 3 entries
+    const int axis = (int)(((long long)blockIdx.x * MB_THREADS + threadIdx.x) % 3);
+    double a = CUDART_INF, b = -CUDART_INF;
+    for (int t = threadIdx.x; t < MB_THREADS; t += 3) {
+      a = smin[t] < a ? smin[t] : a;
+      b = smax[t] > b ? smax[t] : b;
+    }
+    part[(size_t)blockIdx.x * 6 + axis] = a;
+    part[(size_t)blockIdx.x * 6 + 3 + axis] = b;
+  }
+}
+
+__global__ void __launch_bounds__(32)
+k_mesh_bounds_final(const double* __restrict__ part, int nblocks, double* __restrict__ out) {
+  if (threadIdx.x >= 6) return;
+  const bool is_min = threadIdx.x < 3;
+  double r = is_min ? CUDART_INF : -CUDART_INF;
+  for (int b = 0; b < nblocks; ++b) {
+    const double v = part[(size_t)b * 6 + threadIdx.x];
+    r = is_min ? (v < r ? v : r) : (v > r ? v : r);
+  }
+  out[threadIdx.x] = r;
 }
 
 }  // namespace pgrid
