@@ -177,8 +177,11 @@ def build_from_mesh(mesh, dims=None, density=5.0, device=0):
     n = len(T)
     dev = torch.device("cuda", device)
     st = torch.cuda.current_stream(dev).cuda_stream
-    Vd = torch.from_numpy(V).to(dev, non_blocking=False)
-    Td = torch.from_numpy(T).to(dev, non_blocking=False)
+    import warnings
+    with warnings.catch_warnings():   # read-only mesh arrays: the tensors are only read
+        warnings.simplefilter("ignore", UserWarning)
+        Vd = torch.from_numpy(V).to(dev)
+        Td = torch.from_numpy(T).to(dev)
     spec = device_spec_for_mesh(Vd, len(V), n, dims=dims, density=density, device=device, stream=st)
     b = _native.thread_builder(device)
     ms = {p: 0.0 for p in PHASES}
