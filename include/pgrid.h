@@ -154,6 +154,11 @@ int pg_partition(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int6
 int pg_sort_cells(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int64_t n,
                   int64_t ncells, uint32_t *G, uint32_t *O, void *stream);
 
+/* Profiling aid: with PGRID_KTIMES=1 in the environment, every launch of the calling thread's
+ * last pg_count + pg_finish is bracketed by events; this writes "kernel microseconds" lines
+ * (device time between consecutive launch completions) into buf. */
+int pg_kernel_times(char *buf, int len);
+
 /* Page-lock host memory so PG_HOST_* copies run at full PCIe rate (optional). */
 int pg_host_register(void *ptr, uint64_t bytes);
 int pg_host_unregister(void *ptr);

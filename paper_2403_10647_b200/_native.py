@@ -33,7 +33,7 @@ NPHASES = 6
 # every symbol include/pgrid.h declares (checked by tests/test_boundary.py)
 EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
            "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_finish_baseline",
-           "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_build_async",
+           "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_build_async",
            "pg_build_wait", "pg_host_register",
            "pg_host_unregister", "pg_host_alloc", "pg_host_free", "pg_last_launch_count",
            "pg_last_error")
@@ -89,6 +89,7 @@ def load():
                                            ctypes.POINTER(u64)]
         lib.pg_dda_prepare.argtypes = [vp, vp, i64, vp, i64, u32, vp]
         lib.pg_dda_cast.argtypes = [vp, vp, vp, i64, ctypes.POINTER(PgSpec), vp, vp, vp, i64, vp, vp, u32, vp]
+        lib.pg_kernel_times.argtypes = [ctypes.c_char_p, ctypes.c_int]
         lib.pg_grid_stats.argtypes = [vp, vp, u32, vp, ctypes.POINTER(u64)]
         lib.pg_mesh_bounds.argtypes = [vp, vp, i64, u32, vp, ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(ctypes.c_double)]
@@ -102,7 +103,7 @@ def load():
         lib.pg_last_error.restype = ctypes.c_char_p
         for name in ("pg_builder_create", "pg_count", "pg_finish", "pg_stage",
                      "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells",
-                     "pg_finish_baseline", "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
+                     "pg_finish_baseline", "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
                      "pg_last_launch_count"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
@@ -242,6 +243,17 @@ class Builder:
 
 
 _tls = threading.local()
+
+
+def kernel_times():
+    """[(kernel, microseconds)] of this thread's last pg_count + pg_finish (PGRID_KTIMES=1)."""
+    buf = ctypes.create_string_buffer(1 << 16)
+    check(load().pg_kernel_times(buf, len(buf)))
+    out = []
+    for line in buf.value.decode().splitlines():
+        name, us = line.rsplit(" ", 1)
+        out.append((name, float(us)))
+    return out
 
 
 def thread_builder(device=0):

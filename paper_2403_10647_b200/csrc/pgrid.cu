@@ -150,9 +150,39 @@ bool sync_debug() {
   return on;
 }
 
+// PGRID_KTIMES=1: an event after every launch, so pg_kernel_times can report per-kernel
+// device times of the last pg_count / pg_finish (profiling aid; off by default).
+bool ktimes_on() {
+  static const bool on = [] {
+    const char* e = getenv("PGRID_KTIMES");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
+struct KTimer {
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  size_t used = 0;
+  cudaEvent_t next(const char* name) {
+    if (used == ev.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back({name, e});
+    }
+    ev[used].first = name;
+    return ev[used++].second;
+  }
+};
+thread_local KTimer g_kt;
+void ktimer_reset(cudaStream_t st) {
+  if (!ktimes_on()) return;
+  g_kt.used = 0;
+  cudaEventRecord(g_kt.next("start"), st);
+}
+
 #define LAUNCHED(name, st)                                                                         \
   do {                                                                                             \
     CU(cudaGetLastError());                                                                        \
+    if (ktimes_on()) cudaEventRecord(g_kt.next(name), st);                                         \
     if (sync_debug()) {                                                                            \
       cudaError_t e2_ = cudaStreamSynchronize(st);                                                 \
       if (e2_ != cudaSuccess)                                                                      \
@@ -360,6 +390,7 @@ int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64
   DevSpec ds;
   int rc;
   if ((rc = count_setup(b, nv, n, spec, ds))) return rc;
+  ktimer_reset(st);
   if (n == 0) {
     b->no = 0;
     *no_out = 0;
@@ -554,6 +585,7 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
   if (!b || !b->counted) return fail(PG_STATE_ERROR, "pg_finish without a successful pg_count");
   CU(cudaSetDevice(b->device));
   drop_graph(b);
+  if (ktimes_on()) cudaEventRecord(g_kt.next("(host gap)"), static_cast<cudaStream_t>(stream_));
   return finish_impl(b, G, O, flags, static_cast<cudaStream_t>(stream_), phase_ms, Count{nullptr, (unsigned)b->no},
                      b->no);
 }
@@ -1164,6 +1196,23 @@ int pg_mesh_bounds(pg_builder* b, const double* V, int64_t nv, uint32_t flags, v
     lo[k] = h[k];
     hi[k] = h[3 + k];
   }
+  return PG_OK;
+}
+
+int pg_kernel_times(char* buf, int len) {
+  if (!buf || len <= 0) return fail(PG_INVARIANT_ERROR, "null buffer");
+  std::string out;
+  if (g_kt.used > 1) {
+    cudaEventSynchronize(g_kt.ev[g_kt.used - 1].second);
+    char line[128];
+    for (size_t i = 1; i < g_kt.used; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, g_kt.ev[i - 1].second, g_kt.ev[i].second);
+      snprintf(line, sizeof line, "%s %.3f\n", g_kt.ev[i].first, ms * 1e3f);
+      out += line;
+    }
+  }
+  snprintf(buf, (size_t)len, "%s", out.c_str());
   return PG_OK;
 }
 

@@ -643,6 +643,21 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// One bit-slice of warp peer detection: keep the lanes whose bit (x & bit) equals ours.
+// Written in PTX so ptxas emits LOP3.P (bit -> predicate), VOTE, SEL, LOP3 -- 4 instructions
+// per bit and item; the C form compiled to ~7 (the bit extracted twice, once per use).
+__device__ __forceinline__ unsigned peers_step(unsigned pm, unsigned x, unsigned bit) {
+  unsigned r;
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t, bb, m;\n\t"
+      "and.b32 t, %1, %2;\n\tsetp.ne.u32 p, t, 0;\n\t"
+      "vote.sync.ballot.b32 bb, p, 0xffffffff;\n\t"
+      "selp.b32 m, 0, 0xffffffff, p;\n\t"
+      "xor.b32 bb, bb, m;\n\tand.b32 %0, %3, bb;\n\t}"
+      : "=r"(r)
+      : "r"(x), "r"(bit), "r"(pm));
+  return r;
+}
+
 // Block-wide exclusive scan of one value per thread (NW warps); also returns the total.
 template <int NW>
 __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* wsum, unsigned& total) {
@@ -690,24 +705,34 @@ k_tile_counts(const unsigned* __restrict__ keys, Count cno, DigitFn dig, int nbi
   const unsigned t0 = blockIdx.x * TC_TILES;
   for (int b = tid; b < TC_TILES * kMaxBins; b += RS_THREADS) (&h[0][0])[b] = 0u;
   __syncthreads();
+  // full tiles: the next tile's keys are loaded before this tile's histogram atomics
+  constexpr int R = RS_TILE / 4 / RS_THREADS;
+  uint4 k[R];
+  auto full = [&](unsigned tile) { return tile < ntiles && (tile + 1) * (unsigned)RS_TILE <= no; };
+  auto load = [&](unsigned tile) {
+    const uint4* src = reinterpret_cast<const uint4*>(keys + tile * (unsigned)RS_TILE);
+#pragma unroll
+    for (int r = 0; r < R; ++r) k[r] = __ldcs(src + tid + r * RS_THREADS);
+  };
+  if (full(t0)) load(t0);
   for (int q = 0; q < TC_TILES; ++q) {
     const unsigned tile = t0 + q;
     if (tile >= ntiles) break;
-    const unsigned tbase = tile * (unsigned)RS_TILE;
-    const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
-    if (tvalid == (unsigned)RS_TILE) {
-      const uint4* src = reinterpret_cast<const uint4*>(keys + tbase);
-      uint4 k[RS_TILE / 4 / RS_THREADS];
+    if (full(tile)) {
+      uint4 cur[R];
 #pragma unroll
-      for (int r = 0; r < RS_TILE / 4 / RS_THREADS; ++r) k[r] = __ldcs(src + tid + r * RS_THREADS);
+      for (int r = 0; r < R; ++r) cur[r] = k[r];
+      if (q + 1 < TC_TILES && full(tile + 1)) load(tile + 1);
 #pragma unroll
-      for (int r = 0; r < RS_TILE / 4 / RS_THREADS; ++r) {
-        atomicAdd(&h[q][dig(k[r].x)], 1u);
-        atomicAdd(&h[q][dig(k[r].y)], 1u);
-        atomicAdd(&h[q][dig(k[r].z)], 1u);
-        atomicAdd(&h[q][dig(k[r].w)], 1u);
+      for (int r = 0; r < R; ++r) {
+        atomicAdd(&h[q][dig(cur[r].x)], 1u);
+        atomicAdd(&h[q][dig(cur[r].y)], 1u);
+        atomicAdd(&h[q][dig(cur[r].z)], 1u);
+        atomicAdd(&h[q][dig(cur[r].w)], 1u);
       }
     } else {
+      const unsigned tbase = tile * (unsigned)RS_TILE;
+      const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
       for (unsigned e = tid; e < tvalid; e += RS_THREADS) atomicAdd(&h[q][dig(__ldcs(keys + tbase + e))], 1u);
     }
   }
@@ -836,10 +861,7 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
 #pragma unroll
   for (int b = 0; b < BITS; ++b) {
 #pragma unroll
-    for (int j = 0; j < RS_ITEMS; ++j) {
-      const unsigned bb = __ballot_sync(0xffffffffu, (dg[j] >> b) & 1u);
-      pm[j] &= ((dg[j] >> b) & 1u) ? bb : ~bb;
-    }
+    for (int j = 0; j < RS_ITEMS; ++j) pm[j] = peers_step(pm[j], dg[j], 1u << b);
   }
   __syncwarp();
   const unsigned lt = lanemask_lt();
@@ -1042,7 +1064,7 @@ k_cell_offsets(const unsigned* __restrict__ sorted, Count cno, unsigned ncells, 
                unsigned* __restrict__ G) {
   const unsigned no = cno.get();
   __shared__ __align__(16) unsigned mark[G_TILE];
-  __shared__ unsigned sh_wmin[G_THREADS / 32];
+  __shared__ unsigned sh_wmin[G_ITEMS / 4 * (G_THREADS / 32)];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned c0 = blockIdx.x * (unsigned)G_TILE;
   const unsigned c1 = min(c0 + (unsigned)G_TILE, ncells);
@@ -1070,35 +1092,47 @@ k_cell_offsets(const unsigned* __restrict__ sorted, Count cno, unsigned ncells, 
     }
   }
   __syncthreads();
-  // block suffix-min, group by group from the right: in group g thread t owns the four cells
-  // g*1024 + 4t .. +3, so the mark loads are conflict-free and the G stores fully coalesced
-  unsigned carry = i1;  // min over all cells right of the current group
+  // block suffix-min over the tile. Cells are handled in G_ITEMS/4 groups: in group g thread t
+  // owns cells g*1024 + 4t .. +3 (conflict-free mark loads, coalesced G stores). All groups'
+  // warp suffix-mins are computed together and exchanged with ONE barrier.
+  constexpr int NG = G_ITEMS / 4;
+  uint4 a[NG];
+  unsigned suf[NG];
 #pragma unroll
-  for (int g = G_ITEMS / 4 - 1; g >= 0; --g) {
-    const uint4 a = reinterpret_cast<const uint4*>(mark)[g * G_THREADS + tid];
-    unsigned v0 = a.x, v1 = a.y, v2 = a.z, v3 = a.w;
-    unsigned suf = min(min(v0, v1), min(v2, v3));  // inclusive suffix-min over lanes >= lane
+  for (int g = 0; g < NG; ++g) {
+    a[g] = reinterpret_cast<const uint4*>(mark)[g * G_THREADS + tid];
+    suf[g] = min(min(a[g].x, a[g].y), min(a[g].z, a[g].w));
+  }
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const unsigned o = __shfl_down_sync(0xffffffffu, suf, d);
-      if (lane + d < 32) suf = min(suf, o);
+  for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const unsigned o = __shfl_down_sync(0xffffffffu, suf[g], d);
+      if (lane + d < 32) suf[g] = min(suf[g], o);  // inclusive suffix-min over lanes >= lane
     }
-    if (lane == 0) sh_wmin[warp] = suf;
-    __syncthreads();
-    unsigned right = __shfl_down_sync(0xffffffffu, suf, 1);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int g = 0; g < NG; ++g) sh_wmin[g * (G_THREADS / 32) + warp] = suf[g];
+  }
+  __syncthreads();
+  unsigned carry = i1;  // min over every cell right of the current group
+#pragma unroll
+  for (int g = NG - 1; g >= 0; --g) {
+    unsigned right = __shfl_down_sync(0xffffffffu, suf[g], 1);
     if (lane == 31) right = 0xffffffffu;
     unsigned gmin = 0xffffffffu;
 #pragma unroll
     for (int w = 0; w < G_THREADS / 32; ++w) {
-      const unsigned x = sh_wmin[w];
+      const unsigned x = sh_wmin[g * (G_THREADS / 32) + w];
       if (w > warp) right = min(right, x);
       gmin = min(gmin, x);
     }
     right = min(right, carry);
-    v3 = min(v3, right);
-    v2 = min(v2, v3);
-    v1 = min(v1, v2);
-    v0 = min(v0, v1);
+    unsigned v3 = min(a[g].w, right);
+    unsigned v2 = min(a[g].z, v3);
+    unsigned v1 = min(a[g].y, v2);
+    unsigned v0 = min(a[g].x, v1);
     const unsigned cb = c0 + (unsigned)(g * G_THREADS + tid) * 4;
     if (cb + 4 <= c1) {
       *reinterpret_cast<uint4*>(G + cb) = make_uint4(v0, v1, v2, v3);
@@ -1108,7 +1142,6 @@ k_cell_offsets(const unsigned* __restrict__ sorted, Count cno, unsigned ncells, 
       if (cb + 2 < c1) G[cb + 2] = v2;
     }
     carry = min(carry, gmin);
-    __syncthreads();  // sh_wmin is reused by the next group
   }
   if (blockIdx.x == gridDim.x - 1 && tid == 0) G[ncells] = no;
 }
