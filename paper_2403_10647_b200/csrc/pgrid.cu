@@ -529,16 +529,11 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
       k_pair_tile_bounds<<<(rs_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, cno, RS_TILE,
                                                             pbounds);
       LAUNCHED("k_pair_tile_bounds", st);
-      // K2 writes its first-pass tile counts tile-major into the B key buffer (free until
-      // pass 0 scatters into it), then they are transposed into the digit-major matrix
-      unsigned* tm = keysB;
+      // K2 writes its first-pass tile counts straight into the digit-major matrix
       k_pairs_emit<<<rs_tiles, RS_THREADS, sizeof(PeSmem), st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, cno, dxu,
-                                                                 dxyu, plan, pbounds, keysA, valsA, tm);
+                                                                 dxyu, plan, pbounds, keysA, valsA, counts, ld);
       LAUNCHED("k_pairs_emit", st);
-      k_transpose_counts<<<dim3((rs_tiles + 31) / 32, ((1u << plan.bits[0]) + 31) / 32), 256, 0, st>>>(
-          tm, cno, 1 << plan.bits[0], counts, ld);
-      LAUNCHED("k_transpose_counts", st);
-      b->launches += 3;
+      b->launches += 2;
       CU(cudaEventRecord(b->ev[1], st));
       if ((rc = run_passes(b, plan, true, keysA, valsA, keysB, valsB, dO, cno, no, hist, counts, st, &sorted)))
         return rc;

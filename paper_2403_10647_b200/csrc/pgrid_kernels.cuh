@@ -318,9 +318,19 @@ k_scan_tile_sums(const unsigned long long* __restrict__ tile_sum, unsigned ntile
   // warp w owns the contiguous segment [w*seg, (w+1)*seg), read in coalesced 32-wide chunks
   const unsigned seg = ((ntiles + TS_WARPS - 1) / TS_WARPS + 31) & ~31u;
   const unsigned s0 = min((unsigned)warp * seg, ntiles), s1 = min(s0 + seg, ntiles);
+  // loads are batched 8 chunks deep so each pass costs a few memory latencies, not one per chunk
+  constexpr int B = 8;
   unsigned long long part = 0;
-#pragma unroll 4
-  for (unsigned i = s0 + lane; i < s1; i += 32) part += tile_sum[i];
+  for (unsigned c = s0; c < s1; c += 32 * B) {
+    unsigned long long v[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const unsigned i = c + 32 * j + lane;
+      v[j] = i < s1 ? tile_sum[i] : 0ull;
+    }
+#pragma unroll
+    for (int j = 0; j < B; ++j) part += v[j];
+  }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
   if (lane == 0) wsum[warp] = part;
@@ -330,17 +340,25 @@ k_scan_tile_sums(const unsigned long long* __restrict__ tile_sum, unsigned ntile
     carry += w < warp ? wsum[w] : 0ull;
     tot += wsum[w];
   }
-  for (unsigned c = s0; c < s1; c += 32) {
-    const unsigned i = c + lane;
-    const unsigned long long v = i < s1 ? tile_sum[i] : 0ull;
-    unsigned long long inc = v;
+  for (unsigned c = s0; c < s1; c += 32 * B) {
+    unsigned long long v[B];
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const unsigned long long o = __shfl_up_sync(0xffffffffu, inc, d);
-      if (lane >= d) inc += o;
+    for (int j = 0; j < B; ++j) {
+      const unsigned i = c + 32 * j + lane;
+      v[j] = i < s1 ? tile_sum[i] : 0ull;
     }
-    if (i < s1) tile_pre[i] = (unsigned)(carry + inc - v);
-    carry += __shfl_sync(0xffffffffu, inc, 31);
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const unsigned i = c + 32 * j + lane;
+      unsigned long long inc = v[j];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+      }
+      if (i < s1) tile_pre[i] = (unsigned)(carry + inc - v[j]);
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
   }
   if (tid == 0) *total = tot;
 }
@@ -507,6 +525,45 @@ __global__ void k_abs_offsets(const uint4* __restrict__ rec, const unsigned* __r
 // ((#triangles with offset <= p0) - 1), y = one past the last triangle whose run starts
 // inside the tile (#triangles with offset < pend). Hoisting these searches out of the
 // expansion kernels keeps their CTAs from idling on dependent round trips at launch.
+// Two warp-cooperative 32-ary lower_bounds run in lockstep (their loads overlap): smallest
+// i in [lo, hi] with load(i) >= x, for (lo0, hi0, x0) and (lo1, hi1, x1).
+template <typename Load>
+__device__ __forceinline__ void warp_lower_bound2(unsigned long long& lo0, unsigned long long hi0,
+                                                  unsigned long long x0, unsigned long long& lo1,
+                                                  unsigned long long hi1, unsigned long long x1, Load load) {
+  const int lane = threadIdx.x & 31;
+  while (lo0 < hi0 || lo1 < hi1) {
+    const unsigned long long st0 = (hi0 - lo0 + 31) / 32, st1 = (hi1 - lo1 + 31) / 32;
+    const unsigned long long p0 = lo0 + (unsigned long long)lane * st0, p1 = lo1 + (unsigned long long)lane * st1;
+    const bool a0 = lo0 < hi0 && p0 < hi0, a1 = lo1 < hi1 && p1 < hi1;
+    const unsigned long long v0 = a0 ? load(p0) : 0ull, v1 = a1 ? load(p1) : 0ull;
+    const unsigned b0 = __ballot_sync(0xffffffffu, a0 ? v0 >= x0 : true);
+    const unsigned b1 = __ballot_sync(0xffffffffu, a1 ? v1 >= x1 : true);
+    if (lo0 < hi0) {
+      const int f = b0 ? __ffs(b0) - 1 : 32;
+      if (f == 0) {
+        hi0 = lo0;
+      } else {
+        lo0 = lo0 + (unsigned long long)(f - 1) * st0 + 1;
+        if (f < 32) hi0 = min(hi0, (lo0 - 1) + st0);
+      }
+    }
+    if (lo1 < hi1) {
+      const int f = b1 ? __ffs(b1) - 1 : 32;
+      if (f == 0) {
+        hi1 = lo1;
+      } else {
+        lo1 = lo1 + (unsigned long long)(f - 1) * st1 + 1;
+        if (f < 32) hi1 = min(hi1, (lo1 - 1) + st1);
+      }
+    }
+  }
+}
+
+// K2 tile bounds: for pair tile t, a = the object whose pairs contain p0 (last object with
+// offset <= p0) and b = the first object starting at or after the tile end. Two levels:
+// the K1 tile prefixes (tile_pre, L2-resident) locate the 512-object K1 tile, then the
+// objects' offsets inside it; both queries of a tile run in lockstep.
 __global__ void __launch_bounds__(256)
 k_pair_tile_bounds(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno,
                    unsigned tile, int2* __restrict__ bounds) {
@@ -516,9 +573,17 @@ k_pair_tile_bounds(const uint4* __restrict__ rec, const unsigned* __restrict__ t
   if (t >= ntiles) return;
   const unsigned p0 = t * tile;
   const unsigned pend = min(p0 + tile, no);
-  auto ld = [&](unsigned long long i) { return (unsigned long long)tri_offset(rec, tile_pre, i); };
-  const unsigned long long a = warp_lower_bound((unsigned long long)n, (unsigned long long)p0 + 1, ld);
-  const unsigned long long b = warp_lower_bound((unsigned long long)n, (unsigned long long)pend, ld);
+  const unsigned long long nk1 = (unsigned long long)((n + K1_TILE - 1) / K1_TILE);
+  // level 1: J = first K1 tile whose first object's offset >= x; the answer is in
+  // ((J-1)*K1_TILE, J*K1_TILE] (clipped to [0, n])
+  unsigned long long j0 = 0, j1 = 0;
+  warp_lower_bound2(j0, nk1, (unsigned long long)p0 + 1, j1, nk1, (unsigned long long)pend,
+                    [&](unsigned long long j) { return (unsigned long long)__ldg(&tile_pre[j]); });
+  auto range_lo = [&](unsigned long long J) { return J ? (J - 1) * K1_TILE + 1 : 0ull; };
+  auto range_hi = [&](unsigned long long J) { return min(J * (unsigned long long)K1_TILE, (unsigned long long)n); };
+  unsigned long long a = range_lo(j0), b = range_lo(j1);
+  warp_lower_bound2(a, range_hi(j0), (unsigned long long)p0 + 1, b, range_hi(j1), (unsigned long long)pend,
+                    [&](unsigned long long i) { return (unsigned long long)tri_offset(rec, tile_pre, i); });
   if ((threadIdx.x & 31) == 0) bounds[t] = make_int2((int)a - 1, (int)b);
 }
 
@@ -762,12 +827,13 @@ k_transpose_counts(const unsigned* __restrict__ tm, Count cno, int nbins, unsign
   }
 }
 
-constexpr int SC_THREADS = 1024;
-constexpr int SC_ITEMS = 8;
+constexpr int SC_THREADS = 256;
+constexpr int SC_VEC = 5;                  // 16-byte vectors per thread per chunk
+constexpr int SC_ITEMS = 4 * SC_VEC;       // 20 tiles per thread, 5120 per chunk (21M pairs)
 // One CTA per digit row: counts[row][0..ntiles) -> exclusive prefix over tiles, in place.
-// Rows are padded to a multiple of 4 (ld) so each thread moves its 8 entries as two 16-byte
-// accesses; one iteration covers 8192 tiles (33.5M pairs). The row total is the digit's
-// global count (its histogram bin).
+// Rows are padded to a multiple of 4 (ld) so each thread moves its entries as 16-byte
+// accesses, all issued before the scan (one memory latency per chunk); 512 rows x 256
+// threads fit one wave. The row total is the digit's global count (its histogram bin).
 __global__ void __launch_bounds__(SC_THREADS)
 k_scan_tile_counts(unsigned* __restrict__ counts, Count cno, unsigned ld, unsigned* __restrict__ row_total) {
   __shared__ unsigned wsum[SC_THREADS / 32];
@@ -777,34 +843,29 @@ k_scan_tile_counts(unsigned* __restrict__ counts, Count cno, unsigned ld, unsign
   unsigned carry = 0;
   for (unsigned base = 0; base < ntiles; base += SC_THREADS * SC_ITEMS) {
     const unsigned i0 = base + tid * SC_ITEMS;
-    unsigned v[SC_ITEMS];
-    if (i0 + SC_ITEMS <= ld) {
-      const uint4 a = *reinterpret_cast<const uint4*>(row + i0);
-      const uint4 b = *reinterpret_cast<const uint4*>(row + i0 + 4);
-      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-    } else {
+    uint4 v[SC_VEC];
 #pragma unroll
-      for (int q = 0; q < SC_ITEMS; ++q) v[q] = i0 + q < ld ? row[i0 + q] : 0u;
+    for (int q = 0; q < SC_VEC; ++q) {
+      const unsigned i = i0 + 4 * q;
+      v[q] = i < ntiles ? *reinterpret_cast<const uint4*>(row + i) : make_uint4(0u, 0u, 0u, 0u);
     }
-#pragma unroll
-    for (int q = 0; q < SC_ITEMS; ++q)
-      if (i0 + q >= ntiles) v[q] = 0u;  // padding columns hold garbage
     unsigned run = 0;
 #pragma unroll
-    for (int q = 0; q < SC_ITEMS; ++q) {
-      const unsigned c = v[q];
-      v[q] = run;
-      run += c;
+    for (int q = 0; q < SC_VEC; ++q) {
+      const unsigned i = i0 + 4 * q;
+      // padding columns (>= ntiles) hold garbage
+      const unsigned a = i < ntiles ? v[q].x : 0u, b = i + 1 < ntiles ? v[q].y : 0u;
+      const unsigned c = i + 2 < ntiles ? v[q].z : 0u, d = i + 3 < ntiles ? v[q].w : 0u;
+      v[q] = make_uint4(run, run + a, run + a + b, run + a + b + c);
+      run += a + b + c + d;
     }
     unsigned total;
     const unsigned pre = carry + block_excl_scan<SC_THREADS / 32>(run, wsum, total);
-    if (i0 + SC_ITEMS <= ld) {
-      *reinterpret_cast<uint4*>(row + i0) = make_uint4(pre + v[0], pre + v[1], pre + v[2], pre + v[3]);
-      *reinterpret_cast<uint4*>(row + i0 + 4) = make_uint4(pre + v[4], pre + v[5], pre + v[6], pre + v[7]);
-    } else {
 #pragma unroll
-      for (int q = 0; q < SC_ITEMS; ++q)
-        if (i0 + q < ntiles) row[i0 + q] = pre + v[q];
+    for (int q = 0; q < SC_VEC; ++q) {
+      const unsigned i = i0 + 4 * q;
+      if (i < ntiles)  // the vector never crosses ld (a multiple of 4)
+        *reinterpret_cast<uint4*>(row + i) = make_uint4(pre + v[q].x, pre + v[q].y, pre + v[q].z, pre + v[q].w);
     }
     carry += total;
   }
@@ -988,7 +1049,7 @@ static_assert(sizeof(ObjCache) >= RS_TILE * 4, "the object cache doubles as the 
 __global__ void __launch_bounds__(RS_THREADS)
 k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno,
              unsigned dx, unsigned dxy, PassPlan plan, const int2* __restrict__ bounds, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
-             unsigned* __restrict__ counts0) {
+             unsigned* __restrict__ counts0, unsigned ld) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   PeSmem& sm = *reinterpret_cast<PeSmem*>(smem_raw);
   const int tid = threadIdx.x;
@@ -1044,8 +1105,9 @@ k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pr
       if (j < nvalid) atomicAdd(&sm.h[(key[j] >> sh) & mask], 1u);
   }
   __syncthreads();
-  // tile-major row (coalesced); k_transpose_counts makes it digit-major
-  for (int b = tid; b < (1 << plan.bits[0]); b += RS_THREADS) counts0[(size_t)blockIdx.x * kMaxBins + b] = sm.h[b];
+  // straight into the digit-major matrix: one 4-byte entry per digit row (the rows stay in
+  // L2 until the row scan reads them, so the scattered writes cost no extra DRAM traffic)
+  for (int b = tid; b < (1 << plan.bits[0]); b += RS_THREADS) counts0[(size_t)b * ld + blockIdx.x] = sm.h[b];
 }
 
 // ----------------------------------------------------------------------------------------

@@ -192,9 +192,9 @@ def test_launch_count_is_native():
     b = _native.thread_builder()
     nbits = int(spec.ncells - 1).bit_length()
     passes = (nbits + 8) // 9                         # 9-bit digits
-    # K1 + tile scan, tile bounds + K2 + count transpose, K4 + its bounds, and
-    # count/scan/scatter per pass (pass 0 counted by K2)
-    assert b.launches() == 6 + 3 * passes
+    # K1 + tile scan, tile bounds + K2, K4 + its bounds, and count/scan/scatter per pass
+    # (pass 0 counted by K2)
+    assert b.launches() == 5 + 3 * passes
 
 
 def test_index_out_of_range_detected_on_device():
