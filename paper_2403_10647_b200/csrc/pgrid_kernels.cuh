@@ -684,14 +684,32 @@ k_digit_hist(const unsigned* __restrict__ keys, long long n, PassPlan plan, unsi
 // ----------------------------------------------------------------------------------------
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
+#ifndef RS_ITEMS_OVERRIDE
 constexpr int RS_ITEMS = 16;
+#else
+constexpr int RS_ITEMS = RS_ITEMS_OVERRIDE;
+#endif
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 pairs per tile
 constexpr int RS_DPT = kMaxBins / RS_THREADS;  // digits per thread in the per-digit phases
-constexpr int RS_MIN_CTAS = 4;  // 64 registers, 45 KB smem: 4 CTAs (32 warps) per SM
+#ifndef RS_MIN_CTAS_OVERRIDE
+constexpr int RS_MIN_CTAS = 4;
+#else
+constexpr int RS_MIN_CTAS = RS_MIN_CTAS_OVERRIDE;
+#endif  // 64 registers, 45 KB smem: 4 CTAs (32 warps) per SM
 
+#ifndef PGRID_SCATTER_KV
+#define PGRID_SCATTER_KV 0  // 1: packed (value << 32 | key) scatter -- measured slower (register spills)
+#endif
 struct RsSmem {
-  unsigned buf[RS_TILE];                     // tile in digit order: keys, then values
-  unsigned vstage[RS_TILE];                  // values in input order (cp.async staging)
+  union {
+    // PGRID_SCATTER_KV: the tile in digit order as packed (value << 32 | key) words; the
+    // values' cp.async staging area aliases it (read into registers before the scatter)
+    unsigned long long kv[RS_TILE];
+    struct {
+      unsigned buf[RS_TILE];     // tile in digit order: keys, then values
+      unsigned vstage[RS_TILE];  // values in input order (cp.async staging)
+    };
+  };
   unsigned short whist[RS_WARPS][kMaxBins];  // per-warp digit counts -> tile offset of (warp, digit)
   unsigned gbase[kMaxBins];                  // global position of buf[0] for each digit
   unsigned wsum[RS_WARPS];
@@ -759,7 +777,11 @@ struct DigitFn {
 
 // Upsweep of a radix pass: per-tile digit counts, TC_TILES tiles per CTA so every digit row
 // of the digit-major matrix receives TC_TILES consecutive entries (a full 32-byte sector).
+#ifndef TC_TILES_OVERRIDE
 constexpr int TC_TILES = 8;
+#else
+constexpr int TC_TILES = TC_TILES_OVERRIDE;
+#endif
 __global__ void __launch_bounds__(RS_THREADS)
 k_tile_counts(const unsigned* __restrict__ keys, Count cno, DigitFn dig, int nbins, unsigned* __restrict__ counts,
               unsigned ld) {
@@ -975,6 +997,41 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
     lpre += tc[q];
     hpre += hs[q];
   }
+#if PGRID_SCATTER_KV
+  if (!SRC_SMEM) cp_async_wait();
+  __syncthreads();
+  // ranks -> tile positions (the digits die here), values into registers (input order,
+  // conflict-free), then the staging area is free
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j)
+    if (valid(j)) rank[j] += sm.whist[warp][dg[j]];
+  unsigned vreg[RS_ITEMS];
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) vreg[j] = valid(j) ? sm.vstage[elem(j)] : 0u;
+  __syncthreads();
+  // (key, value) pairs: one stable 8-byte local scatter into digit order (key re-read from
+  // L1/L2), then a run-coalesced write-out of both arrays from the same positions
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    if (valid(j)) {
+      sm.kv[rank[j]] = ((unsigned long long)vreg[j] << 32) | (SRC_SMEM ? ksrc[elem(j)] : __ldg(ksrc + elem(j)));
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < RS_ITEMS; ++r) {
+    const unsigned i = tid + r * RS_THREADS;
+    if (FULL || i < tvalid) {
+      const unsigned long long x = sm.kv[i];
+      const unsigned k = (unsigned)x;
+      const unsigned d = digit(k);
+      const unsigned g = sm.gbase[d] + i;
+      if (keys_out) keys_out[g] = TABLE ? k - __ldg(&kbase[d]) : k;
+      vals_out[g] = (unsigned)(x >> 32);
+    }
+  }
+}
+#else
   __syncthreads();
   // keys: stable local scatter into digit order (key re-read from L1/L2), run-coalesced write
 #pragma unroll
@@ -1010,6 +1067,8 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
     if (FULL || i < tvalid) vals_out[gpos[r]] = sm.buf[i];
   }
 }
+
+#endif
 
 template <int BITS, bool TABLE>
 __global__ void __launch_bounds__(RS_THREADS, RS_MIN_CTAS)
