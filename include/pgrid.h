@@ -33,6 +33,7 @@ extern "C" {
 #define PG_INVARIANT_ERROR 2   /* precondition violated (primitives.py:22-25, gridcore.py:44-52) */
 #define PG_CUDA_ERROR 3        /* CUDA runtime failure */
 #define PG_STATE_ERROR 4       /* call sequence violated (finish before count, ...) */
+#define PG_PARSE_ERROR 6        /* pg_load_obj: malformed OBJ (-> ObjParseError) */
 #define PG_CAPACITY_ERROR 5    /* pg_build_wait: NO exceeded the O capacity given to pg_build_async */
 
 /* Flags. */
@@ -104,6 +105,17 @@ int pg_dda_cast(pg_builder *b, const uint32_t *G, const uint32_t *O, int64_t no,
  * geometry.py:20-25); nv == 0 -> PG_INVARIANT_ERROR. Padding and dims stay on the host. */
 int pg_mesh_bounds(pg_builder *b, const double *V, int64_t nv, uint32_t flags, void *stream,
                    double *lo, double *hi);
+
+/* OBJ ingestion on the device (geometry.py:65-112 load_obj): parse the
+ * v/f subset of an OBJ byte buffer (PG_HOST_INPUT: host pointer; < 4 GiB) into vertices
+ * (f64 nv x 3) and fan-triangulated faces (i32 nt x 3) kept in the builder. out[0..5] =
+ * {nv, nt, first bad line (1-based, 0 if none), vertices before that line, that line's
+ * byte range [out[4], out[5])}; a malformed file returns PG_PARSE_ERROR with out[2..5]
+ * set so the caller can report the reference's exact message. pg_obj_fetch copies the
+ * result out (PG_HOST_OUTPUT: host pointers; else device pointers). */
+int pg_load_obj(pg_builder *b, const uint8_t *bytes, uint64_t nbytes, uint32_t flags, void *stream,
+                int64_t *out);
+int pg_obj_fetch(pg_builder *b, double *V, int32_t *T, uint32_t flags, void *stream);
 
 /* Grid statistics (stats.py:42-64) for the mesh of the last pg_count
  * (the grid's spec) and its grid G (u32[ncells+1]; PG_HOST_INPUT: host pointer):

@@ -21,6 +21,7 @@ PG_INVARIANT_ERROR = 2
 PG_CUDA_ERROR = 3
 PG_STATE_ERROR = 4
 PG_CAPACITY_ERROR = 5
+PG_PARSE_ERROR = 6
 
 PG_HOST_INPUT = 1
 PG_HOST_OUTPUT = 2
@@ -33,7 +34,7 @@ NPHASES = 6
 # every symbol include/pgrid.h declares (checked by tests/test_boundary.py)
 EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
            "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_finish_baseline",
-           "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_build_async",
+           "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_build_async",
            "pg_build_wait", "pg_host_register",
            "pg_host_unregister", "pg_host_alloc", "pg_host_free", "pg_last_launch_count",
            "pg_last_error")
@@ -90,6 +91,8 @@ def load():
         lib.pg_dda_prepare.argtypes = [vp, vp, i64, vp, i64, u32, vp]
         lib.pg_dda_cast.argtypes = [vp, vp, vp, i64, ctypes.POINTER(PgSpec), vp, vp, vp, i64, vp, vp, u32, vp]
         lib.pg_kernel_times.argtypes = [ctypes.c_char_p, ctypes.c_int]
+        lib.pg_load_obj.argtypes = [vp, vp, u64, u32, vp, ctypes.POINTER(i64)]
+        lib.pg_obj_fetch.argtypes = [vp, vp, vp, u32, vp]
         lib.pg_grid_stats.argtypes = [vp, vp, u32, vp, ctypes.POINTER(u64)]
         lib.pg_mesh_bounds.argtypes = [vp, vp, i64, u32, vp, ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(ctypes.c_double)]
@@ -103,7 +106,7 @@ def load():
         lib.pg_last_error.restype = ctypes.c_char_p
         for name in ("pg_builder_create", "pg_count", "pg_finish", "pg_stage",
                      "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells",
-                     "pg_finish_baseline", "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
+                     "pg_finish_baseline", "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
                      "pg_last_launch_count"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
@@ -190,6 +193,18 @@ class Builder:
         hi = (ctypes.c_double * 3)()
         check(self._lib.pg_mesh_bounds(self._h, ptr(V), int(nv), flags, stream, lo, hi))
         return np.array(lo[:], np.float64), np.array(hi[:], np.float64)
+
+    def load_obj(self, data, nbytes, flags=PG_HOST_INPUT, stream=None):
+        """Parse an OBJ byte buffer on the device. Returns (rc, out[6]); rc is PG_OK or
+        PG_PARSE_ERROR (out[2..5] locate the first bad line); other codes raise."""
+        out = (ctypes.c_int64 * 6)()
+        rc = self._lib.pg_load_obj(self._h, ptr(data), int(nbytes), flags, stream, out)
+        if rc not in (PG_OK, PG_PARSE_ERROR):
+            check(rc)
+        return rc, [int(x) for x in out]
+
+    def obj_fetch(self, V, T, flags=PG_HOST_OUTPUT, stream=None):
+        check(self._lib.pg_obj_fetch(self._h, ptr(V), ptr(T), flags, stream))
 
     def grid_stats(self, G, flags=0, stream=None):
         """(nonempty cells, in-grid objects, max cells per object, NO) of the last count."""

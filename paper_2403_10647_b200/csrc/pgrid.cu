@@ -16,6 +16,7 @@
 #include "../../include/pgrid.h"
 #include "pgrid_kernels.cuh"
 #include "pgrid_dda.cuh"
+#include "pgrid_obj.cuh"
 
 using namespace pgrid;
 
@@ -226,6 +227,9 @@ struct pg_builder {
   // ray casting (pg_dda_prepare / pg_dda_cast): prepared triangles + staging
   DevBuf tris, dda_err, dda_grid, dda_rays, dda_out;
   int64_t dda_ntri = -1;
+  // OBJ ingestion (pg_load_obj / pg_obj_fetch)
+  DevBuf obj_bytes, obj_lines, obj_info, obj_pre, obj_scan, obj_v, obj_t;
+  int64_t obj_nv = -1, obj_nt = 0;
 };
 
 extern "C" {
@@ -1208,6 +1212,126 @@ int pg_kernel_times(char* buf, int len) {
     }
   }
   snprintf(buf, (size_t)len, "%s", out.c_str());
+  return PG_OK;
+}
+
+int pg_load_obj(pg_builder* b, const uint8_t* bytes, uint64_t nbytes, uint32_t flags, void* stream_, int64_t* out) {
+  if (!b || !out) return fail(PG_INVARIANT_ERROR, "null argument");
+  if (nbytes && !bytes) return fail(PG_INVARIANT_ERROR, "null byte buffer");
+  if (nbytes >= (1ull << 32)) return fail(PG_SIZE_ERROR, "OBJ input of %llu bytes exceeds 4 GiB", (unsigned long long)nbytes);
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  int rc;
+  b->obj_nv = -1;
+  for (int k = 0; k < 6; ++k) out[k] = 0;
+  b->launches = 0;
+  if (nbytes == 0) {
+    b->obj_nv = 0;
+    b->obj_nt = 0;
+    return PG_OK;
+  }
+  const unsigned char* d = bytes;
+  if (flags & PG_HOST_INPUT) {
+    if ((rc = b->obj_bytes.ensure(nbytes))) return rc;
+    CU(cudaMemcpyAsync(b->obj_bytes.p, bytes, nbytes, cudaMemcpyHostToDevice, st));
+    d = b->obj_bytes.as<unsigned char>();
+  }
+  // 1. line breaks: per-chunk counts -> exclusive prefix (+ total) -> break positions
+  const unsigned nchunks = (unsigned)((nbytes + OBJ_CHUNK - 1) / OBJ_CHUNK);
+  const unsigned xt = (unsigned)((nchunks + XS_TILE - 1) / XS_TILE);
+  const size_t cb = align_up((size_t)nchunks * 4), pb = align_up((size_t)(nchunks + 1) * 4);
+  const size_t sb = align_up((size_t)xt * 8), tb = align_up((size_t)xt * 4);
+  if ((rc = b->obj_scan.ensure(cb + pb + sb + tb + 256))) return rc;
+  unsigned* ccount = b->obj_scan.as<unsigned>(0);
+  unsigned* cpre = b->obj_scan.as<unsigned>(cb);
+  unsigned long long* tsum = b->obj_scan.as<unsigned long long>(cb + pb);
+  unsigned* tpre = b->obj_scan.as<unsigned>(cb + pb + sb);
+  unsigned long long* scal = b->obj_scan.as<unsigned long long>(cb + pb + sb + tb);  // [0] total, [1] err
+  k_obj_count_breaks<<<nchunks, 256, 0, st>>>(d, nbytes, ccount);
+  LAUNCHED("k_obj_count_breaks", st);
+  k_tile_reduce<<<xt, XS_THREADS, 0, st>>>(ccount, nchunks, tsum);
+  LAUNCHED("k_tile_reduce", st);
+  k_scan_tile_sums<<<1, TS_THREADS, 0, st>>>(tsum, xt, tpre, scal);
+  LAUNCHED("k_scan_tile_sums", st);
+  k_tile_scan_apply<<<xt, XS_THREADS, 0, st>>>(ccount, nchunks, tpre, scal, cpre);
+  LAUNCHED("k_tile_scan_apply", st);
+  unsigned long long nbreaks = 0;
+  unsigned char last = 0;
+  CU(cudaMemcpyAsync(&nbreaks, scal, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(&last, d + nbytes - 1, 1, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  const unsigned long long L = nbreaks + ((last == '\n' || last == '\r') ? 0 : 1);
+  if ((rc = b->obj_lines.ensure(std::max<size_t>((size_t)L * 4, 16)))) return rc;
+  unsigned* line_end = b->obj_lines.as<unsigned>();
+  k_obj_line_ends<<<nchunks, 256, 0, st>>>(d, nbytes, cpre, line_end);
+  LAUNCHED("k_obj_line_ends", st);
+  if (L > nbreaks) {
+    const unsigned endpos = (unsigned)nbytes;
+    CU(cudaMemcpyAsync(line_end + (L - 1), &endpos, 4, cudaMemcpyHostToDevice, st));
+  }
+  // 2. classify lines, 3. scan (vertices << 32 | triangles), 4. parse
+  const unsigned ot = (unsigned)((L + OS_TILE - 1) / OS_TILE);
+  if ((rc = b->obj_info.ensure(align_up((size_t)L * 8) + align_up((size_t)(ot + 1) * 8)))) return rc;
+  if ((rc = b->obj_pre.ensure((size_t)(L + 1) * 8))) return rc;
+  unsigned long long* info = b->obj_info.as<unsigned long long>();
+  unsigned long long* osum = b->obj_info.as<unsigned long long>(align_up((size_t)L * 8));
+  unsigned long long* pre = b->obj_pre.as<unsigned long long>();
+  unsigned long long* err = scal + 1;
+  const unsigned long long none = ~0ull;
+  CU(cudaMemcpyAsync(err, &none, 8, cudaMemcpyHostToDevice, st));
+  const unsigned lb = (unsigned)((L + 127) / 128);
+  k_obj_classify<<<lb, 128, 0, st>>>(d, nbytes, line_end, L, info, err);
+  LAUNCHED("k_obj_classify", st);
+  k_u64_tile_sums<<<ot, 256, 0, st>>>(info, L, osum);
+  LAUNCHED("k_u64_tile_sums", st);
+  k_u64_scan_sums<<<1, 1024, 0, st>>>(osum, ot);
+  LAUNCHED("k_u64_scan_sums", st);
+  k_u64_tile_apply<<<ot, 256, 0, st>>>(info, L, osum, pre);
+  LAUNCHED("k_u64_tile_apply", st);
+  unsigned long long tot = 0;
+  CU(cudaMemcpyAsync(&tot, osum + ot, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(pre + L, osum + ot, 8, cudaMemcpyDeviceToDevice, st));
+  CU(cudaStreamSynchronize(st));
+  const unsigned long long nv = tot >> 32, nt = tot & 0xffffffffull;
+  if (nv >= (1ull << 31)) return fail(PG_SIZE_ERROR, "%llu vertices exceed the int32 index range", nv);
+  if ((rc = b->obj_v.ensure(std::max<size_t>((size_t)nv * 24, 16)))) return rc;
+  if ((rc = b->obj_t.ensure(std::max<size_t>((size_t)nt * 12, 16)))) return rc;
+  k_obj_parse<<<lb, 128, 0, st>>>(d, nbytes, line_end, L, info, pre, b->obj_v.as<double>(), b->obj_t.as<int>(), err);
+  LAUNCHED("k_obj_parse", st);
+  b->launches = 10;
+  unsigned long long herr = 0;
+  CU(cudaMemcpyAsync(&herr, err, 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  out[0] = (int64_t)nv;
+  out[1] = (int64_t)nt;
+  if (herr != ~0ull) {
+    // first offending line: its number, the vertices read before it, its byte range
+    const unsigned long long li = herr - 1;
+    unsigned long long pv = 0;
+    unsigned e0 = 0, e1 = 0;
+    CU(cudaMemcpy(&pv, pre + li, 8, cudaMemcpyDeviceToHost));
+    if (li > 0) CU(cudaMemcpy(&e0, line_end + li - 1, 4, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(&e1, line_end + li, 4, cudaMemcpyDeviceToHost));
+    out[2] = (int64_t)herr;
+    out[3] = (int64_t)(pv >> 32);
+    out[4] = li > 0 ? (int64_t)e0 + 1 : 0;
+    out[5] = (int64_t)e1;
+    return fail(PG_PARSE_ERROR, "OBJ parse error at line %llu", herr);
+  }
+  b->obj_nv = (int64_t)nv;
+  b->obj_nt = (int64_t)nt;
+  return PG_OK;
+}
+
+int pg_obj_fetch(pg_builder* b, double* V, int32_t* T, uint32_t flags, void* stream_) {
+  if (!b) return fail(PG_INVARIANT_ERROR, "null builder");
+  if (b->obj_nv < 0) return fail(PG_STATE_ERROR, "pg_obj_fetch without a successful pg_load_obj");
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  const cudaMemcpyKind k = (flags & PG_HOST_OUTPUT) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (b->obj_nv) CU(cudaMemcpyAsync(V, b->obj_v.p, (size_t)b->obj_nv * 24, k, st));
+  if (b->obj_nt) CU(cudaMemcpyAsync(T, b->obj_t.p, (size_t)b->obj_nt * 12, k, st));
+  CU(cudaStreamSynchronize(st));
   return PG_OK;
 }
 
