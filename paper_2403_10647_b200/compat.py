@@ -11,6 +11,8 @@ replaces, in place (SURVEY.md §8b "Callers"):
   * pargrid.cli.ALGORITHMS[...] for each replaced builder       (cli.py:30-34)
   * pargrid.stats.compute_stats and pargrid.compute_stats       (stats.py:43; GPU reductions,
     with consumers=True)
+  * pargrid.geometry.load_obj (+ its re-exports)                (geometry.py:84; GPU parser,
+    with consumers=True)
   * pargrid.kernels._BACKENDS["cuda"]                           (kernels/__init__.py:17-19)
     -- radix_sort_pairs and dda_cast on the GPU
 The wrapper returns the reference's own CompactGrid / BuildReport types, raises the
@@ -24,6 +26,7 @@ import types
 from . import builders as _b
 from . import errors as _e
 from . import kernels as _k
+from . import obj as _o
 from . import stats as _s
 
 
@@ -93,6 +96,25 @@ def make_compute_stats(pargrid):
     return compute_stats
 
 
+def make_load_obj(pargrid):
+    perr = pargrid.errors
+    pgeom = sys.modules["pargrid.geometry"]
+
+    def load_obj(path):
+        try:
+            mesh = _o.load_obj(path)
+        except _e.ObjParseError as exc:
+            msg = str(exc)
+            prefix = f"line {exc.line_number}: "
+            raise perr.ObjParseError(msg[len(prefix):] if msg.startswith(prefix) else msg,
+                                     exc.line_number) from exc
+        return pgeom.TriangleMesh(mesh.vertices, mesh.triangles)
+
+    load_obj.__doc__ = _o.load_obj.__doc__
+    load_obj.__wrapped_b200__ = True
+    return load_obj
+
+
 def make_backend(pargrid):
     kernels = sys.modules["pargrid.kernels"]
     lane = kernels._BACKENDS.get("c") or kernels._BACKENDS["python"]
@@ -133,6 +155,11 @@ def install(pargrid=None, backend=True, algos=("parallel",), consumers=False):
         pstats.compute_stats = cs
         pargrid.compute_stats = cs
         cli.compute_stats = cs
+        lo = make_load_obj(pargrid)
+        sys.modules["pargrid.geometry"].load_obj = lo
+        for mod in (pargrid, cli):
+            if hasattr(mod, "load_obj"):
+                mod.load_obj = lo
     if backend:
         sys.modules["pargrid.kernels"]._BACKENDS["cuda"] = make_backend(pargrid)
     return bp
