@@ -410,7 +410,23 @@ def main():
     npasses = (key_bits + 8) // 9        # 9-bit digits (make_plan in pgrid.cu)
     pass_ms = sort_ms / max(npasses, 1)
 
-    # end to end through the public API: pinned host inputs, H2D + build + D2H each step
+    # per-kernel device time: events after every launch (pg_kernel_timing) over a few
+    # synchronous builds on the launching stream; mean duration per launch of each kernel
+    _native.kernel_timing(True)
+    per = {}
+    kt_builds = 5
+    for _ in range(kt_builds):
+        step(timed=False)
+        torch.cuda.synchronize()
+        for name, us in _native.kernel_times():
+            if not name.startswith("("):
+                per.setdefault(name, []).append(us * 1e-3)
+    _native.kernel_timing(False)
+    ktime = {k: {"ms_per_launch": float(np.mean(v)), "launches": len(v) // kt_builds,
+                 "ms_per_build": float(np.sum(v)) / kt_builds} for k, v in per.items()}
+
+    # end to end through the public API: pinned host inputs, H2D + build + D2H every step.
+    # BuildPipeline overlaps build i's sort and G/O read-back with build i+1's input copy.
     e2e_steps = args.e2e_steps or min(args.steps, 10)
     Vh = np.ascontiguousarray(V).copy()
     Th = np.ascontiguousarray(T).copy()
@@ -419,27 +435,57 @@ def main():
     from paper_2403_10647_b200.gridcore import TriangleMesh
     hmesh = TriangleMesh(Vh, Th)
     grid, rep = builders.build_parallel(hmesh, spec, device=local)
-    e2e_t = []
-    for _ in range(e2e_steps):
+    seq_t = []
+    for _ in range(min(e2e_steps, 3)):
         t0 = time.perf_counter()
         grid, rep = builders.build_parallel(hmesh, spec, device=local)
-        e2e_t.append(time.perf_counter() - t0)
-    e2e_sec = statistics.median(e2e_t)
+        seq_t.append(time.perf_counter() - t0)
+    pipe = builders.BuildPipeline(local, depth=2)
+    e2e_parity = True
+
+    def pipe_run(steps):
+        ok = True
+        last = None
+        for i in range(steps):
+            if len(pipe) == 2:
+                last, _ = pipe.result()
+                ok &= int(last.G[-1]) == no
+            pipe.submit(hmesh, spec)
+            last = None           # drop the host grid so its pinned blocks recycle
+        while len(pipe):
+            last, _ = pipe.result()
+            ok &= int(last.G[-1]) == no
+        return ok, last
+
+    pipe_run(4)                   # warm: workspaces and the pinned output pool
+    t0 = time.perf_counter()
+    e2e_parity, g = pipe_run(e2e_steps)
+    e2e_sec = (time.perf_counter() - t0) / e2e_steps
+    e2e_parity &= hashlib.sha256(g.G.tobytes()).hexdigest() == hashlib.sha256(grid.G.tobytes()).hexdigest()
+    e2e_parity &= hashlib.sha256(g.O.tobytes()).hexdigest() == hashlib.sha256(grid.O.tobytes()).hexdigest()
     _native.host_unregister(Vh)
     _native.host_unregister(Th)
 
     peak, peak_kind = peaks()
     B = 12 * n + 24 * nv + 4 * (ncells + 1) + 4 * no          # SURVEY §8d compulsory bytes
+    def kt(name):
+        return ktime.get(name, {"ms_per_launch": 0.0, "launches": 0, "ms_per_build": 0.0})
+    # algorithmic bytes per launch: K1 reads T and V, writes a 16-byte record per
+    # triangle; K2 reads the records and writes the (cell, object) pairs; every radix scatter
+    # reads and writes 8 bytes per pair; K4 reads the sorted cells and writes G
     kern = {
-        "k_boxes_count_scan": {"ms": k1_ms, "launches": 1, "alg_bytes": 12 * n + 24 * nv + 16 * n},
-        "k_expand_pairs": {"ms": k2_ms, "launches": 1, "alg_bytes": 16 * n + 8 * no},
-        "radix_pass": {"ms": pass_ms, "launches": npasses, "alg_bytes": 16 * no},
-        "k_cell_offsets": {"ms": k4_ms, "launches": 1, "alg_bytes": 4 * no + 4 * (ncells + 1)},
+        "k_boxes_count": {"alg_bytes": 12 * n + 24 * nv + 16 * n},
+        "k_pairs_emit": {"alg_bytes": 16 * n + 8 * no},
+        "k_radix_scatter": {"alg_bytes": 16 * no},
+        "k_cell_offsets": {"alg_bytes": 4 * no + 4 * (ncells + 1)},
     }
     for k, v in kern.items():
+        t = kt(k)
+        v.update(ms=t["ms_per_launch"], launches=t["launches"], ms_per_build=t["ms_per_build"])
         v["gbs"] = v["alg_bytes"] / (v["ms"] * 1e-3) / 1e9 if v["ms"] > 0 else None
         v["frac"] = v["gbs"] / peak if v["gbs"] else None
-    dom = max(kern, key=lambda k: kern[k]["ms"] * kern[k]["launches"])
+    glue = {k: round(v["ms_per_build"] * 1e3, 2) for k, v in ktime.items() if k not in kern}
+    dom = max(kern, key=lambda k: kern[k]["ms_per_build"])
     traffic = traffic_table().get(dom)
     value = world / (ms * 1e-3)
     line = {
@@ -462,9 +508,13 @@ def main():
                      "launch_ms": round(kern[dom]["ms"], 4), "peak_kind": peak_kind},
         "kernels": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                     for k, v in kern.items()},
+        "glue_us_per_build": glue,
         "e2e": {"value": round(1.0 / e2e_sec * world, 3), "unit": "builds/s",
                 "h2d_bytes_per_step": int(Vh.nbytes + Th.nbytes),
-                "d2h_bytes_per_step": int(grid.G.nbytes + grid.O.nbytes), "ms_per_step": round(e2e_sec * 1e3, 2)},
+                "d2h_bytes_per_step": int(grid.G.nbytes + grid.O.nbytes), "ms_per_step": round(e2e_sec * 1e3, 2),
+                "api": "builders.BuildPipeline (2 slots: build i+1's H2D overlaps build i's sort + D2H)",
+                "parity": "bit-exact vs build_parallel" if e2e_parity else "MISMATCH",
+                "sequential_build_parallel_ms": round(statistics.median(seq_t) * 1e3, 2)},
         "gpu_launches": launches * args.steps,
         "clocks": clk.summary(),
     }

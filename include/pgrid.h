@@ -42,6 +42,7 @@ extern "C" {
 #define PG_KEEP_STAGES 4u      /* keep the unsorted pairs for pg_stage (record= support) */
 #define PG_HOST_RAYS 8u        /* pg_dda_cast: rays are host pointers (grid stays on device) */
 #define PG_CHECK 16u           /* pg_dda_cast: synchronise and report device-side errors */
+#define PG_ASYNC 32u           /* pg_finish: return once enqueued (host outputs valid after pg_wait) */
 
 /* Grid specification: the exact host doubles of GridSpec (gridcore.py:36-57). */
 typedef struct {
@@ -166,10 +167,14 @@ int pg_partition(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int6
 int pg_sort_cells(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int64_t n,
                   int64_t ncells, uint32_t *G, uint32_t *O, void *stream);
 
+/* Wait for the device work (and PG_HOST_OUTPUT copies) of the last pg_finish on b. */
+int pg_wait(pg_builder *b);
+
 /* Profiling aid: with PGRID_KTIMES=1 in the environment, every launch of the calling thread's
  * last pg_count + pg_finish is bracketed by events; this writes "kernel microseconds" lines
  * (device time between consecutive launch completions) into buf. */
 int pg_kernel_times(char *buf, int len);
+int pg_kernel_timing(int on); /* switch the per-launch events on / off at run time */
 
 /* Page-lock host memory so PG_HOST_* copies run at full PCIe rate (optional). */
 int pg_host_register(void *ptr, uint64_t bytes);

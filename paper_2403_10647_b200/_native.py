@@ -28,13 +28,14 @@ PG_HOST_OUTPUT = 2
 PG_KEEP_STAGES = 4
 PG_HOST_RAYS = 8
 PG_CHECK = 16
+PG_ASYNC = 32
 
 NPHASES = 6
 
 # every symbol include/pgrid.h declares (checked by tests/test_boundary.py)
 EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
            "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_finish_baseline",
-           "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_build_async",
+           "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_build_async",
            "pg_build_wait", "pg_host_register",
            "pg_host_unregister", "pg_host_alloc", "pg_host_free", "pg_last_launch_count",
            "pg_last_error")
@@ -91,6 +92,8 @@ def load():
         lib.pg_dda_prepare.argtypes = [vp, vp, i64, vp, i64, u32, vp]
         lib.pg_dda_cast.argtypes = [vp, vp, vp, i64, ctypes.POINTER(PgSpec), vp, vp, vp, i64, vp, vp, u32, vp]
         lib.pg_kernel_times.argtypes = [ctypes.c_char_p, ctypes.c_int]
+        lib.pg_wait.argtypes = [vp]
+        lib.pg_kernel_timing.argtypes = [ctypes.c_int]
         lib.pg_load_obj.argtypes = [vp, vp, u64, u32, vp, ctypes.POINTER(i64)]
         lib.pg_obj_fetch.argtypes = [vp, vp, vp, u32, vp]
         lib.pg_grid_stats.argtypes = [vp, vp, u32, vp, ctypes.POINTER(u64)]
@@ -106,7 +109,7 @@ def load():
         lib.pg_last_error.restype = ctypes.c_char_p
         for name in ("pg_builder_create", "pg_count", "pg_finish", "pg_stage",
                      "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells",
-                     "pg_finish_baseline", "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
+                     "pg_finish_baseline", "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
                      "pg_last_launch_count"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
@@ -170,6 +173,10 @@ class Builder:
         phases = (ctypes.c_float * NPHASES)() if timed else None
         check(self._lib.pg_finish(self._h, ptr(G), ptr(O), flags, stream, phases))
         return list(phases) if timed else None
+
+    def wait(self):
+        """Wait for the last finish (PG_ASYNC) including its host-output copies."""
+        check(self._lib.pg_wait(self._h))
 
     def finish_baseline(self, algo, G, O, flags=0, stream=None):
         """algo 1 = sorted grid, 2 = compact grid (builders.py:172-231); returns (phases, max_task_work)."""
@@ -258,6 +265,11 @@ class Builder:
 
 
 _tls = threading.local()
+
+
+def kernel_timing(on):
+    """Per-launch device timing (events after every launch) on / off for this process."""
+    check(load().pg_kernel_timing(1 if on else 0))
 
 
 def kernel_times():

@@ -153,12 +153,13 @@ bool sync_debug() {
 
 // PGRID_KTIMES=1: an event after every launch, so pg_kernel_times can report per-kernel
 // device times of the last pg_count / pg_finish (profiling aid; off by default).
+int g_ktimes = -1;  // -1: from the environment; 0/1: set by pg_kernel_timing
 bool ktimes_on() {
-  static const bool on = [] {
+  if (g_ktimes < 0) {
     const char* e = getenv("PGRID_KTIMES");
-    return e && *e && *e != '0';
-  }();
-  return on;
+    g_ktimes = (e && *e && *e != '0') ? 1 : 0;
+  }
+  return g_ktimes == 1;
 }
 struct KTimer {
   std::vector<std::pair<const char*, cudaEvent_t>> ev;
@@ -561,7 +562,7 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
     if (no) CU(cudaMemcpyAsync(O, dO, no * 4, cudaMemcpyDeviceToHost, st));
   }
   CU(cudaEventRecord(b->ev[4], st));
-  if (phase_ms || (flags & PG_HOST_OUTPUT)) CU(cudaEventSynchronize(b->ev[4]));
+  if (phase_ms || ((flags & PG_HOST_OUTPUT) && !(flags & PG_ASYNC))) CU(cudaEventSynchronize(b->ev[4]));
   if (phase_ms) {
     float t01 = 0, t12 = 0, t23 = 0, t34 = 0;
     CU(cudaEventElapsedTime(&t01, b->ev[0], b->ev[1]));
@@ -1195,6 +1196,18 @@ int pg_mesh_bounds(pg_builder* b, const double* V, int64_t nv, uint32_t flags, v
     lo[k] = h[k];
     hi[k] = h[3 + k];
   }
+  return PG_OK;
+}
+
+int pg_wait(pg_builder* b) {
+  if (!b) return fail(PG_INVARIANT_ERROR, "null builder");
+  CU(cudaSetDevice(b->device));
+  CU(cudaEventSynchronize(b->ev[4]));
+  return PG_OK;
+}
+
+int pg_kernel_timing(int on) {
+  g_ktimes = on ? 1 : 0;
   return PG_OK;
 }
 

@@ -244,3 +244,22 @@ def test_sync_free_graph_build_matches_and_reports_capacity(hashes):
     small = torch.empty(1000, dtype=torch.int32, device="cuda")
     b.build_async(Vd, len(mesh.vertices), Td, len(mesh.triangles), spec, Gd, small, 1000)
     assert b.build_wait() == -h["no"]          # capacity exceeded is reported, not silent
+
+
+def test_build_pipeline_matches_build_parallel(kat, hashes):
+    """BuildPipeline / build_many: overlapped builds, results in submission order."""
+    items = [kat_case(kat, name) for name in KAT_NAMES]
+    items += [scene_from_recipe(hashes[k]["recipe"]) for k in ("cfg1", "skewed100k", "walls100k")]
+    items = items * 2
+    got = list(builders.build_many(items, depth=2))
+    assert len(got) == len(items)
+    for (mesh, spec), (grid, rep) in zip(items, got):
+        want, wrep = builders.build_parallel(mesh, spec)
+        assert np.array_equal(grid.G, want.G) and np.array_equal(grid.O, want.O)
+        assert rep.no == wrep.no and rep.total_work == wrep.total_work
+    pipe = builders.BuildPipeline(depth=2)
+    pipe.submit(*items[0])
+    pipe.submit(*items[1])
+    with pytest.raises(RuntimeError):
+        pipe.submit(*items[2])
+    assert pipe.result()[1].no == got[0][1].no and pipe.result()[1].no == got[1][1].no
