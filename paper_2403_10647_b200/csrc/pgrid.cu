@@ -549,8 +549,14 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
     CU(cudaEventRecord(b->ev[1], st));
   }
   CU(cudaEventRecord(b->ev[2], st));
-  k_key_tile_bounds<<<(g_tiles + 1 + 7) / 8, 256, 0, st>>>(sorted, cno, G_TILE, (unsigned)ncells, g_tiles + 1,
-                                                          kbounds);
+  {
+    // narrow K4's bound searches with the last pass's digit totals (when a sort ran)
+    const int lp = plan.npasses - 1;
+    const bool top = lp >= 0 && no > 0 && ncells > 1;
+    k_key_tile_bounds<<<(g_tiles + 1 + 7) / 8, 256, 0, st>>>(sorted, cno, G_TILE, (unsigned)ncells, g_tiles + 1,
+                                                            kbounds, top ? hist + lp * kMaxBins : nullptr,
+                                                            top ? plan.shift[lp] : 0, top ? 1 << plan.bits[lp] : 0);
+  }
   LAUNCHED("k_key_tile_bounds", st);
   k_cell_offsets<<<g_tiles, G_THREADS, 0, st>>>(sorted, cno, (unsigned)ncells, kbounds, dG);
   LAUNCHED("k_cell_offsets", st);

@@ -310,6 +310,7 @@ k_boxes_count(const double* __restrict__ V, long long nv, const int* __restrict_
 // NO <= 2^30 is established) and the total NO (u64, exact).
 constexpr int TS_THREADS = 1024;
 constexpr int TS_WARPS = TS_THREADS / 32;
+constexpr int TS_REG = 20;  // chunks of 32 held in registers per lane (single-pass case)
 __global__ void __launch_bounds__(TS_THREADS)
 k_scan_tile_sums(const unsigned long long* __restrict__ tile_sum, unsigned ntiles, unsigned* __restrict__ tile_pre,
                  unsigned long long* __restrict__ total) {
@@ -318,7 +319,42 @@ k_scan_tile_sums(const unsigned long long* __restrict__ tile_sum, unsigned ntile
   // warp w owns the contiguous segment [w*seg, (w+1)*seg), read in coalesced 32-wide chunks
   const unsigned seg = ((ntiles + TS_WARPS - 1) / TS_WARPS + 31) & ~31u;
   const unsigned s0 = min((unsigned)warp * seg, ntiles), s1 = min(s0 + seg, ntiles);
-  // loads are batched 8 chunks deep so each pass costs a few memory latencies, not one per chunk
+  if (seg <= 32u * TS_REG) {
+    // single pass: every chunk of the segment is loaded at once and kept in registers
+    unsigned long long v[TS_REG];
+    unsigned long long part = 0;
+#pragma unroll
+    for (int j = 0; j < TS_REG; ++j) {
+      const unsigned i = s0 + 32 * j + lane;
+      v[j] = i < s1 ? tile_sum[i] : 0ull;
+      part += v[j];
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
+    if (lane == 0) wsum[warp] = part;
+    __syncthreads();
+    unsigned long long carry = 0, tot = 0;
+    for (int w = 0; w < TS_WARPS; ++w) {
+      const unsigned long long x = wsum[w];
+      carry += w < warp ? x : 0ull;
+      tot += x;
+    }
+#pragma unroll
+    for (int j = 0; j < TS_REG; ++j) {
+      const unsigned i = s0 + 32 * j + lane;
+      unsigned long long inc = v[j];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+      }
+      if (i < s1) tile_pre[i] = (unsigned)(carry + inc - v[j]);
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (tid == 0) *total = tot;
+    return;
+  }
+  // large inputs: two passes over the segment, loads batched 8 chunks deep
   constexpr int B = 8;
   unsigned long long part = 0;
   for (unsigned c = s0; c < s1; c += 32 * B) {
@@ -587,17 +623,55 @@ k_pair_tile_bounds(const uint4* __restrict__ rec, const unsigned* __restrict__ t
   if ((threadIdx.x & 31) == 0) bounds[t] = make_int2((int)a - 1, (int)b);
 }
 
-// lower_bound(sorted, t * step) for t in [0, nq), one warp per query (K4's key ranges).
+// lower_bound(sorted, t * step) for t in [0, nq), one warp per query (K4's key ranges). With
+// top_hist (the last radix pass's digit totals), each query is first narrowed to its top
+// digit's run [start(d), start(d+1)] -- the run starts are a prefix of top_hist -- so the
+// 32-ary search covers ~NO/2^bits keys instead of NO.
 __global__ void __launch_bounds__(256)
 k_key_tile_bounds(const unsigned* __restrict__ sorted, Count cno, unsigned step, unsigned ncells, unsigned nq,
-                  unsigned* __restrict__ out) {
+                  unsigned* __restrict__ out, const unsigned* __restrict__ top_hist = nullptr, int top_shift = 0,
+                  int top_bins = 0) {
+  __shared__ unsigned start[kMaxBins + 1];
   const unsigned no = cno.get();
+  if (top_hist) {
+    if (threadIdx.x < 32) {  // exclusive prefix of the (<= 512) digit totals, 16 per lane
+      const int lane = threadIdx.x;
+      unsigned v[16], run = 0;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int d = lane * 16 + q;
+        v[q] = run;
+        run += d < top_bins ? __ldg(&top_hist[d]) : 0u;
+      }
+      unsigned inc = run;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const unsigned o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) start[lane * 16 + q] = inc - run + v[q];
+      if (lane == 31) start[kMaxBins] = inc;
+    }
+    __syncthreads();
+  }
   const unsigned t = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= nq) return;
   const unsigned long long c = min((unsigned long long)t * step, (unsigned long long)ncells);
-  const unsigned long long v =
-      warp_lower_bound(no, c, [&](unsigned long long i) { return (unsigned long long)__ldg(sorted + i); });
-  if ((threadIdx.x & 31) == 0) out[t] = (unsigned)v;
+  unsigned long long lo = 0, hi = no;
+  if (top_hist) {
+    const unsigned d = (unsigned)(c >> top_shift);
+    if ((int)d < top_bins) {
+      lo = start[d];
+      hi = d + 1 < (unsigned)top_bins ? start[d + 1] : no;
+    } else {
+      lo = hi = no;
+    }
+  }
+  unsigned long long dummy_lo = hi, dummy_hi = hi;
+  warp_lower_bound2(lo, hi, c, dummy_lo, dummy_hi, 0ull,
+                    [&](unsigned long long i) { return (unsigned long long)__ldg(sorted + i); });
+  if ((threadIdx.x & 31) == 0) out[t] = (unsigned)lo;
 }
 
 // Pairs in generation (object-major) order -- used when no radix pass follows
