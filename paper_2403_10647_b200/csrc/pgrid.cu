@@ -132,6 +132,10 @@ void launch_radix_scatter(int bits, unsigned ntiles, cudaStream_t st, const unsi
   }
 }
 
+template <int B>
+cudaError_t set_emit_smem() {
+  return cudaFuncSetAttribute(k_pairs_emit<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PeSmem));
+}
 template <int BITS>
 cudaError_t set_scatter_smem() {
   cudaError_t e = cudaFuncSetAttribute(k_radix_scatter<BITS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -140,6 +144,43 @@ cudaError_t set_scatter_smem() {
   if (e != cudaSuccess || BITS > 4) return e;
   return cudaFuncSetAttribute(k_radix_scatter<(BITS > 4 ? 1 : BITS), true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)rs_smem_bytes());
+}
+
+// PGRID_PRESORT=1 enables the K2 local presort of the first radix digit (measured slower:
+// K2's scattered in-tile stores cost more than the ranking they save in pass 0; off).
+bool presort_on() {
+  static const bool on = [] {
+    const char* e = getenv("PGRID_PRESORT");
+    return kPresortFits && e && *e == '1';
+  }();
+  return on;
+}
+
+void launch_pairs_emit(int presort_bits, unsigned grid, cudaStream_t st, const uint4* rec, const unsigned* tile_pre,
+                       long long n, Count cno, unsigned dx, unsigned dxy, const PassPlan& plan, const int2* bounds,
+                       unsigned* keys, unsigned* vals, unsigned* counts, unsigned ld) {
+  switch (presort_bits) {
+#define PG_CASE(B)                                                                                        \
+  case B:                                                                                                 \
+    k_pairs_emit<B><<<grid, RS_THREADS, sizeof(PeSmem), st>>>(rec, tile_pre, n, cno, dx, dxy, plan, bounds, keys, \
+                                                              vals, counts, ld);                          \
+    break;
+    PG_CASE(0) PG_CASE(1) PG_CASE(2) PG_CASE(3) PG_CASE(4) PG_CASE(5) PG_CASE(6) PG_CASE(7) PG_CASE(8) PG_CASE(9)
+#undef PG_CASE
+    default: break;
+  }
+}
+
+void launch_scatter_presorted(int bits, unsigned ntiles, cudaStream_t st, const unsigned* kin, const unsigned* vin,
+                              unsigned* ko, unsigned* vo, Count n, int shift, const unsigned* hist,
+                              const unsigned* offs, unsigned ld) {
+  switch (bits) {
+#define PG_CASE(B) \
+  case B: k_scatter_presorted<B><<<ntiles, RS_THREADS, 0, st>>>(kin, vin, ko, vo, n, shift, hist, offs, ld); break;
+    PG_CASE(1) PG_CASE(2) PG_CASE(3) PG_CASE(4) PG_CASE(5) PG_CASE(6) PG_CASE(7) PG_CASE(8) PG_CASE(9)
+#undef PG_CASE
+    default: break;
+  }
 }
 
 // PGRID_SYNC_DEBUG=1: synchronise after every launch so a fault names its kernel.
@@ -245,7 +286,9 @@ int pg_builder_create(int device, pg_builder** out) {
   for (auto& e : b->ev) CU(cudaEventCreate(&e));
   CU(cudaMallocHost(&b->h_scalars, 4 * sizeof(unsigned long long)));
   CU(cudaFuncSetAttribute(k_boxes_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem)));
-  CU(cudaFuncSetAttribute(k_pairs_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PeSmem)));
+  CU(set_emit_smem<0>()); CU(set_emit_smem<1>()); CU(set_emit_smem<2>()); CU(set_emit_smem<3>());
+  CU(set_emit_smem<4>()); CU(set_emit_smem<5>()); CU(set_emit_smem<6>()); CU(set_emit_smem<7>());
+  CU(set_emit_smem<8>()); CU(set_emit_smem<9>());
   CU(set_scatter_smem<1>()); CU(set_scatter_smem<2>()); CU(set_scatter_smem<3>());
   CU(set_scatter_smem<4>()); CU(set_scatter_smem<5>()); CU(set_scatter_smem<6>());
   CU(set_scatter_smem<7>()); CU(set_scatter_smem<8>()); CU(set_scatter_smem<9>());
@@ -427,7 +470,7 @@ namespace {
 int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned* keys0, unsigned* vals0,
                unsigned* keys1, unsigned* vals1, unsigned* vals_final, Count cno, uint64_t cap, unsigned* hist,
                unsigned* counts, cudaStream_t st, const unsigned** sorted_keys_out, unsigned* keys2 = nullptr,
-               unsigned* vals2 = nullptr) {
+               unsigned* vals2 = nullptr, bool presorted0 = false) {
   // grids are sized for `cap` pairs; the kernels read the actual count from `cno`
   const unsigned ntiles = (unsigned)((cap + RS_TILE - 1) / RS_TILE);
   const unsigned ld = (ntiles + 3) & ~3u;
@@ -454,9 +497,15 @@ int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned
     }
     k_scan_tile_counts<<<1u << plan.bits[p], SC_THREADS, 0, st>>>(counts, cno, ld, hist + p * kMaxBins);
     LAUNCHED("k_scan_tile_counts", st);
-    launch_radix_scatter(plan.bits[p], ntiles, st, kin, vin, ko, vo, cno, plan.shift[p], hist + p * kMaxBins, counts,
-                         ld);
-    LAUNCHED("k_radix_scatter", st);
+    if (p == 0 && presorted0) {
+      launch_scatter_presorted(plan.bits[p], ntiles, st, kin, vin, ko, vo, cno, plan.shift[p], hist + p * kMaxBins,
+                               counts, ld);
+      LAUNCHED("k_scatter_presorted", st);
+    } else {
+      launch_radix_scatter(plan.bits[p], ntiles, st, kin, vin, ko, vo, cno, plan.shift[p], hist + p * kMaxBins, counts,
+                           ld);
+      LAUNCHED("k_radix_scatter", st);
+    }
     b->launches += 2;
     *sorted_keys_out = ko;
   }
@@ -535,12 +584,16 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
                                                             pbounds);
       LAUNCHED("k_pair_tile_bounds", st);
       // K2 writes its first-pass tile counts straight into the digit-major matrix
-      k_pairs_emit<<<rs_tiles, RS_THREADS, sizeof(PeSmem), st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, cno, dxu,
-                                                                 dxyu, plan, pbounds, keysA, valsA, counts, ld);
+      // with the presort, K2 leaves every tile sorted by the first digit (pass 0 then only moves
+      // digit runs); stage dumps (record=) need generation order, so they skip it
+      const bool presort = presort_on() && !(flags & PG_KEEP_STAGES);
+      launch_pairs_emit(presort ? plan.bits[0] : 0, rs_tiles, st, b->rec.as<uint4>(), b->tile_pre, b->n, cno, dxu,
+                        dxyu, plan, pbounds, keysA, valsA, counts, ld);
       LAUNCHED("k_pairs_emit", st);
       b->launches += 2;
       CU(cudaEventRecord(b->ev[1], st));
-      if ((rc = run_passes(b, plan, true, keysA, valsA, keysB, valsB, dO, cno, no, hist, counts, st, &sorted)))
+      if ((rc = run_passes(b, plan, true, keysA, valsA, keysB, valsB, dO, cno, no, hist, counts, st, &sorted, nullptr,
+                           nullptr, presort)))
         return rc;
     } else {
       CU(cudaEventRecord(b->ev[1], st));

@@ -416,7 +416,11 @@ constexpr int kMaxBins = 1 << kMaxDigitBits;  // 512
 
 // Object cache for one expansion tile: box records of the tile's triangles olo, olo+1, ...
 // (structure of arrays in shared memory); triangles past OC_CAP are read from global.
-constexpr int OC_CAP = 2560;  // (3*OC_CAP words also host K2's <= 4096-bin coarse histogram)
+#ifndef OC_CAP_OVERRIDE
+constexpr int OC_CAP = 2560;
+#else
+constexpr int OC_CAP = OC_CAP_OVERRIDE;
+#endif  // (3*OC_CAP words also host K2's <= 4096-bin coarse histogram)
 struct ObjCache {
   unsigned lo_cell[OC_CAP];
   unsigned mx[OC_CAP];
@@ -756,7 +760,11 @@ k_digit_hist(const unsigned* __restrict__ keys, long long n, PassPlan plan, unsi
 // (A single-kernel onesweep with decoupled look-back was measured first: its per-digit
 //  look-back chains serialised at ~20% of HBM bandwidth on B200.)
 // ----------------------------------------------------------------------------------------
+#ifndef RS_THREADS_OVERRIDE
 constexpr int RS_THREADS = 256;
+#else
+constexpr int RS_THREADS = RS_THREADS_OVERRIDE;
+#endif
 constexpr int RS_WARPS = RS_THREADS / 32;
 #ifndef RS_ITEMS_OVERRIDE
 constexpr int RS_ITEMS = 16;
@@ -1178,8 +1186,99 @@ struct PeSmem {
   int warpmax[RS_WARPS];
 };
 static_assert(sizeof(ObjCache) >= RS_TILE * 4, "the object cache doubles as the value transpose buffer");
+// the presort keeps its values and per-warp counters in the object cache
+constexpr bool kPresortFits = sizeof(ObjCache) >= RS_TILE * 4 + RS_WARPS * kMaxBins * 2 + RS_WARPS * 4;
 
-__global__ void __launch_bounds__(RS_THREADS)
+// K2 with the first radix pass's local sort fused in (PRESORT = that pass's digit bits): the
+// tile's pairs are ranked by the first digit exactly as k_radix_scatter ranks a tile (stable,
+// element order) and written back to the tile's own slots in digit order, so the first pass
+// only has to move whole digit runs (k_scatter_presorted, no ranking). Shared memory reuses
+// the expansion's dead slots (keys) and object cache (values, per-warp counters).
+template <int BITS>
+__device__ __forceinline__ void presort_tile(const unsigned* __restrict__ skey, const unsigned* __restrict__ sval,
+                                             unsigned short (*whist)[kMaxBins], unsigned* wsum, unsigned p0,
+                                             unsigned tvalid, int shift, unsigned* __restrict__ keys,
+                                             unsigned* __restrict__ vals, unsigned* __restrict__ counts0, unsigned ld,
+                                             unsigned tile) {
+  constexpr int NB = 1 << BITS;
+  constexpr unsigned DMASK = (unsigned)NB - 1u;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto elem = [&](int j) { return (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane; };
+  auto valid = [&](int j) { return elem(j) < tvalid; };
+  {
+    unsigned* row = reinterpret_cast<unsigned*>(&whist[warp][0]);
+#pragma unroll
+    for (int q = lane; q < NB / 2; q += 32) row[q] = 0u;
+  }
+  unsigned dg[RS_ITEMS];
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) dg[j] = valid(j) ? (skey[elem(j)] >> shift) & DMASK : 0u;
+  unsigned pm[RS_ITEMS];
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) pm[j] = __ballot_sync(0xffffffffu, valid(j));
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) pm[j] = peers_step(pm[j], dg[j], 1u << b);
+  }
+  __syncwarp();
+  const unsigned lt = lanemask_lt();
+  unsigned rank[RS_ITEMS];
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    const unsigned peers = valid(j) ? pm[j] : 0u;
+    const int leader = __ffs(peers | (1u << lane)) - 1;
+    unsigned old = 0;
+    if (lane == leader && peers) {
+      old = whist[warp][dg[j]];
+      whist[warp][dg[j]] = (unsigned short)(old + __popc(peers));
+    }
+    old = __shfl_sync(0xffffffffu, old, leader);
+    rank[j] = old + __popc(peers & lt);
+    __syncwarp();
+  }
+  __syncthreads();
+  unsigned tc[RS_DPT], tsum = 0;
+#pragma unroll
+  for (int q = 0; q < RS_DPT; ++q) {
+    const int d = tid * RS_DPT + q;
+    unsigned run = 0;
+    if (d < NB) {
+#pragma unroll
+      for (int w = 0; w < RS_WARPS; ++w) {
+        const unsigned c = whist[w][d];
+        whist[w][d] = (unsigned short)run;
+        run += c;
+      }
+    }
+    tc[q] = run;
+    tsum += run;
+  }
+  unsigned ttot;
+  unsigned lpre = block_excl_scan<RS_WARPS>(tsum, wsum, ttot);
+#pragma unroll
+  for (int q = 0; q < RS_DPT; ++q) {
+    const int d = tid * RS_DPT + q;
+    if (d < NB) {
+#pragma unroll
+      for (int w = 0; w < RS_WARPS; ++w) whist[w][d] = (unsigned short)(whist[w][d] + lpre);
+      counts0[(size_t)d * ld + tile] = tc[q];
+    }
+    lpre += tc[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    if (valid(j)) {
+      const unsigned pos = p0 + rank[j] + whist[warp][dg[j]];
+      keys[pos] = skey[elem(j)];
+      vals[pos] = sval[elem(j)];
+    }
+  }
+}
+
+template <int PRESORT>
+__global__ void __launch_bounds__(RS_THREADS, 1024 / RS_THREADS)
 k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno,
              unsigned dx, unsigned dxy, PassPlan plan, const int2* __restrict__ bounds, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
              unsigned* __restrict__ counts0, unsigned ld) {
@@ -1196,6 +1295,24 @@ k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pr
   expand_tile<RS_THREADS, RS_ITEMS>(rec, n, p0, pend, dx, dxy, tile_pre, bounds, sm.slot, sm.warpmax, &sm.oc, key, own);
   const unsigned pbase = p0 + (unsigned)tid * RS_ITEMS;
   const int nvalid = pend > pbase ? (int)min((unsigned)RS_ITEMS, pend - pbase) : 0;
+  if (PRESORT > 0 && kPresortFits) {
+    // the tile in element (generation) order: keys in the dead slots, values in the cache
+    unsigned* skey = reinterpret_cast<unsigned*>(sm.slot);
+    unsigned* sval = sm.oc.lo_cell;
+    auto* whist = reinterpret_cast<unsigned short(*)[kMaxBins]>(sm.oc.lo_cell + RS_TILE);
+    unsigned* wsum = sm.oc.lo_cell + RS_TILE + RS_WARPS * kMaxBins / 2;
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < RS_ITEMS / 4; ++q) {
+      reinterpret_cast<uint4*>(skey)[tid * (RS_ITEMS / 4) + q] =
+          make_uint4(key[4 * q], key[4 * q + 1], key[4 * q + 2], key[4 * q + 3]);
+      reinterpret_cast<uint4*>(sval)[tid * (RS_ITEMS / 4) + q] =
+          make_uint4(own[4 * q], own[4 * q + 1], own[4 * q + 2], own[4 * q + 3]);
+    }
+    __syncthreads();
+    presort_tile<PRESORT>(skey, sval, whist, wsum, p0, pend - p0, plan.shift[0], keys, vals, counts0, ld, blockIdx.x);
+    return;
+  }
   // transpose through shared memory (the expansion's slots and object cache are dead): a
   // thread's 16 consecutive pairs leave as 16-byte chunks striped over the CTA, so every
   // warp store is 512 contiguous bytes; chunk index c is XOR-swizzled against bank conflicts
@@ -1241,6 +1358,79 @@ k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pr
   // straight into the digit-major matrix: one 4-byte entry per digit row (the rows stay in
   // L2 until the row scan reads them, so the scattered writes cost no extra DRAM traffic)
   for (int b = tid; b < (1 << plan.bits[0]); b += RS_THREADS) counts0[(size_t)b * ld + blockIdx.x] = sm.h[b];
+}
+
+
+// First radix pass over tiles that K2 already sorted by the pass's digit (k_pairs_emit<BITS>):
+// every digit run of a tile moves as a block to digit_start + tile_prefix; no ranking.
+template <int BITS>
+__global__ void __launch_bounds__(RS_THREADS, 6)
+k_scatter_presorted(const unsigned* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
+                    unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, Count cno, int shift,
+                    const unsigned* __restrict__ hist, const unsigned* __restrict__ offs, unsigned ld) {
+  constexpr int NB = 1 << BITS;
+  constexpr unsigned DMASK = (unsigned)NB - 1u;
+  __shared__ unsigned short dgt[RS_TILE];
+  __shared__ __align__(16) unsigned vst[RS_TILE];
+  __shared__ unsigned gbase[kMaxBins];
+  __shared__ unsigned wsum[RS_WARPS];
+  const unsigned no = cno.get();
+  const unsigned tile = blockIdx.x;
+  const unsigned tbase = tile * (unsigned)RS_TILE;
+  if (tbase >= no) return;
+  const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
+  const int tid = threadIdx.x;
+  for (unsigned e = tid; e < tvalid; e += RS_THREADS) cp_async4(&vst[e], vals_in + tbase + e);
+  cp_async_commit();
+  unsigned k[RS_ITEMS];
+#pragma unroll
+  for (int r = 0; r < RS_ITEMS; ++r) {
+    const unsigned e = tid + r * RS_THREADS;
+    k[r] = e < tvalid ? __ldg(keys_in + tbase + e) : 0u;
+    dgt[e] = (unsigned short)((k[r] >> shift) & DMASK);
+  }
+  // digit starts: exclusive prefix of the global histogram
+  unsigned hs[RS_DPT], hsum = 0;
+#pragma unroll
+  for (int q = 0; q < RS_DPT; ++q) {
+    const int d = tid * RS_DPT + q;
+    hs[q] = d < NB ? __ldg(&hist[d]) : 0u;
+    hsum += hs[q];
+  }
+  unsigned htot;
+  unsigned hpre = block_excl_scan<RS_WARPS>(hsum, wsum, htot);  // (its barriers also publish dgt)
+  unsigned hp[RS_DPT];
+#pragma unroll
+  for (int q = 0; q < RS_DPT; ++q) {
+    hp[q] = hpre;
+    hpre += hs[q];
+  }
+  // run starts: gbase[d] = global position of the tile's first d-item, minus its tile index
+#pragma unroll
+  for (int q = 0; q < RS_DPT; ++q) {
+    const int d = tid * RS_DPT + q;
+    if (d < NB) gbase[d] = hp[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < RS_ITEMS; ++r) {
+    const unsigned e = tid + r * RS_THREADS;
+    if (e < tvalid) {
+      const unsigned d = dgt[e];
+      if (e == 0 || dgt[e - 1] != d) gbase[d] = gbase[d] + __ldg(&offs[(size_t)d * ld + tile]) - e;
+    }
+  }
+  cp_async_wait();
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < RS_ITEMS; ++r) {
+    const unsigned e = tid + r * RS_THREADS;
+    if (e < tvalid) {
+      const unsigned g = gbase[(k[r] >> shift) & DMASK] + e;
+      keys_out[g] = k[r];
+      vals_out[g] = vst[e];
+    }
+  }
 }
 
 // ----------------------------------------------------------------------------------------
