@@ -20,6 +20,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import _native
+
 COARSE_BITS = 12       # slab cuts at 2^12-bucket granularity of the cell-id range
 MAX_SLABS = 16         # pg_partition's digit table limit
 
@@ -263,14 +265,22 @@ class CudaOps:
         return self.torch.cat(xs) if xs else self.empty_pairs(0)
 
     def to_numpy(self, x):
-        return x.cpu().numpy().view(np.uint32) if hasattr(x, "cpu") else np.asarray(x, np.uint32)
+        """Device u32 tensor -> host array in page-locked memory (PCIe-rate copy)."""
+        if not hasattr(x, "cpu"):
+            return np.asarray(x, np.uint32)
+        out = _native.pinned_pool.empty(int(x.numel()), np.uint32)
+        if out.size:
+            self.torch.from_numpy(out.view(np.int32)).copy_(x.view(self.torch.int32))
+        return out
 
     def count(self, V, T, spec):
         torch = self.torch
         if not isinstance(V, torch.Tensor):
-            V = torch.from_numpy(np.ascontiguousarray(V)).to(self.dev)
-        if not isinstance(T, torch.Tensor):
-            T = torch.from_numpy(np.ascontiguousarray(T)).to(self.dev)
+            # host mesh: the C ABI stages it (one H2D at PCIe rate from page-locked arrays)
+            V = np.ascontiguousarray(V, dtype=np.float64).reshape(-1, 3)
+            T = np.ascontiguousarray(T, dtype=np.int32).reshape(-1, 3)
+            self._V, self._T = V, T
+            return self.b.count(V, V.shape[0], T, T.shape[0], spec, _native.PG_HOST_INPUT, self._sp())
         self._V, self._T = V, T          # keep alive for the stream
         return self.b.count(V, V.shape[0], T, T.shape[0], spec, 0, self._sp())
 
