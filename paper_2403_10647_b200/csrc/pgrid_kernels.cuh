@@ -860,7 +860,7 @@ struct DigitFn {
 // Upsweep of a radix pass: per-tile digit counts, TC_TILES tiles per CTA so every digit row
 // of the digit-major matrix receives TC_TILES consecutive entries (a full 32-byte sector).
 #ifndef TC_TILES_OVERRIDE
-constexpr int TC_TILES = 8;
+constexpr int TC_TILES = 4;
 #else
 constexpr int TC_TILES = TC_TILES_OVERRIDE;
 #endif
@@ -874,30 +874,30 @@ k_tile_counts(const unsigned* __restrict__ keys, Count cno, DigitFn dig, int nbi
   const unsigned t0 = blockIdx.x * TC_TILES;
   for (int b = tid; b < TC_TILES * kMaxBins; b += RS_THREADS) (&h[0][0])[b] = 0u;
   __syncthreads();
-  // full tiles: the next tile's keys are loaded before this tile's histogram atomics
+  // all of the CTA's (full) tiles are loaded before any histogram atomic: TC_TILES x 16 KB in
+  // flight per CTA, enough to cover HBM latency at the kernel's occupancy
   constexpr int R = RS_TILE / 4 / RS_THREADS;
-  uint4 k[R];
+  uint4 k[TC_TILES][R];
   auto full = [&](unsigned tile) { return tile < ntiles && (tile + 1) * (unsigned)RS_TILE <= no; };
-  auto load = [&](unsigned tile) {
-    const uint4* src = reinterpret_cast<const uint4*>(keys + tile * (unsigned)RS_TILE);
 #pragma unroll
-    for (int r = 0; r < R; ++r) k[r] = __ldcs(src + tid + r * RS_THREADS);
-  };
-  if (full(t0)) load(t0);
+  for (int q = 0; q < TC_TILES; ++q) {
+    if (full(t0 + q)) {
+      const uint4* src = reinterpret_cast<const uint4*>(keys + (t0 + q) * (unsigned)RS_TILE);
+#pragma unroll
+      for (int r = 0; r < R; ++r) k[q][r] = __ldcs(src + tid + r * RS_THREADS);
+    }
+  }
+#pragma unroll
   for (int q = 0; q < TC_TILES; ++q) {
     const unsigned tile = t0 + q;
     if (tile >= ntiles) break;
     if (full(tile)) {
-      uint4 cur[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) cur[r] = k[r];
-      if (q + 1 < TC_TILES && full(tile + 1)) load(tile + 1);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        atomicAdd(&h[q][dig(cur[r].x)], 1u);
-        atomicAdd(&h[q][dig(cur[r].y)], 1u);
-        atomicAdd(&h[q][dig(cur[r].z)], 1u);
-        atomicAdd(&h[q][dig(cur[r].w)], 1u);
+        atomicAdd(&h[q][dig(k[q][r].x)], 1u);
+        atomicAdd(&h[q][dig(k[q][r].y)], 1u);
+        atomicAdd(&h[q][dig(k[q][r].z)], 1u);
+        atomicAdd(&h[q][dig(k[q][r].w)], 1u);
       }
     } else {
       const unsigned tbase = tile * (unsigned)RS_TILE;
@@ -1298,9 +1298,10 @@ k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pr
   if (PRESORT > 0 && kPresortFits) {
     // the tile in element (generation) order: keys in the dead slots, values in the cache
     unsigned* skey = reinterpret_cast<unsigned*>(sm.slot);
-    unsigned* sval = sm.oc.lo_cell;
-    auto* whist = reinterpret_cast<unsigned short(*)[kMaxBins]>(sm.oc.lo_cell + RS_TILE);
-    unsigned* wsum = sm.oc.lo_cell + RS_TILE + RS_WARPS * kMaxBins / 2;
+    unsigned* ocw = reinterpret_cast<unsigned*>(&sm.oc);  // the whole object cache as words
+    unsigned* sval = ocw;
+    auto* whist = reinterpret_cast<unsigned short(*)[kMaxBins]>(ocw + RS_TILE);
+    unsigned* wsum = ocw + RS_TILE + RS_WARPS * kMaxBins / 2;
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < RS_ITEMS / 4; ++q) {
