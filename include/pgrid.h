@@ -158,6 +158,20 @@ int pg_radix_sort_pairs(pg_builder *b, const uint32_t *keys, const uint32_t *val
  *   pg_sort_cells -- the Alg. 1 tail over arbitrary pairs with keys in [0, ncells): stable
  *                    radix sort + RLE/scatter/scan into G[ncells+1], O[n]
  *                    (builders.py:120-141) */
+/* Fused partition + exchange (the "dispatch" all-to-all of the sharded build done by the
+ * scatter itself): pg_partition_counts runs the slab upsweep (per-tile slab counts kept in the
+ * builder; slab_counts as in pg_partition), then, once the ranks have exchanged their counts,
+ * pg_partition_send scatters every pair straight into its slab owner's receive buffer:
+ * dst_keys[s] / dst_vals[s] are device pointers (peer memory mapped into this process, e.g.
+ * symmetric memory over NVLink) and dst_offset[s] this rank's element offset in slab s's
+ * buffer; all three are host arrays of nslabs entries. Same pair order as pg_partition +
+ * all-to-all; the caller synchronises the ranks before the receivers read. */
+int pg_partition_counts(pg_builder *b, const uint32_t *keys, int64_t n, const uint32_t *slab_of_bucket,
+                        int bucket_shift, int nslabs, uint32_t *slab_counts, void *stream);
+int pg_partition_send(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int64_t n,
+                      const uint32_t *slab_of_bucket, int bucket_shift, int nslabs, const uint32_t *slab_base,
+                      const uint64_t *dst_keys, const uint64_t *dst_vals, const uint64_t *dst_offset,
+                      void *stream);
 int pg_pairs(pg_builder *b, uint32_t *keys, uint32_t *vals, uint32_t val_offset, int coarse_shift,
              int coarse_bins, uint32_t *coarse_hist, void *stream);
 int pg_partition(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int64_t n,

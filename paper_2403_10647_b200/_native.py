@@ -35,7 +35,7 @@ NPHASES = 6
 # every symbol include/pgrid.h declares (checked by tests/test_boundary.py)
 EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
            "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_finish_baseline",
-           "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_build_async",
+           "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_partition_counts", "pg_partition_send", "pg_build_async",
            "pg_build_wait", "pg_host_register",
            "pg_host_unregister", "pg_host_alloc", "pg_host_free", "pg_last_launch_count",
            "pg_last_error")
@@ -93,6 +93,9 @@ def load():
         lib.pg_dda_cast.argtypes = [vp, vp, vp, i64, ctypes.POINTER(PgSpec), vp, vp, vp, i64, vp, vp, u32, vp]
         lib.pg_kernel_times.argtypes = [ctypes.c_char_p, ctypes.c_int]
         lib.pg_wait.argtypes = [vp]
+        lib.pg_partition_counts.argtypes = [vp, vp, i64, vp, ctypes.c_int, ctypes.c_int, vp, vp]
+        lib.pg_partition_send.argtypes = [vp, vp, vp, i64, vp, ctypes.c_int, ctypes.c_int, vp,
+                                          ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64), vp]
         lib.pg_kernel_timing.argtypes = [ctypes.c_int]
         lib.pg_load_obj.argtypes = [vp, vp, u64, u32, vp, ctypes.POINTER(i64)]
         lib.pg_obj_fetch.argtypes = [vp, vp, vp, u32, vp]
@@ -109,7 +112,7 @@ def load():
         lib.pg_last_error.restype = ctypes.c_char_p
         for name in ("pg_builder_create", "pg_count", "pg_finish", "pg_stage",
                      "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells",
-                     "pg_finish_baseline", "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
+                     "pg_finish_baseline", "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_partition_counts", "pg_partition_send", "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
                      "pg_last_launch_count"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
@@ -258,6 +261,18 @@ class Builder:
         check(self._lib.pg_partition(self._h, ptr(keys), ptr(vals), int(n), ptr(slab_of_bucket),
                                      int(bucket_shift), int(nslabs), ptr(slab_base), ptr(keys_out),
                                      ptr(vals_out), ptr(slab_counts), stream))
+
+    def partition_counts(self, keys, n, table, shift, nslabs, slab_counts, stream=None):
+        check(self._lib.pg_partition_counts(self._h, ptr(keys), int(n), ptr(table), int(shift), int(nslabs),
+                                            ptr(slab_counts), stream))
+
+    def partition_send(self, keys, vals, n, table, shift, nslabs, base, dst_keys, dst_vals, dst_offset,
+                       stream=None):
+        arr = ctypes.c_uint64 * len(dst_keys)
+        check(self._lib.pg_partition_send(self._h, ptr(keys), ptr(vals), int(n), ptr(table), int(shift),
+                                          int(nslabs), ptr(base), arr(*[int(x) for x in dst_keys]),
+                                          arr(*[int(x) for x in dst_vals]), arr(*[int(x) for x in dst_offset]),
+                                          stream))
 
     def sort_cells(self, keys, vals, n, ncells, G, O, stream=None):
         check(self._lib.pg_sort_cells(self._h, ptr(keys), ptr(vals), int(n), int(ncells), ptr(G),

@@ -272,6 +272,9 @@ struct pg_builder {
   // OBJ ingestion (pg_load_obj / pg_obj_fetch)
   DevBuf obj_bytes, obj_lines, obj_info, obj_pre, obj_scan, obj_v, obj_t;
   int64_t obj_nv = -1, obj_nt = 0;
+  // pg_partition_counts -> pg_partition_send
+  int64_t part_n = -1;
+  int part_bits = 0;
 };
 
 extern "C" {
@@ -292,6 +295,8 @@ int pg_builder_create(int device, pg_builder** out) {
   CU(set_scatter_smem<1>()); CU(set_scatter_smem<2>()); CU(set_scatter_smem<3>());
   CU(set_scatter_smem<4>()); CU(set_scatter_smem<5>()); CU(set_scatter_smem<6>());
   CU(set_scatter_smem<7>()); CU(set_scatter_smem<8>()); CU(set_scatter_smem<9>());
+  for (auto f : {k_partition_send<1>, k_partition_send<2>, k_partition_send<3>, k_partition_send<4>})
+    CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem_bytes()));
   *out = b;
   return PG_OK;
 }
@@ -1404,6 +1409,74 @@ int pg_obj_fetch(pg_builder* b, double* V, int32_t* T, uint32_t flags, void* str
   if (b->obj_nv) CU(cudaMemcpyAsync(V, b->obj_v.p, (size_t)b->obj_nv * 24, k, st));
   if (b->obj_nt) CU(cudaMemcpyAsync(T, b->obj_t.p, (size_t)b->obj_nt * 12, k, st));
   CU(cudaStreamSynchronize(st));
+  return PG_OK;
+}
+
+int pg_partition_counts(pg_builder* b, const uint32_t* keys, int64_t n, const uint32_t* slab_of_bucket,
+                        int bucket_shift, int nslabs, uint32_t* slab_counts, void* stream_) {
+  if (!b) return fail(PG_INVARIANT_ERROR, "null builder");
+  if (nslabs < 1 || nslabs > 16) return fail(PG_INVARIANT_ERROR, "nslabs must be in [1, 16]");
+  if (n < 0 || n > kMaxScan) return fail(PG_SIZE_ERROR, "partition of %lld pairs exceeds the size limit", (long long)n);
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  drop_graph(b);
+  b->part_n = -1;
+  const int bits = std::max(1, bit_length((uint64_t)(nslabs - 1)));
+  if (n == 0) {
+    CU(cudaMemsetAsync(slab_counts, 0, (size_t)(1 << bits) * 4, st));
+    b->part_n = 0;
+    b->part_bits = bits;
+    return PG_OK;
+  }
+  const unsigned ntiles = (unsigned)((n + RS_TILE - 1) / RS_TILE);
+  const unsigned ld = (ntiles + 3) & ~3u;
+  int rc;
+  if ((rc = b->sort_sync.ensure((size_t)ld * kMaxBins * 4))) return rc;
+  unsigned* counts = b->sort_sync.as<unsigned>(0);
+  const DigitFn dig{bucket_shift, 0u, slab_of_bucket};
+  const Count cn{nullptr, (unsigned)n};
+  k_tile_counts<<<(ntiles + TC_TILES - 1) / TC_TILES, RS_THREADS, 0, st>>>(keys, cn, dig, 1 << bits, counts, ld);
+  LAUNCHED("k_tile_counts", st);
+  k_scan_tile_counts<<<1u << bits, SC_THREADS, 0, st>>>(counts, cn, ld, slab_counts);
+  LAUNCHED("k_scan_tile_counts", st);
+  b->launches = 2;
+  b->part_n = n;
+  b->part_bits = bits;
+  return PG_OK;
+}
+
+int pg_partition_send(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int64_t n,
+                      const uint32_t* slab_of_bucket, int bucket_shift, int nslabs, const uint32_t* slab_base,
+                      const uint64_t* dst_keys, const uint64_t* dst_vals, const uint64_t* dst_offset, void* stream_) {
+  if (!b || !dst_keys || !dst_vals || !dst_offset) return fail(PG_INVARIANT_ERROR, "null argument");
+  if (b->part_n != n) return fail(PG_STATE_ERROR, "pg_partition_send without pg_partition_counts on these pairs");
+  if (nslabs < 1 || nslabs > 16) return fail(PG_INVARIANT_ERROR, "nslabs must be in [1, 16]");
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  if (n == 0) return PG_OK;
+  P2PDst dst{};
+  for (int s = 0; s < nslabs; ++s) {
+    dst.k[s] = reinterpret_cast<unsigned*>(dst_keys[s]);
+    dst.v[s] = reinterpret_cast<unsigned*>(dst_vals[s]);
+    dst.off[s] = dst_offset[s];
+    if (dst_offset[s] >= (1ull << 32)) return fail(PG_SIZE_ERROR, "receive offset exceeds 32 bits");
+  }
+  const unsigned ntiles = (unsigned)((n + RS_TILE - 1) / RS_TILE);
+  const unsigned ld = (ntiles + 3) & ~3u;
+  const unsigned* counts = b->sort_sync.as<unsigned>(0);
+  const Count cn{nullptr, (unsigned)n};
+  switch (b->part_bits) {
+#define PG_CASE(B)                                                                                          \
+  case B:                                                                                                   \
+    k_partition_send<B><<<ntiles, RS_THREADS, rs_smem_bytes(), st>>>(keys, vals, cn, bucket_shift, counts, ld, \
+                                                                     slab_of_bucket, slab_base, dst);       \
+    break;
+    PG_CASE(1) PG_CASE(2) PG_CASE(3) PG_CASE(4)
+#undef PG_CASE
+    default: return fail(PG_INVARIANT_ERROR, "bad slab digit width");
+  }
+  LAUNCHED("k_partition_send", st);
+  b->launches = 1;
   return PG_OK;
 }
 

@@ -981,7 +981,17 @@ k_scan_tile_counts(unsigned* __restrict__ counts, Count cno, unsigned ld, unsign
 // Values never occupy registers: cp.async stages them in input order and they are
 // permuted shared->shared after the keys have been written. BITS and FULL are compile-time
 // so the ranking loop is branch-free and full tiles carry no bounds predicates.
-template <int BITS, bool FULL, bool TABLE = false, bool SRC_SMEM = false>
+// Fused partition + exchange (sharded build): the destination of slab s is rank s's receive
+// buffer -- a peer GPU's memory mapped into this process (symmetric memory / IPC) -- at
+// element offset off[s] (this rank's place among the senders to slab s).
+constexpr int kMaxP2P = 16;
+struct P2PDst {
+  unsigned* k[kMaxP2P];
+  unsigned* v[kMaxP2P];
+  unsigned long long off[kMaxP2P];
+};
+
+template <int BITS, bool FULL, bool TABLE = false, bool SRC_SMEM = false, bool P2P = false>
 __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* __restrict__ keys_in,
                                                    const unsigned* __restrict__ vals_in,
                                                    unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out,
@@ -989,9 +999,11 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
                                                    int shift, const unsigned* __restrict__ hist,
                                                    const unsigned* __restrict__ offs,
                                                    const unsigned* __restrict__ dtable = nullptr,
-                                                   const unsigned* __restrict__ kbase = nullptr) {
+                                                   const unsigned* __restrict__ kbase = nullptr,
+                                                   const P2PDst* __restrict__ p2p = nullptr) {
   constexpr int NB = 1 << BITS;
   constexpr unsigned DMASK = (unsigned)NB - 1u;
+  static_assert(!P2P || (TABLE && NB <= kMaxP2P), "peer scatter: slab digits only");
   // digit of a key: bit field, or slab id = dtable[key >> shift] (keys then leave rebased
   // by kbase[slab], i.e. relative to their slab's first cell)
   auto digit = [&](unsigned k) -> unsigned { return TABLE ? __ldg(&dtable[k >> shift]) : (k >> shift) & DMASK; };
@@ -1060,7 +1072,7 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
       }
     }
     tc[q] = run;
-    hs[q] = d < NB ? __ldg(&hist[d]) : 0u;
+    hs[q] = (!P2P && d < NB) ? __ldg(&hist[d]) : 0u;
     tsum += run;
     hsum += hs[q];
   }
@@ -1074,7 +1086,8 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
       // fold the tile-local digit start into every warp's offset: one lookup per item below
 #pragma unroll
       for (int w = 0; w < RS_WARPS; ++w) sm.whist[w][d] = (unsigned short)(sm.whist[w][d] + lpre);
-      sm.gbase[d] = hpre + __ldg(&offs[(size_t)d * ld + tile]) - lpre;
+      // P2P: positions inside slab d's receive buffer (32-bit: a receive buffer < 2^32 pairs)
+      sm.gbase[d] = (P2P ? (unsigned)p2p->off[d] : hpre) + __ldg(&offs[(size_t)d * ld + tile]) - lpre;
     }
     lpre += tc[q];
     hpre += hs[q];
@@ -1125,6 +1138,7 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
   }
   __syncthreads();
   unsigned gpos[RS_ITEMS];
+  unsigned dpk[P2P ? (RS_ITEMS + 7) / 8 : 1] = {};  // P2P: the items' slabs, 4 bits each
 #pragma unroll
   for (int r = 0; r < RS_ITEMS; ++r) {
     const unsigned i = tid + r * RS_THREADS;
@@ -1133,7 +1147,12 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
       const unsigned k = sm.buf[i];
       const unsigned d = digit(k);
       gpos[r] = sm.gbase[d] + i;
-      if (keys_out) keys_out[gpos[r]] = TABLE ? k - __ldg(&kbase[d]) : k;
+      if (P2P) {
+        dpk[r / 8] |= d << (4 * (r % 8));
+        p2p->k[d][gpos[r]] = k - __ldg(&kbase[d]);
+      } else if (keys_out) {
+        keys_out[gpos[r]] = TABLE ? k - __ldg(&kbase[d]) : k;
+      }
     }
   }
   if (!SRC_SMEM) cp_async_wait();
@@ -1146,7 +1165,10 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
 #pragma unroll
   for (int r = 0; r < RS_ITEMS; ++r) {
     const unsigned i = tid + r * RS_THREADS;
-    if (FULL || i < tvalid) vals_out[gpos[r]] = sm.buf[i];
+    if (FULL || i < tvalid) {
+      if (P2P) p2p->v[(dpk[r / 8] >> (4 * (r % 8))) & 15u][gpos[r]] = sm.buf[i];
+      else vals_out[gpos[r]] = sm.buf[i];
+    }
   }
 }
 
@@ -1171,6 +1193,27 @@ k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict
   else
     radix_scatter_tile<BITS, false, TABLE>(sm, keys_in, vals_in, keys_out, vals_out, tbase, tvalid, tile, ld, shift,
                                            hist, offs, dtable, kbase);
+}
+
+// Stable partition by slab whose writes land directly in the slab owners' receive buffers.
+template <int BITS>
+__global__ void __launch_bounds__(RS_THREADS, RS_MIN_CTAS)
+k_partition_send(const unsigned* __restrict__ keys_in, const unsigned* __restrict__ vals_in, Count cno, int shift,
+                 const unsigned* __restrict__ offs, unsigned ld, const unsigned* __restrict__ dtable,
+                 const unsigned* __restrict__ kbase, const P2PDst dst) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  RsSmem& sm = *reinterpret_cast<RsSmem*>(smem_raw);
+  const unsigned no = cno.get();
+  const unsigned tile = blockIdx.x;
+  const unsigned tbase = tile * (unsigned)RS_TILE;
+  if (tbase >= no) return;
+  const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
+  if (tvalid == (unsigned)RS_TILE)
+    radix_scatter_tile<BITS, true, true, false, true>(sm, keys_in, vals_in, nullptr, nullptr, tbase, tvalid, tile, ld,
+                                                      shift, nullptr, offs, dtable, kbase, &dst);
+  else
+    radix_scatter_tile<BITS, false, true, false, true>(sm, keys_in, vals_in, nullptr, nullptr, tbase, tvalid, tile, ld,
+                                                       shift, nullptr, offs, dtable, kbase, &dst);
 }
 
 // ----------------------------------------------------------------------------------------

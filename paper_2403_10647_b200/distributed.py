@@ -110,6 +110,22 @@ class ShardState:
         self.send_counts = counts
         return counts
 
+    def phase_partition_counts(self, plan):
+        """Fused exchange, step 1: the slab upsweep only; returns the per-slab send counts."""
+        self.plan = plan
+        self.send_counts = self.ops.partition_counts(self.keys, plan.table, plan.shift, self.world)
+        return self.send_counts
+
+    def phase_send(self, matrix, dst_keys, dst_vals):
+        """Fused exchange, step 2: scatter every pair into its slab owner's receive buffer.
+        matrix[r][s] = pairs rank r sends to slab s; this rank writes after the lower ranks."""
+        m = np.asarray(matrix, dtype=np.int64)
+        off = [int(m[:self.rank, s].sum()) for s in range(self.world)]
+        base = self.plan.cell_lo.astype(np.uint32)
+        self.ops.partition_send(self.keys, self.vals, self.plan.table, self.plan.shift, self.world, base,
+                                dst_keys, dst_vals, off)
+        return int(m[:, self.rank].sum())
+
     def phase_sort(self, krecv, vrecv):
         """Local stable sort of the received slab + its G (relative), O."""
         lo, hi = int(self.plan.cell_lo[self.rank]), int(self.plan.cell_hi[self.rank])
@@ -120,9 +136,11 @@ class ShardState:
         return int(self.plan.pair_base[self.rank]), G, O
 
 
-def build_sharded(ops, comm, V, T, tri_base, spec, gather=True):
+def build_sharded(ops, comm, V, T, tri_base, spec, gather=True, exchange=None):
     """One rank's part of the sharded build (run on every rank of `comm`).
 
+    exchange: a PeerExchange (fused partition + send into the slab owners' receive buffers,
+    peer memory over NVLink) or None (partition pass, then NCCL all-to-all).
     Returns (G, O) on rank 0 when gather=True (None elsewhere); with gather=False each rank
     returns its slab as (cell_lo, cell_hi, pair_base, G_rel, O) with G_rel/O left where the
     ops keep them (device memory for CudaOps)."""
@@ -132,8 +150,16 @@ def build_sharded(ops, comm, V, T, tri_base, spec, gather=True):
     st = ShardState(ops, V, T, tri_base, spec, rank, world)
     hist = comm.allreduce_sum(st.phase_count())
     plan = plan_slabs(hist, st.ncells, world)
-    send, recv = comm.alltoall_counts(st.phase_partition(plan))
-    krecv, vrecv = comm.alltoall_pairs(st.kout, st.vout, send, recv, ops)
+    if exchange is not None:
+        matrix = exchange.allgather_counts(st.phase_partition_counts(plan))
+        exchange.ensure(int(np.asarray(matrix, dtype=np.int64).sum(axis=0).max()))
+        dk, dv = exchange.destinations()
+        nrecv = st.phase_send(matrix, dk, dv)
+        exchange.barrier()
+        krecv, vrecv = exchange.received(nrecv)
+    else:
+        send, recv = comm.alltoall_counts(st.phase_partition(plan))
+        krecv, vrecv = comm.alltoall_pairs(st.kout, st.vout, send, recv, ops)
     base, G_rel, O = st.phase_sort(krecv, vrecv)
     if not gather:
         return int(plan.cell_lo[rank]), int(plan.cell_hi[rank]), base, G_rel, O
@@ -192,7 +218,72 @@ class TorchComm:
         return out
 
 
-def run_emulated(make_ops, V, T, spec, world):
+class PeerExchange:
+    """Receive buffers in symmetric memory (torch.distributed._symmetric_memory: every rank maps
+    every other rank's buffer), so pg_partition_send writes pairs straight into the slab
+    owner's GPU over NVLink -- the dispatch all-to-all fused into the partition kernel.
+    Buffers grow collectively (every rank sees the same count matrix, so they agree on the
+    capacity)."""
+
+    def __init__(self, comm, device):
+        import torch
+        import torch.distributed._symmetric_memory as symm
+        self.torch, self.symm, self.comm, self.dev = torch, symm, comm, device
+        self.cap = 0
+        self.buf = self.hdl = None
+        self.ensure(1 << 20)
+
+    def allgather_counts(self, counts):
+        """counts: this rank's per-slab send counts (device) -> host matrix [rank][slab]."""
+        torch = self.torch
+        w = self.comm.world
+        c = counts[:w].to(torch.int64) if isinstance(counts, torch.Tensor) else torch.as_tensor(counts[:w])
+        out = torch.empty(w * w, dtype=torch.int64, device=c.device)
+        self.comm.dist.all_gather_into_tensor(out, c.contiguous(), group=self.comm.group)
+        return out.view(w, w).cpu().numpy()
+
+    def ensure(self, n):
+        if n <= self.cap:
+            return
+        cap = int(n * 1.25) + 1024
+        group = self.comm.group or self.comm.dist.group.WORLD
+        self.buf = self.symm.empty(2 * cap, dtype=self.torch.int32, device=self.dev)
+        self.hdl = self.symm.rendezvous(self.buf, group)
+        self.cap = cap
+        self.ptrs = [int(p) for p in self.hdl.buffer_ptrs]
+
+    def destinations(self):
+        return list(self.ptrs), [p + 4 * self.cap for p in self.ptrs]
+
+    def barrier(self):
+        self.hdl.barrier()
+
+    def received(self, n):
+        return self.buf[:n], self.buf[self.cap:self.cap + n]
+
+
+class EmulatedExchange:
+    """PeerExchange for run_emulated: every virtual rank's receive buffer lives on this device."""
+
+    def __init__(self, torch, device, world):
+        self.torch, self.dev, self.world = torch, device, world
+        self.cap = 0
+
+    def ensure(self, n):
+        if n > self.cap:
+            self.cap = int(n * 1.25) + 1024
+            self.bufs = [self.torch.empty(2 * self.cap, dtype=self.torch.int32, device=self.dev)
+                         for _ in range(self.world)]
+
+    def destinations(self):
+        ptrs = [int(b.data_ptr()) for b in self.bufs]
+        return ptrs, [p + 4 * self.cap for p in ptrs]
+
+    def received(self, r, n):
+        return self.bufs[r][:n], self.bufs[r][self.cap:self.cap + n]
+
+
+def run_emulated(make_ops, V, T, spec, world, exchange="copy"):
     """Every rank's phases executed in sequence in one process (no inter-rank waiting):
     exercises the kernels and the orchestration of the sharded build on a single device."""
     n = len(T)
@@ -202,6 +293,18 @@ def run_emulated(make_ops, V, T, spec, world):
         states.append(ShardState(make_ops(), V, T[lo:hi], lo, spec, r, world))
     hist = np.sum([s.ops.to_numpy(s.phase_count()).astype(np.int64) for s in states], axis=0)
     plan = plan_slabs(hist, states[0].ncells, world)
+    if exchange == "p2p":       # fused partition + send into the owners' buffers (CudaOps only)
+        matrix = np.array([s.ops.to_numpy(s.phase_partition_counts(plan))[:world] for s in states], np.int64)
+        ex = EmulatedExchange(states[0].ops.torch, states[0].ops.dev, world)
+        ex.ensure(int(matrix.sum(axis=0).max()))
+        dk, dv = ex.destinations()
+        nrecv = [s.phase_send(matrix, dk, dv) for s in states]
+        states[0].ops.torch.cuda.synchronize()
+        slabs = []
+        for r, s in enumerate(states):
+            base, G_rel, O = s.phase_sort(*ex.received(r, nrecv[r]))
+            slabs.append((base, s.ops.to_numpy(G_rel), s.ops.to_numpy(O)))
+        return assemble(slabs, states[0].ncells)
     sends = [[int(x) for x in s.ops.to_numpy(s.phase_partition(plan))[:world]] for s in states]
     slabs = []
     for r, s in enumerate(states):
@@ -300,6 +403,21 @@ class CudaOps:
         counts = self._buf("slab_counts", 16)
         self.b.partition(keys, vals, n, dt, shift, nslabs, db, ko, vo, counts, self._sp())
         return ko, vo, counts
+
+    def partition_counts(self, keys, table, shift, nslabs):
+        torch = self.torch
+        n = int(keys.numel())
+        self._ptab = torch.from_numpy(np.asarray(table, np.uint32).view(np.int32)).to(self.dev)
+        counts = self._buf("slab_counts", 16)
+        self.b.partition_counts(keys, n, self._ptab, shift, nslabs, counts, self._sp())
+        return counts
+
+    def partition_send(self, keys, vals, table, shift, nslabs, base, dst_keys, dst_vals, dst_offset):
+        torch = self.torch
+        n = int(keys.numel())
+        self._pbase = torch.from_numpy(np.asarray(base, np.uint32).view(np.int32)).to(self.dev)
+        self.b.partition_send(keys, vals, n, self._ptab, shift, nslabs, self._pbase, dst_keys, dst_vals,
+                              dst_offset, self._sp())
 
     def sort_cells(self, keys, vals, n, ncells):
         G = self._buf("G", ncells + 1)
