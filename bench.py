@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-budget-s", type=float, default=150.0)
     ap.add_argument("--sharded", action="store_true", help="use the sharded path even at N=1 (testing)")
+    ap.add_argument("--nccl-exchange", action="store_true", help="sharded: partition pass + NCCL all_to_all")
     return ap.parse_args()
 
 
@@ -230,9 +231,24 @@ def run_sharded(args, world, rank, local):
     Td = torch.from_numpy(shard.triangles.copy()).to(dev)
     ops = D.CudaOps(local)
     comm = D.TorchComm(device=dev)
+    # the pair exchange: fused into the partition kernel (peer stores into the slab owners'
+    # symmetric-memory receive buffers) when symmetric memory comes up on every rank, else a
+    # partition pass + NCCL all_to_all; every rank must agree, so the choice is all-reduced
+    ex, why = None, ""
+    if not args.nccl_exchange:
+        try:
+            ex = D.PeerExchange(comm, dev)
+        except Exception as e:          # noqa: BLE001 -- reported in the JSON line
+            why = f"{type(e).__name__}: {e}"[:200]
+    ok = torch.tensor([1 if ex is not None else 0], device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if int(ok.item()) == 0:
+        ex = None
+    exchange_desc = ("fused partition + peer stores (symmetric memory)" if ex is not None
+                     else "partition pass + NCCL all_to_all" + (f" ({why})" if why else ""))
 
     def step():
-        return D.build_sharded(ops, comm, Vd, Td, lo, spec, gather=False)
+        return D.build_sharded(ops, comm, Vd, Td, lo, spec, gather=False, exchange=ex)
 
     res = step()
     launches = ops.b.launches()
@@ -264,7 +280,7 @@ def run_sharded(args, world, rank, local):
     for _ in range(args.e2e_steps or min(args.steps, 5)):
         dist.barrier()
         t0 = time.perf_counter()
-        r = D.build_sharded(ops, comm, Vh, Th, lo, spec, gather=False)
+        r = D.build_sharded(ops, comm, Vh, Th, lo, spec, gather=False, exchange=ex)
         g_host, o_host = ops.to_numpy(r[3]), ops.to_numpy(r[4])     # this rank's slab, D2H
         t = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -281,7 +297,8 @@ def run_sharded(args, world, rank, local):
         "data": "synthetic",
         "config": {"workload": f"{args.config} x{world} (sharded)", "scene": kind, "triangles": n,
                    "triangles_per_gpu": n1, "dims": list(spec.dims), "ncells": spec.ncells, "no": no,
-                   "parallelism": f"triangle shards x{world} -> cell slabs, NCCL all-to-all",
+                   "parallelism": f"triangle shards x{world} -> cell slabs",
+                   "exchange": exchange_desc,
                    "output": "distributed (each rank its G/O slab)",
                    "value_def": f"{world} x builds/s of the {world} x {n1 // 1_000_000}M-triangle scene",
                    "scene_builds_per_s": round(1e3 / ms, 3),

@@ -245,7 +245,7 @@ class PeerExchange:
     def ensure(self, n):
         if n <= self.cap:
             return
-        cap = int(n * 1.25) + 1024
+        cap = (int(n * 1.25) + 1024 + 63) & ~63     # value half 256-byte aligned (vector loads)
         group = self.comm.group or self.comm.dist.group.WORLD
         self.buf = self.symm.empty(2 * cap, dtype=self.torch.int32, device=self.dev)
         self.hdl = self.symm.rendezvous(self.buf, group)
@@ -271,7 +271,7 @@ class EmulatedExchange:
 
     def ensure(self, n):
         if n > self.cap:
-            self.cap = int(n * 1.25) + 1024
+            self.cap = (int(n * 1.25) + 1024 + 63) & ~63
             self.bufs = [self.torch.empty(2 * self.cap, dtype=self.torch.int32, device=self.dev)
                          for _ in range(self.world)]
 

@@ -13,6 +13,8 @@ shard = scenes.gen_arch_shard(n, 7, 4.0, 0, n)
 spec = gridcore.spec_from_bounds(shard.vertices.min(0), shard.vertices.max(0), n, density=4.0)
 Vd = torch.from_numpy(shard.vertices.copy()).cuda(); Td = torch.from_numpy(shard.triangles.copy()).cuda()
 ops = D.CudaOps(0); comm = D.TorchComm(device=torch.device("cuda", 0))
+P2P = "--p2p" in sys.argv
+ex = D.PeerExchange(comm, torch.device("cuda", 0)) if P2P else None
 T = {}
 E = {}
 def tick(name, t0):
@@ -29,9 +31,15 @@ for it in range(6):
     st.keys, st.vals, h = ops.pairs(st.no, 0, st.shift, nb); t = tick("pairs+hist", t)
     h = comm.allreduce_sum(h); t = tick("allreduce", t)
     plan = D.plan_slabs(h, st.ncells, 1); t = tick("plan", t)
-    sc = st.phase_partition(plan); t = tick("partition", t)
-    send, recv = comm.alltoall_counts(sc); t = tick("a2a_counts", t)
-    kr, vr = comm.alltoall_pairs(st.kout, st.vout, send, recv, ops); t = tick("a2a_pairs", t)
+    if P2P:
+        c = st.phase_partition_counts(plan); t = tick("part_counts", t)
+        m = ex.allgather_counts(c); ex.ensure(int(m.sum(axis=0).max())); t = tick("allgather", t)
+        dk, dv = ex.destinations(); nr = st.phase_send(m, dk, dv); t = tick("send", t)
+        ex.barrier(); kr, vr = ex.received(nr); t = tick("barrier", t)
+    else:
+        sc = st.phase_partition(plan); t = tick("partition", t)
+        send, recv = comm.alltoall_counts(sc); t = tick("a2a_counts", t)
+        kr, vr = comm.alltoall_pairs(st.kout, st.vout, send, recv, ops); t = tick("a2a_pairs", t)
     r = st.phase_sort(kr, vr); t = tick("sort_cells", t)
 torch.cuda.synchronize()
 names = list(T)
