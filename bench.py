@@ -272,6 +272,26 @@ def run_sharded(args, world, rank, local):
     dist.all_reduce(no_t)
     no = int(no_t.item())
 
+    # per-kernel device times of one step on this rank (events after every launch)
+    _native.kernel_timing(True)
+    step()
+    torch.cuda.synchronize()
+    kt = {}
+    for name, us in _native.kernel_times():
+        if not name.startswith("("):
+            kt.setdefault(name, []).append(us * 1e-3)
+    _native.kernel_timing(False)
+    peak, peak_kind = peaks()
+    sc = kt.get("k_radix_scatter", [])
+    sc_ms = float(np.mean(sc)) if sc else 0.0
+    sc_bytes = 16 * no_local
+    roofline = {"bound": "hbm", "kernel": "k_radix_scatter (slab sort, rank 0)",
+                "achieved": round(sc_bytes / (sc_ms * 1e-3) / 1e9, 1) if sc_ms else None, "peak": peak,
+                "unit": "GB/s", "frac": round(sc_bytes / (sc_ms * 1e-3) / 1e9 / peak, 4) if sc_ms else None,
+                "traffic": traffic_table().get("k_radix_scatter"), "alg_bytes_per_launch": sc_bytes,
+                "launch_ms": round(sc_ms, 4), "peak_kind": peak_kind}
+    kernels = {k: {"ms_per_launch": round(float(np.mean(v)), 4), "launches": len(v)} for k, v in kt.items()}
+
     # e2e: pinned host shard in, H2D + sharded build + D2H of this rank's G/O slab out
     Vh, Th = shard.vertices.copy(), shard.triangles.copy()
     _native.host_register(Vh)
@@ -304,6 +324,8 @@ def run_sharded(args, world, rank, local):
                    "scene_builds_per_s": round(1e3 / ms, 3),
                    "parity": "orchestration verified by tests/test_distributed.py + test_gpu_distributed.py"},
         "mpairs_per_s": round(no / (ms * 1e-3) / 1e6, 2),
+        "roofline": roofline,
+        "kernels_rank0": kernels,
         "e2e": {"value": round(world / e2e_sec, 3), "unit": "builds/s",
                 "h2d_bytes_per_step": int((Vh.nbytes + Th.nbytes) * world),
                 "d2h_bytes_per_step": int(out_bytes.item()), "ms_per_step": round(e2e_sec * 1e3, 2)},
