@@ -23,6 +23,10 @@ class OracleSizeError(Exception):
     """The oracle reproduced the reference's SizeError condition."""
 
 
+class OracleInvariantError(Exception):
+    """The oracle reproduced the reference's InvariantError condition (an inverted box)."""
+
+
 class _Spec(ctypes.Structure):
     _fields_ = [("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3),
                 ("cell", ctypes.c_double * 3), ("dims", ctypes.c_int64 * 3)]
@@ -107,6 +111,8 @@ def build_parallel(vertices, triangles, spec, stages=False):
     rc = lib().orc_count(_ptr(V), _ptr(T), len(T), ctypes.byref(s), ctypes.byref(no))
     if rc == SIZE_ERROR:
         raise OracleSizeError(f"NO={no.value}")
+    if rc == INVARIANT_ERROR:
+        raise OracleInvariantError("triangle cell box with hi < lo")
     if rc:
         raise MemoryError("oracle count failed")
     NO = no.value

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -272,6 +273,10 @@ struct pg_builder {
   // OBJ ingestion (pg_load_obj / pg_obj_fetch)
   DevBuf obj_bytes, obj_lines, obj_info, obj_pre, obj_scan, obj_v, obj_t;
   int64_t obj_nv = -1, obj_nt = 0;
+  // inputs of the last count (for the inverted-box resolution on the error path)
+  const double* last_V = nullptr;
+  const int32_t* last_T = nullptr;
+  DevSpec last_ds{};
   // pg_partition_counts -> pg_partition_send
   int64_t part_n = -1;
   int part_bits = 0;
@@ -384,6 +389,9 @@ int count_enqueue(pg_builder* b, const double* dV, int64_t nv, const int32_t* dT
                   cudaStream_t st) {
   const unsigned ntiles = (unsigned)((n + K1_TILE - 1) / K1_TILE);
   int rc;
+  b->last_V = dV;
+  b->last_T = dT;
+  b->last_ds = ds;
   if ((rc = b->rec.ensure((size_t)n * sizeof(uint4)))) return rc;
   // K1 area: [tile_sum u64 x ntiles][tile_pre u32 x ntiles][err u32][pad][total u64]
   const size_t ts_bytes = align_up((size_t)ntiles * 8), tp_bytes = align_up((size_t)ntiles * 4);
@@ -412,12 +420,42 @@ int count_enqueue(pg_builder* b, const double* dV, int64_t nv, const int32_t* dT
 }
 
 // Error checks on the NO / flags that count_enqueue copied back (stream synchronised).
+// An inverted kept box (hi < lo on some axis after clipping) is what the reference's count
+// phase produces for an infinite or huge upper corner. The reference then accepts it only
+// when it is the one kept triangle and its signed pair count is 0 (an empty grid); a negative
+// count fails exclusive_sum's non-negativity check and any zero-count group among >= 2 kept
+// objects fails mark_boundaries. (A lone triangle with two inverted axes has a positive
+// count and the reference builds cells from the inverted box; that is reported as an
+// error here.)
+int resolve_inverted(pg_builder* b, bool& accept) {
+  accept = false;
+  DevBuf tmp;
+  int rc;
+  if ((rc = tmp.ensure(32))) return rc;
+  long long init[4] = {0, 0, LLONG_MAX, LLONG_MIN};
+  CU(cudaMemcpy(tmp.p, init, 32, cudaMemcpyHostToDevice));
+  k_inverted_boxes<<<(unsigned)((b->n + 255) / 256), 256>>>(b->last_V, b->last_T, b->n, b->last_ds,
+                                                             tmp.as<long long>());
+  CU(cudaGetLastError());
+  long long r[4];
+  CU(cudaMemcpy(r, tmp.p, 32, cudaMemcpyDeviceToHost));
+  tmp.release();
+  accept = r[0] == 1 && r[1] == 1 && r[2] == 0 && r[3] == 0;
+  return PG_OK;
+}
+
 int count_check(pg_builder* b, uint64_t* no_out) {
-  const uint64_t no = b->h_scalars[0];
+  uint64_t no = b->h_scalars[0];
   const unsigned errf = (unsigned)(b->h_scalars[1] & 0xffffffffu);
-  if (no_out) *no_out = no;
   if (errf & 2u) return fail(PG_INVARIANT_ERROR, "triangle index out of range");
-  if (errf & 1u) return fail(PG_INVARIANT_ERROR, "triangle cell box with hi < lo (non-finite or huge upper corner)");
+  if (errf & 1u) {
+    bool accept = false;
+    int rc = resolve_inverted(b, accept);
+    if (rc) return rc;
+    if (!accept) return fail(PG_INVARIANT_ERROR, "triangle cell box with hi < lo (non-finite or huge upper corner)");
+    no = 0;  // the lone kept triangle has no pairs: an empty grid
+  }
+  if (no_out) *no_out = no;
   if ((int64_t)no > kMaxIds)
     return fail(PG_SIZE_ERROR, "%llu cell/object pairs exceed 32-bit id space", (unsigned long long)no);
   if ((int64_t)no > kMaxScan)

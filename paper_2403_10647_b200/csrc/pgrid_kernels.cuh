@@ -171,10 +171,10 @@ struct K1Smem {
 // rows into shared memory with TMA bulk copies on an mbarrier. If every index of the tile
 // is 3*i+k the boxes are computed from shared memory; otherwise (indexed meshes) the
 // vertices are gathered from global memory. Both paths compute the same IEEE f64 values.
-__device__ __forceinline__ void tri_box(const double* a, const double* b, const double* c, const DevSpec& s,
-                                        unsigned dx, unsigned dxy, uint3& box, unsigned& cnt, bool& bad) {
-  bool keep = true;
-  unsigned lo[3], hi[3];
+// gridcore.py:155-167 for one triangle: keep flag and clamped cell box (lo, hi inclusive)
+__device__ __forceinline__ void tri_box_raw(const double* a, const double* b, const double* c, const DevSpec& s,
+                                            unsigned (&lo)[3], unsigned (&hi)[3], bool& keep) {
+  keep = true;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     const double x0 = a[k], x1 = b[k], x2 = c[k];
@@ -188,9 +188,17 @@ __device__ __forceinline__ void tri_box(const double* a, const double* b, const 
     lo[k] = clip_axis(np_floor_i64(__ddiv_rn(__dsub_rn(mn, s.lo[k]), s.cell[k])), s.dims[k]);
     hi[k] = clip_axis(np_floor_i64(__ddiv_rn(__dsub_rn(mx, s.lo[k]), s.cell[k])), s.dims[k]);
   }
+}
+
+__device__ __forceinline__ void tri_box(const double* a, const double* b, const double* c, const DevSpec& s,
+                                        unsigned dx, unsigned dxy, uint3& box, unsigned& cnt, bool& bad) {
+  bool keep;
+  unsigned lo[3], hi[3];
+  tri_box_raw(a, b, c, s, lo, hi, keep);
   if (keep && (hi[0] < lo[0] || hi[1] < lo[1] || hi[2] < lo[2])) {
-    // +inf / >2^63 upper corners cast to INT64_MIN and clip to 0 below lo: the reference
-    // then fails its non-negative / coincident-mark checks (primitives.py:22-25, 71-72).
+    // +inf / >2^63 upper corners cast to INT64_MIN and clip to 0 below lo (an inverted box);
+    // flagged, and resolved on the host path exactly as the reference's checks do
+    // (k_inverted_boxes, primitives.py:22-25, 71-72)
     bad = true;
     keep = false;
   }
@@ -200,6 +208,36 @@ __device__ __forceinline__ void tri_box(const double* a, const double* b, const 
     const unsigned ex = hi[0] - lo[0] + 1, ey = hi[1] - lo[1] + 1, ez = hi[2] - lo[2] + 1;
     box = make_uint3(lo[0] + dx * lo[1] + dxy * lo[2], ex, ey);
     cnt = ex * ey * ez;  // <= ncells <= 2^30
+  }
+}
+
+// Error path of K1 (some kept box is inverted): the reference's verdict depends on how many
+// triangles are kept in total and on the inverted boxes' signed pair counts
+// prod(hi - lo + 1) (builders.py:90-101 -> primitives.py:22-25 exclusive_sum rejects a
+// negative count; mark_boundaries, primitives.py:58-77, rejects any zero-count group when
+// two or more objects are kept). out = {kept, inverted, min count, max count}.
+__global__ void __launch_bounds__(256)
+k_inverted_boxes(const double* __restrict__ V, const int* __restrict__ T, long long n, DevSpec s,
+                 long long* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  bool keep = false, inv = false;
+  long long c = 0;
+  if (i < n) {
+    unsigned lo[3], hi[3];
+    tri_box_raw(V + 3 * (long long)T[3 * i], V + 3 * (long long)T[3 * i + 1], V + 3 * (long long)T[3 * i + 2], s, lo,
+                hi, keep);
+    inv = keep && (hi[0] < lo[0] || hi[1] < lo[1] || hi[2] < lo[2]);
+    if (inv)
+      c = ((long long)hi[0] - lo[0] + 1) * ((long long)hi[1] - lo[1] + 1) * ((long long)hi[2] - lo[2] + 1);
+  }
+  const unsigned kb = __ballot_sync(0xffffffffu, keep), ib = __ballot_sync(0xffffffffu, inv);
+  if ((threadIdx.x & 31) == 0) {
+    if (kb) atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)__popc(kb));
+    if (ib) atomicAdd(reinterpret_cast<unsigned long long*>(out + 1), (unsigned long long)__popc(ib));
+  }
+  if (inv) {
+    atomicMin(out + 2, c);
+    atomicMax(out + 3, c);
   }
 }
 
@@ -1320,8 +1358,11 @@ __device__ __forceinline__ void presort_tile(const unsigned* __restrict__ skey, 
   }
 }
 
+#ifndef K2_MIN_CTAS
+#define K2_MIN_CTAS (1024 / RS_THREADS)
+#endif
 template <int PRESORT>
-__global__ void __launch_bounds__(RS_THREADS, 1024 / RS_THREADS)
+__global__ void __launch_bounds__(RS_THREADS, K2_MIN_CTAS)
 k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno,
              unsigned dx, unsigned dxy, PassPlan plan, const int2* __restrict__ bounds, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
              unsigned* __restrict__ counts0, unsigned ld) {

@@ -1,0 +1,93 @@
+"""Randomised parity campaign on the GPU: many seeded scenes of every kind and size class,
+random grid resolutions and bounds (dropped / clipped triangles, degenerate axes), injected
+NaN / inf / huge coordinates and indexed meshes -- the CUDA build against the C oracle, bit
+for bit, through build_parallel, the comparison builders and the sync-free graph path."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2403_10647_b200 import _native, builders, gen_scene
+from paper_2403_10647_b200.gridcore import Aabb, GridSpec, TriangleMesh
+
+pytestmark = pytest.mark.gpu
+
+
+def random_case(rng):
+    kind = rng.choice(["uniform", "skewed", "walls", "lognormal", "arch", "indexed"])
+    n = int(rng.choice([1, 2, 7, 100, 1000, 4095, 4096, 4097, 20000, 150000]))
+    if kind == "indexed":
+        nv = max(3, n // 2)
+        V = rng.random((nv, 3)) * rng.choice([1.0, 1e-3, 1e4])
+        T = rng.integers(0, nv, (n, 3)).astype(np.int32)
+    else:
+        m = gen_scene(kind, n, int(rng.integers(1, 1 << 30)), float(rng.choice([1.0, 4.0, 20.0])))
+        V, T = m.vertices.copy(), m.triangles.copy()
+    if rng.random() < 0.3:                       # poison a few coordinates
+        idx = rng.integers(0, len(V), max(1, len(V) // 500))
+        V[idx, rng.integers(0, 3, len(idx))] = rng.choice([np.nan, np.inf, -np.inf, 1e300, -1e300], len(idx))
+    lo, hi = np.nanmin(np.where(np.isfinite(V), V, np.nan), 0), np.nanmax(np.where(np.isfinite(V), V, np.nan), 0)
+    lo, hi = np.nan_to_num(lo), np.nan_to_num(hi, nan=1.0)
+    span = np.maximum(hi - lo, 1e-6)
+    if rng.random() < 0.4:                       # a sub-box: many triangles dropped or clipped
+        a = lo + rng.random(3) * 0.5 * span
+        b = a + (0.1 + rng.random(3) * 0.9) * span
+    else:
+        a, b = lo - 0.01 * span, hi + 0.01 * span
+    dims = tuple(int(x) for x in rng.choice([1, 2, 3, 17, 64, 129, 300], 3))
+    if rng.random() < 0.2:
+        dims = (int(rng.integers(1, 5000)), 1, int(rng.integers(1, 50)))
+    return TriangleMesh(V, T), GridSpec(Aabb(a, b), dims)
+
+
+def oracle_or_error(mesh, spec):
+    try:
+        return oracle.build_parallel(mesh.vertices, mesh.triangles, spec)
+    except oracle.OracleSizeError:
+        return None
+    except oracle.OracleInvariantError:
+        return "invariant"
+
+
+@pytest.mark.parametrize("block", range(8))
+def test_fuzz_build_parallel(block):
+    from paper_2403_10647_b200.errors import InvariantError
+    rng = np.random.default_rng(1000 + block)
+    for case in range(25):
+        mesh, spec = random_case(rng)
+        want = oracle_or_error(mesh, spec)
+        if want is None:
+            continue
+        if isinstance(want, str):
+            with pytest.raises(InvariantError):
+                builders.build_parallel(mesh, spec)
+            continue
+        grid, rep = builders.build_parallel(mesh, spec)
+        assert np.array_equal(grid.G, want[0]) and np.array_equal(grid.O, want[1]), (block, case, spec)
+        if case % 5 == 0:
+            for build in (builders.build_sorted, builders.build_compact):
+                g2, _ = build(mesh, spec)
+                assert np.array_equal(g2.G, want[0]) and np.array_equal(g2.O, want[1]), (build.__name__, case)
+
+
+def test_fuzz_graph_path():
+    """The sync-free CUDA-graph build (pg_build_async) on a stream of random scenes."""
+    rng = np.random.default_rng(77)
+    b = _native.Builder(0)
+    st = torch.cuda.current_stream().cuda_stream
+    for case in range(30):
+        mesh, spec = random_case(rng)
+        want = oracle_or_error(mesh, spec)
+        if want is None or isinstance(want, str) or len(mesh.triangles) == 0:
+            continue
+        Vd = torch.from_numpy(mesh.vertices.copy()).cuda()
+        Td = torch.from_numpy(mesh.triangles.copy()).cuda()
+        cap = len(want[1]) + int(rng.integers(0, 1000))
+        Gd = torch.empty(spec.ncells + 1, dtype=torch.int32, device="cuda")
+        Od = torch.empty(max(cap, 1), dtype=torch.int32, device="cuda")
+        for _ in range(2):                       # eager, then graph replay
+            b.build_async(Vd, len(mesh.vertices), Td, len(mesh.triangles), spec, Gd, Od, cap, st)
+            assert b.build_wait() == len(want[1])
+            assert np.array_equal(Gd.cpu().numpy().view(np.uint32), want[0])
+            assert np.array_equal(Od[:len(want[1])].cpu().numpy().view(np.uint32), want[1])

@@ -263,3 +263,19 @@ def test_build_pipeline_matches_build_parallel(kat, hashes):
     with pytest.raises(RuntimeError):
         pipe.submit(*items[2])
     assert pipe.result()[1].no == got[0][1].no and pipe.result()[1].no == got[1][1].no
+
+
+def test_inverted_boxes_match_reference_verdicts():
+    """A lone zero-count inverted box builds an empty grid; any other inverted box raises."""
+    from test_oracle import _inverted_cases
+    for V, T, spec in _inverted_cases():
+        try:
+            want = oracle.build_parallel(V, T, spec)
+        except oracle.OracleInvariantError:
+            want = None
+        if want is None:
+            with pytest.raises(InvariantError):
+                builders.build_parallel(TriangleMesh(V, T), spec)
+        else:
+            grid, rep = builders.build_parallel(TriangleMesh(V, T), spec)
+            assert np.array_equal(grid.G, want[0]) and np.array_equal(grid.O, want[1]) and rep.no == 0

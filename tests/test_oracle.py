@@ -97,3 +97,46 @@ def test_oracle_size_error():
     V = np.array([[-1, -1, -1], [3, -1, 2], [-1, 3, 2]], np.float64)
     with pytest.raises(oracle.OracleSizeError):
         oracle.build_parallel(V, np.array([[0, 1, 2]], np.int32), spec)
+
+
+def _inverted_cases():
+    """Triangles whose clipped box inverts (an infinite upper corner): the reference accepts
+    only a lone zero-count one (empty grid); every other arrangement raises."""
+    from paper_2403_10647_b200.gridcore import Aabb, GridSpec
+    inv1 = [[0.6, 0.1, 0.1], [np.inf, 0.2, 0.1], [0.7, 0.1, 0.2]]          # one inverted axis
+    inv3 = [[0.6, 0.6, 0.6], [np.inf, np.inf, np.inf], [0.7, 0.7, 0.7]]    # negative count at 4^3
+    good = [[0.1, 0.1, 0.1], [0.2, 0.2, 0.2], [0.1, 0.2, 0.1]]
+    far = [[5.0, 5, 5], [6, 5, 5], [5, 6, 5]]                              # dropped
+    cases = []
+    for tris, dims in (([inv1], (2, 2, 2)), ([inv1, far], (2, 2, 2)), ([far, inv1, far], (3, 3, 3)),
+                       ([good, inv1], (2, 2, 2)), ([inv1, good], (2, 2, 2)), ([inv3], (4, 4, 4)),
+                       ([inv1, inv1], (2, 2, 2))):
+        V = np.array([v for t in tris for v in t], float)
+        T = np.arange(len(V), dtype=np.int32).reshape(-1, 3)
+        cases.append((V, T, GridSpec(Aabb([0, 0, 0], [1, 1, 1]), dims)))
+    return cases
+
+
+def test_oracle_inverted_boxes_vs_live_reference():
+    ref = oracle.reference_module()
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    import warnings
+    from pargrid.geometry import Aabb as RA, TriangleMesh as RM
+    from pargrid.gridcore import GridSpec as RS
+    for V, T, spec in _inverted_cases():
+        rspec = RS(RA(spec.bounds.lo, spec.bounds.hi), spec.dims)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            try:
+                g, _ = ref.build_parallel(RM(V, T), rspec)
+                want = (g.G, g.O)
+            except ref.errors.InvariantError:
+                want = None
+        try:
+            got = oracle.build_parallel(V, T, spec)
+        except oracle.OracleInvariantError:
+            got = None
+        assert (want is None) == (got is None), (V, spec.dims)
+        if want is not None:
+            assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
