@@ -282,13 +282,14 @@ def run_sharded(args, world, rank, local):
             kt.setdefault(name, []).append(us * 1e-3)
     _native.kernel_timing(False)
     peak, peak_kind = peaks()
-    sc = kt.get("k_radix_scatter", [])
+    sc_name = "k_radix_scatter_wc" if "k_radix_scatter_wc" in kt else "k_radix_scatter"
+    sc = kt.get(sc_name, [])
     sc_ms = float(np.mean(sc)) if sc else 0.0
     sc_bytes = 16 * no_local
-    roofline = {"bound": "hbm", "kernel": "k_radix_scatter (slab sort, rank 0)",
+    roofline = {"bound": "hbm", "kernel": sc_name + " (slab sort, rank 0)",
                 "achieved": round(sc_bytes / (sc_ms * 1e-3) / 1e9, 1) if sc_ms else None, "peak": peak,
                 "unit": "GB/s", "frac": round(sc_bytes / (sc_ms * 1e-3) / 1e9 / peak, 4) if sc_ms else None,
-                "traffic": traffic_table().get("k_radix_scatter"), "alg_bytes_per_launch": sc_bytes,
+                "traffic": traffic_table().get(sc_name), "alg_bytes_per_launch": sc_bytes,
                 "launch_ms": round(sc_ms, 4), "peak_kind": peak_kind}
     kernels = {k: {"ms_per_launch": round(float(np.mean(v)), 4), "launches": len(v)} for k, v in kt.items()}
 
@@ -515,7 +516,7 @@ def main():
     kern = {
         "k_boxes_count": {"alg_bytes": 12 * n + 24 * nv + 16 * n},
         "k_pairs_emit": {"alg_bytes": 16 * n + 8 * no},
-        "k_radix_scatter": {"alg_bytes": 16 * no},
+        ("k_radix_scatter_wc" if "k_radix_scatter_wc" in ktime else "k_radix_scatter"): {"alg_bytes": 16 * no},
         "k_cell_offsets": {"alg_bytes": 4 * no + 4 * (ncells + 1)},
     }
     for k, v in kern.items():

@@ -133,6 +133,46 @@ void launch_radix_scatter(int bits, unsigned ntiles, cudaStream_t st, const unsi
   }
 }
 
+// PGRID_WC=1 selects the write-combining scatter (k_radix_scatter_wc). Measured slower on
+// cfg3 (219 vs 135 us per 9-bit pass): it cuts global store sectors 10.1M -> 6.4M per pass,
+// but its carries raise the instruction count 58M -> 100M and its shared memory drops
+// residency to 3 CTAs/SM; off.
+bool wc_on() {
+  static const bool on = [] {
+    const char* e = getenv("PGRID_WC");
+    return e && *e == '1';
+  }();
+  return on;
+}
+
+// resident CTAs of the write-combining scatter on the current device (its grid: every CTA
+// takes a contiguous chunk of tiles, so the chunks are as long as one wave allows)
+unsigned wc_resident() {
+  static const unsigned r = [] {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_scatter_wc<9>, RS_THREADS, sizeof(WcSmem));
+    return (unsigned)std::max(1, sms * std::max(1, occ));
+  }();
+  return r;
+}
+
+void launch_radix_scatter_wc(int bits, unsigned ntiles, cudaStream_t st, const unsigned* kin, const unsigned* vin,
+                             unsigned* ko, unsigned* vo, Count n, int shift, const unsigned* hist,
+                             const unsigned* offs, unsigned ld) {
+  const unsigned grid = std::min(ntiles, wc_resident());
+  switch (bits) {
+#define PG_CASE(B)                                                                                           \
+  case B:                                                                                                    \
+    k_radix_scatter_wc<B><<<grid, RS_THREADS, sizeof(WcSmem), st>>>(kin, vin, ko, vo, n, shift, hist, offs, ld); \
+    break;
+    PG_CASE(1) PG_CASE(2) PG_CASE(3) PG_CASE(4) PG_CASE(5) PG_CASE(6) PG_CASE(7) PG_CASE(8) PG_CASE(9)
+#undef PG_CASE
+    default: break;
+  }
+}
+
 template <int B>
 cudaError_t set_emit_smem() {
   return cudaFuncSetAttribute(k_pairs_emit<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PeSmem));
@@ -302,6 +342,10 @@ int pg_builder_create(int device, pg_builder** out) {
   CU(set_scatter_smem<7>()); CU(set_scatter_smem<8>()); CU(set_scatter_smem<9>());
   for (auto f : {k_partition_send<1>, k_partition_send<2>, k_partition_send<3>, k_partition_send<4>})
     CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem_bytes()));
+  for (auto f : {k_radix_scatter_wc<1>, k_radix_scatter_wc<2>, k_radix_scatter_wc<3>, k_radix_scatter_wc<4>,
+                 k_radix_scatter_wc<5>, k_radix_scatter_wc<6>, k_radix_scatter_wc<7>, k_radix_scatter_wc<8>,
+                 k_radix_scatter_wc<9>})
+    CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(WcSmem)));
   *out = b;
   return PG_OK;
 }
@@ -544,6 +588,10 @@ int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned
       launch_scatter_presorted(plan.bits[p], ntiles, st, kin, vin, ko, vo, cno, plan.shift[p], hist + p * kMaxBins,
                                counts, ld);
       LAUNCHED("k_scatter_presorted", st);
+    } else if (wc_on()) {
+      launch_radix_scatter_wc(plan.bits[p], ntiles, st, kin, vin, ko, vo, cno, plan.shift[p], hist + p * kMaxBins,
+                              counts, ld);
+      LAUNCHED("k_radix_scatter_wc", st);
     } else {
       launch_radix_scatter(plan.bits[p], ntiles, st, kin, vin, ko, vo, cno, plan.shift[p], hist + p * kMaxBins, counts,
                            ld);

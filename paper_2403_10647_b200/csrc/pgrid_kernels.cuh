@@ -1255,6 +1255,214 @@ k_partition_send(const unsigned* __restrict__ keys_in, const unsigned* __restric
 }
 
 // ----------------------------------------------------------------------------------------
+// Write-combining radix scatter (the default bit-field pass). What bounds a pass is the
+// number of 32-byte sectors its warp stores touch, not its bytes: moving 19.86M pairs in
+// runs of 8 items takes 82 us when every run is one aligned sector and 152 us when runs
+// straddle sector boundaries (tools/micro/run_align.cu). A tile's run of a digit (~8 items
+// for 9-bit digits) starts anywhere, so k_radix_scatter writes ~2 partial sectors per run.
+// Here each CTA owns a contiguous chunk of tiles. Digit d's output for the chunk is one
+// contiguous range, so the CTA carries the unfinished tail sector of every digit (<= 7 keys
+// and values in shared memory) into the next tile, lays it out in front of that tile's run,
+// and writes whole aligned sectors only; partial sectors remain at chunk ends alone.
+// Ranking is k_radix_scatter's (bit-sliced ballots, stable in element order).
+// ----------------------------------------------------------------------------------------
+constexpr int WC_CARRY = 7;
+constexpr int WC_CAP = RS_TILE + kMaxBins * WC_CARRY;               // tile + carried items
+constexpr int WC_R = (WC_CAP + RS_THREADS - 1) / RS_THREADS;        // write-out items per thread
+constexpr int WC_MIN_CTAS = 3;
+struct WcSmem {
+  unsigned buf[WC_CAP];                      // digit-major blocks [carry | tile run]: keys, then values
+  unsigned carry_k[kMaxBins * WC_CARRY];     // tail sector of each digit, carried to the next tile
+  unsigned carry_v[kMaxBins * WC_CARRY];
+  unsigned short whist[RS_WARPS][kMaxBins];  // per-warp digit counts -> buffer offset of (warp, digit)
+  unsigned cbase[kMaxBins];                  // global position of buf[0] for digit d's block
+  unsigned wend[kMaxBins];                   // end of digit d's written range this tile
+  unsigned wsum[RS_WARPS];
+};
+
+template <int BITS, bool FULL>
+__device__ __forceinline__ void wc_scatter_tile(WcSmem& sm, const unsigned* __restrict__ keys_in,
+                                                const unsigned* __restrict__ vals_in, unsigned* __restrict__ keys_out,
+                                                unsigned* __restrict__ vals_out, unsigned tbase, unsigned tvalid,
+                                                unsigned tile, unsigned ld, int shift,
+                                                const unsigned* __restrict__ offs, const unsigned (&hpre)[RS_DPT],
+                                                unsigned (&cs)[RS_DPT], bool first, bool last) {
+  constexpr int NB = 1 << BITS;
+  constexpr unsigned DMASK = (unsigned)NB - 1u;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto elem = [&](int j) { return (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane; };
+  auto valid = [&](int j) { return FULL || elem(j) < tvalid; };
+  auto digit = [&](unsigned k) { return (k >> shift) & DMASK; };
+  {
+    unsigned* row = reinterpret_cast<unsigned*>(&sm.whist[warp][0]);
+#pragma unroll
+    for (int q = lane; q < (NB + 1) / 2; q += 32) row[q] = 0u;
+  }
+  unsigned kreg[RS_ITEMS], vreg[RS_ITEMS];
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    kreg[j] = valid(j) ? __ldcs(keys_in + tbase + elem(j)) : 0u;
+    vreg[j] = valid(j) ? __ldcs(vals_in + tbase + elem(j)) : 0u;
+  }
+  unsigned pos[RS_ITEMS];
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) pos[j] = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid(j));
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) pos[j] = peers_step(pos[j], kreg[j], 1u << (shift + b));
+  }
+  __syncwarp();
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    const unsigned peers = valid(j) ? pos[j] : 0u;
+    const unsigned dj = digit(kreg[j]);
+    const int leader = __ffs(peers | (1u << lane)) - 1;
+    unsigned old = 0;
+    if (lane == leader && peers) {
+      old = sm.whist[warp][dj];
+      sm.whist[warp][dj] = (unsigned short)(old + __popc(peers));
+    }
+    old = __shfl_sync(0xffffffffu, old, leader);
+    pos[j] = old + __popc(peers & lt);  // rank among the warp's items of this digit
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit (owner thread): tile count n, run start s, block = carry [cs, s) + run [s, s+n)
+  unsigned n[RS_DPT], s[RS_DPT], cc[RS_DPT], msum = 0;
+#pragma unroll
+  for (int q = 0; q < RS_DPT; ++q) {
+    const int d = tid * RS_DPT + q;
+    unsigned run = 0;
+    s[q] = 0;
+    if (d < NB) {
+#pragma unroll
+      for (int w = 0; w < RS_WARPS; ++w) {
+        const unsigned c = sm.whist[w][d];
+        sm.whist[w][d] = (unsigned short)run;
+        run += c;
+      }
+      s[q] = hpre[q] + __ldg(&offs[(size_t)d * ld + tile]);
+    }
+    if (first) cs[q] = s[q];
+    n[q] = run;
+    cc[q] = s[q] - cs[q];
+    msum += cc[q] + run;
+  }
+  unsigned mtot;
+  unsigned B = block_excl_scan<RS_WARPS>(msum, sm.wsum, mtot);
+  unsigned Bq[RS_DPT];
+#pragma unroll
+  for (int q = 0; q < RS_DPT; ++q) {
+    const int d = tid * RS_DPT + q;
+    Bq[q] = B;
+    if (d < NB) {
+#pragma unroll
+      for (int w = 0; w < RS_WARPS; ++w) sm.whist[w][d] = (unsigned short)(sm.whist[w][d] + B + cc[q]);
+      const unsigned end = s[q] + n[q];
+      const unsigned we = last ? end : max(cs[q], end & ~7u);  // whole sectors only
+      sm.cbase[d] = cs[q] - B;
+      sm.wend[d] = we;
+      for (unsigned i = 0; i < cc[q]; ++i) sm.buf[B + i] = sm.carry_k[d * WC_CARRY + i];
+      cs[q] = we;
+    }
+    B += cc[q] + n[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j) {
+    if (valid(j)) {
+      pos[j] += sm.whist[warp][digit(kreg[j])];
+      sm.buf[pos[j]] = kreg[j];
+    }
+  }
+  __syncthreads();
+  // keys out: buffer position i of digit d is global position cbase[d] + i; items past the
+  // written range become the digit's new carry. Digits are kept (10 bits each) for the values.
+  unsigned dpk[(WC_R + 2) / 3];
+#pragma unroll
+  for (int r = 0; r < WC_R; ++r) {
+    const unsigned i = tid + r * RS_THREADS;
+    if (r % 3 == 0) dpk[r / 3] = 0u;
+    if (i < mtot) {
+      const unsigned k = sm.buf[i];
+      const unsigned d = digit(k);
+      dpk[r / 3] |= d << (10 * (r % 3));
+      const unsigned g = sm.cbase[d] + i, we = sm.wend[d];
+      if (g < we) keys_out[g] = k;
+      else sm.carry_k[d * WC_CARRY + (g - we)] = k;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < RS_ITEMS; ++j)
+    if (valid(j)) sm.buf[pos[j]] = vreg[j];
+#pragma unroll
+  for (int q = 0; q < RS_DPT; ++q) {
+    const int d = tid * RS_DPT + q;
+    if (d < NB)
+      for (unsigned i = 0; i < cc[q]; ++i) sm.buf[Bq[q] + i] = sm.carry_v[d * WC_CARRY + i];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < WC_R; ++r) {
+    const unsigned i = tid + r * RS_THREADS;
+    if (i < mtot) {
+      const unsigned d = (dpk[r / 3] >> (10 * (r % 3))) & 1023u;
+      const unsigned g = sm.cbase[d] + i, we = sm.wend[d];
+      if (g < we) vals_out[g] = sm.buf[i];
+      else sm.carry_v[d * WC_CARRY + (g - we)] = sm.buf[i];
+    }
+  }
+  // the next tile touches buf / cbase / wend / carries only after its ranking barrier
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(RS_THREADS, WC_MIN_CTAS)
+k_radix_scatter_wc(const unsigned* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
+                   unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, Count cno, int shift,
+                   const unsigned* __restrict__ hist, const unsigned* __restrict__ offs, unsigned ld) {
+  constexpr int NB = 1 << BITS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  WcSmem& sm = *reinterpret_cast<WcSmem*>(smem_raw);
+  const unsigned no = cno.get();
+  const unsigned ntiles = (no + RS_TILE - 1) / RS_TILE;
+  const unsigned t0 = (unsigned)((unsigned long long)ntiles * blockIdx.x / gridDim.x);
+  const unsigned t1 = (unsigned)((unsigned long long)ntiles * (blockIdx.x + 1) / gridDim.x);
+  if (t0 >= t1) return;
+  const int tid = threadIdx.x;
+  // per-digit state lives in the registers of the digit's owner thread
+  unsigned hpre[RS_DPT], cs[RS_DPT];
+  {
+    unsigned hs[RS_DPT], hsum = 0, htot;
+#pragma unroll
+    for (int q = 0; q < RS_DPT; ++q) {
+      const int d = tid * RS_DPT + q;
+      hs[q] = d < NB ? __ldg(&hist[d]) : 0u;
+      hsum += hs[q];
+      cs[q] = 0;
+    }
+    unsigned p = block_excl_scan<RS_WARPS>(hsum, sm.wsum, htot);
+#pragma unroll
+    for (int q = 0; q < RS_DPT; ++q) {
+      hpre[q] = p;
+      p += hs[q];
+    }
+  }
+  for (unsigned tile = t0; tile < t1; ++tile) {
+    const unsigned tbase = tile * (unsigned)RS_TILE;
+    const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
+    if (tvalid == (unsigned)RS_TILE)
+      wc_scatter_tile<BITS, true>(sm, keys_in, vals_in, keys_out, vals_out, tbase, tvalid, tile, ld, shift, offs,
+                                  hpre, cs, tile == t0, tile + 1 == t1);
+    else
+      wc_scatter_tile<BITS, false>(sm, keys_in, vals_in, keys_out, vals_out, tbase, tvalid, tile, ld, shift, offs,
+                                   hpre, cs, tile == t0, tile + 1 == t1);
+  }
+}
+
+// ----------------------------------------------------------------------------------------
 // K2: pair expansion on radix-sort tiles. Each CTA expands RS_TILE pairs, writes them in
 // generation (object-major) order with 16-byte stores, and counts the tile's first-pass
 // digits (the per-tile counts the first radix pass needs, so that pass skips its own
