@@ -832,6 +832,7 @@ struct RsSmem {
   };
   unsigned short whist[RS_WARPS][kMaxBins];  // per-warp digit counts -> tile offset of (warp, digit)
   unsigned gbase[kMaxBins];                  // global position of buf[0] for each digit
+  unsigned hsm[kMaxBins];                    // digit totals (staged)
   unsigned wsum[RS_WARPS];
 };
 
@@ -845,6 +846,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all_but_one() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 // One bit-slice of warp peer detection: keep the lanes whose bit (x & bit) equals ours.
 // Written in PTX so ptxas emits LOP3.P (bit -> predicate), VOTE, SEL, LOP3 -- 4 instructions
@@ -1049,6 +1051,18 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
   auto elem = [&](int j) { return (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane; };
   auto valid = [&](int j) { return FULL || elem(j) < tvalid; };
 
+  // the per-digit inputs of this tile (L2 hits: digit totals and this tile's column of the
+  // scanned count matrix) are copied into shared memory now, so their latency hides behind
+  // the ranking without holding registers
+#pragma unroll
+  for (int q = 0; q < RS_DPT; ++q) {
+    const int d = tid * RS_DPT + q;
+    if (d < NB) {
+      if (!P2P) cp_async4(&sm.hsm[d], hist + d);
+      cp_async4(&sm.gbase[d], offs + (size_t)d * ld + tile);
+    }
+  }
+  cp_async_commit();
   // SRC_SMEM: keys_in points at a shared-memory copy of the tile (element order) and
   // sm.vstage already holds the values
   if (!SRC_SMEM) {
@@ -1094,39 +1108,46 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
     rank[j] = old + __popc(peers & lt);
     __syncwarp();
   }
+  if (SRC_SMEM) cp_async_wait();
+  else cp_async_wait_all_but_one();  // the per-digit group (the values' group may stay in flight)
   __syncthreads();
-  // per digit (RS_DPT consecutive digits per thread): warp offsets, tile counts, prefixes
-  unsigned tc[RS_DPT], hs[RS_DPT], tsum = 0, hsum = 0;
+  // per digit (thread t owns digits 2t, 2t+1 -- one 32-bit word of every warp's u16 row):
+  // warp offsets and tile counts of both digits in one pass over the rows
+  static_assert(RS_DPT == 2, "two digits per thread");
+  unsigned* rows = reinterpret_cast<unsigned*>(&sm.whist[0][0]);
+  unsigned tpk = 0;  // tile counts of both digits, packed (u16 lanes never carry: <= RS_TILE)
+  if (tid < NB / 2) {
+#pragma unroll
+    for (int w = 0; w < RS_WARPS; ++w) tpk += rows[w * (kMaxBins / 2) + tid];
+  }
+  const unsigned tc[RS_DPT] = {tpk & 0xffffu, tpk >> 16};
+  unsigned hs[RS_DPT], toff[RS_DPT];
 #pragma unroll
   for (int q = 0; q < RS_DPT; ++q) {
     const int d = tid * RS_DPT + q;
-    unsigned run = 0;
-    if (d < NB) {
-#pragma unroll
-      for (int w = 0; w < RS_WARPS; ++w) {
-        const unsigned c = sm.whist[w][d];
-        sm.whist[w][d] = (unsigned short)run;
-        run += c;
-      }
-    }
-    tc[q] = run;
-    hs[q] = (!P2P && d < NB) ? __ldg(&hist[d]) : 0u;
-    tsum += run;
-    hsum += hs[q];
+    hs[q] = (!P2P && d < NB) ? sm.hsm[d] : 0u;
+    toff[q] = d < NB ? sm.gbase[d] : 0u;
   }
+  const unsigned tsum = tc[0] + tc[1], hsum = hs[0] + hs[1];
   unsigned ttot, htot;
   unsigned lpre = block_excl_scan<RS_WARPS>(tsum, sm.wsum, ttot);
   unsigned hpre = block_excl_scan<RS_WARPS>(hsum, sm.wsum, htot);
+  if (tid < NB / 2) {
+    // every warp's offsets = tile-local digit start + exclusive count over the lower warps
+    // (folded in so the items below need one lookup each)
+    unsigned run = lpre | ((lpre + tc[0]) << 16);
+#pragma unroll
+    for (int w = 0; w < RS_WARPS; ++w) {
+      const unsigned c = rows[w * (kMaxBins / 2) + tid];
+      rows[w * (kMaxBins / 2) + tid] = run;
+      run += c;
+    }
+  }
 #pragma unroll
   for (int q = 0; q < RS_DPT; ++q) {
     const int d = tid * RS_DPT + q;
-    if (d < NB) {
-      // fold the tile-local digit start into every warp's offset: one lookup per item below
-#pragma unroll
-      for (int w = 0; w < RS_WARPS; ++w) sm.whist[w][d] = (unsigned short)(sm.whist[w][d] + lpre);
-      // P2P: positions inside slab d's receive buffer (32-bit: a receive buffer < 2^32 pairs)
-      sm.gbase[d] = (P2P ? (unsigned)p2p->off[d] : hpre) + __ldg(&offs[(size_t)d * ld + tile]) - lpre;
-    }
+    // P2P: positions inside slab d's receive buffer (32-bit: a receive buffer < 2^32 pairs)
+    if (d < NB) sm.gbase[d] = (P2P ? (unsigned)p2p->off[d] : hpre) + toff[q] - lpre;
     lpre += tc[q];
     hpre += hs[q];
   }
