@@ -43,6 +43,10 @@ extern "C" {
 #define PG_HOST_RAYS 8u        /* pg_dda_cast: rays are host pointers (grid stays on device) */
 #define PG_CHECK 16u           /* pg_dda_cast: synchronise and report device-side errors */
 #define PG_ASYNC 32u           /* pg_finish: return once enqueued (host outputs valid after pg_wait) */
+#define PG_DEFER 64u           /* pg_count: no host round trip; *no_out is the pair capacity on entry,
+                                  the sharded building blocks (pg_pairs, pg_partition_counts/_send
+                                  with n = that capacity) run on the device count; pg_count_result
+                                  reports NO (PG_CAPACITY_ERROR if it exceeded the capacity) */
 
 /* Grid specification: the exact host doubles of GridSpec (gridcore.py:36-57). */
 typedef struct {
@@ -180,6 +184,27 @@ int pg_partition(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int6
                  uint32_t *slab_counts, void *stream);
 int pg_sort_cells(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int64_t n,
                   int64_t ncells, uint32_t *G, uint32_t *O, void *stream);
+
+/* Device-side small collectives of the sharded build over peer memory (no NCCL call, no host
+ * round trip between the pair expansion and the slab plan; replaces the all-reduce of the
+ * coarse histogram and the host-side plan_slabs of distributed.py):
+ *   pg_peer_put  -- copy n u32 from src (device) to dsts[r] + dst_offset (elements) for the
+ *                   nranks <= 16 device pointers in the host array dsts (peer memory mapped into
+ *                   this process, e.g. symmetric memory); the caller barriers before readers read
+ *   pg_slab_plan -- from the ranks' coarse histograms hists[r * nbuckets + b] (device u32,
+ *                   nbuckets <= 4096): slab_of_bucket[nbuckets], slab_base[nslabs] (first cell
+ *                   of each slab, u32) and plan[4*nslabs+2] = cuts[nslabs+1] | cell_lo[nslabs] |
+ *                   cell_hi[nslabs] | pair_base[nslabs+1] (int64), all device; the same
+ *                   arithmetic as distributed.plan_slabs */
+int pg_count_result(pg_builder *b, uint64_t *no_out); /* after PG_DEFER + a stream synchronise */
+int pg_peer_put(const uint32_t *src, int64_t n, const uint64_t *dsts, int nranks, int64_t dst_offset,
+                void *stream);
+/* pg_peer_put of the builder's device pair count (NO of its last pg_count, u64 as two u32
+ * words; exact even after a PG_DEFER count), so every rank learns every rank's NO with the
+ * count matrix and they agree on capacity overflows */
+int pg_peer_put_count(pg_builder *b, const uint64_t *dsts, int nranks, int64_t dst_offset, void *stream);
+int pg_slab_plan(const uint32_t *hists, int nranks, int nbuckets, int bucket_shift, int64_t ncells,
+                 int nslabs, uint32_t *slab_of_bucket, uint32_t *slab_base, int64_t *plan, void *stream);
 
 /* Wait for the device work (and PG_HOST_OUTPUT copies) of the last pg_finish on b. */
 int pg_wait(pg_builder *b);

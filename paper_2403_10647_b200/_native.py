@@ -29,13 +29,16 @@ PG_KEEP_STAGES = 4
 PG_HOST_RAYS = 8
 PG_CHECK = 16
 PG_ASYNC = 32
+PG_DEFER = 64
 
 NPHASES = 6
 
 # every symbol include/pgrid.h declares (checked by tests/test_boundary.py)
 EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
            "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_finish_baseline",
-           "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_partition_counts", "pg_partition_send", "pg_build_async",
+           "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_partition_counts", "pg_partition_send", "pg_peer_put", "pg_slab_plan", "pg_count_result",
+           "pg_peer_put_count",
+           "pg_build_async",
            "pg_build_wait", "pg_host_register",
            "pg_host_unregister", "pg_host_alloc", "pg_host_free", "pg_last_launch_count",
            "pg_last_error")
@@ -97,6 +100,10 @@ def load():
         lib.pg_partition_send.argtypes = [vp, vp, vp, i64, vp, ctypes.c_int, ctypes.c_int, vp,
                                           ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64), vp]
         lib.pg_kernel_timing.argtypes = [ctypes.c_int]
+        lib.pg_count_result.argtypes = [vp, ctypes.POINTER(u64)]
+        lib.pg_peer_put_count.argtypes = [vp, ctypes.POINTER(u64), ctypes.c_int, i64, vp]
+        lib.pg_peer_put.argtypes = [vp, i64, ctypes.POINTER(u64), ctypes.c_int, i64, vp]
+        lib.pg_slab_plan.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, i64, ctypes.c_int, vp, vp, vp, vp]
         lib.pg_load_obj.argtypes = [vp, vp, u64, u32, vp, ctypes.POINTER(i64)]
         lib.pg_obj_fetch.argtypes = [vp, vp, vp, u32, vp]
         lib.pg_grid_stats.argtypes = [vp, vp, u32, vp, ctypes.POINTER(u64)]
@@ -112,7 +119,8 @@ def load():
         lib.pg_last_error.restype = ctypes.c_char_p
         for name in ("pg_builder_create", "pg_count", "pg_finish", "pg_stage",
                      "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells",
-                     "pg_finish_baseline", "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_partition_counts", "pg_partition_send", "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
+                     "pg_finish_baseline", "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_partition_counts", "pg_partition_send", "pg_peer_put", "pg_slab_plan",
+           "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
                      "pg_last_launch_count"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
@@ -171,6 +179,31 @@ class Builder:
         check(self._lib.pg_count(self._h, ptr(V), int(nv), ptr(T), int(n), ctypes.byref(s),
                                  flags, stream, ctypes.byref(no)))
         return int(no.value)
+
+    def count_deferred(self, V, nv, T, n, spec, capacity, flags=0, stream=None):
+        """pg_count with PG_DEFER: K1 enqueued, no host round trip; the pair building blocks
+        run on the device count bounded by `capacity`. Returns the capacity."""
+        s = PgSpec.from_spec(spec)
+        no = ctypes.c_uint64(int(capacity))
+        check(self._lib.pg_count(self._h, ptr(V), int(nv), ptr(T), int(n), ctypes.byref(s),
+                                 flags | PG_DEFER, stream, ctypes.byref(no)))
+        return int(capacity)
+
+    def count_result(self):
+        """NO of the last PG_DEFER count (the stream must have been synchronised since);
+        -NO when it exceeded the capacity."""
+        no = ctypes.c_uint64(0)
+        rc = self._lib.pg_count_result(self._h, ctypes.byref(no))
+        if rc == PG_CAPACITY_ERROR:
+            return -int(no.value)
+        check(rc)
+        return int(no.value)
+
+    def peer_put_count(self, dsts, dst_offset, stream=None):
+        """Put this builder's device NO (two u32 words) into every dsts[r] + dst_offset."""
+        arr = ctypes.c_uint64 * len(dsts)
+        check(self._lib.pg_peer_put_count(self._h, arr(*[int(x) for x in dsts]), len(dsts), int(dst_offset),
+                                          stream))
 
     def finish(self, G, O, flags=0, stream=None, timed=True):
         phases = (ctypes.c_float * NPHASES)() if timed else None
@@ -280,6 +313,21 @@ class Builder:
 
 
 _tls = threading.local()
+
+
+def peer_put(src, n, dsts, dst_offset, stream=None):
+    """Copy n u32 from src (device) to every pointer in dsts at element offset dst_offset
+    (one launch; peer memory over NVLink). No host synchronisation."""
+    arr = ctypes.c_uint64 * len(dsts)
+    check(load().pg_peer_put(ptr(src), int(n), arr(*[int(x) for x in dsts]), len(dsts), int(dst_offset), stream))
+
+
+def slab_plan(hists, nranks, nbuckets, shift, ncells, nslabs, table, slab_base, plan, stream=None):
+    """distributed.plan_slabs on the device from the ranks' coarse histograms (device u32
+    [nranks * nbuckets]): table u32[nbuckets], slab_base u32[nslabs], plan int64[4*nslabs+2] =
+    cuts | cell_lo | cell_hi | pair_base. No host synchronisation."""
+    check(load().pg_slab_plan(ptr(hists), int(nranks), int(nbuckets), int(shift), int(ncells), int(nslabs),
+                              ptr(table), ptr(slab_base), ptr(plan), stream))
 
 
 def kernel_timing(on):

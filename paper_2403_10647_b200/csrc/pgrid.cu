@@ -288,6 +288,7 @@ struct pg_builder {
   DevBuf pairs, sort_sync, stage, stage0, gbuf, obuf, cells;
   // state of the last pg_count
   bool counted = false;
+  bool deferred = false;  // PG_DEFER: NO is on the device only; `no` holds the capacity
   int64_t n = 0;
   uint64_t no = 0;
   int64_t ncells = 0;
@@ -398,6 +399,7 @@ namespace {
 // Validation + builder state for a build of (n triangles, spec); fills the device spec.
 int count_setup(pg_builder* b, int64_t nv, int64_t n, const pg_spec* spec, DevSpec& ds) {
   b->counted = false;
+  b->deferred = false;
   b->stages_kept = false;
   b->k1_timed = false;
   b->launches = 0;
@@ -544,8 +546,34 @@ int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64
     dT = b->in_t.as<int32_t>();
   }
   if ((rc = count_enqueue(b, dV, nv, dT, n, ds, st))) return rc;
+  if (flags & PG_DEFER) {
+    // no host round trip: the sharded building blocks run on the device count, bounded by
+    // the capacity the caller passed in *no_out; pg_count_result checks it afterwards
+    const uint64_t cap = *no_out;
+    if (cap < 1 || (int64_t)cap > kMaxScan) return fail(PG_INVARIANT_ERROR, "PG_DEFER capacity out of range");
+    b->no = cap;
+    b->deferred = true;
+    b->counted = true;
+    return PG_OK;
+  }
   CU(cudaStreamSynchronize(st));
   return count_check(b, no_out);
+}
+
+int pg_count_result(pg_builder* b, uint64_t* no_out) {
+  if (!b || !no_out) return fail(PG_INVARIANT_ERROR, "null argument");
+  if (!b->counted || !b->deferred) return fail(PG_STATE_ERROR, "pg_count_result without a PG_DEFER pg_count");
+  CU(cudaSetDevice(b->device));
+  const uint64_t cap = b->no;
+  int rc = count_check(b, no_out);  // reads the scalars copied back by the (synchronised) stream
+  b->deferred = true;
+  b->counted = rc == PG_OK;
+  b->no = cap;
+  if (rc) return rc;
+  if (*no_out > cap)
+    return fail(PG_CAPACITY_ERROR, "%llu pairs exceed the PG_DEFER capacity %llu", (unsigned long long)*no_out,
+                (unsigned long long)cap);
+  return PG_OK;
 }
 
 namespace {
@@ -1054,7 +1082,8 @@ int pg_pairs(pg_builder* b, uint32_t* keys, uint32_t* vals, uint32_t val_offset,
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   CU(cudaSetDevice(b->device));
   drop_graph(b);
-  const uint64_t no = b->no;
+  const uint64_t no = b->no;  // PG_DEFER: the capacity (grids); the kernels read the device count
+  const Count cno{b->deferred ? b->d_total : nullptr, (unsigned)no};
   const unsigned k2_tiles = (unsigned)((no + K2_TILE - 1) / K2_TILE);
   int rc;
   const size_t pb_bytes = align_up((size_t)k2_tiles * 8 + 8);
@@ -1064,10 +1093,10 @@ int pg_pairs(pg_builder* b, uint32_t* keys, uint32_t* vals, uint32_t val_offset,
   if (dcoarse) CU(cudaMemsetAsync(dcoarse, 0, (size_t)coarse_bins * 4, st));
   if (no > 0) {
     const unsigned dxu = (unsigned)b->dims[0], dxyu = (unsigned)b->dims[0] * (unsigned)b->dims[1];
-    k_pair_tile_bounds<<<(k2_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n,
-                                                          Count{nullptr, (unsigned)no}, K2_TILE, pbounds);
+    k_pair_tile_bounds<<<(k2_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, cno, K2_TILE,
+                                                          pbounds);
     LAUNCHED("k_pair_tile_bounds", st);
-    k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, Count{nullptr, (unsigned)no},
+    k_expand_pairs<<<k2_tiles, K2_THREADS, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, cno,
                                                    dxu, dxyu,
                                                    pbounds, keys, vals, val_offset, dcoarse, coarse_shift,
                                                    coarse_bins);
@@ -1520,7 +1549,9 @@ int pg_partition_counts(pg_builder* b, const uint32_t* keys, int64_t n, const ui
   if ((rc = b->sort_sync.ensure((size_t)ld * kMaxBins * 4))) return rc;
   unsigned* counts = b->sort_sync.as<unsigned>(0);
   const DigitFn dig{bucket_shift, 0u, slab_of_bucket};
-  const Count cn{nullptr, (unsigned)n};
+  // after a PG_DEFER count these are this builder's pairs: n is their capacity, the device
+  // count bounds the kernels
+  const Count cn{b->deferred ? b->d_total : nullptr, (unsigned)n};
   k_tile_counts<<<(ntiles + TC_TILES - 1) / TC_TILES, RS_THREADS, 0, st>>>(keys, cn, dig, 1 << bits, counts, ld);
   LAUNCHED("k_tile_counts", st);
   k_scan_tile_counts<<<1u << bits, SC_THREADS, 0, st>>>(counts, cn, ld, slab_counts);
@@ -1550,7 +1581,7 @@ int pg_partition_send(pg_builder* b, const uint32_t* keys, const uint32_t* vals,
   const unsigned ntiles = (unsigned)((n + RS_TILE - 1) / RS_TILE);
   const unsigned ld = (ntiles + 3) & ~3u;
   const unsigned* counts = b->sort_sync.as<unsigned>(0);
-  const Count cn{nullptr, (unsigned)n};
+  const Count cn{b->deferred ? b->d_total : nullptr, (unsigned)n};
   switch (b->part_bits) {
 #define PG_CASE(B)                                                                                          \
   case B:                                                                                                   \
@@ -1563,6 +1594,39 @@ int pg_partition_send(pg_builder* b, const uint32_t* keys, const uint32_t* vals,
   }
   LAUNCHED("k_partition_send", st);
   b->launches = 1;
+  return PG_OK;
+}
+
+int pg_peer_put(const uint32_t* src, int64_t n, const uint64_t* dsts, int nranks, int64_t dst_offset, void* stream_) {
+  if (!dsts || (n > 0 && !src)) return fail(PG_INVARIANT_ERROR, "null argument");
+  if (nranks < 1 || nranks > kMaxP2P) return fail(PG_INVARIANT_ERROR, "nranks must be in [1, %d]", kMaxP2P);
+  if (n < 0 || n > (1ll << 30) || dst_offset < 0) return fail(PG_INVARIANT_ERROR, "bad peer put size");
+  if (n == 0) return PG_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  PeerPtrs p{};
+  for (int r = 0; r < nranks; ++r) p.p[r] = reinterpret_cast<unsigned*>(dsts[r]);
+  k_peer_put<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, (unsigned)n, p, nranks, (unsigned long long)dst_offset);
+  CU(cudaGetLastError());
+  return PG_OK;
+}
+
+int pg_peer_put_count(pg_builder* b, const uint64_t* dsts, int nranks, int64_t dst_offset, void* stream_) {
+  if (!b || !b->counted || !b->d_total) return fail(PG_STATE_ERROR, "pg_peer_put_count without a pg_count");
+  return pg_peer_put(reinterpret_cast<const uint32_t*>(b->d_total), 2, dsts, nranks, dst_offset, stream_);
+}
+
+int pg_slab_plan(const uint32_t* hists, int nranks, int nbuckets, int bucket_shift, int64_t ncells, int nslabs,
+                 uint32_t* slab_of_bucket, uint32_t* slab_base, int64_t* plan, void* stream_) {
+  if (!hists || !slab_of_bucket || !slab_base || !plan) return fail(PG_INVARIANT_ERROR, "null argument");
+  if (nranks < 1 || nranks > kMaxP2P) return fail(PG_INVARIANT_ERROR, "nranks must be in [1, %d]", kMaxP2P);
+  if (nslabs < 1 || nslabs > kMaxP2P) return fail(PG_INVARIANT_ERROR, "nslabs must be in [1, %d]", kMaxP2P);
+  if (nbuckets < 1 || nbuckets > PLAN_MAX_BUCKETS)
+    return fail(PG_INVARIANT_ERROR, "nbuckets must be in [1, %d]", PLAN_MAX_BUCKETS);
+  if (bucket_shift < 0 || bucket_shift > 40 || ncells < 1) return fail(PG_INVARIANT_ERROR, "bad slab geometry");
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  k_slab_plan<<<1, PLAN_THREADS, 0, st>>>(hists, nranks, nbuckets, bucket_shift, (long long)ncells, nslabs,
+                                          slab_of_bucket, slab_base, reinterpret_cast<long long*>(plan));
+  CU(cudaGetLastError());
   return PG_OK;
 }
 

@@ -1276,6 +1276,108 @@ k_partition_send(const unsigned* __restrict__ keys_in, const unsigned* __restric
 }
 
 // ----------------------------------------------------------------------------------------
+// Sharded build: device-side small collectives over peer memory.
+// k_peer_put copies one rank's small array (its coarse histogram, its slab counts) into the
+// same slot of every rank's exchange buffer (peer memory mapped into this process); after a
+// device barrier every rank holds all ranks' arrays and reduces them itself, so no NCCL call
+// and no host round trip sits between the pair expansion and the slab plan.
+// ----------------------------------------------------------------------------------------
+struct PeerPtrs {
+  unsigned* p[kMaxP2P];
+};
+__global__ void __launch_bounds__(256) k_peer_put(const unsigned* __restrict__ src, unsigned n, PeerPtrs dst,
+                                                  int nranks, unsigned long long offset) {
+  const unsigned i = blockIdx.x * 256u + threadIdx.x;
+  if (i >= n) return;
+  const unsigned v = __ldg(src + i);
+  for (int r = 0; r < nranks; ++r) dst.p[r][offset + i] = v;
+}
+
+// Slab plan on the device, the same arithmetic as distributed.plan_slabs: sum the ranks'
+// coarse histograms (hists[r * nb + b]), cum = exclusive scan (nb + 1 entries), cut s =
+// first bucket with cum >= ceil(s * total / P) (np.searchsorted, side left), clamped to nb;
+// outputs the bucket -> slab table, each slab's first cell (u32, the key rebase) and
+// plan = cuts[P+1] | cell_lo[P] | cell_hi[P] | pair_base[P+1] (int64).
+constexpr int PLAN_THREADS = 1024;
+constexpr int PLAN_MAX_BUCKETS = 4096;
+__global__ void __launch_bounds__(PLAN_THREADS)
+k_slab_plan(const unsigned* __restrict__ hists, int nranks, int nb, int shift, long long ncells, int P,
+            unsigned* __restrict__ table, unsigned* __restrict__ slab_base, long long* __restrict__ plan) {
+  __shared__ unsigned long long cum[PLAN_MAX_BUCKETS + 1];
+  __shared__ unsigned long long wsum[PLAN_THREADS / 32];
+  __shared__ long long cuts[kMaxP2P + 1];
+  constexpr int PER = PLAN_MAX_BUCKETS / PLAN_THREADS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned long long h[PER], run = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int b = tid * PER + q;
+    unsigned long long x = 0;
+    if (b < nb)
+      for (int r = 0; r < nranks; ++r) x += __ldg(&hists[(size_t)r * nb + b]);
+    h[q] = x;
+    run += x;
+  }
+  unsigned long long inc = run;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  unsigned long long pre = inc - run;
+  for (int w = 0; w < warp; ++w) pre += wsum[w];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int b = tid * PER + q;
+    if (b < nb) cum[b] = pre;
+    pre += h[q];
+  }
+  if (tid == PLAN_THREADS - 1) cum[nb] = pre;  // the last thread's running sum is the total
+  __syncthreads();
+  const unsigned long long total = cum[nb];
+  if (tid <= P) {
+    long long c;
+    if (tid == 0) {
+      c = 0;
+    } else if (tid == P) {
+      c = nb;
+    } else {
+      const unsigned long long target = ((unsigned long long)tid * total + (unsigned long long)P - 1) / (unsigned long long)P;
+      int lo = 0, hi = nb + 1;  // first i in [0, nb] with cum[i] >= target (nb + 1 if none)
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cum[mid] >= target) hi = mid;
+        else lo = mid + 1;
+      }
+      c = lo < nb ? lo : nb;
+    }
+    cuts[tid] = c;
+  }
+  __syncthreads();
+  if (tid == 0) {  // cuts[s] = max(cuts[s-1], ...): searchsorted of rising targets is monotone already
+    for (int s2 = 1; s2 <= P; ++s2) cuts[s2] = max(cuts[s2], cuts[s2 - 1]);
+  }
+  __syncthreads();
+  for (int b = tid; b < nb; b += PLAN_THREADS) {
+    int sl = 0;
+    while (sl + 1 < P && (long long)b >= cuts[sl + 1]) ++sl;
+    table[b] = (unsigned)sl;
+  }
+  if (tid < P) {
+    const long long lo = min(cuts[tid] << shift, ncells), hi = min(cuts[tid + 1] << shift, ncells);
+    slab_base[tid] = (unsigned)lo;
+    plan[P + 1 + tid] = lo;
+    plan[2 * P + 1 + tid] = hi;
+  }
+  if (tid <= P) {
+    plan[tid] = cuts[tid];
+    plan[3 * P + 1 + tid] = (long long)cum[cuts[tid]];
+  }
+}
+
+// ----------------------------------------------------------------------------------------
 // Write-combining radix scatter (the default bit-field pass). What bounds a pass is the
 // number of 32-byte sectors its warp stores touch, not its bytes: moving 19.86M pairs in
 // runs of 8 items takes 82 us when every run is one aligned sector and 152 us when runs

@@ -24,6 +24,8 @@ from . import _native
 
 COARSE_BITS = 12       # slab cuts at 2^12-bucket granularity of the cell-id range
 MAX_SLABS = 16         # pg_partition's digit table limit
+CTL_HIST = 1 << COARSE_BITS   # words per rank slot of the exchange control buffer (histograms)
+CTL_CNT = 32                  # words per rank slot for slab counts [0, 16) and the rank's NO [16, 18)
 
 
 @dataclass
@@ -93,13 +95,41 @@ class ShardState:
         self.ncells = int(spec.dims[0]) * int(spec.dims[1]) * int(spec.dims[2])
         self.V, self.T, self.tri_base = V, T, tri_base
 
-    def phase_count(self):
-        """K1 + K2 on the shard; returns the local coarse histogram (computed by K2)."""
-        self.no = self.ops.count(self.V, self.T, self.spec)
+    def phase_count(self, capacity=None):
+        """K1 + K2 on the shard; returns the local coarse histogram (computed by K2). With a
+        pair capacity (ops with PG_DEFER), no host round trip: NO stays on the device and the
+        pair buffers hold `capacity` pairs."""
+        self.deferred = bool(capacity) and hasattr(self.ops, "count_deferred")
+        if self.deferred:
+            self.no = self.ops.count_deferred(self.V, self.T, self.spec, capacity)
+        else:
+            self.no = self.ops.count(self.V, self.T, self.spec)
         self.shift = coarse_shift(self.ncells)
         nb = ((self.ncells - 1) >> self.shift) + 1
+        self.nb_coarse = nb
         self.keys, self.vals, hist = self.ops.pairs(self.no, self.tri_base, self.shift, nb)
         return hist
+
+    def phase_plan_device(self, hists):
+        """Slab plan on the device from every rank's coarse histogram (exchange buffer);
+        partition tables stay on the device. The host learns the plan with the count matrix."""
+        self.nb = ((self.ncells - 1) >> self.shift) + 1
+        self.table_d, self.base_d, self.plan_d = self.ops.slab_plan(hists, self.world, self.nb, self.shift,
+                                                                    self.ncells, self.world)
+        return self.plan_d
+
+    def set_plan(self, plan_arr):
+        """Host copy of the device plan (cuts | cell_lo | cell_hi | pair_base) -> SlabPlan."""
+        P = self.world
+        a = np.asarray(plan_arr, dtype=np.int64)
+        self.plan = SlabPlan(self.shift, self.nb, a[:P + 1], a[P + 1:2 * P + 1], a[2 * P + 1:3 * P + 1],
+                             a[3 * P + 1:4 * P + 2], self.table_d)
+        return self.plan
+
+    def phase_partition_counts_device(self):
+        """Fused exchange, step 1 with the device plan: slab upsweep; per-slab counts (device)."""
+        self.send_counts = self.ops.partition_counts(self.keys, self.table_d, self.shift, self.world)
+        return self.send_counts
 
     def phase_partition(self, plan):
         """Stable partition by slab; returns the per-slab send counts."""
@@ -121,7 +151,9 @@ class ShardState:
         matrix[r][s] = pairs rank r sends to slab s; this rank writes after the lower ranks."""
         m = np.asarray(matrix, dtype=np.int64)
         off = [int(m[:self.rank, s].sum()) for s in range(self.world)]
-        base = self.plan.cell_lo.astype(np.uint32)
+        base = getattr(self, "base_d", None)
+        if base is None:
+            base = self.plan.cell_lo.astype(np.uint32)
         self.ops.partition_send(self.keys, self.vals, self.plan.table, self.plan.shift, self.world, base,
                                 dst_keys, dst_vals, off)
         return int(m[:, self.rank].sum())
@@ -148,16 +180,38 @@ def build_sharded(ops, comm, V, T, tri_base, spec, gather=True, exchange=None):
     if world > MAX_SLABS:
         raise ValueError(f"at most {MAX_SLABS} ranks")
     st = ShardState(ops, V, T, tri_base, spec, rank, world)
-    hist = comm.allreduce_sum(st.phase_count())
-    plan = plan_slabs(hist, st.ncells, world)
     if exchange is not None:
-        matrix = exchange.allgather_counts(st.phase_partition_counts(plan))
+        # histograms, plan and slab counts stay on the device: each rank puts its array into
+        # every rank's exchange buffer (peer stores), a device barrier, then every rank reduces
+        # / plans itself; the host reads the count matrix, every rank's NO and the plan once.
+        # After the first build the pair count is not read back either (PG_DEFER): the pair
+        # buffers are sized by a capacity all ranks agree on (1.25 x the largest NO seen), and
+        # an overflow -- visible to every rank in the exchanged NOs -- repeats the build with
+        # the host-counted path.
+        while True:
+            cap = exchange.no_capacity
+            hist = st.phase_count(cap)
+            exchange.put_hist(hist, rank)
+            exchange.barrier()
+            st.phase_plan_device(exchange.hists(st.nb_coarse))
+            exchange.put_counts(st.phase_partition_counts_device(), rank, ops)
+            exchange.barrier()
+            matrix, nos, plan_arr = exchange.read_counts(st.plan_d)
+            exchange.no_capacity = int(nos.max() * 1.25) + 4096
+            if not cap or int(nos.max()) <= cap:
+                break
+        if st.deferred:
+            st.no = ops.count_result()     # validation of the deferred count (errors raise here)
+            assert st.no == int(nos[rank]) == int(matrix[rank].sum()), (st.no, nos, matrix)
+        plan = st.set_plan(plan_arr)
         exchange.ensure(int(np.asarray(matrix, dtype=np.int64).sum(axis=0).max()))
         dk, dv = exchange.destinations()
         nrecv = st.phase_send(matrix, dk, dv)
         exchange.barrier()
         krecv, vrecv = exchange.received(nrecv)
     else:
+        hist = comm.allreduce_sum(st.phase_count())
+        plan = plan_slabs(hist, st.ncells, world)
         send, recv = comm.alltoall_counts(st.phase_partition(plan))
         krecv, vrecv = comm.alltoall_pairs(st.kout, st.vout, send, recv, ops)
     base, G_rel, O = st.phase_sort(krecv, vrecv)
@@ -232,6 +286,40 @@ class PeerExchange:
         self.cap = 0
         self.buf = self.hdl = None
         self.ensure(1 << 20)
+        # control buffer: every rank's coarse histogram (slot r of CTL_HIST words) and slab
+        # counts (slot r of 16 words), written by the ranks themselves with peer stores
+        w = comm.world
+        group = comm.group or comm.dist.group.WORLD
+        self.ctl = symm.empty(w * (CTL_HIST + CTL_CNT), dtype=torch.int32, device=device)
+        self.ctl_hdl = symm.rendezvous(self.ctl, group)
+        self.ctl_ptrs = [int(p) for p in self.ctl_hdl.buffer_ptrs]
+        self._read_c = torch.empty(w * CTL_CNT, dtype=torch.int32).pin_memory()
+        self._read_p = torch.empty(4 * w + 2, dtype=torch.int64).pin_memory()
+        self.no_capacity = None      # pair capacity of deferred counts (set after the first build)
+
+    def _stream(self):
+        return self.torch.cuda.current_stream(self.dev).cuda_stream
+
+    def put_hist(self, hist, rank):
+        nb = int(hist.numel())
+        _native.peer_put(hist, nb, self.ctl_ptrs, rank * nb, self._stream())
+
+    def hists(self, nb):
+        return self.ctl[:self.comm.world * nb]
+
+    def put_counts(self, counts, rank, ops):
+        w = self.comm.world
+        _native.peer_put(counts, w, self.ctl_ptrs, w * CTL_HIST + rank * CTL_CNT, self._stream())
+        ops.b.peer_put_count(self.ctl_ptrs, w * CTL_HIST + rank * CTL_CNT + 16, self._stream())
+
+    def read_counts(self, plan_d):
+        """The count matrix [rank][slab], every rank's NO and the device plan: one host
+        round trip (two small copies into page-locked memory, one synchronise)."""
+        torch, w = self.torch, self.comm.world
+        self._read_c.copy_(self.ctl[w * CTL_HIST:w * (CTL_HIST + CTL_CNT)], non_blocking=True)
+        self._read_p.copy_(plan_d, non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        return _split_counts(self._read_c.numpy(), w) + (self._read_p.numpy().copy(),)
 
     def allgather_counts(self, counts):
         """counts: this rank's per-slab send counts (device) -> host matrix [rank][slab]."""
@@ -268,6 +356,27 @@ class EmulatedExchange:
     def __init__(self, torch, device, world):
         self.torch, self.dev, self.world = torch, device, world
         self.cap = 0
+        self.ctl = [torch.zeros(world * (CTL_HIST + CTL_CNT), dtype=torch.int32, device=device)
+                    for _ in range(world)]
+        self.ctl_ptrs = [int(c.data_ptr()) for c in self.ctl]
+
+    def put_hist(self, hist, rank):
+        nb = int(hist.numel())
+        _native.peer_put(hist, nb, self.ctl_ptrs, rank * nb, self.torch.cuda.current_stream(self.dev).cuda_stream)
+
+    def hists(self, r, nb):
+        return self.ctl[r][:self.world * nb]
+
+    def put_counts(self, counts, rank, ops):
+        w = self.world
+        sp = self.torch.cuda.current_stream(self.dev).cuda_stream
+        _native.peer_put(counts, w, self.ctl_ptrs, w * CTL_HIST + rank * CTL_CNT, sp)
+        ops.b.peer_put_count(self.ctl_ptrs, w * CTL_HIST + rank * CTL_CNT + 16, sp)
+
+    def read_counts(self, r, plan_d):
+        w = self.world
+        c = self.ctl[r][w * CTL_HIST:w * (CTL_HIST + CTL_CNT)].cpu().numpy()
+        return _split_counts(c, w) + (plan_d.cpu().numpy(),)
 
     def ensure(self, n):
         if n > self.cap:
@@ -283,9 +392,17 @@ class EmulatedExchange:
         return self.bufs[r][:n], self.bufs[r][self.cap:self.cap + n]
 
 
-def run_emulated(make_ops, V, T, spec, world, exchange="copy"):
+def _split_counts(c, w):
+    """Control-buffer count slots (int32 [w][CTL_CNT]) -> (matrix [rank][slab], NO per rank)."""
+    c = np.asarray(c).view(np.uint32).reshape(w, CTL_CNT).astype(np.int64)
+    return c[:, :w].copy(), c[:, 16] | (c[:, 17] << 32)
+
+
+def run_emulated(make_ops, V, T, spec, world, exchange="copy", capacity=None):
     """Every rank's phases executed in sequence in one process (no inter-rank waiting):
-    exercises the kernels and the orchestration of the sharded build on a single device."""
+    exercises the kernels and the orchestration of the sharded build on a single device.
+    exchange="p2p": the fused exchange with the device plan; capacity: deferred counts with
+    that pair capacity (returns None when some rank's pairs exceeded it)."""
     n = len(T)
     states = []
     for r in range(world):
@@ -294,8 +411,32 @@ def run_emulated(make_ops, V, T, spec, world, exchange="copy"):
     hist = np.sum([s.ops.to_numpy(s.phase_count()).astype(np.int64) for s in states], axis=0)
     plan = plan_slabs(hist, states[0].ncells, world)
     if exchange == "p2p":       # fused partition + send into the owners' buffers (CudaOps only)
-        matrix = np.array([s.ops.to_numpy(s.phase_partition_counts(plan))[:world] for s in states], np.int64)
+        # as build_sharded with a PeerExchange: histograms, plan and counts through the
+        # (emulated) peer buffers, slab plans computed on the device by every rank
         ex = EmulatedExchange(states[0].ops.torch, states[0].ops.dev, world)
+        hists = [s.phase_count(capacity) for s in states]
+        for r, s in enumerate(states):
+            ex.put_hist(hists[r], r)
+        for r, s in enumerate(states):
+            s.phase_plan_device(ex.hists(r, s.nb_coarse))
+        for r, s in enumerate(states):
+            ex.put_counts(s.phase_partition_counts_device(), r, s.ops)
+        plans = []
+        for r, s in enumerate(states):
+            matrix, nos, plan_arr = ex.read_counts(r, s.plan_d)
+            if capacity and int(nos.max()) > capacity:
+                assert all(s2.ops.b.count_result() < 0 for s2, n2 in zip(states, nos) if n2 > capacity)
+                return None
+            if s.deferred:
+                s.no = s.ops.count_result()
+            assert int(nos[r]) == int(matrix[r].sum()) == s.no
+            plans.append(s.set_plan(plan_arr))
+        host = plan_slabs(np.sum([s.ops.to_numpy(h).astype(np.int64) for s, h in zip(states, hists)], axis=0),
+                          states[0].ncells, world)
+        for p in plans:              # the device plan is plan_slabs bit for bit
+            for f in ("cuts", "cell_lo", "cell_hi", "pair_base"):
+                assert np.array_equal(getattr(p, f), getattr(host, f)), f
+            assert np.array_equal(states[0].ops.to_numpy(p.table)[:host.nbuckets], host.table)
         ex.ensure(int(matrix.sum(axis=0).max()))
         dk, dv = ex.destinations()
         nrecv = [s.phase_send(matrix, dk, dv) for s in states]
@@ -387,6 +528,22 @@ class CudaOps:
         self._V, self._T = V, T          # keep alive for the stream
         return self.b.count(V, V.shape[0], T, T.shape[0], spec, 0, self._sp())
 
+    def count_deferred(self, V, T, spec, capacity):
+        """K1 without the NO read back (PG_DEFER)."""
+        flags = 0
+        if not isinstance(V, self.torch.Tensor):
+            V = np.ascontiguousarray(V, dtype=np.float64).reshape(-1, 3)
+            T = np.ascontiguousarray(T, dtype=np.int32).reshape(-1, 3)
+            flags = _native.PG_HOST_INPUT
+        self._V, self._T = V, T
+        return self.b.count_deferred(V, V.shape[0], T, T.shape[0], spec, capacity, flags, self._sp())
+
+    def count_result(self):
+        no = self.b.count_result()
+        if no < 0:
+            raise RuntimeError(f"deferred pair count {-no} exceeded its capacity")
+        return no
+
     def pairs(self, no, tri_base, shift, nbuckets):
         k, v = self._buf("pair_k", no), self._buf("pair_v", no)
         hist = self._buf("coarse", nbuckets)
@@ -404,18 +561,32 @@ class CudaOps:
         self.b.partition(keys, vals, n, dt, shift, nslabs, db, ko, vo, counts, self._sp())
         return ko, vo, counts
 
+    def slab_plan(self, hists, nranks, nbuckets, shift, ncells, nslabs):
+        table = self._buf("slab_table", nbuckets)
+        base = self._buf("slab_base", nslabs)
+        plan = self._bufs.get("slab_plan")
+        if plan is None or plan.numel() < 4 * nslabs + 2:
+            plan = self.torch.empty(4 * MAX_SLABS + 2, dtype=self.torch.int64, device=self.dev)
+            self._bufs["slab_plan"] = plan
+        plan = plan[:4 * nslabs + 2]
+        _native.slab_plan(hists, nranks, nbuckets, shift, ncells, nslabs, table, base, plan, self._sp())
+        return table, base, plan
+
+    def _dev_u32(self, a):
+        if isinstance(a, self.torch.Tensor):
+            return a
+        return self.torch.from_numpy(np.asarray(a, np.uint32).view(np.int32)).to(self.dev)
+
     def partition_counts(self, keys, table, shift, nslabs):
-        torch = self.torch
         n = int(keys.numel())
-        self._ptab = torch.from_numpy(np.asarray(table, np.uint32).view(np.int32)).to(self.dev)
+        self._ptab = self._dev_u32(table)
         counts = self._buf("slab_counts", 16)
         self.b.partition_counts(keys, n, self._ptab, shift, nslabs, counts, self._sp())
         return counts
 
     def partition_send(self, keys, vals, table, shift, nslabs, base, dst_keys, dst_vals, dst_offset):
-        torch = self.torch
         n = int(keys.numel())
-        self._pbase = torch.from_numpy(np.asarray(base, np.uint32).view(np.int32)).to(self.dev)
+        self._pbase = self._dev_u32(base)
         self.b.partition_send(keys, vals, n, self._ptab, shift, nslabs, self._pbase, dst_keys, dst_vals,
                               dst_offset, self._sp())
 

@@ -132,3 +132,69 @@ def test_single_rank_nccl_path(tmp_path):
             assert np.array_equal(G, Gr) and np.array_equal(O, Or)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8, 16])
+def test_device_slab_plan_matches_plan_slabs(world):
+    """pg_slab_plan (the device plan of the fused exchange) == distributed.plan_slabs, on
+    skewed, sparse, empty and tiny histograms."""
+    rng = np.random.default_rng(world)
+    ops = D.CudaOps()
+    for ncells, kind in [(40_001_688, "lognormal"), (40_001_688, "spike"), (5_000_211, "sparse"),
+                         (4096, "zero"), (7, "uniform"), (1 << 30, "uniform")]:
+        shift = D.coarse_shift(ncells)
+        nb = ((ncells - 1) >> shift) + 1
+        per_rank = []
+        for _ in range(world):
+            if kind == "lognormal":
+                h = rng.lognormal(3, 2, nb).astype(np.int64)
+            elif kind == "spike":
+                h = np.zeros(nb, np.int64)
+                h[rng.integers(0, nb, 3)] = rng.integers(1, 10**6, 3)
+            elif kind == "sparse":
+                h = np.where(rng.random(nb) < 0.01, rng.integers(0, 1000, nb), 0)
+            elif kind == "zero":
+                h = np.zeros(nb, np.int64)
+            else:
+                h = rng.integers(0, 50, nb)
+            per_rank.append(np.minimum(h, 2**31 - 1).astype(np.uint32))
+        hists = torch.from_numpy(np.concatenate(per_rank).view(np.int32)).cuda()
+        table, base, plan = ops.slab_plan(hists, world, nb, shift, ncells, world)
+        ref = D.plan_slabs(np.sum([h.astype(np.int64) for h in per_rank], axis=0), ncells, world)
+        a = plan.cpu().numpy()
+        P = world
+        assert np.array_equal(a[:P + 1], ref.cuts), kind
+        assert np.array_equal(a[P + 1:2 * P + 1], ref.cell_lo), kind
+        assert np.array_equal(a[2 * P + 1:3 * P + 1], ref.cell_hi), kind
+        assert np.array_equal(a[3 * P + 1:], ref.pair_base), kind
+        assert np.array_equal(ops.to_numpy(table)[:nb], ref.table), kind
+        assert np.array_equal(ops.to_numpy(base)[:P], ref.cell_lo.astype(np.uint32)), kind
+
+
+def test_peer_put_fills_every_slot():
+    from paper_2403_10647_b200 import _native
+    world = 5
+    bufs = [torch.full((world * 100,), -1, dtype=torch.int32, device="cuda") for _ in range(world)]
+    ptrs = [b.data_ptr() for b in bufs]
+    srcs = [torch.arange(r * 1000, r * 1000 + 77, dtype=torch.int32, device="cuda") for r in range(world)]
+    for r in range(world):
+        _native.peer_put(srcs[r], 77, ptrs, r * 100, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for b in bufs:
+        v = b.view(world, 100).cpu().numpy()
+        for r in range(world):
+            assert np.array_equal(v[r, :77], np.arange(r * 1000, r * 1000 + 77)) and (v[r, 77:] == -1).all()
+
+
+@pytest.mark.parametrize("world", [1, 3, 8])
+def test_emulated_fused_exchange_deferred_count(world):
+    """PG_DEFER counts (no NO read back; pair buffers sized by a capacity) == oracle; a
+    capacity below some rank's NO is detected by every rank (the exchanged NOs)."""
+    mesh = gen_scene("walls", 30000, 4)
+    spec = spec_for_mesh(mesh, dims=(61, 47, 53))
+    Gr, Or = oracle.build_parallel(mesh.vertices, mesh.triangles, spec)
+    G, O = D.run_emulated(D.CudaOps, mesh.vertices, mesh.triangles, spec, world, exchange="p2p",
+                          capacity=len(Or))
+    assert np.array_equal(G, Gr) and np.array_equal(O, Or)
+    assert D.run_emulated(D.CudaOps, mesh.vertices, mesh.triangles, spec, world, exchange="p2p",
+                          capacity=len(Or) // world // 2) is None

@@ -26,17 +26,27 @@ for it in range(6):
     t = time.perf_counter()
     e0 = torch.cuda.Event(enable_timing=True); e0.record(); E.setdefault("_start", []).append(e0)
     st = D.ShardState(ops, Vd, Td, 0, spec, 0, 1)
-    st.no = ops.count(Vd, Td, spec); t = tick("count", t)
+    if P2P and ex.no_capacity:   # deferred count (no NO read back), as build_sharded
+        st.deferred = True; st.no = ops.count_deferred(Vd, Td, spec, ex.no_capacity)
+    else:
+        st.deferred = False; st.no = ops.count(Vd, Td, spec)
+    t = tick("count", t)
     st.shift = D.coarse_shift(st.ncells); nb = ((st.ncells - 1) >> st.shift) + 1
+    st.nb_coarse = nb
     st.keys, st.vals, h = ops.pairs(st.no, 0, st.shift, nb); t = tick("pairs+hist", t)
-    h = comm.allreduce_sum(h); t = tick("allreduce", t)
-    plan = D.plan_slabs(h, st.ncells, 1); t = tick("plan", t)
-    if P2P:
-        c = st.phase_partition_counts(plan); t = tick("part_counts", t)
-        m = ex.allgather_counts(c); ex.ensure(int(m.sum(axis=0).max())); t = tick("allgather", t)
+    if P2P:   # device plan: peer put + barrier + plan kernel; counts the same way; one readback
+        ex.put_hist(h, 0); ex.barrier(); t = tick("put_hist", t)
+        st.phase_plan_device(ex.hists(nb)); t = tick("plan_dev", t)
+        ex.put_counts(st.phase_partition_counts_device(), 0, ops); t = tick("part_counts", t)
+        ex.barrier(); m, nos, pa = ex.read_counts(st.plan_d); st.set_plan(pa)
+        ex.no_capacity = int(nos.max() * 1.25) + 4096
+        if st.deferred: ops.count_result()
+        ex.ensure(int(m.sum(axis=0).max())); t = tick("read_counts", t)
         dk, dv = ex.destinations(); nr = st.phase_send(m, dk, dv); t = tick("send", t)
         ex.barrier(); kr, vr = ex.received(nr); t = tick("barrier", t)
     else:
+        h = comm.allreduce_sum(h); t = tick("allreduce", t)
+        plan = D.plan_slabs(h, st.ncells, 1); t = tick("plan", t)
         sc = st.phase_partition(plan); t = tick("partition", t)
         send, recv = comm.alltoall_counts(sc); t = tick("a2a_counts", t)
         kr, vr = comm.alltoall_pairs(st.kout, st.vout, send, recv, ops); t = tick("a2a_pairs", t)
