@@ -15,7 +15,8 @@ METRICS = {"gpu__time_duration.sum": "time_us", "dram__bytes_read.sum": "dram_re
            "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_pct",
            "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
            "launch__registers_per_thread": "regs", "launch__grid_size": "grid", "launch__block_size": "block",
-           "smsp__inst_executed.sum": "warp_instructions"}
+           "smsp__inst_executed.sum": "warp_instructions",
+           "l1tex__throughput.avg.pct_of_peak_sustained_active": "l1tex_pct"}
 SCALE = {"time_us": {"ns": 1e-3, "us": 1.0, "ms": 1e3}, "dram_read_bytes": {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9},
          "dram_write_bytes": {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}}
 
