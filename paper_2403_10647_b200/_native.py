@@ -191,11 +191,11 @@ class Builder:
 
     def count_result(self):
         """NO of the last PG_DEFER count (the stream must have been synchronised since);
-        -NO when it exceeded the capacity."""
+        -NO-1 when the deferred steps are void (NO exceeded the capacity, or an inverted box)."""
         no = ctypes.c_uint64(0)
         rc = self._lib.pg_count_result(self._h, ctypes.byref(no))
         if rc == PG_CAPACITY_ERROR:
-            return -int(no.value)
+            return -int(no.value) - 1      # always negative: rebuild on the host-counted path
         check(rc)
         return int(no.value)
 

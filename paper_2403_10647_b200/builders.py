@@ -215,25 +215,51 @@ class BuildPipeline:
         self._slots = [(_native.Builder(device), torch.cuda.Stream(device)) for _ in range(depth)]
         self._next = 0
         self._pending = collections.deque()
+        self._cap = None    # pair capacity of deferred counts: 1.25 x the largest NO seen
 
     def submit(self, mesh, spec):
+        """Enqueue one build. After the first, the pair count is not read back (PG_DEFER):
+        the copy in, Alg. 1 and the copies out are all enqueued without a host round trip, so
+        the next submit's input copy follows this one's on the copy engine at once. O is
+        copied at the capacity and cut to NO in result(); an overflow rebuilds that mesh."""
         if len(self._pending) == len(self._slots):
             raise RuntimeError("pipeline full: collect a result() first")
         b, st = self._slots[self._next]
         self._next = (self._next + 1) % len(self._slots)
         V, T = _mesh_arrays(mesh)
         t0 = time.perf_counter()
-        no = b.count(V, len(V), T, len(T), spec, flags=_native.PG_HOST_INPUT, stream=st.cuda_stream)
+        deferred = self._cap is not None and len(T) > 0
+        if deferred:
+            no = b.count_deferred(V, len(V), T, len(T), spec, self._cap, flags=_native.PG_HOST_INPUT,
+                                  stream=st.cuda_stream)
+        else:
+            no = b.count(V, len(V), T, len(T), spec, flags=_native.PG_HOST_INPUT, stream=st.cuda_stream)
         count_ms = (time.perf_counter() - t0) * 1e3
         ncells = int(spec.dims[0]) * int(spec.dims[1]) * int(spec.dims[2])
         G = _native.pinned_pool.empty(ncells + 1, np.uint32)
         O = _native.pinned_pool.empty(no, np.uint32)
         b.finish(G, O, flags=_native.PG_HOST_OUTPUT | _native.PG_ASYNC, stream=st.cuda_stream, timed=False)
-        self._pending.append((b, spec, G, O, no, count_ms))
+        self._pending.append((b, mesh, spec, G, O, no, count_ms, deferred))
+
+    def _learn(self, no):
+        cap = int(no * 1.0625) + 4096      # the O copy-out carries the slack
+        self._cap = cap if self._cap is None else max(self._cap, cap)
+
+    @property
+    def capacity(self):
+        """Pairs copied out per deferred build (O is read back at this size, then cut)."""
+        return self._cap
 
     def result(self):
-        b, spec, G, O, no, count_ms = self._pending.popleft()
+        b, mesh, spec, G, O, no, count_ms, deferred = self._pending.popleft()
         b.wait()
+        if deferred:
+            no = b.count_result()
+            if no < 0:            # over the capacity (or a corner the host path resolves): rebuild
+                self._learn(-no - 1)
+                return build_parallel(mesh, spec, device=self.device)
+            O = O[:no]
+        self._learn(no)
         ms = {p: 0.0 for p in PHASES}
         ms["count"] = count_ms
         report = BuildReport("parallel", no=no, max_task_work=PAIRGEN_OPS_PER_PAIR if no else 0,

@@ -565,11 +565,15 @@ int pg_count_result(pg_builder* b, uint64_t* no_out) {
   if (!b->counted || !b->deferred) return fail(PG_STATE_ERROR, "pg_count_result without a PG_DEFER pg_count");
   CU(cudaSetDevice(b->device));
   const uint64_t cap = b->no;
+  const bool inverted = (b->h_scalars[1] & 1u) != 0;
   int rc = count_check(b, no_out);  // reads the scalars copied back by the (synchronised) stream
   b->deferred = true;
   b->counted = rc == PG_OK;
   b->no = cap;
   if (rc) return rc;
+  // an accepted inverted box (the reference's empty grid) ran the device steps on the raw
+  // count: the results are void, report it like an overflow so the caller rebuilds
+  if (inverted) return fail(PG_CAPACITY_ERROR, "deferred build of a mesh with an inverted cell box");
   if (*no_out > cap)
     return fail(PG_CAPACITY_ERROR, "%llu pairs exceed the PG_DEFER capacity %llu", (unsigned long long)*no_out,
                 (unsigned long long)cap);
@@ -764,8 +768,10 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
   CU(cudaSetDevice(b->device));
   drop_graph(b);
   if (ktimes_on()) cudaEventRecord(g_kt.next("(host gap)"), static_cast<cudaStream_t>(stream_));
-  return finish_impl(b, G, O, flags, static_cast<cudaStream_t>(stream_), phase_ms, Count{nullptr, (unsigned)b->no},
-                     b->no);
+  // after a PG_DEFER count, b->no is the capacity and the kernels read NO from the device
+  // (O, host or device, must hold the capacity); pg_count_result validates NO afterwards
+  return finish_impl(b, G, O, flags, static_cast<cudaStream_t>(stream_), phase_ms,
+                     Count{b->deferred ? b->d_total : nullptr, (unsigned)b->no}, b->no);
 }
 
 // Sync-free build on device-resident data: the whole of Alg. 1 is enqueued without reading

@@ -282,8 +282,15 @@ k_boxes_count(const double* __restrict__ V, long long nv, const int* __restrict_
   }
   const bool soup = __syncthreads_and(mine) && spec_v;
   if (!__syncthreads_and(inrange)) {
-    if (tid == 0) atomicOr(err, 2u);
-    return;  // never gather through an out-of-range index
+    if (tid == 0) {
+      atomicOr(err, 2u);
+      tile_sum[tile] = 0;
+    }
+    // never gather through an out-of-range index; the tile contributes no pairs, so steps
+    // that run on the device count before the host sees the error (PG_DEFER, the graph
+    // build) stay in bounds
+    for (int i = tid; i < tcount; i += K1_THREADS) rec[tbase + i] = make_uint4(0u, 1u, 1u, 0u);
+    return;
   }
 
   const unsigned dx = (unsigned)s.dims[0], dxy = (unsigned)s.dims[0] * (unsigned)s.dims[1];

@@ -541,7 +541,7 @@ class CudaOps:
     def count_result(self):
         no = self.b.count_result()
         if no < 0:
-            raise RuntimeError(f"deferred pair count {-no} exceeded its capacity")
+            raise RuntimeError(f"deferred pair count void (NO {-no - 1} over the capacity, or an inverted box)")
         return no
 
     def pairs(self, no, tri_base, shift, nbuckets):

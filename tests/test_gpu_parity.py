@@ -279,3 +279,35 @@ def test_inverted_boxes_match_reference_verdicts():
         else:
             grid, rep = builders.build_parallel(TriangleMesh(V, T), spec)
             assert np.array_equal(grid.G, want[0]) and np.array_equal(grid.O, want[1]) and rep.no == 0
+
+
+def test_build_pipeline_deferred_corners(hashes):
+    """Deferred submits (no NO read back): inverted boxes and out-of-range indices give the
+    reference's verdicts at result(), and the pipeline keeps working afterwards."""
+    import types
+    from test_oracle import _inverted_cases
+    mesh0, spec0 = scene_from_recipe(hashes["cfg1"]["recipe"])
+    want0, _ = builders.build_parallel(mesh0, spec0)
+    pipe = builders.BuildPipeline(depth=1)
+    pipe.submit(mesh0, spec0)
+    pipe.result()                       # learns a capacity: every later submit is deferred
+    for V, T, spec in _inverted_cases():
+        try:
+            want = oracle.build_parallel(V, T, spec)
+        except oracle.OracleInvariantError:
+            want = None
+        pipe.submit(TriangleMesh(V, T), spec)
+        if want is None:
+            with pytest.raises(InvariantError):
+                pipe.result()
+        else:
+            grid, rep = pipe.result()
+            assert np.array_equal(grid.G, want[0]) and np.array_equal(grid.O, want[1]) and rep.no == 0
+    bad = mesh0.triangles.copy()
+    bad[5, 1] = len(mesh0.vertices) + 7   # bypasses TriangleMesh's host check
+    pipe.submit(types.SimpleNamespace(vertices=mesh0.vertices, triangles=bad), spec0)
+    with pytest.raises(InvariantError):
+        pipe.result()
+    pipe.submit(mesh0, spec0)
+    grid, rep = pipe.result()
+    assert np.array_equal(grid.G, want0.G) and np.array_equal(grid.O, want0.O)
