@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--cpu-budget-s", type=float, default=150.0)
     ap.add_argument("--sharded", action="store_true", help="use the sharded path even at N=1 (testing)")
     ap.add_argument("--nccl-exchange", action="store_true", help="sharded: partition pass + NCCL all_to_all")
+    ap.add_argument("--fused-dispatch", action="store_true",
+                    help="sharded: expansion + dispatch in one kernel (pg_pairs_send; measured slower, off)")
     return ap.parse_args()
 
 
@@ -240,11 +242,14 @@ def run_sharded(args, world, rank, local):
             ex = D.PeerExchange(comm, dev)
         except Exception as e:          # noqa: BLE001 -- reported in the JSON line
             why = f"{type(e).__name__}: {e}"[:200]
+    if ex is not None and args.fused_dispatch:
+        ex.fused = True
     ok = torch.tensor([1 if ex is not None else 0], device=dev)
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     if int(ok.item()) == 0:
         ex = None
-    exchange_desc = ("fused partition + peer stores (symmetric memory)" if ex is not None
+    exchange_desc = (("expansion + slab dispatch in one kernel, peer stores (symmetric memory)" if ex.fused else
+                      "fused partition + peer stores (symmetric memory)") if ex is not None
                      else "partition pass + NCCL all_to_all" + (f" ({why})" if why else ""))
 
     def step():

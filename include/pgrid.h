@@ -197,6 +197,22 @@ int pg_sort_cells(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int
  *                   cell_hi[nslabs] | pair_base[nslabs+1] (int64), all device; the same
  *                   arithmetic as distributed.plan_slabs */
 int pg_count_result(pg_builder *b, uint64_t *no_out); /* after PG_DEFER + a stream synchronise */
+/* Fused dispatch of the sharded build (pair expansion + slab partition + peer stores in one
+ * kernel; replaces pg_pairs + pg_partition_counts + pg_partition_send):
+ *   pg_coarse_hist -- after pg_count: the histogram of cell >> coarse_shift (coarse_bins <=
+ *                     4096 u32 bins, device) computed from the triangles' cell boxes, before
+ *                     any pair exists; equals pg_pairs' coarse histogram
+ *   pg_pairs_send  -- expand the counted shard's pairs (triangle ids += val_offset), rank each
+ *                    4096-pair tile by slab = slab_of_bucket[cell >> bucket_shift] and store
+ *                    every pair into its slab owner's receive buffer (dst_keys/dst_vals[s] +
+ *                    dst_offset[s] + this rank's running slab count; keys rebased by
+ *                    slab_base[s]). The running counts are a decoupled look-back over the
+ *                    tiles. Same pair order as pg_partition_send; the caller barriers the ranks
+ *                    before the receivers read. Host arrays of nslabs device pointers/offsets. */
+int pg_coarse_hist(pg_builder *b, int coarse_shift, int coarse_bins, uint32_t *coarse_hist, void *stream);
+int pg_pairs_send(pg_builder *b, uint32_t val_offset, const uint32_t *slab_of_bucket, int bucket_shift,
+                  int nslabs, const uint32_t *slab_base, const uint64_t *dst_keys, const uint64_t *dst_vals,
+                  const uint64_t *dst_offset, void *stream);
 int pg_peer_put(const uint32_t *src, int64_t n, const uint64_t *dsts, int nranks, int64_t dst_offset,
                 void *stream);
 /* pg_peer_put of the builder's device pair count (NO of its last pg_count, u64 as two u32

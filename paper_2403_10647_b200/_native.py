@@ -37,7 +37,7 @@ NPHASES = 6
 EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
            "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_finish_baseline",
            "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_partition_counts", "pg_partition_send", "pg_peer_put", "pg_slab_plan", "pg_count_result",
-           "pg_peer_put_count",
+           "pg_peer_put_count", "pg_coarse_hist", "pg_pairs_send",
            "pg_build_async",
            "pg_build_wait", "pg_host_register",
            "pg_host_unregister", "pg_host_alloc", "pg_host_free", "pg_last_launch_count",
@@ -101,6 +101,9 @@ def load():
                                           ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64), vp]
         lib.pg_kernel_timing.argtypes = [ctypes.c_int]
         lib.pg_count_result.argtypes = [vp, ctypes.POINTER(u64)]
+        lib.pg_coarse_hist.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp]
+        lib.pg_pairs_send.argtypes = [vp, u32, vp, ctypes.c_int, ctypes.c_int, vp, ctypes.POINTER(u64),
+                                      ctypes.POINTER(u64), ctypes.POINTER(u64), vp]
         lib.pg_peer_put_count.argtypes = [vp, ctypes.POINTER(u64), ctypes.c_int, i64, vp]
         lib.pg_peer_put.argtypes = [vp, i64, ctypes.POINTER(u64), ctypes.c_int, i64, vp]
         lib.pg_slab_plan.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, i64, ctypes.c_int, vp, vp, vp, vp]
@@ -286,6 +289,17 @@ class Builder:
         also the histogram of cell >> coarse_shift. No host synchronisation."""
         check(self._lib.pg_pairs(self._h, ptr(keys), ptr(vals), int(val_offset), int(coarse_shift),
                                  int(coarse_bins), ptr(coarse_hist), stream))
+
+    def coarse_hist(self, coarse_shift, coarse_bins, coarse_hist, stream=None):
+        """Histogram of cell >> coarse_shift of the counted mesh's pairs, from its cell boxes."""
+        check(self._lib.pg_coarse_hist(self._h, int(coarse_shift), int(coarse_bins), ptr(coarse_hist), stream))
+
+    def pairs_send(self, val_offset, table, shift, nslabs, base, dst_keys, dst_vals, dst_offset, stream=None):
+        """Fused dispatch: expand the pairs and store each into its slab owner's buffer."""
+        arr = ctypes.c_uint64 * len(dst_keys)
+        check(self._lib.pg_pairs_send(self._h, int(val_offset), ptr(table), int(shift), int(nslabs), ptr(base),
+                                      arr(*[int(x) for x in dst_keys]), arr(*[int(x) for x in dst_vals]),
+                                      arr(*[int(x) for x in dst_offset]), stream))
 
     def partition(self, keys, vals, n, slab_of_bucket, bucket_shift, nslabs, slab_base, keys_out,
                   vals_out, slab_counts, stream=None):

@@ -286,6 +286,7 @@ struct pg_builder {
   DevBuf rec, k1_sync;
   // pair buffers and sort scratch
   DevBuf pairs, sort_sync, stage, stage0, gbuf, obuf, cells;
+  DevBuf send;  // fused dispatch: tile bounds, look-back status, ticket
   // state of the last pg_count
   bool counted = false;
   bool deferred = false;  // PG_DEFER: NO is on the device only; `no` holds the capacity
@@ -343,6 +344,10 @@ int pg_builder_create(int device, pg_builder** out) {
   CU(set_scatter_smem<7>()); CU(set_scatter_smem<8>()); CU(set_scatter_smem<9>());
   for (auto f : {k_partition_send<1>, k_partition_send<2>, k_partition_send<3>, k_partition_send<4>})
     CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem_bytes()));
+  for (auto f : {k_pairs_send<1>, k_pairs_send<2>, k_pairs_send<3>, k_pairs_send<4>})
+    CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SendSmem)));
+  CU(cudaFuncSetAttribute(k_coarse_from_boxes, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PLAN_MAX_BUCKETS));
+  CU(cudaFuncSetAttribute(k_coarse_big, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PLAN_MAX_BUCKETS));
   for (auto f : {k_radix_scatter_wc<1>, k_radix_scatter_wc<2>, k_radix_scatter_wc<3>, k_radix_scatter_wc<4>,
                  k_radix_scatter_wc<5>, k_radix_scatter_wc<6>, k_radix_scatter_wc<7>, k_radix_scatter_wc<8>,
                  k_radix_scatter_wc<9>})
@@ -362,7 +367,7 @@ void pg_builder_destroy(pg_builder* b) {
   if (b->g_out) cudaEventDestroy(b->g_out);
   if (b->gst) cudaStreamDestroy(b->gst);
   for (DevBuf* d : {&b->in_v, &b->in_t, &b->rec, &b->k1_sync, &b->pairs, &b->sort_sync, &b->stage, &b->stage0,
-                    &b->gbuf, &b->obuf, &b->cells})
+                    &b->gbuf, &b->obuf, &b->cells, &b->send})
     d->release();
   delete b;
 }
@@ -1600,6 +1605,86 @@ int pg_partition_send(pg_builder* b, const uint32_t* keys, const uint32_t* vals,
   }
   LAUNCHED("k_partition_send", st);
   b->launches = 1;
+  return PG_OK;
+}
+
+int pg_coarse_hist(pg_builder* b, int coarse_shift, int coarse_bins, uint32_t* coarse_hist, void* stream_) {
+  if (!b || !b->counted) return fail(PG_STATE_ERROR, "pg_coarse_hist without a successful pg_count");
+  if (!coarse_hist || coarse_bins < 1 || coarse_bins > PLAN_MAX_BUCKETS || coarse_shift < 0 || coarse_shift > 31)
+    return fail(PG_INVARIANT_ERROR, "coarse_bins must be in [1, %d]", PLAN_MAX_BUCKETS);
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  drop_graph(b);
+  CU(cudaMemsetAsync(coarse_hist, 0, (size_t)coarse_bins * 4, st));
+  if (b->n == 0 || b->no == 0) return PG_OK;
+  const Count cno{b->deferred ? b->d_total : nullptr, (unsigned)b->no};
+  const unsigned dxu = (unsigned)b->dims[0], dxyu = (unsigned)b->dims[0] * (unsigned)b->dims[1];
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
+  // queue of objects with many rows (walls): [count][ids...]; a full queue falls back inline
+  const unsigned big_cap = 1u << 16;
+  int rc;
+  if ((rc = b->send.ensure(((size_t)big_cap + 64) * 4))) return rc;
+  unsigned* big = b->send.as<unsigned>(0);
+  CU(cudaMemsetAsync(big, 0, 4, st));
+  const unsigned grid = (unsigned)std::min<long long>((b->n + 255) / 256, 4LL * sms);
+  k_coarse_from_boxes<<<grid, 256, (size_t)coarse_bins * 4, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, cno, dxu,
+                                                                  dxyu, coarse_shift, coarse_bins, coarse_hist, big,
+                                                                  big_cap);
+  LAUNCHED("k_coarse_from_boxes", st);
+  k_coarse_big<<<2 * sms, 256, (size_t)coarse_bins * 4, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, cno, dxu, dxyu,
+                                                              coarse_shift, coarse_bins, coarse_hist, big, big_cap);
+  LAUNCHED("k_coarse_big", st);
+  b->launches = 2;
+  return PG_OK;
+}
+
+int pg_pairs_send(pg_builder* b, uint32_t val_offset, const uint32_t* slab_of_bucket, int bucket_shift, int nslabs,
+                  const uint32_t* slab_base, const uint64_t* dst_keys, const uint64_t* dst_vals,
+                  const uint64_t* dst_offset, void* stream_) {
+  if (!b || !b->counted) return fail(PG_STATE_ERROR, "pg_pairs_send without a successful pg_count");
+  if (!dst_keys || !dst_vals || !dst_offset || !slab_of_bucket || !slab_base)
+    return fail(PG_INVARIANT_ERROR, "null argument");
+  if (nslabs < 1 || nslabs > kMaxP2P) return fail(PG_INVARIANT_ERROR, "nslabs must be in [1, %d]", kMaxP2P);
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  CU(cudaSetDevice(b->device));
+  drop_graph(b);
+  const uint64_t no = b->no;  // PG_DEFER: the capacity (grid); the kernels read the device count
+  if (no == 0) return PG_OK;
+  P2PDst dst{};
+  for (int s2 = 0; s2 < nslabs; ++s2) {
+    dst.k[s2] = reinterpret_cast<unsigned*>(dst_keys[s2]);
+    dst.v[s2] = reinterpret_cast<unsigned*>(dst_vals[s2]);
+    dst.off[s2] = dst_offset[s2];
+    if (dst_offset[s2] >= (1ull << 32)) return fail(PG_SIZE_ERROR, "receive offset exceeds 32 bits");
+  }
+  const Count cno{b->deferred ? b->d_total : nullptr, (unsigned)no};
+  const unsigned ntiles = (unsigned)((no + RS_TILE - 1) / RS_TILE);
+  const size_t bnd_bytes = align_up((size_t)ntiles * 8 + 8), st_bytes = align_up((size_t)ntiles * kMaxP2P * 8);
+  int rc;
+  if ((rc = b->send.ensure(bnd_bytes + st_bytes + 256))) return rc;
+  int2* bounds = b->send.as<int2>(0);
+  unsigned long long* status = b->send.as<unsigned long long>(bnd_bytes);
+  unsigned* ticket = b->send.as<unsigned>(bnd_bytes + st_bytes);
+  CU(cudaMemsetAsync(status, 0, st_bytes + 256, st));  // look-back flags and the ticket
+  const unsigned dxu = (unsigned)b->dims[0], dxyu = (unsigned)b->dims[0] * (unsigned)b->dims[1];
+  k_pair_tile_bounds<<<(ntiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, cno, RS_TILE, bounds);
+  LAUNCHED("k_pair_tile_bounds", st);
+  const int bits = std::max(1, bit_length((uint64_t)(nslabs - 1)));
+  const LookBack lb{status};
+  switch (bits) {
+#define PG_CASE(B)                                                                                                   \
+  case B:                                                                                                            \
+    k_pairs_send<B><<<ntiles, RS_THREADS, sizeof(SendSmem), st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, cno, dxu,    \
+                                                                  dxyu, bounds, val_offset, bucket_shift,             \
+                                                                  slab_of_bucket, slab_base, dst, lb, ticket);        \
+    break;
+    PG_CASE(1) PG_CASE(2) PG_CASE(3) PG_CASE(4)
+#undef PG_CASE
+    default: return fail(PG_INVARIANT_ERROR, "bad slab digit width");
+  }
+  LAUNCHED("k_pairs_send", st);
+  b->launches = 2;
   return PG_OK;
 }
 

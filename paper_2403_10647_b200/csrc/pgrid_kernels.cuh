@@ -1038,7 +1038,22 @@ struct P2PDst {
   unsigned long long off[kMaxP2P];
 };
 
-template <int BITS, bool FULL, bool TABLE = false, bool SRC_SMEM = false, bool P2P = false>
+// Decoupled look-back over <= 16 slab counters per tile (the fused pair dispatch): status[tile]
+// [slab] = flag << 62 | count, flag LB_AGG (this tile's count) or LB_PREFIX (inclusive prefix).
+// Tiles are claimed in order from a ticket, so every predecessor is resident and publishes.
+struct LookBack {
+  unsigned long long* status;
+};
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <int BITS, bool FULL, bool TABLE = false, bool SRC_SMEM = false, bool P2P = false, bool LB = false>
 __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* __restrict__ keys_in,
                                                    const unsigned* __restrict__ vals_in,
                                                    unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out,
@@ -1047,10 +1062,12 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
                                                    const unsigned* __restrict__ offs,
                                                    const unsigned* __restrict__ dtable = nullptr,
                                                    const unsigned* __restrict__ kbase = nullptr,
-                                                   const P2PDst* __restrict__ p2p = nullptr) {
+                                                   const P2PDst* __restrict__ p2p = nullptr,
+                                                   const LookBack* __restrict__ lb = nullptr) {
   constexpr int NB = 1 << BITS;
   constexpr unsigned DMASK = (unsigned)NB - 1u;
   static_assert(!P2P || (TABLE && NB <= kMaxP2P), "peer scatter: slab digits only");
+  static_assert(!LB || NB <= kMaxP2P, "look-back: slab digits only");
   // digit of a key: bit field, or slab id = dtable[key >> shift] (keys then leave rebased
   // by kbase[slab], i.e. relative to their slab's first cell)
   auto digit = [&](unsigned k) -> unsigned { return TABLE ? __ldg(&dtable[k >> shift]) : (k >> shift) & DMASK; };
@@ -1066,7 +1083,7 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
     const int d = tid * RS_DPT + q;
     if (d < NB) {
       if (!P2P) cp_async4(&sm.hsm[d], hist + d);
-      cp_async4(&sm.gbase[d], offs + (size_t)d * ld + tile);
+      if (!LB) cp_async4(&sm.gbase[d], offs + (size_t)d * ld + tile);
     }
   }
   cp_async_commit();
@@ -1133,9 +1150,53 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
   for (int q = 0; q < RS_DPT; ++q) {
     const int d = tid * RS_DPT + q;
     hs[q] = (!P2P && d < NB) ? sm.hsm[d] : 0u;
-    toff[q] = d < NB ? sm.gbase[d] : 0u;
+    toff[q] = (!LB && d < NB) ? sm.gbase[d] : 0u;
   }
   const unsigned tsum = tc[0] + tc[1], hsum = hs[0] + hs[1];
+  if constexpr (LB) {
+    // this tile's exclusive prefix per slab over the preceding tiles: decoupled look-back,
+    // one warp per slab reading a window of 32 predecessors per round trip
+    unsigned long long* row = lb->status + (size_t)tile * kMaxP2P;
+    const int lane = tid & 31;
+#pragma unroll
+    for (int q = 0; q < RS_DPT; ++q) {
+      const int d = tid * RS_DPT + q;
+      if (d < NB) {
+        st_release_u64(row + d, (tile ? LB_AGG : LB_PREFIX) | tc[q]);
+        sm.hsm[d] = tc[q];  // (hsm is unused by the peer scatter)
+      }
+    }
+    __syncthreads();
+    for (int d = warp; d < NB; d += RS_WARPS) {
+      unsigned long long pre = 0;
+      if (tile) {
+        for (long long j0 = (long long)tile - 1;; j0 -= 32) {
+          const long long j = j0 - lane;
+          unsigned long long v = 0;
+          if (j >= 0) {
+            do {
+              v = ld_acquire_u64(lb->status + (size_t)j * kMaxP2P + d);
+            } while (!(v >> 62));
+          }
+          const unsigned pm = __ballot_sync(0xffffffffu, j < 0 || (v >> 62) == 2ull);
+          const int first = pm ? __ffs(pm) - 1 : 31;  // the closest inclusive prefix ends the walk
+          unsigned long long x = (lane <= first && j >= 0) ? (v & LB_VALUE) : 0ull;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+          pre += x;
+          if (pm) break;
+        }
+        if (lane == 0) st_release_u64(row + d, LB_PREFIX | (pre + sm.hsm[d]));
+      }
+      if (lane == 0) sm.gbase[d] = (unsigned)pre;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < RS_DPT; ++q) {
+      const int d = tid * RS_DPT + q;
+      toff[q] = d < NB ? sm.gbase[d] : 0u;
+    }
+  }
   unsigned ttot, htot;
   unsigned lpre = block_excl_scan<RS_WARPS>(tsum, sm.wsum, ttot);
   unsigned hpre = block_excl_scan<RS_WARPS>(hsum, sm.wsum, htot);
@@ -1783,6 +1844,159 @@ k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pr
   for (int b = tid; b < (1 << plan.bits[0]); b += RS_THREADS) counts0[(size_t)b * ld + blockIdx.x] = sm.h[b];
 }
 
+
+// ----------------------------------------------------------------------------------------
+// Sharded build, fused dispatch: pair expansion + slab partition + peer stores in ONE kernel.
+// Each CTA claims the next 4096-pair tile from a ticket, expands it exactly as K2 does, ranks
+// the pairs by slab (table digit, <= 16 slabs) and writes them straight into the slab
+// owners' receive buffers (peer memory) at offset[slab] + tile prefix + rank; the tile
+// prefixes come from a decoupled look-back over the slab counters (LookBack). So the pairs
+// never touch this GPU's memory: no local pair buffer, no partition pass.
+// ----------------------------------------------------------------------------------------
+struct SendSmem {
+  __align__(16) int slot[RS_TILE];  // expansion slots, then the tile's keys in element order
+  union {
+    struct {
+      __align__(16) ObjCache oc;
+      int warpmax[RS_WARPS];
+    } pe;
+    RsSmem rs;  // the slab scatter (its vstage receives the values)
+  } u;
+  unsigned tile;
+};
+
+template <int BITS>
+__global__ void __launch_bounds__(RS_THREADS, 3)
+k_pairs_send(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno,
+             unsigned dx, unsigned dxy, const int2* __restrict__ bounds, unsigned val_offset, int shift,
+             const unsigned* __restrict__ dtable, const unsigned* __restrict__ kbase, const P2PDst dst,
+             LookBack lb, unsigned* __restrict__ ticket) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  SendSmem& sm = *reinterpret_cast<SendSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  if (tid == 0) sm.tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const unsigned tile = sm.tile;
+  const unsigned no = cno.get();
+  const unsigned p0 = tile * (unsigned)RS_TILE;
+  if (p0 >= no) return;
+  const unsigned pend = min(p0 + (unsigned)RS_TILE, no);
+  unsigned key[RS_ITEMS];
+  int own[RS_ITEMS];
+  expand_tile<RS_THREADS, RS_ITEMS>(rec, n, p0, pend, dx, dxy, tile_pre, bounds, sm.slot, sm.u.pe.warpmax,
+                                    &sm.u.pe.oc, key, own);
+  __syncthreads();  // the object cache is dead: the scatter's buffers overlay it
+  unsigned* skey = reinterpret_cast<unsigned*>(sm.slot);
+#pragma unroll
+  for (int q = 0; q < RS_ITEMS / 4; ++q) {
+    reinterpret_cast<uint4*>(skey)[tid * (RS_ITEMS / 4) + q] =
+        make_uint4(key[4 * q], key[4 * q + 1], key[4 * q + 2], key[4 * q + 3]);
+    reinterpret_cast<uint4*>(sm.u.rs.vstage)[tid * (RS_ITEMS / 4) + q] =
+        make_uint4(own[4 * q] + val_offset, own[4 * q + 1] + val_offset, own[4 * q + 2] + val_offset,
+                   own[4 * q + 3] + val_offset);
+  }
+  __syncthreads();
+  const unsigned tvalid = pend - p0;
+  if (tvalid == (unsigned)RS_TILE)
+    radix_scatter_tile<BITS, true, true, true, true, true>(sm.u.rs, skey, nullptr, nullptr, nullptr, 0, tvalid, tile,
+                                                           0, shift, nullptr, nullptr, dtable, kbase, &dst, &lb);
+  else
+    radix_scatter_tile<BITS, false, true, true, true, true>(sm.u.rs, skey, nullptr, nullptr, nullptr, 0, tvalid, tile,
+                                                            0, shift, nullptr, nullptr, dtable, kbase, &dst, &lb);
+}
+
+// Coarse histogram of the pair cell ids (cell >> shift) straight from K1's box records,
+// before any pair exists (the fused dispatch plans the slabs first): object i's cells are
+// my*mz rows of mx consecutive ids lo + y*dx + z*dxy (x fastest, builders.py:104-117); each
+// row adds its overlap with every bucket it spans. Counts equal K2's coarse histogram.
+// Objects with more than COARSE_BIG rows (walls, floors: up to 65K rows) are queued and
+// spread over a whole CTA by k_coarse_big, so no thread walks a wall alone.
+constexpr unsigned COARSE_BIG = 256;
+__device__ __forceinline__ void coarse_row(unsigned* hsh, unsigned a, unsigned mx, int shift) {
+  const unsigned e = a + mx;  // cells [a, e)
+  unsigned b = a >> shift;
+  const unsigned bl = (e - 1) >> shift;
+  if (b == bl) {
+    atomicAdd(&hsh[b], mx);
+  } else {
+    for (; b <= bl; ++b) {
+      const unsigned lo = max(a, b << shift), hi = min(e, (b + 1) << shift);
+      atomicAdd(&hsh[b], hi - lo);
+    }
+  }
+}
+__device__ __forceinline__ unsigned coarse_count(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre,
+                                                 long long n, unsigned no, long long i, uint4& r) {
+  r = __ldg(&rec[i]);
+  const unsigned off = __ldg(&tile_pre[i / K1_TILE]) + r.w;
+  const unsigned nxt = i + 1 < n ? tri_offset(rec, tile_pre, i + 1) : no;
+  return nxt > off ? nxt - off : 0u;
+}
+
+__global__ void __launch_bounds__(256)
+k_coarse_from_boxes(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno,
+                    unsigned dx, unsigned dxy, int shift, int nbins, unsigned* __restrict__ coarse,
+                    unsigned* __restrict__ big, unsigned big_cap) {
+  extern __shared__ unsigned hsh[];
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x) hsh[b] = 0u;
+  __syncthreads();
+  const unsigned no = cno.get();
+  // COARSE_U objects per thread per round, their loads issued together (latency-bound loop)
+  constexpr int COARSE_U = 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += stride * COARSE_U) {
+    uint4 r[COARSE_U];
+    unsigned cnt[COARSE_U];
+#pragma unroll
+    for (int u = 0; u < COARSE_U; ++u) {
+      const long long i = i0 + u * stride;
+      cnt[u] = i < n ? coarse_count(rec, tile_pre, n, no, i, r[u]) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < COARSE_U; ++u) {
+      if (!cnt[u]) continue;
+      const unsigned mx = r[u].y, my = r[u].z, rows = cnt[u] / mx, mz = rows / my;
+      if (rows > COARSE_BIG) {
+        const unsigned slot = atomicAdd(&big[0], 1u);
+        if (slot < big_cap) {
+          big[1 + slot] = (unsigned)(i0 + u * stride);
+          continue;
+        }
+      }
+      for (unsigned z = 0; z < mz; ++z)
+        for (unsigned y = 0; y < my; ++y) coarse_row(hsh, r[u].x + y * dx + z * dxy, mx, shift);
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x)
+    if (hsh[b]) atomicAdd(&coarse[b], hsh[b]);
+}
+
+// The queued objects, one CTA at a time, rows strided over the CTA's threads.
+__global__ void __launch_bounds__(256)
+k_coarse_big(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno, unsigned dx,
+             unsigned dxy, int shift, int nbins, unsigned* __restrict__ coarse, const unsigned* __restrict__ big,
+             unsigned big_cap) {
+  extern __shared__ unsigned hsh[];
+  const unsigned nbig = min(big[0], big_cap);
+  if (!nbig) return;
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x) hsh[b] = 0u;
+  __syncthreads();
+  const unsigned no = cno.get();
+  // every CTA takes a slice of every queued object's rows
+  for (unsigned e = 0; e < nbig; ++e) {
+    uint4 r;
+    const unsigned cnt = coarse_count(rec, tile_pre, n, no, big[1 + e], r);
+    const unsigned mx = r.y, my = r.z, rows = cnt / mx;
+    for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < rows; q += gridDim.x * blockDim.x) {
+      const unsigned z = q / my, y = q - z * my;
+      coarse_row(hsh, r.x + y * dx + z * dxy, mx, shift);
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x)
+    if (hsh[b]) atomicAdd(&coarse[b], hsh[b]);
+}
 
 // First radix pass over tiles that K2 already sorted by the pass's digit (k_pairs_emit<BITS>):
 // every digit run of a tile moves as a block to digit_start + tile_prefix; no ranking.

@@ -110,6 +110,25 @@ class ShardState:
         self.keys, self.vals, hist = self.ops.pairs(self.no, self.tri_base, self.shift, nb)
         return hist
 
+    def phase_count_fused(self, capacity=None):
+        """K1 + the coarse histogram from the cell boxes (no pairs yet: the fused dispatch
+        expands them straight into the slab owners' buffers after the plan)."""
+        self.deferred = bool(capacity)
+        if self.deferred:
+            self.no = self.ops.count_deferred(self.V, self.T, self.spec, capacity)
+        else:
+            self.no = self.ops.count(self.V, self.T, self.spec)
+        self.shift = coarse_shift(self.ncells)
+        self.nb_coarse = ((self.ncells - 1) >> self.shift) + 1
+        return self.ops.coarse_hist(self.shift, self.nb_coarse)
+
+    def phase_pairs_send(self, matrix, dst_keys, dst_vals):
+        """Fused dispatch: expand + partition + peer-store every pair (pg_pairs_send)."""
+        m = np.asarray(matrix, dtype=np.int64)
+        off = [int(m[:self.rank, s].sum()) for s in range(self.world)]
+        self.ops.pairs_send(self.tri_base, self.table_d, self.shift, self.world, self.base_d, dst_keys, dst_vals, off)
+        return int(m[:, self.rank].sum())
+
     def phase_plan_device(self, hists):
         """Slab plan on the device from every rank's coarse histogram (exchange buffer);
         partition tables stay on the device. The host learns the plan with the count matrix."""
@@ -180,7 +199,32 @@ def build_sharded(ops, comm, V, T, tri_base, spec, gather=True, exchange=None):
     if world > MAX_SLABS:
         raise ValueError(f"at most {MAX_SLABS} ranks")
     st = ShardState(ops, V, T, tri_base, spec, rank, world)
-    if exchange is not None:
+    if exchange is not None and getattr(exchange, "fused", False):
+        # fused dispatch: K1, the coarse histogram from the cell boxes, peer-put histograms and
+        # NOs, a device barrier, the device plan, ONE host read (histograms, NOs, plan), then a
+        # single kernel expands every pair straight into its slab owner's receive buffer
+        while True:
+            cap = exchange.no_capacity
+            hist = st.phase_count_fused(cap)
+            exchange.put_hist(hist, rank)
+            exchange.put_no(rank, ops)
+            exchange.barrier()
+            st.phase_plan_device(exchange.hists(st.nb_coarse))
+            hists, nos, plan_arr = exchange.read_hists(st.nb_coarse, st.plan_d)
+            exchange.no_capacity = int(nos.max() * 1.0625) + 4096
+            if not cap or int(nos.max()) <= cap:
+                break
+        if st.deferred:
+            st.no = ops.count_result()
+        plan = st.set_plan(plan_arr)
+        matrix = slab_matrix(hists, plan.cuts)
+        assert st.no == int(nos[rank]) == int(hists[rank].sum()), (st.no, nos[rank], int(hists[rank].sum()))
+        exchange.ensure(int(matrix.sum(axis=0).max()))
+        dk, dv = exchange.destinations()
+        nrecv = st.phase_pairs_send(matrix, dk, dv)
+        exchange.barrier()
+        krecv, vrecv = exchange.received(nrecv)
+    elif exchange is not None:
         # histograms, plan and slab counts stay on the device: each rank puts its array into
         # every rank's exchange buffer (peer stores), a device barrier, then every rank reduces
         # / plans itself; the host reads the count matrix, every rank's NO and the plan once.
@@ -295,7 +339,12 @@ class PeerExchange:
         self.ctl_ptrs = [int(p) for p in self.ctl_hdl.buffer_ptrs]
         self._read_c = torch.empty(w * CTL_CNT, dtype=torch.int32).pin_memory()
         self._read_p = torch.empty(4 * w + 2, dtype=torch.int64).pin_memory()
+        self._read_h = torch.empty(w * CTL_HIST, dtype=torch.int32).pin_memory()
         self.no_capacity = None      # pair capacity of deferred counts (set after the first build)
+        # pg_pairs_send (expansion + dispatch in one kernel, look-back slab offsets): correct
+        # but measured slower at world 1 (1.23 vs 1.09 ms/build: the coarse histogram from the
+        # cell boxes re-reads every record, latency-bound, before the expansion can start); off
+        self.fused = False
 
     def _stream(self):
         return self.torch.cuda.current_stream(self.dev).cuda_stream
@@ -311,6 +360,20 @@ class PeerExchange:
         w = self.comm.world
         _native.peer_put(counts, w, self.ctl_ptrs, w * CTL_HIST + rank * CTL_CNT, self._stream())
         ops.b.peer_put_count(self.ctl_ptrs, w * CTL_HIST + rank * CTL_CNT + 16, self._stream())
+
+    def put_no(self, rank, ops):
+        w = self.comm.world
+        ops.b.peer_put_count(self.ctl_ptrs, w * CTL_HIST + rank * CTL_CNT + 16, self._stream())
+
+    def read_hists(self, nb, plan_d):
+        """Every rank's coarse histogram and NO, and the device plan: one host round trip."""
+        torch, w = self.torch, self.comm.world
+        self._read_h[:w * nb].copy_(self.ctl[:w * nb], non_blocking=True)
+        self._read_c.copy_(self.ctl[w * CTL_HIST:w * (CTL_HIST + CTL_CNT)], non_blocking=True)
+        self._read_p.copy_(plan_d, non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        hists = self._read_h[:w * nb].numpy().view(np.uint32).reshape(w, nb).astype(np.int64)
+        return hists, _split_counts(self._read_c.numpy(), w)[1], self._read_p.numpy().copy()
 
     def read_counts(self, plan_d):
         """The count matrix [rank][slab], every rank's NO and the device plan: one host
@@ -373,6 +436,17 @@ class EmulatedExchange:
         _native.peer_put(counts, w, self.ctl_ptrs, w * CTL_HIST + rank * CTL_CNT, sp)
         ops.b.peer_put_count(self.ctl_ptrs, w * CTL_HIST + rank * CTL_CNT + 16, sp)
 
+    def put_no(self, rank, ops):
+        w = self.world
+        ops.b.peer_put_count(self.ctl_ptrs, w * CTL_HIST + rank * CTL_CNT + 16,
+                             self.torch.cuda.current_stream(self.dev).cuda_stream)
+
+    def read_hists(self, r, nb, plan_d):
+        w = self.world
+        h = self.ctl[r][:w * nb].cpu().numpy().view(np.uint32).reshape(w, nb).astype(np.int64)
+        c = self.ctl[r][w * CTL_HIST:w * (CTL_HIST + CTL_CNT)].cpu().numpy()
+        return h, _split_counts(c, w)[1], plan_d.cpu().numpy()
+
     def read_counts(self, r, plan_d):
         w = self.world
         c = self.ctl[r][w * CTL_HIST:w * (CTL_HIST + CTL_CNT)].cpu().numpy()
@@ -390,6 +464,13 @@ class EmulatedExchange:
 
     def received(self, r, n):
         return self.bufs[r][:n], self.bufs[r][self.cap:self.cap + n]
+
+
+def slab_matrix(hists, cuts):
+    """matrix[r][s] = pairs rank r sends to slab s, from the ranks' coarse histograms."""
+    cum = np.concatenate([np.zeros((len(hists), 1), np.int64), np.cumsum(hists, axis=1)], axis=1)
+    cuts = np.asarray(cuts, np.int64)
+    return cum[:, cuts[1:]] - cum[:, cuts[:-1]]
 
 
 def _split_counts(c, w):
@@ -410,6 +491,33 @@ def run_emulated(make_ops, V, T, spec, world, exchange="copy", capacity=None):
         states.append(ShardState(make_ops(), V, T[lo:hi], lo, spec, r, world))
     hist = np.sum([s.ops.to_numpy(s.phase_count()).astype(np.int64) for s in states], axis=0)
     plan = plan_slabs(hist, states[0].ncells, world)
+    if exchange == "fused":     # expansion + dispatch in one kernel (pg_pairs_send; CudaOps only)
+        ex = EmulatedExchange(states[0].ops.torch, states[0].ops.dev, world)
+        hists = [s.phase_count_fused(capacity) for s in states]
+        for r, s in enumerate(states):
+            ex.put_hist(hists[r], r)
+            ex.put_no(r, s.ops)
+        for r, s in enumerate(states):
+            s.phase_plan_device(ex.hists(r, s.nb_coarse))
+        for r, s in enumerate(states):
+            h, nos, plan_arr = ex.read_hists(r, s.nb_coarse, s.plan_d)
+            if capacity and int(nos.max()) > capacity:
+                return None
+            if s.deferred:
+                s.no = s.ops.count_result()
+            assert int(nos[r]) == int(h[r].sum()) == s.no
+            s.set_plan(plan_arr)
+        # the histograms from the cell boxes equal K2's (pg_pairs) coarse histograms
+        matrix = slab_matrix(h, states[0].plan.cuts)
+        ex.ensure(int(matrix.sum(axis=0).max()))
+        dk, dv = ex.destinations()
+        nrecv = [s.phase_pairs_send(matrix, dk, dv) for s in states]
+        states[0].ops.torch.cuda.synchronize()
+        slabs = []
+        for r, s in enumerate(states):
+            base, G_rel, O = s.phase_sort(*ex.received(r, nrecv[r]))
+            slabs.append((base, s.ops.to_numpy(G_rel), s.ops.to_numpy(O)))
+        return assemble(slabs, states[0].ncells)
     if exchange == "p2p":       # fused partition + send into the owners' buffers (CudaOps only)
         # as build_sharded with a PeerExchange: histograms, plan and counts through the
         # (emulated) peer buffers, slab plans computed on the device by every rank
@@ -537,6 +645,16 @@ class CudaOps:
             flags = _native.PG_HOST_INPUT
         self._V, self._T = V, T
         return self.b.count_deferred(V, V.shape[0], T, T.shape[0], spec, capacity, flags, self._sp())
+
+    def coarse_hist(self, shift, nbuckets):
+        hist = self._buf("coarse", nbuckets)
+        self.b.coarse_hist(shift, nbuckets, hist, self._sp())
+        return hist
+
+    def pairs_send(self, tri_base, table, shift, nslabs, base, dst_keys, dst_vals, dst_offset):
+        self._ptab, self._pbase = self._dev_u32(table), self._dev_u32(base)
+        self.b.pairs_send(tri_base, self._ptab, shift, nslabs, self._pbase, dst_keys, dst_vals, dst_offset,
+                          self._sp())
 
     def count_result(self):
         no = self.b.count_result()

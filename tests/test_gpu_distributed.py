@@ -130,6 +130,11 @@ def test_single_rank_nccl_path(tmp_path):
         for _ in range(2):
             G, O = D.build_sharded(D.CudaOps(), comm, mesh.vertices, mesh.triangles, 0, spec, exchange=ex)
             assert np.array_equal(G, Gr) and np.array_equal(O, Or)
+        ex.fused = True                  # expansion + dispatch in one kernel (pg_pairs_send)
+        ex.no_capacity = None
+        for _ in range(2):
+            G, O = D.build_sharded(D.CudaOps(), comm, mesh.vertices, mesh.triangles, 0, spec, exchange=ex)
+            assert np.array_equal(G, Gr) and np.array_equal(O, Or)
     finally:
         dist.destroy_process_group()
 
@@ -198,3 +203,43 @@ def test_emulated_fused_exchange_deferred_count(world):
     assert np.array_equal(G, Gr) and np.array_equal(O, Or)
     assert D.run_emulated(D.CudaOps, mesh.vertices, mesh.triangles, spec, world, exchange="p2p",
                           capacity=len(Or) // world // 2) is None
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8, 16])
+def test_emulated_fused_dispatch(world):
+    """pg_coarse_hist + device plan + pg_pairs_send (expansion, slab ranking with a decoupled
+    look-back and peer stores in one kernel) == oracle, with and without a deferred count."""
+    mesh = gen_scene("walls", 30000, 4)
+    spec = spec_for_mesh(mesh, dims=(61, 47, 53))
+    Gr, Or = oracle.build_parallel(mesh.vertices, mesh.triangles, spec)
+    for cap in (None, len(Or)):
+        G, O = D.run_emulated(D.CudaOps, mesh.vertices, mesh.triangles, spec, world, exchange="fused",
+                              capacity=cap)
+        assert np.array_equal(G, Gr) and np.array_equal(O, Or)
+    assert D.run_emulated(D.CudaOps, mesh.vertices, mesh.triangles, spec, world, exchange="fused",
+                          capacity=max(1, len(Or) // world // 2)) is None
+
+
+def test_emulated_fused_dispatch_cfg2_hash(hashes):
+    h = hashes["cfg2"]
+    mesh, spec = scene_from_recipe(h["recipe"])
+    G, O = D.run_emulated(D.CudaOps, mesh.vertices, mesh.triangles, spec, 8, exchange="fused")
+    assert len(O) == h["no"] and sha(G) == h["G_sha256"] and sha(O) == h["O_sha256"]
+
+
+@pytest.mark.parametrize("scene,n,dims", [("walls", 20000, None), ("skewed", 20000, (50, 40, 30)),
+                                          ("lognormal", 50000, None), ("uniform", 30000, (4096, 2, 3)),
+                                          ("walls", 5000, (1, 1, 7)), ("uniform", 30000, (97, 1, 1))])
+def test_coarse_hist_from_boxes_matches_pairs(scene, n, dims):
+    """The coarse histogram from the cell boxes (before any pair exists) == pg_pairs' one,
+    including rows that span many buckets (flat grids)."""
+    mesh = gen_scene(scene, n, 3)
+    spec = spec_for_mesh(mesh, dims=dims) if dims else spec_for_mesh(mesh)
+    ops = D.CudaOps()
+    ncells = int(np.prod(spec.dims))
+    shift = D.coarse_shift(ncells)
+    nb = ((ncells - 1) >> shift) + 1
+    no = ops.count(mesh.vertices, mesh.triangles, spec)
+    h1 = ops.to_numpy(ops.coarse_hist(shift, nb)).copy()
+    _, _, h2 = ops.pairs(no, 0, shift, nb)
+    assert np.array_equal(h1, ops.to_numpy(h2)) and int(h1.sum()) == no

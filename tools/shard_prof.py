@@ -13,7 +13,8 @@ shard = scenes.gen_arch_shard(n, 7, 4.0, 0, n)
 spec = gridcore.spec_from_bounds(shard.vertices.min(0), shard.vertices.max(0), n, density=4.0)
 Vd = torch.from_numpy(shard.vertices.copy()).cuda(); Td = torch.from_numpy(shard.triangles.copy()).cuda()
 ops = D.CudaOps(0); comm = D.TorchComm(device=torch.device("cuda", 0))
-P2P = "--p2p" in sys.argv
+P2P = "--p2p" in sys.argv or "--fused" in sys.argv
+FUSED = "--fused" in sys.argv
 ex = D.PeerExchange(comm, torch.device("cuda", 0)) if P2P else None
 T = {}
 E = {}
@@ -26,6 +27,18 @@ for it in range(6):
     t = time.perf_counter()
     e0 = torch.cuda.Event(enable_timing=True); e0.record(); E.setdefault("_start", []).append(e0)
     st = D.ShardState(ops, Vd, Td, 0, spec, 0, 1)
+    if FUSED:
+        h = st.phase_count_fused(ex.no_capacity); t = tick("count+coarse", t)
+        ex.put_hist(h, 0); ex.put_no(0, ops); ex.barrier(); t = tick("put+barrier", t)
+        st.phase_plan_device(ex.hists(st.nb_coarse)); t = tick("plan_dev", t)
+        hists, nos, pa = ex.read_hists(st.nb_coarse, st.plan_d); t = tick("read", t)
+        ex.no_capacity = int(nos.max() * 1.0625) + 4096
+        if st.deferred: ops.count_result()
+        plan = st.set_plan(pa); m = D.slab_matrix(hists, plan.cuts); ex.ensure(int(m.sum(axis=0).max()))
+        dk, dv = ex.destinations(); nr = st.phase_pairs_send(m, dk, dv); t = tick("pairs_send", t)
+        ex.barrier(); kr, vr = ex.received(nr); t = tick("barrier", t)
+        r = st.phase_sort(kr, vr); t = tick("sort_cells", t)
+        continue
     if P2P and ex.no_capacity:   # deferred count (no NO read back), as build_sharded
         st.deferred = True; st.no = ops.count_deferred(Vd, Td, spec, ex.no_capacity)
     else:
