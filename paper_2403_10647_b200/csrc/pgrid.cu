@@ -863,6 +863,7 @@ int pg_build_wait(pg_builder* b, uint64_t* no_out) {
 int pg_finish_baseline(pg_builder* b, int algo, uint32_t* G, uint32_t* O, uint32_t flags, void* stream_,
                        float* phase_ms, uint64_t* max_task_work) {
   if (!b || !b->counted) return fail(PG_STATE_ERROR, "pg_finish_baseline without a successful pg_count");
+  if (b->deferred) return fail(PG_STATE_ERROR, "pg_finish_baseline after a PG_DEFER count");
   if (algo != 1 && algo != 2) return fail(PG_INVARIANT_ERROR, "algo must be 1 (sorted) or 2 (compact)");
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   CU(cudaSetDevice(b->device));
@@ -1002,6 +1003,7 @@ int pg_finish_baseline(pg_builder* b, int algo, uint32_t* G, uint32_t* O, uint32
 
 int pg_stage(pg_builder* b, int stage, void* dst, uint32_t flags, void* stream_) {
   if (!b || !b->counted) return fail(PG_STATE_ERROR, "no build to read stages from");
+  if (b->deferred) return fail(PG_STATE_ERROR, "pg_stage after a PG_DEFER count");
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   CU(cudaSetDevice(b->device));
   const cudaMemcpyKind kind = (flags & PG_HOST_OUTPUT) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
@@ -1313,6 +1315,7 @@ int pg_dda_cast(pg_builder* b, const uint32_t* G, const uint32_t* O, int64_t no,
 int pg_grid_stats(pg_builder* b, const uint32_t* G, uint32_t flags, void* stream_, uint64_t* out) {
   if (!b || !out) return fail(PG_INVARIANT_ERROR, "null argument");
   if (!b->counted) return fail(PG_STATE_ERROR, "pg_grid_stats before pg_count");
+  if (b->deferred) return fail(PG_STATE_ERROR, "pg_grid_stats after a PG_DEFER count");
   if (!G) return fail(PG_INVARIANT_ERROR, "null G");
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   CU(cudaSetDevice(b->device));
