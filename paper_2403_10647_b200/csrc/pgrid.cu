@@ -425,6 +425,7 @@ int count_setup(pg_builder* b, int64_t nv, int64_t n, const pg_spec* spec, DevSp
     ds.lo[k] = spec->lo[k];
     ds.hi[k] = spec->hi[k];
     ds.cell[k] = spec->cell[k];
+    ds.rcell[k] = 1.0 / spec->cell[k];
     ds.dims[k] = (int)spec->dims[k];
     b->dims[k] = (int)spec->dims[k];
   }

@@ -33,6 +33,7 @@ struct DevSpec {
   double hi[3];
   double cell[3];
   int dims[3];
+  double rcell[3];  // RN(1 / cell): the fast path of floor_quot
 };
 
 // Per-pass digit plan for the radix sort.
@@ -86,6 +87,21 @@ __device__ __forceinline__ long long np_floor_i64(double q) {
   return (f >= -9223372036854775808.0 && f < 9223372036854775808.0) ? (long long)f
                                                                      : (long long)(-9223372036854775807LL - 1);
 }
+// floor(RN(x / c)) -- numpy's `floor((a - lo) / cell_size)` (gridcore.py:161-162) -- exactly,
+// mostly without the division: p = RN(x * RN(1/c)) is within 3 ulp of RN(x / c) (two
+// roundings of relative size 2^-53 each, plus the quotient's own), so when the window p +-
+// 2^-50 |p| holds no integer both have the same floor. Integral or near-integral products,
+// huge or non-finite values and degenerate cell sizes take the IEEE division.
+__device__ __forceinline__ double floor_quot(double x, double c, double rc) {
+  const double p = __dmul_rn(x, rc);
+  const double f = floor(p);
+  const double ap = fabs(p);
+  const double tol = __dmul_rn(ap, 0x1p-50);
+  if (ap < 0x1p52 && rc > 0.0 && rc < 1.0e308 && __dsub_rn(p, f) > tol && __dsub_rn(__dadd_rn(f, 1.0), p) > tol)
+    return f;
+  return floor(__ddiv_rn(x, c));
+}
+
 __device__ __forceinline__ unsigned clip_axis(long long v, int dim) {
   return v < 0 ? 0u : (v > (long long)(dim - 1) ? (unsigned)(dim - 1) : (unsigned)v);
 }
@@ -185,8 +201,8 @@ __device__ __forceinline__ void tri_box_raw(const double* a, const double* b, co
     const double mx = fmax(fmax(x0, x1), x2);
     keep &= !nan && (mx >= s.lo[k]) && (mn <= s.hi[k]);
     // one IEEE subtract, one IEEE divide, floor (gridcore.py:161-162)
-    lo[k] = clip_axis(np_floor_i64(__ddiv_rn(__dsub_rn(mn, s.lo[k]), s.cell[k])), s.dims[k]);
-    hi[k] = clip_axis(np_floor_i64(__ddiv_rn(__dsub_rn(mx, s.lo[k]), s.cell[k])), s.dims[k]);
+    lo[k] = clip_axis(np_floor_i64(floor_quot(__dsub_rn(mn, s.lo[k]), s.cell[k], s.rcell[k])), s.dims[k]);
+    hi[k] = clip_axis(np_floor_i64(floor_quot(__dsub_rn(mx, s.lo[k]), s.cell[k], s.rcell[k])), s.dims[k]);
   }
 }
 

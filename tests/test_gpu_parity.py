@@ -311,3 +311,27 @@ def test_build_pipeline_deferred_corners(hashes):
     pipe.submit(mesh0, spec0)
     grid, rep = pipe.result()
     assert np.array_equal(grid.G, want0.G) and np.array_equal(grid.O, want0.O)
+
+
+def test_cell_boundary_coordinates_bit_exact():
+    """K1 floors (a - lo) / cell with a reciprocal-product fast path that defers to the IEEE
+    division near integers: vertices exactly on, and a few ulps either side of, cell
+    boundaries (and the padded bounds themselves) give the oracle's boxes."""
+    rng = np.random.default_rng(11)
+    dims = (37, 23, 41)
+    lo, hi = np.array([-1.3, 0.7, 2.0]), np.array([4.1, 3.3, 9.7])
+    spec = GridSpec(Aabb(lo, hi), dims)
+    cell = np.asarray(spec.cell_size, dtype=np.float64)
+    n = 60000
+    k = rng.integers(0, np.array(dims) + 1, size=(3 * n, 3))
+    V = np.asarray(spec.bounds.lo) + k * cell                 # exactly on boundaries (as rounded)
+    ulps = rng.integers(-4, 5, size=V.shape)
+    V = np.where(ulps > 0, np.nextafter(V, np.inf), V)
+    V = np.where(ulps < 0, np.nextafter(V, -np.inf), V)
+    m = rng.random(V.shape) < 0.3
+    V[m] = (np.asarray(spec.bounds.lo) + rng.random(V.shape) * (hi - lo))[m]
+    V[0], V[1], V[2] = spec.bounds.lo, spec.bounds.hi, -np.asarray(spec.bounds.lo)
+    T = np.arange(3 * n, dtype=np.int32).reshape(n, 3)
+    grid, rep = builders.build_parallel(TriangleMesh(V, T), spec)
+    G, O = oracle.build_parallel(V, T, spec)
+    assert np.array_equal(grid.G, G) and np.array_equal(grid.O, O) and rep.no == len(O)
