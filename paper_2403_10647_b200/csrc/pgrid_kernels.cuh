@@ -511,28 +511,47 @@ __device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long 
   // slots live in 16-byte chunks whose index is XOR-swizzled (slot_at) so the per-thread
   // chunk reads of the max-scan below are bank-conflict free
   auto slot_at = [](unsigned e) { return ((((e >> 2) ^ ((e >> 5) & 7u)) << 2) | (e & 3u)); };
+  // the first EXP_PRE records of this thread are requested before the slot initialisation and
+  // its barrier, which then hide their DRAM latency (the stall that dominated this phase)
+  constexpr int EXP_PRE = 4;
+  uint4 pr[EXP_PRE];
+  unsigned pt[EXP_PRE];
+#pragma unroll
+  for (int u = 0; u < EXP_PRE; ++u) {
+    const long long o = olo + 1 + tid + (long long)u * THREADS;
+    if (o < oend) {
+      pr[u] = __ldg(&rec[o]);
+      pt[u] = __ldg(&tile_pre[o / K1_TILE]);
+    }
+  }
+  uint4 r0 = make_uint4(0u, 0u, 0u, 0u);
+  if (tid == 0) r0 = __ldg(&rec[olo]);
   for (int i = tid; i < TILE; i += THREADS) slot[i] = -1;
   __syncthreads();
   if (tid == 0) {
     slot[0] = (int)olo;  // slot_at(0) == 0
-    const uint4 r = __ldg(&rec[olo]);
-    oc->lo_cell[0] = r.x;
-    oc->mx[0] = r.y;
-    oc->my[0] = r.z;
+    oc->lo_cell[0] = r0.x;
+    oc->mx[0] = r0.y;
+    oc->my[0] = r0.z;
   }
-  // run starts inside the tile (independent loads, no barrier per chunk)
-#pragma unroll 4
-  for (long long o = olo + 1 + tid; o < oend; o += THREADS) {
-    const uint4 r = __ldg(&rec[o]);
-    const unsigned off = __ldg(&tile_pre[o / K1_TILE]) + r.w;
-    atomicMax(&slot[slot_at(off - p0)], (int)o);  // zero-count triangles share the next start; max wins
+  auto start = [&](long long o, const uint4& r, unsigned tp) {
+    atomicMax(&slot[slot_at(tp + r.w - p0)], (int)o);  // zero-count triangles share the next start; max wins
     const long long ci = o - olo;
     if (ci < OC_CAP) {
       oc->lo_cell[ci] = r.x;
       oc->mx[ci] = r.y;
       oc->my[ci] = r.z;
     }
+  };
+#pragma unroll
+  for (int u = 0; u < EXP_PRE; ++u) {
+    const long long o = olo + 1 + tid + (long long)u * THREADS;
+    if (o < oend) start(o, pr[u], pt[u]);
   }
+  // the remaining run starts inside the tile (independent loads, no barrier per chunk)
+#pragma unroll 4
+  for (long long o = olo + 1 + tid + (long long)EXP_PRE * THREADS; o < oend; o += THREADS)
+    start(o, __ldg(&rec[o]), __ldg(&tile_pre[o / K1_TILE]));
   __syncthreads();
   // inclusive max-scan over the slots (blocked: thread t owns slots [ITEMS*t, ITEMS*t + ITEMS))
 #pragma unroll
