@@ -34,7 +34,7 @@ extern "C" {
 #define PG_CUDA_ERROR 3        /* CUDA runtime failure */
 #define PG_STATE_ERROR 4       /* call sequence violated (finish before count, ...) */
 #define PG_PARSE_ERROR 6        /* pg_load_obj: malformed OBJ (-> ObjParseError) */
-#define PG_CAPACITY_ERROR 5    /* pg_build_wait: NO exceeded the O capacity given to pg_build_async */
+#define PG_CAPACITY_ERROR 5    /* pg_build_wait / pg_count_result: NO exceeded the capacity given */
 
 /* Flags. */
 #define PG_HOST_INPUT 1u       /* V/T (or sort inputs) are host pointers: copied H2D in-call */
@@ -43,10 +43,14 @@ extern "C" {
 #define PG_HOST_RAYS 8u        /* pg_dda_cast: rays are host pointers (grid stays on device) */
 #define PG_CHECK 16u           /* pg_dda_cast: synchronise and report device-side errors */
 #define PG_ASYNC 32u           /* pg_finish: return once enqueued (host outputs valid after pg_wait) */
-#define PG_DEFER 64u           /* pg_count: no host round trip; *no_out is the pair capacity on entry,
-                                  the sharded building blocks (pg_pairs, pg_partition_counts/_send
-                                  with n = that capacity) run on the device count; pg_count_result
-                                  reports NO (PG_CAPACITY_ERROR if it exceeded the capacity) */
+#define PG_DEFER 64u           /* pg_count: no host round trip; *no_out is the pair capacity on entry.
+                                  pg_finish (O must hold the capacity), pg_pairs, pg_coarse_hist,
+                                  pg_pairs_send and pg_partition_counts/_send (n = that capacity)
+                                  then run on the device count; after a stream synchronise
+                                  pg_count_result reports NO, or PG_CAPACITY_ERROR when NO exceeded
+                                  the capacity or a lone inverted box voided the deferred steps
+                                  (rebuild without PG_DEFER). pg_finish_baseline, pg_stage and
+                                  pg_grid_stats refuse a deferred count. */
 
 /* Grid specification: the exact host doubles of GridSpec (gridcore.py:36-57). */
 typedef struct {
