@@ -83,3 +83,25 @@ def test_empty_and_tiny_scenes_emulated():
     G, O = D.run_emulated(NumpyOps, mesh.vertices, mesh.triangles, spec, 4)
     Gr, Or = oracle.build_parallel(mesh.vertices, mesh.triangles, spec)
     assert np.array_equal(G, Gr) and np.array_equal(O, Or)
+
+
+def test_slab_matrix_and_count_slots():
+    """Host helpers of the device-side exchange: the per-rank slab matrix from coarse
+    histograms equals summing each rank's buckets by slab, and the control-buffer count slots
+    decode to the matrix and the 64-bit NOs."""
+    rng = np.random.default_rng(3)
+    for world in (1, 2, 5, 16):
+        nb = 4096
+        hists = rng.integers(0, 1000, size=(world, nb)).astype(np.int64)
+        hists[:, rng.integers(0, nb, 50)] = 0
+        plan = D.plan_slabs(hists.sum(axis=0), 1 << 26, world)
+        m = D.slab_matrix(hists, plan.cuts)
+        want = np.array([[h[plan.table == s].sum() for s in range(world)] for h in hists])
+        assert np.array_equal(m, want) and np.array_equal(m.sum(axis=1), hists.sum(axis=1))
+        slots = np.zeros((world, D.CTL_CNT), np.uint32)
+        nos = rng.integers(0, 1 << 40, size=world)
+        slots[:, :world] = m.astype(np.uint32)
+        slots[:, 16] = nos & 0xFFFFFFFF
+        slots[:, 17] = nos >> 32
+        mm, nn = D._split_counts(slots.view(np.int32).reshape(-1), world)
+        assert np.array_equal(mm, m) and np.array_equal(nn, nos)
