@@ -318,6 +318,23 @@ def run_sharded(args, world, rank, local):
         out_nbytes = g_host.nbytes + o_host.nbytes
         del r, g_host, o_host
     e2e_sec = statistics.median(e2e)
+    # gathered-to-rank-0 output: device-resident shards, the slabs sent to rank 0
+    # point-to-point and rebased there, then rank 0 copies the whole G/O to the host
+    gat = []
+    for i in range(2 + min(args.steps, 5)):
+        dist.barrier()
+        t0 = time.perf_counter()
+        r = D.build_sharded(ops, comm, Vd, Td, lo, spec, gather="device", exchange=ex)
+        if rank == 0:
+            gh, oh = ops.to_numpy(r[0]), ops.to_numpy(r[1])
+            del gh, oh
+        torch.cuda.synchronize()
+        t = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if i >= 2:
+            gat.append(float(t.item()))
+        del r
+    gathered_ms = statistics.median(gat) * 1e3
     out_bytes = torch.tensor([out_nbytes], device=dev, dtype=torch.int64)
     dist.all_reduce(out_bytes)
     line = {
@@ -341,6 +358,9 @@ def run_sharded(args, world, rank, local):
         "e2e": {"value": round(world / e2e_sec, 3), "unit": "builds/s",
                 "h2d_bytes_per_step": int((Vh.nbytes + Th.nbytes) * world),
                 "d2h_bytes_per_step": int(out_bytes.item()), "ms_per_step": round(e2e_sec * 1e3, 2)},
+        "gathered_output": {"ms_per_step": round(gathered_ms, 3),
+                            "what": "device-resident shards -> slabs sent to rank 0 (NCCL p2p), G rebased, "
+                                    "full G/O copied to rank 0's host; max over ranks, wall clock"},
         "gpu_launches": launches * args.steps,
         "clocks": clk.summary(),
     }

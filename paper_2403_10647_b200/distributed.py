@@ -261,6 +261,10 @@ def build_sharded(ops, comm, V, T, tri_base, spec, gather=True, exchange=None):
     base, G_rel, O = st.phase_sort(krecv, vrecv)
     if not gather:
         return int(plan.cell_lo[rank]), int(plan.cell_hi[rank]), base, G_rel, O
+    if gather == "device":
+        # the slabs travel to rank 0's GPU (NCCL point-to-point), G rebased there; rank 0
+        # returns device tensors (G int32[ncells+1], O int32[NO] holding u32 bit patterns)
+        return comm.gather_slabs_device(plan, st.ncells, G_rel, O)
     slabs = comm.gather_to_root((base, ops.to_numpy(G_rel), ops.to_numpy(O)))
     if rank != 0:
         return None
@@ -309,6 +313,44 @@ class TorchComm:
         self.dist.all_to_all_single(kr, ops.as_tensor(keys), recv, send, group=self.group)
         self.dist.all_to_all_single(vr, ops.as_tensor(vals), recv, send, group=self.group)
         return kr, vr
+
+    def gather_slabs_device(self, plan, ncells, G_rel, O):
+        """Every rank's (G_rel, O) slab into one G / O on rank 0 (device tensors, sends in
+        rank order); G rebased by the slab's pair base (u32 arithmetic on int32 bits)."""
+        import torch
+        rank, world = self.rank, self.world
+        as_t = lambda a: a if isinstance(a, torch.Tensor) else torch.from_numpy(np.asarray(a, np.uint32).view(np.int32))
+        G_rel, O = as_t(G_rel), as_t(O)
+        lo, hi = plan.cell_lo.astype(np.int64), plan.cell_hi.astype(np.int64)
+        base = plan.pair_base.astype(np.int64)
+        if rank != 0:
+            if hi[rank] > lo[rank]:
+                self.dist.send(G_rel[:hi[rank] - lo[rank]].contiguous(), 0, group=self.group)
+                if int(O.numel()):
+                    self.dist.send(O.contiguous(), 0, group=self.group)
+            return None
+        dev = G_rel.device
+        no = int(base[world])
+        G = torch.empty(ncells + 1, dtype=torch.int32, device=dev)
+        Oall = torch.empty(max(no, 1), dtype=torch.int32, device=dev)[:no]
+        for r in range(world):
+            k, n_r = int(hi[r] - lo[r]), int(base[r + 1] - base[r])
+            if k == 0:
+                continue
+            g = G[lo[r]:hi[r]]
+            o = Oall[base[r]:base[r + 1]]
+            if r == 0:
+                g.copy_(G_rel[:k])
+                if n_r:
+                    o.copy_(O[:n_r])
+            else:
+                self.dist.recv(g, r, group=self.group)
+                if n_r:
+                    self.dist.recv(o, r, group=self.group)
+            if base[r]:
+                g.add_(int(np.int64(base[r]).astype(np.uint32).view(np.int32)))   # wraps like u32
+        G[ncells] = int(np.uint32(no).view(np.int32))
+        return G, Oall
 
     def gather_to_root(self, obj):
         out = [None] * self.world if self.rank == 0 else None

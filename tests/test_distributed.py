@@ -50,6 +50,37 @@ def test_sharded_build_gloo(tmp_path, world, kind, n, seed, dims):
     assert np.array_equal(res["G"], G) and np.array_equal(res["O"], O)
 
 
+def _gather_worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from np_ops import NumpyOps
+        mesh = gen_scene("walls", 3000, 5)
+        spec = spec_for_mesh(mesh, dims=(40, 30, 20))
+        lo, hi = D.shard_range(mesh.ntriangles, rank, world)
+        res = D.build_sharded(NumpyOps(), D.TorchComm(), mesh.vertices, mesh.triangles[lo:hi], lo, spec,
+                              gather="device")
+        if rank == 0:
+            np.savez(out_path, G=res[0].numpy().view(np.uint32), O=res[1].numpy().view(np.uint32))
+        else:
+            assert res is None
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gather_slabs_to_rank0_gloo(tmp_path, world):
+    """gather="device": the slabs go to rank 0 point-to-point (tensors; NCCL on GPUs) and G is
+    rebased there -- the gathered-output mode of SURVEY.md §8e."""
+    out = str(tmp_path / "g.npz")
+    mp.spawn(_gather_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    res = np.load(out)
+    mesh = gen_scene("walls", 3000, 5)
+    G, O = oracle.build_parallel(mesh.vertices, mesh.triangles, spec_for_mesh(mesh, dims=(40, 30, 20)))
+    assert np.array_equal(res["G"], G) and np.array_equal(res["O"], O)
+
+
 @pytest.mark.parametrize("world", [1, 2, 4, 8, 16])
 def test_emulated_ranks_match_oracle(world):
     from np_ops import NumpyOps

@@ -130,6 +130,9 @@ def test_single_rank_nccl_path(tmp_path):
         for _ in range(2):
             G, O = D.build_sharded(D.CudaOps(), comm, mesh.vertices, mesh.triangles, 0, spec, exchange=ex)
             assert np.array_equal(G, Gr) and np.array_equal(O, Or)
+        Gd, Od = D.build_sharded(D.CudaOps(), comm, mesh.vertices, mesh.triangles, 0, spec, gather="device",
+                                 exchange=ex)
+        assert np.array_equal(Gd.cpu().numpy().view(np.uint32), Gr) and np.array_equal(Od.cpu().numpy().view(np.uint32), Or)
         ex.fused = True                  # expansion + dispatch in one kernel (pg_pairs_send)
         ex.no_capacity = None
         for _ in range(2):
