@@ -535,6 +535,13 @@ int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64
   if ((rc = count_setup(b, nv, n, spec, ds))) return rc;
   ktimer_reset(st);
   if (n == 0) {
+    // an empty mesh (or an empty shard of a sharded build): NO = 0, also on the device for
+    // the steps that read the count there (pg_peer_put_count, deferred grids)
+    if ((rc = b->k1_sync.ensure(256))) return rc;
+    b->d_total = b->k1_sync.as<unsigned long long>(0);
+    CU(cudaMemsetAsync(b->d_total, 0, 8, st));
+    b->h_scalars[0] = 0;
+    b->h_scalars[1] = 0;
     b->no = 0;
     *no_out = 0;
     b->counted = true;

@@ -495,8 +495,8 @@ class EmulatedExchange:
         return _split_counts(c, w) + (plan_d.cpu().numpy(),)
 
     def ensure(self, n):
-        if n > self.cap:
-            self.cap = (int(n * 1.25) + 1024 + 63) & ~63
+        if n > self.cap or not hasattr(self, "bufs"):   # (an all-dropped mesh still needs buffers)
+            self.cap = (int(max(n, self.cap) * 1.25) + 1024 + 63) & ~63
             self.bufs = [self.torch.empty(2 * self.cap, dtype=self.torch.int32, device=self.dev)
                          for _ in range(self.world)]
 

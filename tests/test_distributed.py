@@ -136,3 +136,14 @@ def test_slab_matrix_and_count_slots():
         slots[:, 17] = nos >> 32
         mm, nn = D._split_counts(slots.view(np.int32).reshape(-1), world)
         assert np.array_equal(mm, m) and np.array_equal(nn, nos)
+
+
+@pytest.mark.parametrize("n", [1, 3, 7])
+def test_emulated_more_ranks_than_triangles(n):
+    """Ranks with empty shards (N < P) still take part in the plan and the exchange."""
+    from np_ops import NumpyOps
+    mesh = gen_scene("uniform", n, 11)
+    spec = spec_for_mesh(mesh, dims=(9, 5, 7))
+    G, O = D.run_emulated(NumpyOps, mesh.vertices, mesh.triangles, spec, 8)
+    Gr, Or = oracle.build_parallel(mesh.vertices, mesh.triangles, spec)
+    assert np.array_equal(G, Gr) and np.array_equal(O, Or)

@@ -246,3 +246,14 @@ def test_coarse_hist_from_boxes_matches_pairs(scene, n, dims):
     h1 = ops.to_numpy(ops.coarse_hist(shift, nb)).copy()
     _, _, h2 = ops.pairs(no, 0, shift, nb)
     assert np.array_equal(h1, ops.to_numpy(h2)) and int(h1.sum()) == no
+
+
+@pytest.mark.parametrize("mode", ["copy", "p2p", "fused"])
+def test_emulated_more_ranks_than_triangles(mode):
+    """Empty shards (N < P) on the device paths: the device NO of an empty count is 0."""
+    for n in (1, 3, 7):
+        mesh = gen_scene("uniform", n, 11)
+        spec = spec_for_mesh(mesh, dims=(9, 5, 7))
+        G, O = D.run_emulated(D.CudaOps, mesh.vertices, mesh.triangles, spec, 8, exchange=mode)
+        Gr, Or = oracle.build_parallel(mesh.vertices, mesh.triangles, spec)
+        assert np.array_equal(G, Gr) and np.array_equal(O, Or)

@@ -3,6 +3,8 @@ random grid resolutions and bounds (dropped / clipped triangles, degenerate axes
 NaN / inf / huge coordinates and indexed meshes -- the CUDA build against the C oracle, bit
 for bit, through build_parallel, the comparison builders and the sync-free graph path."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -12,6 +14,7 @@ from paper_2403_10647_b200 import _native, builders, gen_scene
 from paper_2403_10647_b200.gridcore import Aabb, GridSpec, TriangleMesh
 
 pytestmark = pytest.mark.gpu
+FUZZ_BLOCKS = int(os.environ.get("PGRID_FUZZ_BLOCKS", "8"))   # 25 random scenes per block
 
 
 def random_case(rng):
@@ -50,7 +53,7 @@ def oracle_or_error(mesh, spec):
         return "invariant"
 
 
-@pytest.mark.parametrize("block", range(8))
+@pytest.mark.parametrize("block", range(FUZZ_BLOCKS))
 def test_fuzz_build_parallel(block):
     from paper_2403_10647_b200.errors import InvariantError
     rng = np.random.default_rng(1000 + block)
@@ -91,3 +94,53 @@ def test_fuzz_graph_path():
             assert b.build_wait() == len(want[1])
             assert np.array_equal(Gd.cpu().numpy().view(np.uint32), want[0])
             assert np.array_equal(Od[:len(want[1])].cpu().numpy().view(np.uint32), want[1])
+
+
+@pytest.mark.parametrize("block", range(max(1, FUZZ_BLOCKS // 4)))
+def test_fuzz_pipeline_deferred(block):
+    """BuildPipeline (deferred counts after the first build, rebuilds on overflow) on a stream
+    of random scenes: results in order and equal to the oracle's."""
+    from paper_2403_10647_b200.errors import InvariantError
+    rng = np.random.default_rng(5000 + block)
+    cases = []
+    while len(cases) < 20:
+        mesh, spec = random_case(rng)
+        want = oracle_or_error(mesh, spec)
+        if want is not None:
+            cases.append((mesh, spec, want))
+    pipe = builders.BuildPipeline(depth=2)
+    pending = []
+    def collect():
+        mesh, spec, want = pending.pop(0)
+        if isinstance(want, str):
+            with pytest.raises(InvariantError):
+                pipe.result()
+            return
+        grid, rep = pipe.result()
+        assert np.array_equal(grid.G, want[0]) and np.array_equal(grid.O, want[1]), (block, spec)
+    for c in cases:
+        if len(pending) == 2:
+            collect()
+        pipe.submit(c[0], c[1])
+        pending.append(c)
+    while pending:
+        collect()
+
+
+@pytest.mark.parametrize("block", range(max(1, FUZZ_BLOCKS // 4)))
+def test_fuzz_sharded_emulated(block):
+    """The sharded orchestration (device plan + peer-store partition, and the fused dispatch)
+    on random scenes and rank counts, every virtual rank on this GPU."""
+    from paper_2403_10647_b200 import distributed as D
+    rng = np.random.default_rng(9000 + block)
+    done = 0
+    while done < 6:
+        mesh, spec = random_case(rng)
+        want = oracle_or_error(mesh, spec)
+        if want is None or isinstance(want, str) or len(mesh.triangles) < 2:
+            continue
+        world = int(rng.integers(1, 9))
+        for mode in ("p2p", "fused"):
+            G, O = D.run_emulated(D.CudaOps, mesh.vertices, mesh.triangles, spec, world, exchange=mode)
+            assert np.array_equal(G, want[0]) and np.array_equal(O, want[1]), (block, mode, world, spec)
+        done += 1
