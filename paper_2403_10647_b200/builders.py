@@ -17,6 +17,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native
+from .errors import GridError
 from .gridcore import CompactGrid
 
 PHASES = ("count", "scan", "pairgen", "sort", "rle", "finalize")   # builders.py:19
@@ -218,7 +219,8 @@ class BuildPipeline:
         self._cap = None    # pair capacity of deferred counts: 1.25 x the largest NO seen
 
     def submit(self, mesh, spec):
-        """Enqueue one build. After the first, the pair count is not read back (PG_DEFER):
+        """Enqueue one build (errors of the build are raised by its result()). After the first,
+        the pair count is not read back (PG_DEFER):
         the copy in, Alg. 1 and the copies out are all enqueued without a host round trip, so
         the next submit's input copy follows this one's on the copy engine at once. O is
         copied at the capacity and cut to NO in result(); an overflow rebuilds that mesh."""
@@ -229,11 +231,15 @@ class BuildPipeline:
         V, T = _mesh_arrays(mesh)
         t0 = time.perf_counter()
         deferred = self._cap is not None and len(T) > 0
-        if deferred:
-            no = b.count_deferred(V, len(V), T, len(T), spec, self._cap, flags=_native.PG_HOST_INPUT,
-                                  stream=st.cuda_stream)
-        else:
-            no = b.count(V, len(V), T, len(T), spec, flags=_native.PG_HOST_INPUT, stream=st.cuda_stream)
+        try:
+            if deferred:
+                no = b.count_deferred(V, len(V), T, len(T), spec, self._cap, flags=_native.PG_HOST_INPUT,
+                                      stream=st.cuda_stream)
+            else:
+                no = b.count(V, len(V), T, len(T), spec, flags=_native.PG_HOST_INPUT, stream=st.cuda_stream)
+        except GridError as e:        # reported by result(), in submission order, like deferred errors
+            self._pending.append((e,))
+            return
         count_ms = (time.perf_counter() - t0) * 1e3
         ncells = int(spec.dims[0]) * int(spec.dims[1]) * int(spec.dims[2])
         G = _native.pinned_pool.empty(ncells + 1, np.uint32)
@@ -251,7 +257,10 @@ class BuildPipeline:
         return self._cap
 
     def result(self):
-        b, mesh, spec, G, O, no, count_ms, deferred = self._pending.popleft()
+        entry = self._pending.popleft()
+        if len(entry) == 1:
+            raise entry[0]
+        b, mesh, spec, G, O, no, count_ms, deferred = entry
         b.wait()
         if deferred:
             no = b.count_result()
