@@ -533,6 +533,7 @@ __device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long 
     oc->lo_cell[0] = r0.x;
     oc->mx[0] = r0.y;
     oc->my[0] = r0.z;
+    warpmax[2 * (THREADS / 32)] = (int)(__ldg(&tile_pre[olo / K1_TILE]) + r0.w);  // olo's absolute offset
   }
   auto start = [&](long long o, const uint4& r, unsigned tp) {
     atomicMax(&slot[slot_at(tp + r.w - p0)], (int)o);  // zero-count triangles share the next start; max wins
@@ -562,21 +563,42 @@ __device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long 
     own[4 * q + 2] = a.z;
     own[4 * q + 3] = a.w;
   }
+  // alongside the owners, the tile position of the latest run start (a marked slot past
+  // position 0, which holds the tile's first owner whatever its start): a thread's first pair
+  // then knows its offset in its run without reading the owner's record back
+  constexpr int NW = THREADS / 32;
+  int prun = -1;
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j)
+    if (own[j] != -1 && tid * ITEMS + j > 0) prun = tid * ITEMS + j;
+  const bool first_starts = tid > 0 && own[0] != -1;
 #pragma unroll
   for (int j = 1; j < ITEMS; ++j) own[j] = max(own[j], own[j - 1]);
   int run = own[ITEMS - 1];
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const int o = __shfl_up_sync(0xffffffffu, run, d);
-    if (lane >= d) run = max(run, o);
+    const int po = __shfl_up_sync(0xffffffffu, prun, d);
+    if (lane >= d) {
+      run = max(run, o);
+      prun = max(prun, po);
+    }
   }
-  if (lane == 31) warpmax[warp] = run;
+  if (lane == 31) {
+    warpmax[warp] = run;
+    warpmax[NW + warp] = prun;
+  }
   __syncthreads();
   int carry = __shfl_up_sync(0xffffffffu, run, 1);
-  if (lane == 0) carry = -1;
-  for (int w = 0; w < warp; ++w) carry = max(carry, warpmax[w]);
+  int pcarry = __shfl_up_sync(0xffffffffu, prun, 1);
+  if (lane == 0) carry = pcarry = -1;
+  for (int w = 0; w < warp; ++w) {
+    carry = max(carry, warpmax[w]);
+    pcarry = max(pcarry, warpmax[NW + w]);
+  }
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) own[j] = max(own[j], carry);
+  const int start0 = first_starts ? tid * ITEMS : pcarry;  // tile position of own[0]'s run, or -1
 
   auto box = [&](int o, unsigned& lc, unsigned& bx, unsigned& by) {
     const long long ci = (long long)o - olo;
@@ -594,7 +616,7 @@ __device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long 
   const unsigned pbase = p0 + (unsigned)tid * ITEMS;
   unsigned cell = 0, x = 0, y = 0, mx = 1, my = 1;
   if (pbase < pend) {  // first pair: may sit anywhere inside its run
-    const unsigned rel = pbase - tri_offset(rec, tile_pre, own[0]);
+    const unsigned rel = start0 >= 0 ? (unsigned)(tid * ITEMS - start0) : pbase - (unsigned)warpmax[2 * NW];
     unsigned lc;
     box(own[0], lc, mx, my);
     if (rel == 0) {
@@ -766,7 +788,7 @@ k_expand_pairs(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_
                unsigned* __restrict__ vals, unsigned val_offset, unsigned* __restrict__ coarse, int coarse_shift,
                int coarse_bins) {
   __shared__ __align__(16) int slot[K2_TILE];
-  __shared__ int warpmax[K2_THREADS / 32];
+  __shared__ int warpmax[2 * (K2_THREADS / 32) + 1];
   __shared__ ObjCache oc;
   const unsigned no = cno.get();
   const unsigned p0 = blockIdx.x * (unsigned)K2_TILE;
@@ -1698,7 +1720,7 @@ struct PeSmem {
   __align__(16) int slot[RS_TILE];  // expansion slots, then the transposed keys
   unsigned h[kMaxBins];
   __align__(16) ObjCache oc;        // object cache, then the transposed values
-  int warpmax[RS_WARPS];
+  int warpmax[2 * RS_WARPS + 1];
 };
 static_assert(sizeof(ObjCache) >= RS_TILE * 4, "the object cache doubles as the value transpose buffer");
 // the presort keeps its values and per-warp counters in the object cache
@@ -1893,7 +1915,7 @@ struct SendSmem {
   union {
     struct {
       __align__(16) ObjCache oc;
-      int warpmax[RS_WARPS];
+      int warpmax[2 * RS_WARPS + 1];
     } pe;
     RsSmem rs;  // the slab scatter (its vstage receives the values)
   } u;
