@@ -189,6 +189,14 @@ cudaError_t set_scatter_smem() {
 
 // PGRID_PRESORT=1 enables the K2 local presort of the first radix digit (measured slower:
 // K2's scattered in-tile stores cost more than the ranking they save in pass 0; off).
+bool packed0_on() {
+  static const bool on = [] {
+    const char* e = getenv("PGRID_PACKED0");
+    return !e || *e != '0';
+  }();
+  return on;
+}
+
 bool presort_on() {
   static const bool on = [] {
     const char* e = getenv("PGRID_PRESORT");
@@ -199,12 +207,12 @@ bool presort_on() {
 
 void launch_pairs_emit(int presort_bits, unsigned grid, cudaStream_t st, const uint4* rec, const unsigned* tile_pre,
                        long long n, Count cno, unsigned dx, unsigned dxy, const PassPlan& plan, const int2* bounds,
-                       unsigned* keys, unsigned* vals, unsigned* counts, unsigned ld) {
+                       unsigned* keys, unsigned* vals, unsigned* counts, unsigned ld, unsigned* packed0 = nullptr) {
   switch (presort_bits) {
 #define PG_CASE(B)                                                                                        \
   case B:                                                                                                 \
     k_pairs_emit<B><<<grid, RS_THREADS, sizeof(PeSmem), st>>>(rec, tile_pre, n, cno, dx, dxy, plan, bounds, keys, \
-                                                              vals, counts, ld);                          \
+                                                              vals, counts, ld, packed0);                 \
     break;
     PG_CASE(0) PG_CASE(1) PG_CASE(2) PG_CASE(3) PG_CASE(4) PG_CASE(5) PG_CASE(6) PG_CASE(7) PG_CASE(8) PG_CASE(9)
 #undef PG_CASE
@@ -602,7 +610,7 @@ namespace {
 int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned* keys0, unsigned* vals0,
                unsigned* keys1, unsigned* vals1, unsigned* vals_final, Count cno, uint64_t cap, unsigned* hist,
                unsigned* counts, cudaStream_t st, const unsigned** sorted_keys_out, unsigned* keys2 = nullptr,
-               unsigned* vals2 = nullptr, bool presorted0 = false) {
+               unsigned* vals2 = nullptr, bool presorted0 = false, const unsigned* packed0 = nullptr) {
   // grids are sized for `cap` pairs; the kernels read the actual count from `cno`
   const unsigned ntiles = (unsigned)((cap + RS_TILE - 1) / RS_TILE);
   const unsigned ld = (ntiles + 3) & ~3u;
@@ -627,8 +635,14 @@ int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned
       LAUNCHED("k_tile_counts", st);
       ++b->launches;
     }
-    k_scan_tile_counts<<<1u << plan.bits[p], SC_THREADS, 0, st>>>(counts, cno, ld, hist + p * kMaxBins);
-    LAUNCHED("k_scan_tile_counts", st);
+    if (p == 0 && counts0_ready && packed0) {
+      k_scan_tile_counts_packed<<<1u << (plan.bits[p] - 1), SC_THREADS, 0, st>>>(packed0, cno, ld, counts,
+                                                                                hist + p * kMaxBins);
+      LAUNCHED("k_scan_tile_counts", st);
+    } else {
+      k_scan_tile_counts<<<1u << plan.bits[p], SC_THREADS, 0, st>>>(counts, cno, ld, hist + p * kMaxBins);
+      LAUNCHED("k_scan_tile_counts", st);
+    }
     if (p == 0 && presorted0) {
       launch_scatter_presorted(plan.bits[p], ntiles, st, kin, vin, ko, vo, cno, plan.shift[p], hist + p * kMaxBins,
                                counts, ld);
@@ -682,7 +696,7 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
   const size_t hist_bytes = align_up(kMaxPasses * kMaxBins * 4);
   const size_t pb_bytes = align_up((size_t)std::max(rs_tiles, k2_tiles) * 8 + 8);
   const size_t kb_bytes = align_up((size_t)(g_tiles + 1) * 4);
-  if ((rc = b->sort_sync.ensure(hist_bytes + pb_bytes + kb_bytes + (size_t)((rs_tiles + 3) & ~3u) * kMaxBins * 4)))
+  if ((rc = b->sort_sync.ensure(hist_bytes + pb_bytes + kb_bytes + (size_t)((rs_tiles + 3) & ~3u) * kMaxBins * 6)))
     return rc;
   unsigned* hist = b->sort_sync.as<unsigned>(0);
   int2* pbounds = b->sort_sync.as<int2>(hist_bytes);
@@ -723,13 +737,15 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
       // with the presort, K2 leaves every tile sorted by the first digit (pass 0 then only moves
       // digit runs); stage dumps (record=) need generation order, so they skip it
       const bool presort = presort_on() && !(flags & PG_KEEP_STAGES);
+      // K2's first-pass counts two digits per word (the row scan unpacks them): PGRID_PACKED0=0 off
+      unsigned* packed0 = (!presort && packed0_on() && plan.bits[0] >= 1) ? counts + (size_t)kMaxBins * ld : nullptr;
       launch_pairs_emit(presort ? plan.bits[0] : 0, rs_tiles, st, b->rec.as<uint4>(), b->tile_pre, b->n, cno, dxu,
-                        dxyu, plan, pbounds, keysA, valsA, counts, ld);
+                        dxyu, plan, pbounds, keysA, valsA, counts, ld, packed0);
       LAUNCHED("k_pairs_emit", st);
       b->launches += 2;
       CU(cudaEventRecord(b->ev[1], st));
       if ((rc = run_passes(b, plan, true, keysA, valsA, keysB, valsB, dO, cno, no, hist, counts, st, &sorted, nullptr,
-                           nullptr, presort)))
+                           nullptr, presort, packed0)))
         return rc;
     } else {
       CU(cudaEventRecord(b->ev[1], st));

@@ -1080,6 +1080,61 @@ k_scan_tile_counts(unsigned* __restrict__ counts, Count cno, unsigned ld, unsign
   if (tid == 0) row_total[blockIdx.x] = carry;
 }
 
+// k_scan_tile_counts for K2's packed first-pass counts: CTA b scans packed row b (digits 2b in
+// the low and 2b+1 in the high half of every word) into rows 2b and 2b+1 of the u32 matrix.
+__global__ void __launch_bounds__(SC_THREADS)
+k_scan_tile_counts_packed(const unsigned* __restrict__ packed, Count cno, unsigned ld, unsigned* __restrict__ counts,
+                          unsigned* __restrict__ row_total) {
+  __shared__ unsigned wsum[SC_THREADS / 32];
+  const unsigned ntiles = (cno.get() + RS_TILE - 1) / RS_TILE;
+  const int tid = threadIdx.x;
+  const unsigned* prow = packed + (size_t)blockIdx.x * ld;
+  unsigned* row0 = counts + (size_t)(2 * blockIdx.x) * ld;
+  unsigned* row1 = row0 + ld;
+  unsigned carry0 = 0, carry1 = 0;
+  for (unsigned base = 0; base < ntiles; base += SC_THREADS * SC_ITEMS) {
+    const unsigned i0 = base + tid * SC_ITEMS;
+    uint4 v[SC_VEC];
+#pragma unroll
+    for (int q = 0; q < SC_VEC; ++q) {
+      const unsigned i = i0 + 4 * q;
+      v[q] = i < ntiles ? *reinterpret_cast<const uint4*>(prow + i) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    unsigned run0 = 0, run1 = 0;
+    uint4 lo[SC_VEC], hi[SC_VEC];
+#pragma unroll
+    for (int q = 0; q < SC_VEC; ++q) {
+      const unsigned i = i0 + 4 * q;
+      // padding columns (>= ntiles) hold garbage
+      const unsigned a = i < ntiles ? v[q].x : 0u, b = i + 1 < ntiles ? v[q].y : 0u;
+      const unsigned c = i + 2 < ntiles ? v[q].z : 0u, d = i + 3 < ntiles ? v[q].w : 0u;
+      const unsigned a0 = a & 0xffffu, b0 = b & 0xffffu, c0 = c & 0xffffu, d0 = d & 0xffffu;
+      const unsigned a1 = a >> 16, b1 = b >> 16, c1 = c >> 16, d1 = d >> 16;
+      lo[q] = make_uint4(run0, run0 + a0, run0 + a0 + b0, run0 + a0 + b0 + c0);
+      hi[q] = make_uint4(run1, run1 + a1, run1 + a1 + b1, run1 + a1 + b1 + c1);
+      run0 += a0 + b0 + c0 + d0;
+      run1 += a1 + b1 + c1 + d1;
+    }
+    unsigned tot0, tot1;
+    const unsigned pre0 = carry0 + block_excl_scan<SC_THREADS / 32>(run0, wsum, tot0);
+    const unsigned pre1 = carry1 + block_excl_scan<SC_THREADS / 32>(run1, wsum, tot1);
+#pragma unroll
+    for (int q = 0; q < SC_VEC; ++q) {
+      const unsigned i = i0 + 4 * q;
+      if (i < ntiles) {
+        *reinterpret_cast<uint4*>(row0 + i) = make_uint4(pre0 + lo[q].x, pre0 + lo[q].y, pre0 + lo[q].z, pre0 + lo[q].w);
+        *reinterpret_cast<uint4*>(row1 + i) = make_uint4(pre1 + hi[q].x, pre1 + hi[q].y, pre1 + hi[q].z, pre1 + hi[q].w);
+      }
+    }
+    carry0 += tot0;
+    carry1 += tot1;
+  }
+  if (tid == 0) {
+    row_total[2 * blockIdx.x] = carry0;
+    row_total[2 * blockIdx.x + 1] = carry1;
+  }
+}
+
 // Scatter one tile of a digit pass. Item j of lane l of warp w is tile element
 // w*512 + j*32 + l (coalesced loads); ranks follow element order, so the pass is stable.
 // Values never occupy registers: cp.async stages them in input order and they are
@@ -1821,7 +1876,7 @@ template <int PRESORT>
 __global__ void __launch_bounds__(RS_THREADS, K2_MIN_CTAS)
 k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno,
              unsigned dx, unsigned dxy, PassPlan plan, const int2* __restrict__ bounds, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
-             unsigned* __restrict__ counts0, unsigned ld) {
+             unsigned* __restrict__ counts0, unsigned ld, unsigned* __restrict__ packed0) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   PeSmem& sm = *reinterpret_cast<PeSmem*>(smem_raw);
   const int tid = threadIdx.x;
@@ -1898,7 +1953,12 @@ k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pr
   __syncthreads();
   // straight into the digit-major matrix: one 4-byte entry per digit row (the rows stay in
   // L2 until the row scan reads them, so the scattered writes cost no extra DRAM traffic)
-  for (int b = tid; b < (1 << plan.bits[0]); b += RS_THREADS) counts0[(size_t)b * ld + blockIdx.x] = sm.h[b];
+  if (packed0) {  // two digits per word (a tile counts <= 4096 < 2^16): half the scattered stores
+    for (int b = tid; b < (1 << plan.bits[0]) / 2; b += RS_THREADS)
+      packed0[(size_t)b * ld + blockIdx.x] = sm.h[2 * b] | (sm.h[2 * b + 1] << 16);
+  } else {
+    for (int b = tid; b < (1 << plan.bits[0]); b += RS_THREADS) counts0[(size_t)b * ld + blockIdx.x] = sm.h[b];
+  }
 }
 
 
