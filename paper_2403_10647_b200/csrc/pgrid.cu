@@ -628,14 +628,16 @@ int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned
     unsigned* vin = vbuf[p & 1];
     unsigned* ko = kbuf[(p + 1) & 1];
     unsigned* vo = last ? vals_final : vbuf[(p + 1) & 1];
+    // with a packed region (packed0), every pass's tile counts travel two digits per word
+    const bool packed = packed0 != nullptr && plan.bits[p] >= 1;
     if (p > 0 || !counts0_ready) {
       const DigitFn dig{plan.shift[p], (1u << plan.bits[p]) - 1u, nullptr};
-      k_tile_counts<<<(ntiles + TC_TILES - 1) / TC_TILES, RS_THREADS, 0, st>>>(kin, cno, dig, 1 << plan.bits[p],
-                                                                              counts, ld);
+      k_tile_counts<<<(ntiles + TC_TILES - 1) / TC_TILES, RS_THREADS, 0, st>>>(
+          kin, cno, dig, 1 << plan.bits[p], counts, ld, packed ? const_cast<unsigned*>(packed0) : nullptr);
       LAUNCHED("k_tile_counts", st);
       ++b->launches;
     }
-    if (p == 0 && counts0_ready && packed0) {
+    if (packed) {
       k_scan_tile_counts_packed<<<1u << (plan.bits[p] - 1), SC_THREADS, 0, st>>>(packed0, cno, ld, counts,
                                                                                 hist + p * kMaxBins);
       LAUNCHED("k_scan_tile_counts", st);

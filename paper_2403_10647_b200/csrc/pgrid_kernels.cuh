@@ -970,7 +970,7 @@ constexpr int TC_TILES = TC_TILES_OVERRIDE;
 #endif
 __global__ void __launch_bounds__(RS_THREADS)
 k_tile_counts(const unsigned* __restrict__ keys, Count cno, DigitFn dig, int nbins, unsigned* __restrict__ counts,
-              unsigned ld) {
+              unsigned ld, unsigned* __restrict__ packed = nullptr) {
   __shared__ unsigned h[TC_TILES][kMaxBins];
   const unsigned no = cno.get();
   const int tid = threadIdx.x;
@@ -1010,9 +1010,16 @@ k_tile_counts(const unsigned* __restrict__ keys, Count cno, DigitFn dig, int nbi
     }
   }
   __syncthreads();
-  for (int i = tid; i < nbins * TC_TILES; i += RS_THREADS) {
-    const int b = i / TC_TILES, q = i % TC_TILES;
-    if (t0 + q < ntiles) counts[(size_t)b * ld + t0 + q] = h[q][b];
+  if (packed) {  // two digits per word, as K2 writes pass 0 (k_scan_tile_counts_packed unpacks)
+    for (int i = tid; i < (nbins / 2) * TC_TILES; i += RS_THREADS) {
+      const int b = i / TC_TILES, q = i % TC_TILES;
+      if (t0 + q < ntiles) packed[(size_t)b * ld + t0 + q] = h[q][2 * b] | (h[q][2 * b + 1] << 16);
+    }
+  } else {
+    for (int i = tid; i < nbins * TC_TILES; i += RS_THREADS) {
+      const int b = i / TC_TILES, q = i % TC_TILES;
+      if (t0 + q < ntiles) counts[(size_t)b * ld + t0 + q] = h[q][b];
+    }
   }
 }
 
