@@ -25,6 +25,38 @@ namespace {
 
 thread_local std::string g_err;
 
+// PGRID_PDL: 0 launches the build's kernel chain without programmatic dependent launch, 1 uses
+// it for every link, 2 only for the glue kernels (scans, bounds), 3 only for the bulk passes.
+int pdl_mode() {
+  static const int m = [] {
+    const char* e = getenv("PGRID_PDL");
+    return e && *e ? atoi(e) : 1;
+  }();
+  return m;
+}
+
+// Launch `k` with the programmatic-serialization attribute: its launch is processed while the
+// previous kernel on `st` retires instead of after it (the launch latency between links).
+// Only for kernels that open with PDL_ENTRY() (griddepcontrol.wait before any global access);
+// after a non-kernel stream operation the launch is an ordinary serialised one.
+template <typename... KArgs, typename... Args>
+void pdl_launch(bool glue, void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                Args&&... args) {
+  const int m = pdl_mode();
+  const bool on = m == 1 || (m == 2 && glue) || (m == 3 && !glue);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = on ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 int fail(int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -103,8 +135,8 @@ template <int BITS, bool TABLE>
 void launch_scatter_bits(unsigned ntiles, cudaStream_t st, const unsigned* kin, const unsigned* vin, unsigned* ko,
                          unsigned* vo, Count n, int shift, const unsigned* hist, const unsigned* offs, unsigned ld,
                          const unsigned* dtable, const unsigned* kbase) {
-  k_radix_scatter<BITS, TABLE><<<ntiles, RS_THREADS, rs_smem_bytes(), st>>>(kin, vin, ko, vo, n, shift, hist, offs,
-                                                                           ld, dtable, kbase);
+  pdl_launch(false, k_radix_scatter<BITS, TABLE>, ntiles, RS_THREADS, rs_smem_bytes(), st, kin, vin, ko, vo, n, shift,
+             hist, offs, ld, dtable, kbase);
 }
 
 // bit-field digits of 1..9 bits, or (dtable != null) slab-table digits of 1..4 bits
@@ -211,8 +243,8 @@ void launch_pairs_emit(int presort_bits, unsigned grid, cudaStream_t st, const u
   switch (presort_bits) {
 #define PG_CASE(B)                                                                                        \
   case B:                                                                                                 \
-    k_pairs_emit<B><<<grid, RS_THREADS, sizeof(PeSmem), st>>>(rec, tile_pre, n, cno, dx, dxy, plan, bounds, keys, \
-                                                              vals, counts, ld, packed0);                 \
+    pdl_launch(false, k_pairs_emit<B>, grid, RS_THREADS, sizeof(PeSmem), st, rec, tile_pre, n, cno, dx, dxy, plan, \
+               bounds, keys, vals, counts, ld, packed0);                                                  \
     break;
     PG_CASE(0) PG_CASE(1) PG_CASE(2) PG_CASE(3) PG_CASE(4) PG_CASE(5) PG_CASE(6) PG_CASE(7) PG_CASE(8) PG_CASE(9)
 #undef PG_CASE
@@ -469,7 +501,7 @@ int count_enqueue(pg_builder* b, const double* dV, int64_t nv, const int32_t* dT
   k_boxes_count<<<ntiles, K1_THREADS, sizeof(K1Smem), st>>>(dV, nv, reinterpret_cast<const int*>(dT), n, ds, bulk_ok,
                                                             b->rec.as<uint4>(), tile_sum, err);
   LAUNCHED("k_boxes_count", st);
-  k_scan_tile_sums<<<1, TS_THREADS, 0, st>>>(tile_sum, ntiles, tile_pre, total);
+  pdl_launch(true, k_scan_tile_sums, 1, TS_THREADS, 0, st, tile_sum, ntiles, tile_pre, total);
   LAUNCHED("k_scan_tile_sums", st);
   CU(cudaEventRecord(b->ev[6], st));
   b->launches = 2;
@@ -632,17 +664,18 @@ int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned
     const bool packed = packed0 != nullptr && plan.bits[p] >= 1;
     if (p > 0 || !counts0_ready) {
       const DigitFn dig{plan.shift[p], (1u << plan.bits[p]) - 1u, nullptr};
-      k_tile_counts<<<(ntiles + TC_TILES - 1) / TC_TILES, RS_THREADS, 0, st>>>(
-          kin, cno, dig, 1 << plan.bits[p], counts, ld, packed ? const_cast<unsigned*>(packed0) : nullptr);
+      pdl_launch(false, k_tile_counts, (ntiles + TC_TILES - 1) / TC_TILES, RS_THREADS, 0, st, kin, cno, dig,
+                 1 << plan.bits[p], counts, ld, packed ? const_cast<unsigned*>(packed0) : nullptr);
       LAUNCHED("k_tile_counts", st);
       ++b->launches;
     }
     if (packed) {
-      k_scan_tile_counts_packed<<<1u << (plan.bits[p] - 1), SC_THREADS, 0, st>>>(packed0, cno, ld, counts,
-                                                                                hist + p * kMaxBins);
+      pdl_launch(true, k_scan_tile_counts_packed, 1u << (plan.bits[p] - 1), SC_THREADS, 0, st, packed0, cno, ld,
+                 counts, hist + p * kMaxBins);
       LAUNCHED("k_scan_tile_counts", st);
     } else {
-      k_scan_tile_counts<<<1u << plan.bits[p], SC_THREADS, 0, st>>>(counts, cno, ld, hist + p * kMaxBins);
+      pdl_launch(true, k_scan_tile_counts, 1u << plan.bits[p], SC_THREADS, 0, st, counts, cno, ld,
+                 hist + p * kMaxBins);
       LAUNCHED("k_scan_tile_counts", st);
     }
     if (p == 0 && presorted0) {
@@ -760,12 +793,12 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
     // narrow K4's bound searches with the last pass's digit totals (when a sort ran)
     const int lp = plan.npasses - 1;
     const bool top = lp >= 0 && no > 0 && ncells > 1;
-    k_key_tile_bounds<<<(g_tiles + 1 + 7) / 8, 256, 0, st>>>(sorted, cno, G_TILE, (unsigned)ncells, g_tiles + 1,
-                                                            kbounds, top ? hist + lp * kMaxBins : nullptr,
-                                                            top ? plan.shift[lp] : 0, top ? 1 << plan.bits[lp] : 0);
+    pdl_launch(true, k_key_tile_bounds, (g_tiles + 1 + 7) / 8, 256, 0, st, sorted, cno, G_TILE, (unsigned)ncells,
+               g_tiles + 1, kbounds, top ? hist + lp * kMaxBins : nullptr, top ? plan.shift[lp] : 0,
+               top ? 1 << plan.bits[lp] : 0);
   }
   LAUNCHED("k_key_tile_bounds", st);
-  k_cell_offsets<<<g_tiles, G_THREADS, 0, st>>>(sorted, cno, (unsigned)ncells, kbounds, dG);
+  pdl_launch(false, k_cell_offsets, g_tiles, G_THREADS, 0, st, sorted, cno, (unsigned)ncells, kbounds, dG);
   LAUNCHED("k_cell_offsets", st);
   b->launches += 2;
   b->sorted_keys = sorted;

@@ -28,6 +28,31 @@ namespace pgrid {
 // ----------------------------------------------------------------------------------------
 // common helpers
 // ----------------------------------------------------------------------------------------
+
+// Programmatic dependent launch (the build's kernel chain, pgrid.cu pdl_launch): a kernel
+// launched with the programmatic-serialization attribute may become resident while its
+// predecessor drains. pdl_wait() returns once the predecessor grid has completed and its
+// writes are visible (a no-op for a normal launch), so it comes before any global access, and
+// every kernel's wait also orders it after all earlier grids (each waited on its own).
+// pdl_trigger() after it would let the successor launch before this grid retires (off, below).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// The early trigger is compiled out: with every link triggering at kernel entry a cfg3 build
+// replayed 6% slower (0.815 vs 0.767 ms; glue-only or bulk-only links were neutral), while the
+// untriggered chain (successor launches as the predecessor retires) measured 0.765 ms.
+#ifndef PGRID_PDL_TRIGGER
+#define PGRID_PDL_TRIGGER 0
+#endif
+__device__ __forceinline__ void pdl_trigger() {
+#if PGRID_PDL_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+#define PDL_ENTRY() \
+  do {              \
+    pdl_wait();     \
+    pdl_trigger();  \
+  } while (0)
+
 struct DevSpec {
   double lo[3];
   double hi[3];
@@ -265,6 +290,7 @@ __global__ void __launch_bounds__(K1_THREADS)
 k_boxes_count(const double* __restrict__ V, long long nv, const int* __restrict__ T, long long n, DevSpec s,
               int bulk_ok, uint4* __restrict__ rec, unsigned long long* __restrict__ tile_sum,
               unsigned* __restrict__ err) {
+  PDL_ENTRY();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   K1Smem& sm = *reinterpret_cast<K1Smem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -375,6 +401,7 @@ constexpr int TS_REG = 20;  // chunks of 32 held in registers per lane (single-p
 __global__ void __launch_bounds__(TS_THREADS)
 k_scan_tile_sums(const unsigned long long* __restrict__ tile_sum, unsigned ntiles, unsigned* __restrict__ tile_pre,
                  unsigned long long* __restrict__ total) {
+  PDL_ENTRY();
   __shared__ unsigned long long wsum[TS_WARPS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // warp w owns the contiguous segment [w*seg, (w+1)*seg), read in coalesced 32-wide chunks
@@ -709,6 +736,7 @@ __device__ __forceinline__ void warp_lower_bound2(unsigned long long& lo0, unsig
 __global__ void __launch_bounds__(256)
 k_pair_tile_bounds(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno,
                    unsigned tile, int2* __restrict__ bounds) {
+  PDL_ENTRY();
   const unsigned no = cno.get();
   const unsigned ntiles = (no + tile - 1) / tile;
   const unsigned t = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -737,6 +765,7 @@ __global__ void __launch_bounds__(256)
 k_key_tile_bounds(const unsigned* __restrict__ sorted, Count cno, unsigned step, unsigned ncells, unsigned nq,
                   unsigned* __restrict__ out, const unsigned* __restrict__ top_hist = nullptr, int top_shift = 0,
                   int top_bins = 0) {
+  PDL_ENTRY();
   __shared__ unsigned start[kMaxBins + 1];
   const unsigned no = cno.get();
   if (top_hist) {
@@ -971,6 +1000,7 @@ constexpr int TC_TILES = TC_TILES_OVERRIDE;
 __global__ void __launch_bounds__(RS_THREADS)
 k_tile_counts(const unsigned* __restrict__ keys, Count cno, DigitFn dig, int nbins, unsigned* __restrict__ counts,
               unsigned ld, unsigned* __restrict__ packed = nullptr) {
+  PDL_ENTRY();
   __shared__ unsigned h[TC_TILES][kMaxBins];
   const unsigned no = cno.get();
   const int tid = threadIdx.x;
@@ -1051,6 +1081,7 @@ constexpr int SC_ITEMS = 4 * SC_VEC;       // 20 tiles per thread, 5120 per chun
 // threads fit one wave. The row total is the digit's global count (its histogram bin).
 __global__ void __launch_bounds__(SC_THREADS)
 k_scan_tile_counts(unsigned* __restrict__ counts, Count cno, unsigned ld, unsigned* __restrict__ row_total) {
+  PDL_ENTRY();
   __shared__ unsigned wsum[SC_THREADS / 32];
   const unsigned ntiles = (cno.get() + RS_TILE - 1) / RS_TILE;
   const int tid = threadIdx.x;
@@ -1092,6 +1123,7 @@ k_scan_tile_counts(unsigned* __restrict__ counts, Count cno, unsigned ld, unsign
 __global__ void __launch_bounds__(SC_THREADS)
 k_scan_tile_counts_packed(const unsigned* __restrict__ packed, Count cno, unsigned ld, unsigned* __restrict__ counts,
                           unsigned* __restrict__ row_total) {
+  PDL_ENTRY();
   __shared__ unsigned wsum[SC_THREADS / 32];
   const unsigned ntiles = (cno.get() + RS_TILE - 1) / RS_TILE;
   const int tid = threadIdx.x;
@@ -1426,6 +1458,7 @@ k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict
                 unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, Count cno, int shift,
                 const unsigned* __restrict__ hist, const unsigned* __restrict__ offs, unsigned ld,
                 const unsigned* __restrict__ dtable, const unsigned* __restrict__ kbase) {
+  PDL_ENTRY();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   RsSmem& sm = *reinterpret_cast<RsSmem*>(smem_raw);
   const unsigned no = cno.get();
@@ -1884,6 +1917,7 @@ __global__ void __launch_bounds__(RS_THREADS, K2_MIN_CTAS)
 k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno,
              unsigned dx, unsigned dxy, PassPlan plan, const int2* __restrict__ bounds, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
              unsigned* __restrict__ counts0, unsigned ld, unsigned* __restrict__ packed0) {
+  PDL_ENTRY();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   PeSmem& sm = *reinterpret_cast<PeSmem*>(smem_raw);
   const int tid = threadIdx.x;
@@ -2208,6 +2242,7 @@ constexpr int G_TILE = G_THREADS * G_ITEMS;  // cells per CTA
 __global__ void __launch_bounds__(G_THREADS)
 k_cell_offsets(const unsigned* __restrict__ sorted, Count cno, unsigned ncells, const unsigned* __restrict__ kb,
                unsigned* __restrict__ G) {
+  PDL_ENTRY();
   const unsigned no = cno.get();
   __shared__ __align__(16) unsigned mark[G_TILE];
   __shared__ unsigned sh_wmin[G_ITEMS / 4 * (G_THREADS / 32)];
