@@ -485,16 +485,17 @@ int count_enqueue(pg_builder* b, const double* dV, int64_t nv, const int32_t* dT
   b->last_T = dT;
   b->last_ds = ds;
   if ((rc = b->rec.ensure((size_t)n * sizeof(uint4)))) return rc;
-  // K1 area: [tile_sum u64 x ntiles][tile_pre u32 x ntiles][err u32][pad][total u64]
+  // K1 area: [tile_sum u64 x ntiles][tile_pre u32 x ntiles][total u64][err u32][pad]
   const size_t ts_bytes = align_up((size_t)ntiles * 8), tp_bytes = align_up((size_t)ntiles * 4);
   if ((rc = b->k1_sync.ensure(ts_bytes + tp_bytes + 256))) return rc;
   unsigned long long* tile_sum = b->k1_sync.as<unsigned long long>();
   unsigned* tile_pre = b->k1_sync.as<unsigned>(ts_bytes);
-  unsigned* err = b->k1_sync.as<unsigned>(ts_bytes + tp_bytes);
-  unsigned long long* total = b->k1_sync.as<unsigned long long>(ts_bytes + tp_bytes + 8);
+  // [total u64][err u32][pad u32]: one 16-byte copy lands them in h_scalars[0] and [1]
+  unsigned long long* total = b->k1_sync.as<unsigned long long>(ts_bytes + tp_bytes);
+  unsigned* err = b->k1_sync.as<unsigned>(ts_bytes + tp_bytes + 8);
   b->tile_pre = tile_pre;
   b->d_total = total;
-  CU(cudaMemsetAsync(err, 0, 16, st));
+  CU(cudaMemsetAsync(total, 0, 16, st));
   CU(cudaEventRecord(b->ev[5], st));
   // TMA bulk staging needs 16-byte aligned sources
   const int bulk_ok = ((reinterpret_cast<uintptr_t>(dV) | reinterpret_cast<uintptr_t>(dT)) & 15) == 0;
@@ -506,8 +507,7 @@ int count_enqueue(pg_builder* b, const double* dV, int64_t nv, const int32_t* dT
   CU(cudaEventRecord(b->ev[6], st));
   b->launches = 2;
   b->k1_timed = true;
-  CU(cudaMemcpyAsync(&b->h_scalars[0], total, 8, cudaMemcpyDeviceToHost, st));
-  CU(cudaMemcpyAsync(&b->h_scalars[1], err, 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(&b->h_scalars[0], total, 16, cudaMemcpyDeviceToHost, st));
   return PG_OK;
 }
 
