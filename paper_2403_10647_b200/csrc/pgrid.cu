@@ -478,7 +478,7 @@ int count_setup(pg_builder* b, int64_t nv, int64_t n, const pg_spec* spec, DevSp
 // K1 + cross-tile scan on device-resident V/T (n >= 1); NO and the error flags are copied
 // to the pinned b->h_scalars asynchronously (read them after the stream is synchronised).
 int count_enqueue(pg_builder* b, const double* dV, int64_t nv, const int32_t* dT, int64_t n, const DevSpec& ds,
-                  cudaStream_t st) {
+                  cudaStream_t st, bool readback = true) {
   const unsigned ntiles = (unsigned)((n + K1_TILE - 1) / K1_TILE);
   int rc;
   b->last_V = dV;
@@ -507,7 +507,7 @@ int count_enqueue(pg_builder* b, const double* dV, int64_t nv, const int32_t* dT
   CU(cudaEventRecord(b->ev[6], st));
   b->launches = 2;
   b->k1_timed = true;
-  CU(cudaMemcpyAsync(&b->h_scalars[0], total, 16, cudaMemcpyDeviceToHost, st));
+  if (readback) CU(cudaMemcpyAsync(&b->h_scalars[0], total, 16, cudaMemcpyDeviceToHost, st));
   return PG_OK;
 }
 
@@ -740,7 +740,9 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
   const unsigned ld = (rs_tiles + 3) & ~3u;  // counts row stride
 
   CU(cudaEventRecord(b->ev[0], st));
-  CU(cudaMemsetAsync(hist, 0, hist_bytes, st));
+  // with radix passes, the pair-tile bounds kernel ahead of K2 clears hist itself
+  const bool zero_in_bounds = no > 0 && plan.npasses > 0;
+  if (!zero_in_bounds) CU(cudaMemsetAsync(hist, 0, hist_bytes, st));
   const unsigned* sorted = keysA;
   if (no > 0) {
     const unsigned dxu = (unsigned)b->dims[0], dxyu = (unsigned)b->dims[0] * (unsigned)b->dims[1];
@@ -765,8 +767,8 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
     }
     if (plan.npasses > 0) {
       // K2 on radix tiles: pairs in generation order + first-pass tile counts
-      k_pair_tile_bounds<<<(rs_tiles + 7) / 8, 256, 0, st>>>(b->rec.as<uint4>(), b->tile_pre, b->n, cno, RS_TILE,
-                                                            pbounds);
+      pdl_launch(true, k_pair_tile_bounds, (rs_tiles + 7) / 8, 256, 0, st, b->rec.as<uint4>(), b->tile_pre, b->n,
+                 cno, RS_TILE, pbounds, hist, (unsigned)(hist_bytes / 4));
       LAUNCHED("k_pair_tile_bounds", st);
       // K2 writes its first-pass tile counts straight into the digit-major matrix
       // with the presort, K2 leaves every tile sorted by the first digit (pass 0 then only moves
@@ -877,8 +879,12 @@ int pg_build_async(pg_builder* b, const double* V, int64_t nv, const int32_t* T,
     if (n == 0 || !V || !T) return fail(PG_INVARIANT_ERROR, "pg_build_async needs a non-empty device mesh");
     auto enqueue = [&](cudaStream_t s2) -> int {
       int r;
-      if ((r = count_enqueue(b, V, nv, T, n, ds, s2))) return r;
-      return finish_impl(b, G, O, 0, s2, nullptr, Count{b->d_total, (unsigned)cap}, cap);
+      // NO and the error flags are read back after the build (only the host's post-build
+      // check reads them), so K1's scan chains straight into the pair expansion
+      if ((r = count_enqueue(b, V, nv, T, n, ds, s2, false))) return r;
+      if ((r = finish_impl(b, G, O, 0, s2, nullptr, Count{b->d_total, (unsigned)cap}, cap))) return r;
+      CU(cudaMemcpyAsync(&b->h_scalars[0], b->d_total, 16, cudaMemcpyDeviceToHost, s2));
+      return PG_OK;
     };
     if ((rc = enqueue(b->gst))) return rc;  // eager run: sizes the workspace
     b->glaunches = b->launches;

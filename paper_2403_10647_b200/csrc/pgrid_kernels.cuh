@@ -735,8 +735,13 @@ __device__ __forceinline__ void warp_lower_bound2(unsigned long long& lo0, unsig
 // objects' offsets inside it; both queries of a tile run in lockstep.
 __global__ void __launch_bounds__(256)
 k_pair_tile_bounds(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno,
-                   unsigned tile, int2* __restrict__ bounds) {
+                   unsigned tile, int2* __restrict__ bounds, unsigned* __restrict__ zero = nullptr,
+                   unsigned nzero = 0) {
   PDL_ENTRY();
+  // optional: clear the radix digit totals here (the row scans that fill them run later),
+  // so no memset node breaks the launch chain
+  if (zero)
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < nzero; i += gridDim.x * blockDim.x) zero[i] = 0;
   const unsigned no = cno.get();
   const unsigned ntiles = (no + tile - 1) / tile;
   const unsigned t = blockIdx.x * 8 + (threadIdx.x >> 5);
