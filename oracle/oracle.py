@@ -117,11 +117,16 @@ def build_parallel(vertices, triangles, spec, stages=False):
         raise MemoryError("oracle count failed")
     NO = no.value
     ncells = int(spec.dims[0]) * int(spec.dims[1]) * int(spec.dims[2])
-    G = np.empty(ncells + 1, np.uint32)
+    # ncells > 2^30 fails the G scan (SizeError) before G is written: no 4 GB buffer for it
+    G = np.empty(ncells + 1 if ncells <= (1 << 30) else 1, np.uint32)
     O = np.empty(NO, np.uint32)
     st = [np.empty(NO, np.uint32) for _ in range(4)] if stages else [None] * 4
     rc = lib().orc_build_parallel(_ptr(V), _ptr(T), len(T), ctypes.byref(s), _ptr(G), _ptr(O),
                                   *[_ptr(a) for a in st])
+    if rc == SIZE_ERROR:
+        raise OracleSizeError(f"ncells={ncells}")
+    if rc == INVARIANT_ERROR:
+        raise OracleInvariantError("cell of an inverted box outside [0, ncells)")
     if rc:
         raise MemoryError("oracle build failed")
     if not stages:

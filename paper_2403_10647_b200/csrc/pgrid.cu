@@ -359,6 +359,14 @@ struct pg_builder {
   const double* last_V = nullptr;
   const int32_t* last_T = nullptr;
   DevSpec last_ds{};
+  // positive-count inverted boxes of the last count (two inverted axes): their pairs are
+  // rewritten with the reference's cells after the expansion (k_inverted_pairs). inv holds
+  // [count u32][err u32][pad][list of triangle ids]
+  bool inv_fix = false;
+  DevBuf inv;
+  // G / O of the last pg_build_async (pg_build_wait's host-counted rebuild)
+  uint32_t* g_G = nullptr;
+  uint32_t* g_O = nullptr;
   // pg_partition_counts -> pg_partition_send
   int64_t part_n = -1;
   int part_bits = 0;
@@ -442,9 +450,12 @@ int pg_last_launch_count(pg_builder* b) { return b ? b->launches : 0; }
 namespace {
 
 // Validation + builder state for a build of (n triangles, spec); fills the device spec.
-int count_setup(pg_builder* b, int64_t nv, int64_t n, const pg_spec* spec, DevSpec& ds) {
+// late_ncells: the host-counted path reports ncells > 2^30 after the count checks, where the
+// reference does (its G scan, builders.py:130, runs last); the device-count paths check it here.
+int count_setup(pg_builder* b, int64_t nv, int64_t n, const pg_spec* spec, DevSpec& ds, bool late_ncells = false) {
   b->counted = false;
   b->deferred = false;
+  b->inv_fix = false;
   b->stages_kept = false;
   b->k1_timed = false;
   b->launches = 0;
@@ -458,7 +469,7 @@ int count_setup(pg_builder* b, int64_t nv, int64_t n, const pg_spec* spec, DevSp
   }
   // The reference raises SizeError once the G scan sees more than 2^30 cells
   // (primitives.py:29-31 via builders.py:130); every successful build has ncells <= 2^30.
-  if (ncells > kMaxScan)
+  if (ncells > kMaxScan && !late_ncells)
     return fail(PG_SIZE_ERROR, "array of %lld elements exceeds the scan size limit", (long long)ncells);
   if (n > kMaxScan) return fail(PG_SIZE_ERROR, "%lld triangles exceed the scan size limit", (long long)n);
   for (int k = 0; k < 3; ++k) {
@@ -511,47 +522,87 @@ int count_enqueue(pg_builder* b, const double* dV, int64_t nv, const int32_t* dT
   return PG_OK;
 }
 
-// Error checks on the NO / flags that count_enqueue copied back (stream synchronised).
-// An inverted kept box (hi < lo on some axis after clipping) is what the reference's count
-// phase produces for an infinite or huge upper corner. The reference then accepts it only
-// when it is the one kept triangle and its signed pair count is 0 (an empty grid); a negative
-// count fails exclusive_sum's non-negativity check and any zero-count group among >= 2 kept
-// objects fails mark_boundaries. (A lone triangle with two inverted axes has a positive
-// count and the reference builds cells from the inverted box; that is reported as an
-// error here.)
-int resolve_inverted(pg_builder* b, bool& accept) {
-  accept = false;
-  DevBuf tmp;
+// Error path of a count whose K1 flagged an inverted kept box (hi < lo on some axis after
+// clipping: an infinite or huge upper corner). Counts the kept triangles and the inverted
+// boxes by the sign of their pair count, lists the positive ones (two inverted axes) and, if
+// any, checks that every cell the reference computes for them lies in [0, ncells).
+struct InvStats {
+  unsigned long long kept, inverted, negative, zero, positive;
+  bool cells_ok;
+};
+int resolve_inverted(pg_builder* b, InvStats& r) {
   int rc;
-  if ((rc = tmp.ensure(32))) return rc;
-  long long init[4] = {0, 0, LLONG_MAX, LLONG_MIN};
-  CU(cudaMemcpy(tmp.p, init, 32, cudaMemcpyHostToDevice));
-  k_inverted_boxes<<<(unsigned)((b->n + 255) / 256), 256>>>(b->last_V, b->last_T, b->n, b->last_ds,
-                                                             tmp.as<long long>());
+  const size_t head = 256;
+  if ((rc = b->inv.ensure(head + (size_t)std::max<int64_t>(b->n, 1) * 4))) return rc;
+  unsigned long long* out = b->inv.as<unsigned long long>(16);
+  unsigned* nlist = b->inv.as<unsigned>(0);
+  unsigned* err = nlist + 1;
+  unsigned* list = b->inv.as<unsigned>(head);
+  CU(cudaMemset(b->inv.p, 0, head));
+  k_inverted_boxes<<<(unsigned)((b->n + 255) / 256), 256>>>(b->last_V, b->last_T, b->n, b->last_ds, out, list,
+                                                            nlist);
   CU(cudaGetLastError());
-  long long r[4];
-  CU(cudaMemcpy(r, tmp.p, 32, cudaMemcpyDeviceToHost));
-  tmp.release();
-  accept = r[0] == 1 && r[1] == 1 && r[2] == 0 && r[3] == 0;
+  unsigned long long h[4];
+  CU(cudaMemcpy(h, out, 32, cudaMemcpyDeviceToHost));
+  r = {h[0], h[1], h[2], h[3], h[1] - h[2] - h[3], true};
+  if (r.positive && !r.negative) {
+    k_inverted_pairs<<<(unsigned)std::min<unsigned long long>(r.positive, 4096), 256>>>(
+        b->last_V, b->last_T, b->last_ds, nullptr, nullptr, list, nlist, b->ncells, nullptr, nullptr, 0, err);
+    CU(cudaGetLastError());
+    unsigned he = 0;
+    CU(cudaMemcpy(&he, err, 4, cudaMemcpyDeviceToHost));
+    r.cells_ok = he == 0;
+  }
   return PG_OK;
 }
 
+// The reference's cells for the pairs of positive-count inverted boxes, written over K2's
+// placeholders in `keys` (generation order); `coarse` (sharded builds) is kept consistent.
+int fix_inverted(pg_builder* b, unsigned* keys, cudaStream_t st, unsigned* coarse = nullptr, int coarse_shift = 0) {
+  if (!b->inv_fix) return PG_OK;
+  unsigned* nlist = b->inv.as<unsigned>(0);
+  k_inverted_pairs<<<4096, 256, 0, st>>>(b->last_V, b->last_T, b->last_ds, b->rec.as<uint4>(), b->tile_pre,
+                                         b->inv.as<unsigned>(256), nlist, b->ncells, keys, coarse, coarse_shift,
+                                         nlist + 1);
+  LAUNCHED("k_inverted_pairs", st);
+  ++b->launches;
+  return PG_OK;
+}
+
+// Error checks on the NO / flags that count_enqueue copied back (stream synchronised), in
+// the reference's order (builders.py:90-101, 155-160, 125-130): index range (the mesh's own
+// check, geometry.py:41-43); a negative pair count (exclusive_sum, primitives.py:22-25);
+// NO > 2^32-1 (builders.py:99-100); a zero count among >= 2 kept triangles (mark_boundaries,
+// primitives.py:66-72; a lone zero-count triangle gives an empty grid); NO > 2^30
+// (inclusive_sum, primitives.py:29-31); cells of two-axis inverted boxes outside [0, ncells)
+// (radix_sort_pairs / scatter, primitives.py:102-111, 135-136); ncells > 2^30 (the G scan).
 int count_check(pg_builder* b, uint64_t* no_out) {
   uint64_t no = b->h_scalars[0];
   const unsigned errf = (unsigned)(b->h_scalars[1] & 0xffffffffu);
+  b->inv_fix = false;
   if (errf & 2u) return fail(PG_INVARIANT_ERROR, "triangle index out of range");
+  InvStats r{};
   if (errf & 1u) {
-    bool accept = false;
-    int rc = resolve_inverted(b, accept);
+    int rc = resolve_inverted(b, r);
     if (rc) return rc;
-    if (!accept) return fail(PG_INVARIANT_ERROR, "triangle cell box with hi < lo (non-finite or huge upper corner)");
-    no = 0;  // the lone kept triangle has no pairs: an empty grid
+    if (r.negative) return fail(PG_INVARIANT_ERROR, "index arrays are non-negative (inverted cell box, negative count)");
   }
   if (no_out) *no_out = no;
   if ((int64_t)no > kMaxIds)
     return fail(PG_SIZE_ERROR, "%llu cell/object pairs exceed 32-bit id space", (unsigned long long)no);
+  if (r.zero) {
+    if (r.kept >= 2) return fail(PG_INVARIANT_ERROR, "coincident boundary marks (zero-count group?)");
+    no = 0;  // the lone kept triangle has no pairs: an empty grid
+    if (no_out) *no_out = 0;
+  }
   if ((int64_t)no > kMaxScan)
     return fail(PG_SIZE_ERROR, "array of %llu elements exceeds the scan size limit", (unsigned long long)no);
+  if (r.positive) {
+    if (!r.cells_ok) return fail(PG_INVARIANT_ERROR, "cell of an inverted box outside [0, ncells)");
+    b->inv_fix = true;
+  }
+  if (b->ncells > kMaxScan)
+    return fail(PG_SIZE_ERROR, "array of %lld elements exceeds the scan size limit", (long long)b->ncells);
   b->no = no;
   b->counted = true;
   return PG_OK;
@@ -572,9 +623,11 @@ int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64
   drop_graph(b);
   DevSpec ds;
   int rc;
-  if ((rc = count_setup(b, nv, n, spec, ds))) return rc;
+  if ((rc = count_setup(b, nv, n, spec, ds, !(flags & PG_DEFER)))) return rc;
   ktimer_reset(st);
   if (n == 0) {
+    if (b->ncells > kMaxScan)
+      return fail(PG_SIZE_ERROR, "array of %lld elements exceeds the scan size limit", (long long)b->ncells);
     // an empty mesh (or an empty shard of a sharded build): NO = 0, also on the device for
     // the steps that read the count there (pg_peer_put_count, deferred grids)
     if ((rc = b->k1_sync.ensure(256))) return rc;
@@ -757,6 +810,7 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
                                                      keysA, v0, 0u, nullptr, 0, 0);
       LAUNCHED("k_expand_pairs", st);
       b->launches += 2;
+      if ((rc = fix_inverted(b, keysA, st))) return rc;
       if (flags & PG_KEEP_STAGES) {
         if ((rc = b->stage.ensure(2 * sec))) return rc;
         CU(cudaMemcpyAsync(b->stage.as<unsigned>(0), keysA, no * 4, cudaMemcpyDeviceToDevice, st));
@@ -773,16 +827,19 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
       // K2 writes its first-pass tile counts straight into the digit-major matrix
       // with the presort, K2 leaves every tile sorted by the first digit (pass 0 then only moves
       // digit runs); stage dumps (record=) need generation order, so they skip it
-      const bool presort = presort_on() && !(flags & PG_KEEP_STAGES);
+      const bool presort = presort_on() && !(flags & PG_KEEP_STAGES) && !b->inv_fix;
       // K2's first-pass counts two digits per word (the row scan unpacks them): PGRID_PACKED0=0 off
-      unsigned* packed0 = (!presort && packed0_on() && plan.bits[0] >= 1) ? counts + (size_t)kMaxBins * ld : nullptr;
+      unsigned* packed0 = (!presort && !b->inv_fix && packed0_on() && plan.bits[0] >= 1)
+                              ? counts + (size_t)kMaxBins * ld : nullptr;
       launch_pairs_emit(presort ? plan.bits[0] : 0, rs_tiles, st, b->rec.as<uint4>(), b->tile_pre, b->n, cno, dxu,
                         dxyu, plan, pbounds, keysA, valsA, counts, ld, packed0);
       LAUNCHED("k_pairs_emit", st);
       b->launches += 2;
+      // two-axis inverted boxes: their keys are rewritten, so pass 0 recounts its digits
+      if ((rc = fix_inverted(b, keysA, st))) return rc;
       CU(cudaEventRecord(b->ev[1], st));
-      if ((rc = run_passes(b, plan, true, keysA, valsA, keysB, valsB, dO, cno, no, hist, counts, st, &sorted, nullptr,
-                           nullptr, presort, packed0)))
+      if ((rc = run_passes(b, plan, !b->inv_fix, keysA, valsA, keysB, valsB, dO, cno, no, hist, counts, st, &sorted,
+                           nullptr, nullptr, presort, packed0)))
         return rc;
     } else {
       CU(cudaEventRecord(b->ev[1], st));
@@ -905,6 +962,8 @@ int pg_build_async(pg_builder* b, const double* V, int64_t nv, const int32_t* T,
     }
   }
   b->g_cap = cap;
+  b->g_G = G;
+  b->g_O = O;
   CU(cudaEventRecord(b->g_out, b->gst));
   CU(cudaStreamWaitEvent(st, b->g_out, 0));
   return PG_OK;
@@ -919,6 +978,14 @@ int pg_build_wait(pg_builder* b, uint64_t* no_out) {
   if (b->no > b->g_cap)
     return fail(PG_CAPACITY_ERROR, "NO = %llu exceeds the O capacity %llu", (unsigned long long)b->no,
                 (unsigned long long)b->g_cap);
+  if (b->inv_fix) {
+    // boxes inverted on two axes: the device-count build left placeholders for their pairs;
+    // finish again from the host-checked count (K1's records are current), then the graph is
+    // re-captured by the next call
+    drop_graph(b);
+    if ((rc = finish_impl(b, b->g_G, b->g_O, 0, b->gst, nullptr, Count{nullptr, (unsigned)b->no}, b->no))) return rc;
+    CU(cudaStreamSynchronize(b->gst));
+  }
   return PG_OK;
 }
 
@@ -930,6 +997,11 @@ int pg_finish_baseline(pg_builder* b, int algo, uint32_t* G, uint32_t* O, uint32
   if (!b || !b->counted) return fail(PG_STATE_ERROR, "pg_finish_baseline without a successful pg_count");
   if (b->deferred) return fail(PG_STATE_ERROR, "pg_finish_baseline after a PG_DEFER count");
   if (algo != 1 && algo != 2) return fail(PG_INVARIANT_ERROR, "algo must be 1 (sorted) or 2 (compact)");
+  // the reference's per-object walks (_ckernels.pyx:53-109) skip a box inverted on two axes
+  // while its count says otherwise: its pairs are uninitialised memory there (np.empty)
+  if (b->inv_fix)
+    return fail(PG_INVARIANT_ERROR, "cell box inverted on two axes: undefined in the reference's %s builder",
+                algo == 1 ? "sorted" : "compact");
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   CU(cudaSetDevice(b->device));
   drop_graph(b);
@@ -1180,6 +1252,7 @@ int pg_pairs(pg_builder* b, uint32_t* keys, uint32_t* vals, uint32_t val_offset,
                                                    coarse_bins);
     LAUNCHED("k_expand_pairs", st);
     b->launches += 2;
+    if ((rc = fix_inverted(b, keys, st, dcoarse, coarse_shift))) return rc;
   }
   return PG_OK;
 }

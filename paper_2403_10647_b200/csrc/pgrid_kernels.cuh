@@ -231,54 +231,121 @@ __device__ __forceinline__ void tri_box_raw(const double* a, const double* b, co
   }
 }
 
+// Signed pair count prod(hi - lo + 1) of a kept box (builders.py:96): an inverted box (hi < lo
+// on some axis: an infinite / > 2^63-cell upper corner casts to INT64_MIN and clips to 0,
+// gridcore.py:161-165) counts <= 0, or > 0 when exactly two axes invert.
+__device__ __forceinline__ long long signed_count(const unsigned (&lo)[3], const unsigned (&hi)[3]) {
+  return ((long long)hi[0] - lo[0] + 1) * ((long long)hi[1] - lo[1] + 1) * ((long long)hi[2] - lo[2] + 1);
+}
+
 __device__ __forceinline__ void tri_box(const double* a, const double* b, const double* c, const DevSpec& s,
                                         unsigned dx, unsigned dxy, uint3& box, unsigned& cnt, bool& bad) {
   bool keep;
   unsigned lo[3], hi[3];
   tri_box_raw(a, b, c, s, lo, hi, keep);
-  if (keep && (hi[0] < lo[0] || hi[1] < lo[1] || hi[2] < lo[2])) {
-    // +inf / >2^63 upper corners cast to INT64_MIN and clip to 0 below lo (an inverted box);
-    // flagged, and resolved on the host path exactly as the reference's checks do
-    // (k_inverted_boxes, primitives.py:22-25, 71-72)
-    bad = true;
-    keep = false;
-  }
   box = make_uint3(0u, 1u, 1u);
   cnt = 0;
-  if (keep) {
-    const unsigned ex = hi[0] - lo[0] + 1, ey = hi[1] - lo[1] + 1, ez = hi[2] - lo[2] + 1;
-    box = make_uint3(lo[0] + dx * lo[1] + dxy * lo[2], ex, ey);
-    cnt = ex * ey * ez;  // <= ncells <= 2^30
+  if (!keep) return;
+  if (hi[0] < lo[0] || hi[1] < lo[1] || hi[2] < lo[2]) {
+    // inverted box: flagged for the host's verdict (count_check). A positive count (two
+    // inverted axes) keeps its pairs, {lo_cell 0, mx = count, my = 1} so the expansion stays
+    // in [0, count) < ncells; k_inverted_pairs rewrites them with the reference's cells.
+    bad = true;
+    const long long sc = signed_count(lo, hi);
+    if (sc > 0) {
+      box = make_uint3(0u, (unsigned)sc, 1u);
+      cnt = (unsigned)sc;  // < ncells: |hi - lo + 1| <= dims - 2 on an inverted axis
+    }
+    return;
   }
+  const unsigned ex = hi[0] - lo[0] + 1, ey = hi[1] - lo[1] + 1, ez = hi[2] - lo[2] + 1;
+  box = make_uint3(lo[0] + dx * lo[1] + dxy * lo[2], ex, ey);
+  cnt = ex * ey * ez;  // <= ncells
 }
 
-// Error path of K1 (some kept box is inverted): the reference's verdict depends on how many
-// triangles are kept in total and on the inverted boxes' signed pair counts
-// prod(hi - lo + 1) (builders.py:90-101 -> primitives.py:22-25 exclusive_sum rejects a
-// negative count; mark_boundaries, primitives.py:58-77, rejects any zero-count group when
-// two or more objects are kept). out = {kept, inverted, min count, max count}.
+// Error path of K1 (some kept box is inverted): the reference's verdict depends on the
+// number of kept triangles and on the inverted boxes' signed counts (builders.py:90-101 ->
+// exclusive_sum rejects a negative count, primitives.py:22-25; mark_boundaries rejects a
+// zero count among >= 2 kept objects, primitives.py:66-72). out = {kept, inverted, negative
+// counts, zero counts}; positive-count inverted boxes are listed in `list` (*nlist of them).
 __global__ void __launch_bounds__(256)
 k_inverted_boxes(const double* __restrict__ V, const int* __restrict__ T, long long n, DevSpec s,
-                 long long* __restrict__ out) {
+                 unsigned long long* __restrict__ out, unsigned* __restrict__ list, unsigned* __restrict__ nlist) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  bool keep = false, inv = false;
-  long long c = 0;
+  bool keep = false, inv = false, neg = false, zero = false;
   if (i < n) {
     unsigned lo[3], hi[3];
     tri_box_raw(V + 3 * (long long)T[3 * i], V + 3 * (long long)T[3 * i + 1], V + 3 * (long long)T[3 * i + 2], s, lo,
                 hi, keep);
     inv = keep && (hi[0] < lo[0] || hi[1] < lo[1] || hi[2] < lo[2]);
-    if (inv)
-      c = ((long long)hi[0] - lo[0] + 1) * ((long long)hi[1] - lo[1] + 1) * ((long long)hi[2] - lo[2] + 1);
+    if (inv) {
+      const long long c = signed_count(lo, hi);
+      neg = c < 0;
+      zero = c == 0;
+      if (c > 0 && list) list[atomicAdd(nlist, 1u)] = (unsigned)i;
+    }
   }
-  const unsigned kb = __ballot_sync(0xffffffffu, keep), ib = __ballot_sync(0xffffffffu, inv);
+  const unsigned b[4] = {__ballot_sync(0xffffffffu, keep), __ballot_sync(0xffffffffu, inv),
+                         __ballot_sync(0xffffffffu, neg), __ballot_sync(0xffffffffu, zero)};
   if ((threadIdx.x & 31) == 0) {
-    if (kb) atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)__popc(kb));
-    if (ib) atomicAdd(reinterpret_cast<unsigned long long*>(out + 1), (unsigned long long)__popc(ib));
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (b[q]) atomicAdd(out + q, (unsigned long long)__popc(b[q]));
   }
-  if (inv) {
-    atomicMin(out + 2, c);
-    atomicMax(out + 3, c);
+}
+
+// absolute pair offset of triangle o (K1 tiles of K1_TILE triangles)
+__device__ __forceinline__ unsigned tri_offset(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre,
+                                               long long o) {
+  return __ldg(&tile_pre[o / K1_TILE]) + __ldg(&rec[o].w);
+}
+
+// numpy's `//` on int64 (floor division), as _make_cell_ids uses it (builders.py:111-112)
+__device__ __forceinline__ long long floordiv_i64(long long a, long long b) {
+  const long long q = a / b;
+  return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+
+// Pairs of the listed positive-count inverted boxes, one CTA per box: the reference's cell of
+// relative offset rel (_make_cell_ids, builders.py:104-117, signed extents, floor division).
+// A cell outside [0, ncells) is the reference's InvariantError (radix_sort_pairs / scatter
+// range checks, primitives.py:102-111, 135-136): err |= 1. With `keys` (the pairs in
+// generation order, K2's output) the cells are written at the box's pair offset, and a
+// coarse histogram of the keys (sharded builds) is corrected for the rewritten keys.
+__global__ void __launch_bounds__(256)
+k_inverted_pairs(const double* __restrict__ V, const int* __restrict__ T, DevSpec s, const uint4* __restrict__ rec,
+                 const unsigned* __restrict__ tile_pre, const unsigned* __restrict__ list,
+                 const unsigned* __restrict__ nlist, long long ncells, unsigned* __restrict__ keys,
+                 unsigned* __restrict__ coarse, int coarse_shift, unsigned* __restrict__ err) {
+  const unsigned nl = *nlist;
+  const long long dx = s.dims[0], dy = s.dims[1];
+  for (unsigned e = blockIdx.x; e < nl; e += gridDim.x) {
+    const long long i = list[e];
+    unsigned lo[3], hi[3];
+    bool keep;
+    tri_box_raw(V + 3 * (long long)T[3 * i], V + 3 * (long long)T[3 * i + 1], V + 3 * (long long)T[3 * i + 2], s, lo,
+                hi, keep);
+    const long long mx = (long long)hi[0] - lo[0] + 1, my = (long long)hi[1] - lo[1] + 1;
+    const long long cnt = signed_count(lo, hi), mxy = mx * my;
+    const unsigned off = keys ? tri_offset(rec, tile_pre, i) : 0u;
+    for (long long rel = threadIdx.x; rel < cnt; rel += blockDim.x) {
+      const long long z = floordiv_i64(rel, mxy);
+      const long long y = floordiv_i64(rel - z * mxy, mx);
+      const long long x = rel - mx * (y + my * z);
+      const long long c = ((long long)lo[0] + x) + dx * (((long long)lo[1] + y) + dy * ((long long)lo[2] + z));
+      if (c < 0 || c >= ncells) {
+        atomicOr(err, 1u);
+        continue;
+      }
+      if (keys) {
+        const unsigned p = off + (unsigned)rel;
+        if (coarse) {
+          atomicSub(&coarse[keys[p] >> coarse_shift], 1u);
+          atomicAdd(&coarse[(unsigned)c >> coarse_shift], 1u);
+        }
+        keys[p] = (unsigned)c;
+      }
+    }
   }
 }
 
@@ -487,11 +554,6 @@ k_scan_tile_sums(const unsigned long long* __restrict__ tile_sum, unsigned ntile
   if (tid == 0) *total = tot;
 }
 
-// absolute pair offset of triangle o (K1 tiles of K1_TILE triangles)
-__device__ __forceinline__ unsigned tri_offset(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre,
-                                               long long o) {
-  return __ldg(&tile_pre[o / K1_TILE]) + __ldg(&rec[o].w);
-}
 
 // ----------------------------------------------------------------------------------------
 // K2: load-balanced pair expansion + radix digit histograms

@@ -100,17 +100,23 @@ def test_oracle_size_error():
 
 
 def _inverted_cases():
-    """Triangles whose clipped box inverts (an infinite upper corner): the reference accepts
-    only a lone zero-count one (empty grid); every other arrangement raises."""
+    """Triangles whose clipped box inverts (an infinite upper corner): the reference accepts a
+    lone zero-count one (empty grid) and builds cells from a box inverted on two axes (a
+    positive count) when they land in [0, ncells); every other arrangement raises."""
     from paper_2403_10647_b200.gridcore import Aabb, GridSpec
     inv1 = [[0.6, 0.1, 0.1], [np.inf, 0.2, 0.1], [0.7, 0.1, 0.2]]          # one inverted axis
     inv3 = [[0.6, 0.6, 0.6], [np.inf, np.inf, np.inf], [0.7, 0.7, 0.7]]    # negative count at 4^3
+    inv2 = [[0.6, 0.6, 0.1], [np.inf, np.inf, 0.2], [0.7, 0.7, 0.2]]       # two axes: one pair, cell 10
+    inv2w = [[0.8, 0.8, 0.3], [np.inf, np.inf, 0.6], [0.85, 0.85, 0.3]]    # 8 pairs at 5^3
+    inv2n = [[0.1, 0.8, 0.8], [np.inf, 1e300, np.inf], [0.1, 0.85, 0.85]]  # 3 axes: 1 x -3 x -3 ... at 5^3
     good = [[0.1, 0.1, 0.1], [0.2, 0.2, 0.2], [0.1, 0.2, 0.1]]
     far = [[5.0, 5, 5], [6, 5, 5], [5, 6, 5]]                              # dropped
     cases = []
     for tris, dims in (([inv1], (2, 2, 2)), ([inv1, far], (2, 2, 2)), ([far, inv1, far], (3, 3, 3)),
                        ([good, inv1], (2, 2, 2)), ([inv1, good], (2, 2, 2)), ([inv3], (4, 4, 4)),
-                       ([inv1, inv1], (2, 2, 2))):
+                       ([inv1, inv1], (2, 2, 2)), ([inv2], (4, 4, 4)), ([good, inv2, far], (4, 4, 4)),
+                       ([inv2, good, inv2], (4, 4, 4)), ([inv2w], (5, 5, 5)), ([good, inv2w], (5, 5, 5)),
+                       ([inv2n], (5, 5, 5)), ([inv2, inv1], (4, 4, 4))):
         V = np.array([v for t in tris for v in t], float)
         T = np.arange(len(V), dtype=np.int32).reshape(-1, 3)
         cases.append((V, T, GridSpec(Aabb([0, 0, 0], [1, 1, 1]), dims)))
@@ -140,3 +146,22 @@ def test_oracle_inverted_boxes_vs_live_reference():
         assert (want is None) == (got is None), (V, spec.dims)
         if want is not None:
             assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+def test_oracle_inverted_golden():
+    """Every golden inverted-box verdict (and grid) of the reference, make_golden_inverted.py."""
+    from util import inverted_cases
+    n_grid = 0
+    for name, V, T, spec, verdict, G, O in inverted_cases():
+        try:
+            got = oracle.build_parallel(V, T, spec)
+            code = 0
+        except oracle.OracleSizeError:
+            code = 1
+        except oracle.OracleInvariantError:
+            code = 2
+        assert code == verdict, name
+        if verdict == 0:
+            n_grid += 1
+            assert np.array_equal(got[0], G) and np.array_equal(got[1], O), name
+    assert n_grid >= 40

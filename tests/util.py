@@ -43,3 +43,19 @@ def ray_case(rays, name):
     else:
         mesh, spec = scene_from_recipe(recipe)
     return (mesh, spec, arrays[f"{name}/origins"], arrays[f"{name}/dirs"], arrays[f"{name}/t_max"])
+
+
+def inverted_cases():
+    """Golden inverted-box scenes (tests/golden/make_golden_inverted.py, the reference's own
+    verdicts): [(name, mesh arrays V, T, spec, verdict 0 grid / 1 SizeError / 2 InvariantError,
+    G, O)]."""
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "inverted.npz")
+    out = []
+    with np.load(path) as z:
+        for name in z["names"]:
+            name = str(name)
+            spec = GridSpec(Aabb([0, 0, 0], [1, 1, 1]), tuple(int(d) for d in z[f"{name}/dims"]))
+            out.append((name, z[f"{name}/V"], z[f"{name}/T"], spec, int(z[f"{name}/verdict"]),
+                        z[f"{name}/G"], z[f"{name}/O"]))
+    return out
