@@ -6,12 +6,20 @@ A "step" is one full build_parallel of the config's scene (default cfg3: the 10M
 architectural scene, density 4, 342^3 cells -- BASELINE.json configs[2], the paper's 25 Hz
 case). `value` = builds/s with inputs resident in HBM (device pointers through the C ABI);
 `e2e` = the same through the public numpy API (pinned host inputs, H2D + build + D2H of G
-and O inside the timed region). Rank 0 prints one JSON line.
+and O inside the timed region; the single drop-in call with pageable numpy inputs is
+reported beside it). Rank 0 prints one JSON line.
 
-N > 1 (torchrun): the sharded build of SURVEY.md §8e on an N x 10M-triangle architectural
-scene (weak scaling: 10M triangles per GPU): each rank generates and counts its triangle
-shard, pairs are routed to cell slabs by one NCCL all-to-all, every rank sorts its slab and
-writes its G/O slice (distributed output).
+N > 1: `--gpus N` launches N ranks itself (torchrun, one process per GPU, 127.0.0.1) unless
+it already runs under torchrun (WORLD_SIZE set; it must equal N). The sharded build of
+SURVEY.md §8e: each rank generates and counts its triangle shard, pairs are routed to cell
+slabs (peer stores into symmetric memory, or one NCCL all-to-all), every rank sorts its slab
+and writes its G/O slice (distributed output).
+  * cfg1..cfg4 (default cfg3): weak scaling, an N x 10M-triangle scene (10M per GPU);
+    `value` = N x builds/s of it, i.e. 10M-scene builds/s, the unit of the N=1 line.
+  * cfg5 / cfg5a (100M uniform / arch, BASELINE configs[4]): strong scaling, one 100M scene
+    split N ways; `value` = builds/s of the whole scene.
+`--dry-run` (CPU, gloo): the sharded orchestration with the numpy test ops on a small scene
+-- proves the launcher and the N-rank plumbing without a GPU; no measurement.
 `--impl reference` times the reference's own CPU build (oracle/_ref, C lane, all host
 threads) on the same config instead.
 """
@@ -46,7 +54,54 @@ def parse():
     ap.add_argument("--nccl-exchange", action="store_true", help="sharded: partition pass + NCCL all_to_all")
     ap.add_argument("--fused-dispatch", action="store_true",
                     help="sharded: expansion + dispatch in one kernel (pg_pairs_send; measured slower, off)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU only: N gloo ranks run the sharded orchestration (numpy test ops), no timing")
     return ap.parse_args()
+
+
+def free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(args):
+    """--gpus N outside torchrun: re-run this command as N ranks (one process per GPU) under
+    torch.distributed.run on 127.0.0.1; returns its exit code. Fails loudly when fewer than N
+    devices are visible."""
+    if not args.dry_run and args.impl != "reference":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd[1:6])} ...", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def config_dict(config, kind, n, spec, no):
+    """The workload keys every arm reports identically (the driver compares the arms)."""
+    return {"workload": config, "scene": kind, "triangles": int(n), "dims": [int(d) for d in spec.dims],
+            "ncells": int(spec.ncells), "no": int(no), "key_bits": int(spec.ncells - 1).bit_length()}
+
+
+def sharded_config(config, world, kind, n, spec, no):
+    d = config_dict(config, kind, n, spec, no)
+    strong = sharded_mode(config, world)[0]
+    d["workload"] = (f"{config} split x{world} (sharded, strong scaling)" if strong else
+                     f"{config} x{world} (sharded, weak scaling: {world} x 10M triangles)")
+    return d
+
+
+def sharded_mode(config, world):
+    """(strong, triangles of the whole scene, triangles per rank) of a sharded run."""
+    from paper_2403_10647_b200 import scenes
+    n1 = scenes.CONFIGS[config][1]
+    strong = n1 >= 50_000_000            # config 5: one 100M scene split N ways
+    n = n1 if strong else n1 * world
+    return strong, n, n // world
 
 
 def dist_env():
@@ -142,7 +197,9 @@ def run_reference(args, world, rank):
     ref = oracle.reference_module()
     mesh, spec = scenes.config_scene(args.config)
     cores = os.cpu_count() or 1
-    if ref is not None:
+    # config 5 (100M triangles): the reference needs ~40 GB of int64 temporaries and minutes
+    # per build; its C restatement (the oracle port, one thread) stands in there
+    if ref is not None and mesh.ntriangles <= 20_000_000:
         kind = "reference"
         rmesh = ref.TriangleMesh(mesh.vertices, mesh.triangles)
         rspec = ref.GridSpec(ref.Aabb(spec.bounds.lo, spec.bounds.hi), spec.dims)
@@ -178,8 +235,14 @@ def run_reference(args, world, rank):
             "n_gpus": world, "steps": steps, "warmup": 1, "ms_per_step": round(sec * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32",
             "data": "synthetic", "mpairs_per_s": round(no / sec / 1e6, 4),
-            "config": {"workload": args.config, "triangles": mesh.ntriangles, "dims": list(spec.dims),
-                       "no": int(no)},
+            "config": (config_dict(args.config, scenes.CONFIGS[args.config][0], mesh.ntriangles, spec, no)
+                       if world == 1 else
+                       sharded_config(args.config, world, scenes.CONFIGS[args.config][0], mesh.ntriangles, spec,
+                                      no)),
+            "run": {"parallelism": f"CPU, {cores} host thread(s)",
+                    "note": ("" if world == 1 else
+                             "the reference times one scene of the config on rank 0's host; builds/s of it "
+                             "is the unit of the GPU arm's value")},
             "cpu_baseline": {"value": round(value, 6), "unit": "builds/s", "cores": cores, "kind": kind,
                              "sample": sample},
             "e2e": {"value": round(value, 6), "unit": "builds/s", "h2d_bytes_per_step": 0,
@@ -192,7 +255,7 @@ def cpu_baseline(args, mesh, spec):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
     ref = oracle.reference_module()
-    if ref is not None:
+    if ref is not None and mesh.ntriangles <= 20_000_000:
         rmesh = ref.TriangleMesh(mesh.vertices, mesh.triangles)
         rspec = ref.GridSpec(ref.Aabb(spec.bounds.lo, spec.bounds.hi), spec.dims)
         t0 = time.perf_counter()
@@ -217,12 +280,12 @@ def run_sharded(args, world, rank, local):
     from paper_2403_10647_b200 import distributed as D
     from paper_2403_10647_b200 import gridcore, scenes
 
-    kind, n1, seed, density = scenes.CONFIGS[args.config]
-    if kind != "arch":
-        raise SystemExit("sharded bench supports the arch configs")
-    n = n1 * world
+    kind, _, seed, density = scenes.CONFIGS[args.config]
+    if kind not in ("arch", "uniform"):
+        raise SystemExit("sharded bench supports the arch and uniform configs")
+    strong, n, n1 = sharded_mode(args.config, world)
     lo, hi = D.shard_range(n, rank, world)
-    shard = scenes.gen_arch_shard(n, seed, density, lo, hi)
+    shard = scenes.gen_shard(kind, n, seed, density, lo, hi)
     dev = torch.device("cuda", local)
     bmin = torch.from_numpy(shard.vertices.min(axis=0).copy()).to(dev)
     bmax = torch.from_numpy(shard.vertices.max(axis=0).copy()).to(dev)
@@ -337,25 +400,26 @@ def run_sharded(args, world, rank, local):
     gathered_ms = statistics.median(gat) * 1e3
     out_bytes = torch.tensor([out_nbytes], device=dev, dtype=torch.int64)
     dist.all_reduce(out_bytes)
+    # whole-job throughput in the metric's unit. Weak scaling (10M per GPU): 10M-triangle-scene
+    # builds per second = N x builds/s of the N x 10M scene, so efficiency is value(N) / (N
+    # value(1)). Strong scaling (config 5): builds/s of the one 100M scene.
+    value = 1e3 / ms if strong else world * 1e3 / ms
+    value_def = (f"builds/s of the {n // 1_000_000}M-triangle scene split {world} ways" if strong else
+                 f"{world} x builds/s of the {world} x {n1 // 1_000_000}M-triangle scene")
     line = {
-        # whole-job throughput in the metric's unit: 10M-triangle-scene builds per second
-        # (N x builds/s of the N x 10M scene), so weak scaling is value(N) / (N value(1))
-        "metric": METRIC, "value": round(world * 1e3 / ms, 3), "unit": "builds/s", "n_gpus": world,
+        "metric": METRIC, "value": round(value, 3), "unit": "builds/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32",
-        "data": "synthetic",
-        "config": {"workload": f"{args.config} x{world} (sharded)", "scene": kind, "triangles": n,
-                   "triangles_per_gpu": n1, "dims": list(spec.dims), "ncells": spec.ncells, "no": no,
-                   "parallelism": f"triangle shards x{world} -> cell slabs",
-                   "exchange": exchange_desc,
-                   "output": "distributed (each rank its G/O slab)",
-                   "value_def": f"{world} x builds/s of the {world} x {n1 // 1_000_000}M-triangle scene",
-                   "scene_builds_per_s": round(1e3 / ms, 3),
-                   "parity": "orchestration verified by tests/test_distributed.py + test_gpu_distributed.py"},
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+        "dtype": "f64+u32", "data": "synthetic",
+        "config": sharded_config(args.config, world, kind, n, spec, no),
+        "run": {"triangles_per_gpu": n1, "parallelism": f"triangle shards x{world} -> cell slabs",
+                "exchange": exchange_desc, "output": "distributed (each rank its G/O slab)",
+                "value_def": value_def, "scene_builds_per_s": round(1e3 / ms, 3),
+                "parity": "orchestration verified by tests/test_distributed.py + test_gpu_distributed.py"},
         "mpairs_per_s": round(no / (ms * 1e-3) / 1e6, 2),
         "roofline": roofline,
         "kernels_rank0": kernels,
-        "e2e": {"value": round(world / e2e_sec, 3), "unit": "builds/s",
+        "e2e": {"value": round((1.0 if strong else world) / e2e_sec, 3), "unit": "builds/s",
                 "h2d_bytes_per_step": int((Vh.nbytes + Th.nbytes) * world),
                 "d2h_bytes_per_step": int(out_bytes.item()), "ms_per_step": round(e2e_sec * 1e3, 2)},
         "gathered_output": {"ms_per_step": round(gathered_ms, 3),
@@ -368,9 +432,54 @@ def run_sharded(args, world, rank, local):
         print(json.dumps(line), flush=True)
 
 
+def run_dry(args, world, rank):
+    """--dry-run: the N-rank plumbing on CPU. Every rank runs the sharded orchestration over
+    gloo with the numpy per-rank steps of the tests (tests/np_ops.py, test infrastructure)
+    on a small scene; rank 0 checks the gathered grid against the C oracle and prints one
+    line. Nothing is timed; `value` is null."""
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", str(free_port()))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sys.path[:0] = [os.path.join(ROOT, "tests"), os.path.join(ROOT, "oracle")]
+        import oracle
+        from np_ops import NumpyOps
+        from paper_2403_10647_b200 import distributed as D
+        from paper_2403_10647_b200 import gen_scene, spec_for_mesh
+        mesh = gen_scene("walls", 3000, 5)
+        spec = spec_for_mesh(mesh, dims=(40, 30, 20))
+        lo, hi = D.shard_range(mesh.ntriangles, rank, world)
+        comm = D.TorchComm()
+        res = D.build_sharded(NumpyOps(), comm, mesh.vertices, mesh.triangles[lo:hi], lo, spec)
+        print(f"[bench] rank {comm.rank}/{comm.world} (gloo): shard [{lo}, {hi})", file=sys.stderr, flush=True)
+        if rank == 0:
+            G, O = oracle.build_parallel(mesh.vertices, mesh.triangles, spec)
+            ok = np.array_equal(res[0], G) and np.array_equal(res[1], O)
+            line = {"metric": METRIC, "value": None, "unit": "builds/s", "n_gpus": world, "steps": 0,
+                    "warmup": 0, "dry_run": True, "higher_is_better": True,
+                    "scaling": "strong" if sharded_mode(args.config, world)[0] else "weak",
+                    "config": {"workload": "dry run: walls 3000 triangles, dims (40, 30, 20)",
+                               "parallelism": f"triangle shards x{world} -> cell slabs (gloo, numpy test ops)"},
+                    "parity": "bit-exact vs the C oracle" if ok else "MISMATCH"}
+            print(json.dumps(line), flush=True)
+            if not ok:
+                raise SystemExit(1)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(self_launch(args))
     world, rank, local = dist_env()
+    if "WORLD_SIZE" in os.environ and args.gpus not in (1, world):
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        run_dry(args, world, rank)
+        return
     if args.impl == "reference":
         if world > 1:
             import torch.distributed as dist
@@ -390,6 +499,10 @@ def main():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29533")
             dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        # one line per rank on stderr: the communicator really spans `world` ranks / GPUs
+        print(f"[bench] rank {dist.get_rank()}/{dist.get_world_size()}: NCCL "
+              f"{'.'.join(map(str, torch.cuda.nccl.version()))} communicator on cuda:{local} "
+              f"({torch.cuda.get_device_name(local)})", file=sys.stderr, flush=True)
         try:
             run_sharded(args, world, rank, local)
         finally:
@@ -463,8 +576,8 @@ def main():
         torch.cuda.synchronize()
     if b.build_wait() != no:
         raise SystemExit("sync-free build exceeded its capacity")
-        if world > 1:
-            torch.distributed.barrier()
+    if world > 1:
+        torch.distributed.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -564,11 +677,10 @@ def main():
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32",
         "data": "synthetic",
-        "config": {"workload": args.config, "scene": scenes.CONFIGS[args.config][0],
-                   "triangles": n, "dims": list(spec.dims), "ncells": ncells, "no": no,
-                   "key_bits": key_bits, "parallelism": f"replicas{world}" if world > 1 else "single",
-                   "l2": "inputs larger than L2 (%.0f MB read per build)" % ((12 * n + 24 * nv) / 1e6),
-                   "parity": parity},
+        "config": config_dict(args.config, scenes.CONFIGS[args.config][0], n, spec, no),
+        "run": {"parallelism": "single GPU",
+                "l2": "inputs larger than L2 (%.0f MB read per build)" % ((12 * n + 24 * nv) / 1e6),
+                "parity": parity},
         "mpairs_per_s": round(no / (ms * 1e-3) / 1e6 * world, 2),
         "hbm": {"compulsory_bytes": B, "achieved_gbs": round(B / (ms * 1e-3) / 1e9, 1),
                 "frac_of_peak": round(B / (ms * 1e-3) / 1e9 / peak, 4), "peak_gbs": peak,

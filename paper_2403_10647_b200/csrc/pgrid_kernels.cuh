@@ -70,16 +70,18 @@ struct PassPlan {
 };
 
 // A pair count known either on the host (dev == nullptr: val) or only on the device (the
-// sync-free build: min(*dev, val), val = the capacity the buffers were sized for). Kernels
+// sync-free build: *dev, bounded by val = the capacity the buffers were sized for). Kernels
 // downstream of K1 take their NO this way so a whole build can be enqueued -- and captured
-// in a CUDA graph -- without reading NO back first.
+// in a CUDA graph -- without reading NO back first. A device count above the capacity voids
+// the build (the host reports it afterwards: capacity / SizeError), so every kernel then
+// sees 0 pairs: no kernel ever walks offsets that wrapped past 2^32 (NO > 2^32-1).
 struct Count {
   const unsigned long long* dev;
   unsigned val;
   __device__ __forceinline__ unsigned get() const {
     if (!dev) return val;
     const unsigned long long v = *dev;
-    return v < (unsigned long long)val ? (unsigned)v : val;
+    return v <= (unsigned long long)val ? (unsigned)v : 0u;
   }
 };
 

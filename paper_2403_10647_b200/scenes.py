@@ -98,6 +98,22 @@ def gen_uniform_chunked(n, seed, chunk=10_000_000):
     return TriangleMesh(V, np.arange(3 * n, dtype=np.int32).reshape(n, 3))
 
 
+def gen_uniform_shard(n, seed, lo, hi):
+    """Triangles [lo, hi) of gen_scene("uniform", n, seed) as an unshared-vertex soup."""
+    size = min(0.05, 0.6 * n ** (-1.0 / 3.0))
+    return _soup(_small_triangles_range(lo, hi, seed, 10, size))
+
+
+def gen_shard(kind, n, seed, density, lo, hi):
+    """Triangles [lo, hi) of the uniform / arch scene of n triangles (sharded builds: each
+    rank generates only its own shard)."""
+    if kind == "uniform":
+        return gen_uniform_shard(n, seed, lo, hi)
+    if kind == "arch":
+        return gen_arch_shard(n, seed, density, lo, hi)
+    raise InvariantError(f"no shard generator for {kind!r}")
+
+
 def gen_arch_shard(n, seed, density, lo, hi):
     """Triangles [lo, hi) of gen_scene("arch", n, seed, density) as an unshared-vertex soup
     (for sharded builds: each rank generates only its own shard)."""
@@ -185,12 +201,31 @@ CONFIGS = {
     "cfg2": ("lognormal", 1_000_000, 7, 5.0),
     "cfg3": ("arch", 10_000_000, 7, 4.0),
     "cfg3u": ("uniform", 10_000_000, 7, 5.0),
+    # config 4: the 10M uniform scene at grid densities 1 -> 64 (24 -> 30 key bits)
+    **{f"cfg4_d{d}": ("uniform", 10_000_000, 7, float(d)) for d in (1, 2, 4, 8, 16, 32, 64)},
+    # config 5: 100M triangles (uniform; arch for the sharded north-star run)
+    "cfg5": ("uniform", 100_000_000, 7, 5.0),
+    "cfg5a": ("arch", 100_000_000, 7, 4.0),
 }
+
+
+def gen_scene_large(kind, n, seed, density=5.0, chunk=10_000_000):
+    """gen_scene(kind, n, seed, density) with bounded temporaries for 100M+ triangles
+    (uniform / arch): generated chunk by chunk, bit-identical to the one-shot generator."""
+    if kind == "uniform":
+        return gen_uniform_chunked(n, seed, chunk)
+    if kind != "arch":
+        return gen_scene(kind, n, seed, density)
+    V = np.empty((3 * n, 3), dtype=np.float64)
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
+        V[3 * a:3 * b] = gen_arch_shard(n, seed, density, a, b).vertices
+    return TriangleMesh(V, np.arange(3 * n, dtype=np.int32).reshape(n, 3))
 
 
 def config_scene(name):
     """(mesh, spec) for a named BASELINE config."""
     from .gridcore import spec_for_mesh
     kind, n, seed, density = CONFIGS[name]
-    mesh = gen_scene(kind, n, seed, density)
+    mesh = gen_scene_large(kind, n, seed, density) if n > 20_000_000 else gen_scene(kind, n, seed, density)
     return mesh, spec_for_mesh(mesh, density=density)

@@ -336,3 +336,36 @@ def test_cell_boundary_coordinates_bit_exact():
     grid, rep = builders.build_parallel(TriangleMesh(V, T), spec)
     G, O = oracle.build_parallel(V, T, spec)
     assert np.array_equal(grid.G, G) and np.array_equal(grid.O, O) and rep.no == len(O)
+
+
+def test_no_above_2_32_on_device_count_paths():
+    """NO > 2^32-1 (17 full-cover triangles on 2^28 cells): the reference's SizeError
+    (builders.py:99-100) on the paths that never read NO back before the expansion -- the
+    sync-free graph build and the deferred BuildPipeline -- without a device fault (the
+    over-capacity device count voids every kernel after K1)."""
+    import torch
+    V = np.array([[-1, -1, -1], [3, -1, 2], [-1, 3, 2]], np.float64)
+    T = np.zeros((17, 3), np.int32)
+    T[:] = [0, 1, 2]
+    spec = GridSpec(Aabb([0, 0, 0], [1, 1, 1]), (1024, 512, 512))
+    b = _native.Builder(0)
+    Vd = torch.from_numpy(V).cuda()
+    Td = torch.from_numpy(T).cuda()
+    Gd = torch.empty(spec.ncells + 1, dtype=torch.int32, device="cuda")
+    Od = torch.empty(4096, dtype=torch.int32, device="cuda")
+    for _ in range(2):
+        b.build_async(Vd, len(V), Td, len(T), spec, Gd, Od, 4096)
+        with pytest.raises(SizeError):
+            b.build_wait()
+    torch.cuda.synchronize()                      # the context survived
+    small = gen_scene("uniform", 500, 1)
+    sspec = spec_for_mesh(small)
+    pipe = builders.BuildPipeline(depth=2)
+    pipe.submit(small, sspec)
+    want, _ = pipe.result()                       # learns a capacity: the next submit is deferred
+    pipe.submit(TriangleMesh(V, T), spec)
+    pipe.submit(small, sspec)
+    with pytest.raises(SizeError):
+        pipe.result()
+    again, _ = pipe.result()
+    assert grids_equal(want, again)
