@@ -51,6 +51,10 @@ extern "C" {
                                   the capacity or a lone inverted box voided the deferred steps
                                   (rebuild without PG_DEFER). pg_finish_baseline, pg_stage and
                                   pg_grid_stats refuse a deferred count. */
+#define PG_STATS 128u          /* pg_count (sharded builds): no local verdict. The count's raw
+                                  statistics are kept for pg_count_stats and the caller combines
+                                  every rank's into the global verdict (the reference's checks
+                                  apply to the whole mesh, not to one shard) */
 
 /* Grid specification: the exact host doubles of GridSpec (gridcore.py:36-57). */
 typedef struct {
@@ -201,6 +205,14 @@ int pg_sort_cells(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int
  *                   cell_hi[nslabs] | pair_base[nslabs+1] (int64), all device; the same
  *                   arithmetic as distributed.plan_slabs */
 int pg_count_result(pg_builder *b, uint64_t *no_out); /* after PG_DEFER + a stream synchronise */
+/* After a PG_STATS pg_count: out[6] = {NO of this shard, index out of range (0/1), inverted
+ * boxes with a negative count, with a zero count, with a positive count (two inverted axes),
+ * positive ones with a cell outside [0, ncells)}. Summed over the ranks these give the
+ * reference's verdict in its order (distributed.count_verdict): index range; negative count
+ * (primitives.py:22-25); NO > 2^32-1 (builders.py:99-100); a zero count with any other kept
+ * triangle (mark_boundaries, primitives.py:66-72); NO > 2^30 (primitives.py:29-31); cells of
+ * inverted boxes (primitives.py:102-111, 135-136); ncells > 2^30 (builders.py:130). */
+int pg_count_stats(pg_builder *b, int64_t *out);
 /* Fused dispatch of the sharded build (pair expansion + slab partition + peer stores in one
  * kernel; replaces pg_pairs + pg_partition_counts + pg_partition_send):
  *   pg_coarse_hist -- after pg_count: the histogram of cell >> coarse_shift (coarse_bins <=
@@ -219,9 +231,10 @@ int pg_pairs_send(pg_builder *b, uint32_t val_offset, const uint32_t *slab_of_bu
                   const uint64_t *dst_offset, void *stream);
 int pg_peer_put(const uint32_t *src, int64_t n, const uint64_t *dsts, int nranks, int64_t dst_offset,
                 void *stream);
-/* pg_peer_put of the builder's device pair count (NO of its last pg_count, u64 as two u32
- * words; exact even after a PG_DEFER count), so every rank learns every rank's NO with the
- * count matrix and they agree on capacity overflows */
+/* pg_peer_put of the builder's device pair count and K1 error flags (NO of its last pg_count,
+ * u64 as two u32 words, then the flag word; exact even after a PG_DEFER count), so every rank
+ * learns every rank's NO and flags with the count matrix: they agree on capacity overflows
+ * and on falling back to the host-checked count when any shard flagged an error */
 int pg_peer_put_count(pg_builder *b, const uint64_t *dsts, int nranks, int64_t dst_offset, void *stream);
 int pg_slab_plan(const uint32_t *hists, int nranks, int nbuckets, int bucket_shift, int64_t ncells,
                  int nslabs, uint32_t *slab_of_bucket, uint32_t *slab_base, int64_t *plan, void *stream);

@@ -30,6 +30,7 @@ PG_HOST_RAYS = 8
 PG_CHECK = 16
 PG_ASYNC = 32
 PG_DEFER = 64
+PG_STATS = 128
 
 NPHASES = 6
 
@@ -37,7 +38,7 @@ NPHASES = 6
 EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
            "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_finish_baseline",
            "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_partition_counts", "pg_partition_send", "pg_peer_put", "pg_slab_plan", "pg_count_result",
-           "pg_peer_put_count", "pg_coarse_hist", "pg_pairs_send",
+           "pg_peer_put_count", "pg_coarse_hist", "pg_pairs_send", "pg_count_stats",
            "pg_build_async",
            "pg_build_wait", "pg_host_register",
            "pg_host_unregister", "pg_host_alloc", "pg_host_free", "pg_last_launch_count",
@@ -101,6 +102,7 @@ def load():
                                           ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64), vp]
         lib.pg_kernel_timing.argtypes = [ctypes.c_int]
         lib.pg_count_result.argtypes = [vp, ctypes.POINTER(u64)]
+        lib.pg_count_stats.argtypes = [vp, ctypes.POINTER(i64)]
         lib.pg_coarse_hist.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp]
         lib.pg_pairs_send.argtypes = [vp, u32, vp, ctypes.c_int, ctypes.c_int, vp, ctypes.POINTER(u64),
                                       ctypes.POINTER(u64), ctypes.POINTER(u64), vp]
@@ -122,7 +124,7 @@ def load():
         lib.pg_last_error.restype = ctypes.c_char_p
         for name in ("pg_builder_create", "pg_count", "pg_finish", "pg_stage",
                      "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells",
-                     "pg_finish_baseline", "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_partition_counts", "pg_partition_send", "pg_peer_put", "pg_slab_plan",
+                     "pg_finish_baseline", "pg_count_stats", "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_partition_counts", "pg_partition_send", "pg_peer_put", "pg_slab_plan",
            "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
                      "pg_last_launch_count"):
             getattr(lib, name).restype = ctypes.c_int
@@ -191,6 +193,18 @@ class Builder:
         check(self._lib.pg_count(self._h, ptr(V), int(nv), ptr(T), int(n), ctypes.byref(s),
                                  flags | PG_DEFER, stream, ctypes.byref(no)))
         return int(capacity)
+
+    def count_stats(self, V, nv, T, n, spec, flags=0, stream=None):
+        """pg_count with PG_STATS (sharded builds): no local verdict; returns the shard's raw
+        statistics int64[6] = {NO, index out of range, inverted boxes with negative / zero /
+        positive counts, positive ones with a cell outside the grid}."""
+        s = PgSpec.from_spec(spec)
+        no = ctypes.c_uint64(0)
+        check(self._lib.pg_count(self._h, ptr(V), int(nv), ptr(T), int(n), ctypes.byref(s),
+                                 flags | PG_STATS, stream, ctypes.byref(no)))
+        out = (ctypes.c_int64 * 6)()
+        check(self._lib.pg_count_stats(self._h, out))
+        return np.array(out[:], np.int64)
 
     def count_result(self):
         """NO of the last PG_DEFER count (the stream must have been synchronised since);

@@ -364,6 +364,7 @@ struct pg_builder {
   // [count u32][err u32][pad][list of triangle ids]
   bool inv_fix = false;
   DevBuf inv;
+  int64_t stats[6] = {};  // PG_STATS: raw statistics of the last count (pg_count_stats)
   // G / O of the last pg_build_async (pg_build_wait's host-counted rebuild)
   uint32_t* g_G = nullptr;
   uint32_t* g_O = nullptr;
@@ -608,6 +609,32 @@ int count_check(pg_builder* b, uint64_t* no_out) {
   return PG_OK;
 }
 
+// PG_STATS: the raw statistics of the count (stream synchronised) instead of a verdict; the
+// sharded build sums them over the ranks and decides for the whole mesh.
+int count_stats(pg_builder* b, uint64_t* no_out) {
+  const uint64_t no = b->h_scalars[0];
+  const unsigned errf = (unsigned)(b->h_scalars[1] & 0xffffffffu);
+  b->inv_fix = false;
+  int64_t* st = b->stats;
+  for (int k = 0; k < 6; ++k) st[k] = 0;
+  st[0] = (int64_t)no;
+  st[1] = (errf & 2u) ? 1 : 0;
+  if ((errf & 1u) && !(errf & 2u)) {  // never gather through out-of-range indices
+    InvStats r{};
+    int rc = resolve_inverted(b, r);
+    if (rc) return rc;
+    st[2] = (int64_t)r.negative;
+    st[3] = (int64_t)r.zero;
+    st[4] = (int64_t)r.positive;
+    st[5] = (r.positive && !r.negative && !r.cells_ok) ? (int64_t)r.positive : 0;
+    b->inv_fix = r.positive && !r.negative && r.cells_ok;
+  }
+  if (no_out) *no_out = no;
+  b->no = no;
+  b->counted = true;
+  return PG_OK;
+}
+
 void drop_graph(pg_builder* b) {
   if (b->gexec) cudaGraphExecDestroy(b->gexec);
   b->gexec = nullptr;
@@ -625,14 +652,15 @@ int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64
   int rc;
   if ((rc = count_setup(b, nv, n, spec, ds, !(flags & PG_DEFER)))) return rc;
   ktimer_reset(st);
+  for (int k = 0; k < 6; ++k) b->stats[k] = 0;
   if (n == 0) {
-    if (b->ncells > kMaxScan)
+    if (b->ncells > kMaxScan && !(flags & PG_STATS))
       return fail(PG_SIZE_ERROR, "array of %lld elements exceeds the scan size limit", (long long)b->ncells);
-    // an empty mesh (or an empty shard of a sharded build): NO = 0, also on the device for
-    // the steps that read the count there (pg_peer_put_count, deferred grids)
+    // an empty mesh (or an empty shard of a sharded build): NO = 0 and no error flags, also
+    // on the device for the steps that read them there (pg_peer_put_count, deferred grids)
     if ((rc = b->k1_sync.ensure(256))) return rc;
     b->d_total = b->k1_sync.as<unsigned long long>(0);
-    CU(cudaMemsetAsync(b->d_total, 0, 8, st));
+    CU(cudaMemsetAsync(b->d_total, 0, 16, st));
     b->h_scalars[0] = 0;
     b->h_scalars[1] = 0;
     b->no = 0;
@@ -663,7 +691,15 @@ int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64
     return PG_OK;
   }
   CU(cudaStreamSynchronize(st));
+  if (flags & PG_STATS) return count_stats(b, no_out);
   return count_check(b, no_out);
+}
+
+int pg_count_stats(pg_builder* b, int64_t* out) {
+  if (!b || !out) return fail(PG_INVARIANT_ERROR, "null argument");
+  if (!b->counted) return fail(PG_STATE_ERROR, "pg_count_stats without a PG_STATS pg_count");
+  for (int k = 0; k < 6; ++k) out[k] = b->stats[k];
+  return PG_OK;
 }
 
 int pg_count_result(pg_builder* b, uint64_t* no_out) {
@@ -1844,7 +1880,7 @@ int pg_peer_put(const uint32_t* src, int64_t n, const uint64_t* dsts, int nranks
 
 int pg_peer_put_count(pg_builder* b, const uint64_t* dsts, int nranks, int64_t dst_offset, void* stream_) {
   if (!b || !b->counted || !b->d_total) return fail(PG_STATE_ERROR, "pg_peer_put_count without a pg_count");
-  return pg_peer_put(reinterpret_cast<const uint32_t*>(b->d_total), 2, dsts, nranks, dst_offset, stream_);
+  return pg_peer_put(reinterpret_cast<const uint32_t*>(b->d_total), 3, dsts, nranks, dst_offset, stream_);
 }
 
 int pg_slab_plan(const uint32_t* hists, int nranks, int nbuckets, int bucket_shift, int64_t ncells, int nslabs,

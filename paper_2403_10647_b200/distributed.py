@@ -21,11 +21,43 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native
+from .errors import InvariantError, SizeError
 
 COARSE_BITS = 12       # slab cuts at 2^12-bucket granularity of the cell-id range
 MAX_SLABS = 16         # pg_partition's digit table limit
 CTL_HIST = 1 << COARSE_BITS   # words per rank slot of the exchange control buffer (histograms)
-CTL_CNT = 32                  # words per rank slot for slab counts [0, 16) and the rank's NO [16, 18)
+CTL_CNT = 32                  # words per rank slot: slab counts [0, 16), the rank's NO [16, 18), K1 flags [18]
+MAX_IDS = (1 << 32) - 1       # gridcore.py:11
+MAX_SCAN = 1 << 30            # primitives.py:17
+
+
+def count_verdict(stats, ncells):
+    """The reference's verdict for the WHOLE mesh from the shards' count statistics summed
+    over the ranks (pg_count_stats: NO, index out of range, inverted boxes with negative /
+    zero / positive counts, positive ones with a cell outside the grid). Raised identically
+    on every rank, in the reference's order: the mesh's index check (geometry.py:41-43);
+    exclusive_sum's non-negativity (primitives.py:22-25); NO > 2^32-1 (builders.py:99-100);
+    mark_boundaries' zero-count group, i.e. a zero count next to any other kept triangle --
+    every kept non-inverted box counts >= 1, so that is NO > 0 or a second zero
+    (primitives.py:66-72); NO > 2^30 (inclusive_sum, primitives.py:29-31); the radix sort /
+    scatter range checks on the inverted boxes' cells (primitives.py:102-111, 135-136); the
+    G scan's ncells > 2^30 (builders.py:130). Returns the global NO."""
+    no, oob, neg, zero, pos, bad = (int(x) for x in np.asarray(stats, dtype=np.int64)[:6])
+    if oob:
+        raise InvariantError("triangle index out of range")
+    if neg:
+        raise InvariantError("index arrays are non-negative (inverted cell box, negative count)")
+    if no > MAX_IDS:
+        raise SizeError(f"{no} cell/object pairs exceed 32-bit id space")
+    if zero and (zero >= 2 or no > 0):
+        raise InvariantError("coincident boundary marks (zero-count group?)")
+    if no > MAX_SCAN:
+        raise SizeError(f"array of {no} elements exceeds the scan size limit")
+    if bad:
+        raise InvariantError("cell of an inverted box outside [0, ncells)")
+    if ncells > MAX_SCAN:
+        raise SizeError(f"array of {ncells} elements exceeds the scan size limit")
+    return no
 
 
 @dataclass
@@ -95,29 +127,47 @@ class ShardState:
         self.ncells = int(spec.dims[0]) * int(spec.dims[1]) * int(spec.dims[2])
         self.V, self.T, self.tri_base = V, T, tri_base
 
-    def phase_count(self, capacity=None):
+    def phase_count(self, capacity=None, comm=None):
         """K1 + K2 on the shard; returns the local coarse histogram (computed by K2). With a
         pair capacity (ops with PG_DEFER), no host round trip: NO stays on the device and the
-        pair buffers hold `capacity` pairs."""
+        pair buffers hold `capacity` pairs. Otherwise the shards' count statistics are summed
+        over `comm` and the whole mesh's verdict is raised on every rank before any pair
+        exists (count_verdict)."""
+        stats = self.phase_count_only(capacity)
+        if stats is not None:
+            count_verdict(comm.allreduce_sum(stats) if comm is not None else stats, self.ncells)
+        return self.phase_pairs()
+
+    def phase_count_only(self, capacity=None):
+        """K1 alone: the shard's count statistics (None when deferred)."""
         self.deferred = bool(capacity) and hasattr(self.ops, "count_deferred")
         if self.deferred:
             self.no = self.ops.count_deferred(self.V, self.T, self.spec, capacity)
-        else:
-            self.no = self.ops.count(self.V, self.T, self.spec)
+            return None
+        stats = self.ops.count_stats(self.V, self.T, self.spec)
+        self.no = int(stats[0])
+        return stats
+
+    def phase_pairs(self):
+        """K2 on the counted shard; returns the local coarse histogram."""
         self.shift = coarse_shift(self.ncells)
         nb = ((self.ncells - 1) >> self.shift) + 1
         self.nb_coarse = nb
         self.keys, self.vals, hist = self.ops.pairs(self.no, self.tri_base, self.shift, nb)
         return hist
 
-    def phase_count_fused(self, capacity=None):
+    def phase_count_fused(self, capacity=None, comm=None):
         """K1 + the coarse histogram from the cell boxes (no pairs yet: the fused dispatch
         expands them straight into the slab owners' buffers after the plan)."""
         self.deferred = bool(capacity)
         if self.deferred:
             self.no = self.ops.count_deferred(self.V, self.T, self.spec, capacity)
         else:
-            self.no = self.ops.count(self.V, self.T, self.spec)
+            stats = self.ops.count_stats(self.V, self.T, self.spec)
+            total = comm.allreduce_sum(stats) if comm is not None else stats
+            count_verdict(total, self.ncells)
+            self.global_positive = int(total[4])
+            self.no = int(stats[0])
         self.shift = coarse_shift(self.ncells)
         self.nb_coarse = ((self.ncells - 1) >> self.shift) + 1
         return self.ops.coarse_hist(self.shift, self.nb_coarse)
@@ -194,26 +244,54 @@ def build_sharded(ops, comm, V, T, tri_base, spec, gather=True, exchange=None):
     peer memory over NVLink) or None (partition pass, then NCCL all-to-all).
     Returns (G, O) on rank 0 when gather=True (None elsewhere); with gather=False each rank
     returns its slab as (cell_lo, cell_hi, pair_base, G_rel, O) with G_rel/O left where the
-    ops keep them (device memory for CudaOps)."""
+    ops keep them (device memory for CudaOps).
+
+    Errors: the reference's verdicts (SizeError / InvariantError) are decided for the whole
+    mesh from every shard's count statistics and raised on every rank at the same point
+    (count_verdict), so no rank is left waiting in a collective. Any other failure on a rank
+    (a CUDA error, ...) aborts the communicator, so the peers' collectives fail instead of
+    hanging."""
     rank, world = comm.rank, comm.world
     if world > MAX_SLABS:
         raise ValueError(f"at most {MAX_SLABS} ranks")
+    try:
+        return _build_sharded(ops, comm, V, T, tri_base, spec, gather, exchange)
+    except (InvariantError, SizeError):
+        raise
+    except Exception:
+        comm.abort()
+        raise
+
+
+def _build_sharded(ops, comm, V, T, tri_base, spec, gather, exchange):
+    rank, world = comm.rank, comm.world
     st = ShardState(ops, V, T, tri_base, spec, rank, world)
-    if exchange is not None and getattr(exchange, "fused", False):
+    fused = exchange is not None and getattr(exchange, "fused", False)
+    force_host = False      # some shard flagged an error on a deferred count: decide on host counts
+    if fused:
         # fused dispatch: K1, the coarse histogram from the cell boxes, peer-put histograms and
         # NOs, a device barrier, the device plan, ONE host read (histograms, NOs, plan), then a
         # single kernel expands every pair straight into its slab owner's receive buffer
         while True:
-            cap = exchange.no_capacity
-            hist = st.phase_count_fused(cap)
+            cap = None if force_host else exchange.no_capacity
+            hist = st.phase_count_fused(cap, comm)
+            if not st.deferred and st.global_positive:
+                # boxes inverted on two axes: their pairs are rewritten after a plain
+                # expansion (pg_pairs); the fused kernel has no such step
+                fused = False
+                break
             exchange.put_hist(hist, rank)
             exchange.put_no(rank, ops)
             exchange.barrier()
             st.phase_plan_device(exchange.hists(st.nb_coarse))
-            hists, nos, plan_arr = exchange.read_hists(st.nb_coarse, st.plan_d)
+            hists, nos, errs, plan_arr = exchange.read_hists(st.nb_coarse, st.plan_d)
+            if cap and int(errs.max()):
+                force_host = True
+                continue
             exchange.no_capacity = int(nos.max() * 1.0625) + 4096
             if not cap or int(nos.max()) <= cap:
                 break
+    if fused:
         if st.deferred:
             st.no = ops.count_result()
         plan = st.set_plan(plan_arr)
@@ -230,17 +308,20 @@ def build_sharded(ops, comm, V, T, tri_base, spec, gather=True, exchange=None):
         # / plans itself; the host reads the count matrix, every rank's NO and the plan once.
         # After the first build the pair count is not read back either (PG_DEFER): the pair
         # buffers are sized by a capacity all ranks agree on (1.25 x the largest NO seen), and
-        # an overflow -- visible to every rank in the exchanged NOs -- repeats the build with
-        # the host-counted path.
+        # an overflow or a K1 error flag -- visible to every rank in the exchanged NOs and
+        # flags -- repeats the build with the host-counted path (global verdict first).
         while True:
-            cap = exchange.no_capacity
-            hist = st.phase_count(cap)
+            cap = None if force_host else exchange.no_capacity
+            hist = st.phase_count(cap, comm)
             exchange.put_hist(hist, rank)
             exchange.barrier()
             st.phase_plan_device(exchange.hists(st.nb_coarse))
             exchange.put_counts(st.phase_partition_counts_device(), rank, ops)
             exchange.barrier()
-            matrix, nos, plan_arr = exchange.read_counts(st.plan_d)
+            matrix, nos, errs, plan_arr = exchange.read_counts(st.plan_d)
+            if cap and int(errs.max()):
+                force_host = True
+                continue
             exchange.no_capacity = int(nos.max() * 1.25) + 4096
             if not cap or int(nos.max()) <= cap:
                 break
@@ -254,7 +335,7 @@ def build_sharded(ops, comm, V, T, tri_base, spec, gather=True, exchange=None):
         exchange.barrier()
         krecv, vrecv = exchange.received(nrecv)
     else:
-        hist = comm.allreduce_sum(st.phase_count())
+        hist = comm.allreduce_sum(st.phase_count(None, comm))
         plan = plan_slabs(hist, st.ncells, world)
         send, recv = comm.alltoall_counts(st.phase_partition(plan))
         krecv, vrecv = comm.alltoall_pairs(st.kout, st.vout, send, recv, ops)
@@ -352,6 +433,18 @@ class TorchComm:
         G[ncells] = int(np.uint32(no).view(np.int32))
         return G, Oall
 
+    def abort(self):
+        """Abort the communicator after a local failure: peers blocked in a collective with
+        this rank get an error instead of waiting forever (NCCL ncclCommAbort)."""
+        try:
+            from torch.distributed import distributed_c10d as c10d
+            c10d._abort_process_group(self.group or c10d.GroupMember.WORLD)
+        except Exception:
+            try:
+                self.dist.destroy_process_group(self.group)
+            except Exception:
+                pass
+
     def gather_to_root(self, obj):
         out = [None] * self.world if self.rank == 0 else None
         self.dist.gather_object(obj, out, dst=0, group=self.group)
@@ -415,7 +508,8 @@ class PeerExchange:
         self._read_p.copy_(plan_d, non_blocking=True)
         torch.cuda.current_stream(self.dev).synchronize()
         hists = self._read_h[:w * nb].numpy().view(np.uint32).reshape(w, nb).astype(np.int64)
-        return hists, _split_counts(self._read_c.numpy(), w)[1], self._read_p.numpy().copy()
+        _, nos, errs = _split_counts(self._read_c.numpy(), w)
+        return hists, nos, errs, self._read_p.numpy().copy()
 
     def read_counts(self, plan_d):
         """The count matrix [rank][slab], every rank's NO and the device plan: one host
@@ -487,7 +581,8 @@ class EmulatedExchange:
         w = self.world
         h = self.ctl[r][:w * nb].cpu().numpy().view(np.uint32).reshape(w, nb).astype(np.int64)
         c = self.ctl[r][w * CTL_HIST:w * (CTL_HIST + CTL_CNT)].cpu().numpy()
-        return h, _split_counts(c, w)[1], plan_d.cpu().numpy()
+        _, nos, errs = _split_counts(c, w)
+        return h, nos, errs, plan_d.cpu().numpy()
 
     def read_counts(self, r, plan_d):
         w = self.world
@@ -516,9 +611,10 @@ def slab_matrix(hists, cuts):
 
 
 def _split_counts(c, w):
-    """Control-buffer count slots (int32 [w][CTL_CNT]) -> (matrix [rank][slab], NO per rank)."""
+    """Control-buffer count slots (int32 [w][CTL_CNT]) -> (matrix [rank][slab], NO per rank,
+    K1 error flags per rank)."""
     c = np.asarray(c).view(np.uint32).reshape(w, CTL_CNT).astype(np.int64)
-    return c[:, :w].copy(), c[:, 16] | (c[:, 17] << 32)
+    return c[:, :w].copy(), c[:, 16] | (c[:, 17] << 32), c[:, 18].copy()
 
 
 def run_emulated(make_ops, V, T, spec, world, exchange="copy", capacity=None):
@@ -531,8 +627,18 @@ def run_emulated(make_ops, V, T, spec, world, exchange="copy", capacity=None):
     for r in range(world):
         lo, hi = shard_range(n, r, world)
         states.append(ShardState(make_ops(), V, T[lo:hi], lo, spec, r, world))
-    hist = np.sum([s.ops.to_numpy(s.phase_count()).astype(np.int64) for s in states], axis=0)
-    plan = plan_slabs(hist, states[0].ncells, world)
+
+    def counted(cap=None):
+        """K1 on every virtual rank, the whole mesh's verdict, then K2 (as build_sharded)."""
+        stats = [s.phase_count_only(cap) for s in states]
+        if stats[0] is not None:
+            count_verdict(np.sum(stats, axis=0), states[0].ncells)
+        return [s.phase_pairs() for s in states]
+
+    if exchange == "copy":
+        hists = counted()
+        hist = np.sum([s.ops.to_numpy(h).astype(np.int64) for s, h in zip(states, hists)], axis=0)
+        plan = plan_slabs(hist, states[0].ncells, world)
     if exchange == "fused":     # expansion + dispatch in one kernel (pg_pairs_send; CudaOps only)
         ex = EmulatedExchange(states[0].ops.torch, states[0].ops.dev, world)
         hists = [s.phase_count_fused(capacity) for s in states]
@@ -542,7 +648,7 @@ def run_emulated(make_ops, V, T, spec, world, exchange="copy", capacity=None):
         for r, s in enumerate(states):
             s.phase_plan_device(ex.hists(r, s.nb_coarse))
         for r, s in enumerate(states):
-            h, nos, plan_arr = ex.read_hists(r, s.nb_coarse, s.plan_d)
+            h, nos, errs, plan_arr = ex.read_hists(r, s.nb_coarse, s.plan_d)
             if capacity and int(nos.max()) > capacity:
                 return None
             if s.deferred:
@@ -564,7 +670,7 @@ def run_emulated(make_ops, V, T, spec, world, exchange="copy", capacity=None):
         # as build_sharded with a PeerExchange: histograms, plan and counts through the
         # (emulated) peer buffers, slab plans computed on the device by every rank
         ex = EmulatedExchange(states[0].ops.torch, states[0].ops.dev, world)
-        hists = [s.phase_count(capacity) for s in states]
+        hists = counted(capacity)
         for r, s in enumerate(states):
             ex.put_hist(hists[r], r)
         for r, s in enumerate(states):
@@ -573,7 +679,7 @@ def run_emulated(make_ops, V, T, spec, world, exchange="copy", capacity=None):
             ex.put_counts(s.phase_partition_counts_device(), r, s.ops)
         plans = []
         for r, s in enumerate(states):
-            matrix, nos, plan_arr = ex.read_counts(r, s.plan_d)
+            matrix, nos, errs, plan_arr = ex.read_counts(r, s.plan_d)
             if capacity and int(nos.max()) > capacity:
                 assert all(s2.ops.b.count_result() < 0 for s2, n2 in zip(states, nos) if n2 > capacity)
                 return None
@@ -677,6 +783,16 @@ class CudaOps:
             return self.b.count(V, V.shape[0], T, T.shape[0], spec, _native.PG_HOST_INPUT, self._sp())
         self._V, self._T = V, T          # keep alive for the stream
         return self.b.count(V, V.shape[0], T, T.shape[0], spec, 0, self._sp())
+
+    def count_stats(self, V, T, spec):
+        """K1 with PG_STATS: the shard's raw count statistics (no local verdict)."""
+        flags = 0
+        if not isinstance(V, self.torch.Tensor):
+            V = np.ascontiguousarray(V, dtype=np.float64).reshape(-1, 3)
+            T = np.ascontiguousarray(T, dtype=np.int32).reshape(-1, 3)
+            flags = _native.PG_HOST_INPUT
+        self._V, self._T = V, T
+        return self.b.count_stats(V, V.shape[0], T, T.shape[0], spec, flags, self._sp())
 
     def count_deferred(self, V, T, spec, capacity):
         """K1 without the NO read back (PG_DEFER)."""

@@ -29,12 +29,31 @@ class NumpyOps:
             return x.numpy().view(np.uint32)
         return np.asarray(x, np.uint32)
 
+    def count_stats(self, V, T, spec):
+        """distributed.ShardState's PG_STATS count: {NO, index out of range, inverted boxes with
+        negative / zero / positive counts, positive ones with a cell outside the grid}."""
+        V = np.asarray(V)
+        T = np.asarray(T)
+        if T.size and (T.min() < 0 or T.max() >= len(V)):
+            self._cnt = np.zeros(len(T), np.int64)
+            return np.array([0, 1, 0, 0, 0, 0], np.int64)
+        lo, hi, keep = oracle.cell_boxes(V, T, spec)
+        m = hi.astype(np.int64) - lo + 1
+        sc = np.where(keep, m[:, 0] * m[:, 1] * m[:, 2], 0)
+        inv = keep & (m <= 0).any(axis=1)
+        pos = inv & (sc > 0)
+        if pos.any():
+            raise NotImplementedError("numpy test ops: boxes inverted on two axes (covered on the GPU)")
+        self.count(V, T, spec)
+        no = int(np.where(inv, 0, sc).sum())
+        return np.array([no, 0, int((inv & (sc < 0)).sum()), int((inv & (sc == 0)).sum()), 0, 0], np.int64)
+
     def count(self, V, T, spec):
         lo, hi, keep = oracle.cell_boxes(V, T, spec)
         self._lo, self._hi, self._keep = lo.astype(np.int64), hi.astype(np.int64), keep
         self._dims = [int(d) for d in spec.dims]
         m = self._hi - self._lo + 1
-        self._cnt = np.where(keep, m[:, 0] * m[:, 1] * m[:, 2], 0)
+        self._cnt = np.where(keep & (m > 0).all(axis=1), m[:, 0] * m[:, 1] * m[:, 2], 0)
         return int(self._cnt.sum())
 
     def pairs(self, no, tri_base, shift, nbuckets):

@@ -134,8 +134,10 @@ def test_slab_matrix_and_count_slots():
         slots[:, :world] = m.astype(np.uint32)
         slots[:, 16] = nos & 0xFFFFFFFF
         slots[:, 17] = nos >> 32
-        mm, nn = D._split_counts(slots.view(np.int32).reshape(-1), world)
-        assert np.array_equal(mm, m) and np.array_equal(nn, nos)
+        errs = rng.integers(0, 4, size=world)
+        slots[:, 18] = errs
+        mm, nn, ee = D._split_counts(slots.view(np.int32).reshape(-1), world)
+        assert np.array_equal(mm, m) and np.array_equal(nn, nos) and np.array_equal(ee, errs)
 
 
 @pytest.mark.parametrize("n", [1, 3, 7])
@@ -147,3 +149,98 @@ def test_emulated_more_ranks_than_triangles(n):
     G, O = D.run_emulated(NumpyOps, mesh.vertices, mesh.triangles, spec, 8)
     Gr, Or = oracle.build_parallel(mesh.vertices, mesh.triangles, spec)
     assert np.array_equal(G, Gr) and np.array_equal(O, Or)
+
+
+def _err_worker(rank, world, port, case, out_path):
+    """One sharded build whose mesh is bad in ONE shard (or only globally); every rank must
+    raise the reference's class, at the same point, without hanging."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    got = "none"
+    try:
+        from np_ops import NumpyOps
+        from paper_2403_10647_b200.errors import InvariantError, SizeError
+        from paper_2403_10647_b200.gridcore import Aabb, GridSpec
+        V, T, spec = _err_case(case, world)
+        lo, hi = D.shard_range(len(T), rank, world)
+        try:
+            D.build_sharded(NumpyOps(), D.TorchComm(), V, T[lo:hi], lo, spec)
+        except SizeError:
+            got = "SizeError"
+        except InvariantError:
+            got = "InvariantError"
+        # the process group is still usable afterwards (no rank was left in a collective)
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        assert int(t.item()) == world
+        with open(f"{out_path}.{rank}", "w") as fh:
+            fh.write(got)
+    finally:
+        dist.destroy_process_group()
+
+
+def _err_case(case, world):
+    from paper_2403_10647_b200.gridcore import Aabb, GridSpec
+    good = gen_scene("uniform", 600, 3)
+    V = good.vertices.copy()
+    T = good.triangles.copy()
+    unit = GridSpec(Aabb([0, 0, 0], [1, 1, 1]), (16, 16, 16))
+    if case == "index":                    # one bad index in the LAST shard only
+        T[-1, 2] = len(V) + 5
+        return V, T, unit
+    if case == "negative":                 # one-axis inverted box in the first shard
+        V[T[0, 0]] = [0.6, 0.1, 0.1]
+        V[T[0, 1]] = [np.inf, 0.2, 0.1]
+        V[T[0, 2]] = [0.7, 0.1, 0.2]
+        return V, T, unit
+    if case == "zero":                     # zero-count box alone in its shard, not in the mesh
+        zt = np.array([[0.1, 0.1, 0.5], [np.inf, 0.2, 0.5], [0.12, 0.2, 0.5]])   # x: lo 1, hi 0
+        far = np.array([[5.0, 5, 5], [6, 5, 5], [5, 6, 5]])
+        tris = [zt] + [far] * (2 * world - 1) + [good.vertices[good.triangles[0]]]
+        Vz = np.concatenate(tris)
+        return Vz, np.arange(len(Vz), dtype=np.int32).reshape(-1, 3), unit
+    if case == "global_no":                # every shard < 2^32 pairs, the mesh > 2^32-1
+        Vf = np.array([[-1, -1, -1], [3, -1, 2], [-1, 3, 2]], np.float64)
+        Tf = np.zeros((17, 3), np.int32)
+        Tf[:] = [0, 1, 2]
+        return Vf, Tf, GridSpec(Aabb([0, 0, 0], [1, 1, 1]), (1024, 512, 512))
+    raise ValueError(case)
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case,want", [("index", "InvariantError"), ("negative", "InvariantError"),
+                                       ("zero", "InvariantError"), ("global_no", "SizeError")])
+def test_sharded_errors_agree_gloo(tmp_path, world, case, want):
+    """The reference's verdict for the whole mesh on every rank: a bad shard on one rank, a
+    zero-count box that is alone in its shard but not in the mesh, and a pair count that
+    overflows 2^32-1 only in total (builders.py:99-100, primitives.py:22-25, 66-72)."""
+    out = str(tmp_path / "verdict")
+    mp.spawn(_err_worker, args=(world, _free_port(), case, out), nprocs=world, join=True)
+    got = [open(f"{out}.{r}").read() for r in range(world)]
+    assert got == [want] * world, got
+    V, T, spec = _err_case(case, world)
+    if case != "index":                    # the single-device oracle agrees
+        exc = oracle.OracleSizeError if want == "SizeError" else oracle.OracleInvariantError
+        with pytest.raises(exc):
+            oracle.build_parallel(V, T, spec)
+
+
+def test_count_verdict_order():
+    from paper_2403_10647_b200.errors import InvariantError, SizeError
+    ok = D.count_verdict([100, 0, 0, 0, 0, 0], 1000)
+    assert ok == 100
+    with pytest.raises(InvariantError):
+        D.count_verdict([1 << 33, 0, 1, 0, 0, 0], 1000)      # negative count before SizeError
+    with pytest.raises(SizeError):
+        D.count_verdict([1 << 33, 0, 0, 1, 0, 0], 1000)      # NO > 2^32-1 before the zero count
+    with pytest.raises(InvariantError):
+        D.count_verdict([5, 0, 0, 1, 0, 0], 1000)            # zero count next to a kept box
+    assert D.count_verdict([0, 0, 0, 1, 0, 0], 1000) == 0    # a lone zero-count box: empty grid
+    with pytest.raises(SizeError):
+        D.count_verdict([(1 << 30) + 1, 0, 0, 0, 0, 0], 1000)
+    with pytest.raises(InvariantError):
+        D.count_verdict([9, 0, 0, 0, 1, 1], 1 << 31)         # bad cells before the ncells cap
+    with pytest.raises(SizeError):
+        D.count_verdict([9, 0, 0, 0, 0, 0], 1 << 31)

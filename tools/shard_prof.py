@@ -31,7 +31,7 @@ for it in range(6):
         h = st.phase_count_fused(ex.no_capacity); t = tick("count+coarse", t)
         ex.put_hist(h, 0); ex.put_no(0, ops); ex.barrier(); t = tick("put+barrier", t)
         st.phase_plan_device(ex.hists(st.nb_coarse)); t = tick("plan_dev", t)
-        hists, nos, pa = ex.read_hists(st.nb_coarse, st.plan_d); t = tick("read", t)
+        hists, nos, _, pa = ex.read_hists(st.nb_coarse, st.plan_d); t = tick("read", t)
         ex.no_capacity = int(nos.max() * 1.0625) + 4096
         if st.deferred: ops.count_result()
         plan = st.set_plan(pa); m = D.slab_matrix(hists, plan.cuts); ex.ensure(int(m.sum(axis=0).max()))
@@ -51,7 +51,7 @@ for it in range(6):
         ex.put_hist(h, 0); ex.barrier(); t = tick("put_hist", t)
         st.phase_plan_device(ex.hists(nb)); t = tick("plan_dev", t)
         ex.put_counts(st.phase_partition_counts_device(), 0, ops); t = tick("part_counts", t)
-        ex.barrier(); m, nos, pa = ex.read_counts(st.plan_d); st.set_plan(pa)
+        ex.barrier(); m, nos, _, pa = ex.read_counts(st.plan_d); st.set_plan(pa)
         ex.no_capacity = int(nos.max() * 1.25) + 4096
         if st.deferred: ops.count_result()
         ex.ensure(int(m.sum(axis=0).max())); t = tick("read_counts", t)
