@@ -306,6 +306,8 @@ def run_sharded(args, world, rank, local):
         except Exception as e:          # noqa: BLE001 -- reported in the JSON line
             why = f"{type(e).__name__}: {e}"[:200]
     if ex is not None and args.fused_dispatch:
+        if not _native.features() & _native.PG_FEATURE_FUSED_DISPATCH:
+            raise SystemExit("--fused-dispatch needs libpgrid built with -DPGRID_FUSED_DISPATCH=1")
         ex.fused = True
     ok = torch.tensor([1 if ex is not None else 0], device=dev)
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)

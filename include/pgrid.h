@@ -226,6 +226,11 @@ int pg_count_stats(pg_builder *b, int64_t *out);
  *                    tiles. Same pair order as pg_partition_send; the caller barriers the ranks
  *                    before the receivers read. Host arrays of nslabs device pointers/offsets. */
 int pg_coarse_hist(pg_builder *b, int coarse_shift, int coarse_bins, uint32_t *coarse_hist, void *stream);
+/* Optional parts compiled into this libpgrid (bit mask). The fused dispatch (pg_coarse_hist +
+ * pg_pairs_send) measured slower than pg_partition_send and ships only in builds with
+ * -DPGRID_FUSED_DISPATCH=1; without it both calls return PG_STATE_ERROR. */
+#define PG_FEATURE_FUSED_DISPATCH 1
+int pg_features(void);
 int pg_pairs_send(pg_builder *b, uint32_t val_offset, const uint32_t *slab_of_bucket, int bucket_shift,
                   int nslabs, const uint32_t *slab_base, const uint64_t *dst_keys, const uint64_t *dst_vals,
                   const uint64_t *dst_offset, void *stream);

@@ -38,7 +38,7 @@ NPHASES = 6
 EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
            "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_finish_baseline",
            "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_partition_counts", "pg_partition_send", "pg_peer_put", "pg_slab_plan", "pg_count_result",
-           "pg_peer_put_count", "pg_coarse_hist", "pg_pairs_send", "pg_count_stats",
+           "pg_peer_put_count", "pg_coarse_hist", "pg_pairs_send", "pg_count_stats", "pg_features",
            "pg_build_async",
            "pg_build_wait", "pg_host_register",
            "pg_host_unregister", "pg_host_alloc", "pg_host_free", "pg_last_launch_count",
@@ -122,6 +122,8 @@ def load():
         lib.pg_host_free.argtypes = [vp]
         lib.pg_last_launch_count.argtypes = [vp]
         lib.pg_last_error.restype = ctypes.c_char_p
+        lib.pg_features.argtypes = []
+        lib.pg_features.restype = ctypes.c_int
         for name in ("pg_builder_create", "pg_count", "pg_finish", "pg_stage",
                      "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells",
                      "pg_finish_baseline", "pg_count_stats", "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_partition_counts", "pg_partition_send", "pg_peer_put", "pg_slab_plan",
@@ -356,6 +358,14 @@ def slab_plan(hists, nranks, nbuckets, shift, ncells, nslabs, table, slab_base, 
     cuts | cell_lo | cell_hi | pair_base. No host synchronisation."""
     check(load().pg_slab_plan(ptr(hists), int(nranks), int(nbuckets), int(shift), int(ncells), int(nslabs),
                               ptr(table), ptr(slab_base), ptr(plan), stream))
+
+
+PG_FEATURE_FUSED_DISPATCH = 1
+
+
+def features():
+    """Bit mask of the optional parts compiled into libpgrid (pg_features)."""
+    return int(load().pg_features())
 
 
 def kernel_timing(on):

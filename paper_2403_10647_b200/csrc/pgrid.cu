@@ -35,6 +35,9 @@ int pdl_mode() {
   return m;
 }
 
+// First launch error of pdl_launch (cudaLaunchKernelEx's return code) since LAUNCHED last ran.
+thread_local cudaError_t g_launch_err = cudaSuccess;
+
 // Launch `k` with the programmatic-serialization attribute: its launch is processed while the
 // previous kernel on `st` retires instead of after it (the launch latency between links).
 // Only for kernels that open with PDL_ENTRY() (griddepcontrol.wait before any global access);
@@ -54,7 +57,8 @@ void pdl_launch(bool glue, void (*k)(KArgs...), unsigned grid, unsigned block, s
   cfg.stream = st;
   cfg.attrs = at;
   cfg.numAttrs = on ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+  if (e != cudaSuccess && g_launch_err == cudaSuccess) g_launch_err = e;  // reported by LAUNCHED
 }
 
 int fail(int code, const char* fmt, ...) {
@@ -165,50 +169,6 @@ void launch_radix_scatter(int bits, unsigned ntiles, cudaStream_t st, const unsi
   }
 }
 
-// PGRID_WC=1 selects the write-combining scatter (k_radix_scatter_wc). Measured slower on
-// cfg3 (219 vs 135 us per 9-bit pass): it cuts global store sectors 10.1M -> 6.4M per pass,
-// but its carries raise the instruction count 58M -> 100M and its shared memory drops
-// residency to 3 CTAs/SM; off.
-bool wc_on() {
-  static const bool on = [] {
-    const char* e = getenv("PGRID_WC");
-    return e && *e == '1';
-  }();
-  return on;
-}
-
-// resident CTAs of the write-combining scatter on the current device (its grid: every CTA
-// takes a contiguous chunk of tiles, so the chunks are as long as one wave allows)
-unsigned wc_resident() {
-  static const unsigned r = [] {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_scatter_wc<9>, RS_THREADS, sizeof(WcSmem));
-    return (unsigned)std::max(1, sms * std::max(1, occ));
-  }();
-  return r;
-}
-
-void launch_radix_scatter_wc(int bits, unsigned ntiles, cudaStream_t st, const unsigned* kin, const unsigned* vin,
-                             unsigned* ko, unsigned* vo, Count n, int shift, const unsigned* hist,
-                             const unsigned* offs, unsigned ld) {
-  const unsigned grid = std::min(ntiles, wc_resident());
-  switch (bits) {
-#define PG_CASE(B)                                                                                           \
-  case B:                                                                                                    \
-    k_radix_scatter_wc<B><<<grid, RS_THREADS, sizeof(WcSmem), st>>>(kin, vin, ko, vo, n, shift, hist, offs, ld); \
-    break;
-    PG_CASE(1) PG_CASE(2) PG_CASE(3) PG_CASE(4) PG_CASE(5) PG_CASE(6) PG_CASE(7) PG_CASE(8) PG_CASE(9)
-#undef PG_CASE
-    default: break;
-  }
-}
-
-template <int B>
-cudaError_t set_emit_smem() {
-  return cudaFuncSetAttribute(k_pairs_emit<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PeSmem));
-}
 template <int BITS>
 cudaError_t set_scatter_smem() {
   cudaError_t e = cudaFuncSetAttribute(k_radix_scatter<BITS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -219,49 +179,12 @@ cudaError_t set_scatter_smem() {
                               (int)rs_smem_bytes());
 }
 
-// PGRID_PRESORT=1 enables the K2 local presort of the first radix digit (measured slower:
-// K2's scattered in-tile stores cost more than the ranking they save in pass 0; off).
 bool packed0_on() {
   static const bool on = [] {
     const char* e = getenv("PGRID_PACKED0");
     return !e || *e != '0';
   }();
   return on;
-}
-
-bool presort_on() {
-  static const bool on = [] {
-    const char* e = getenv("PGRID_PRESORT");
-    return kPresortFits && e && *e == '1';
-  }();
-  return on;
-}
-
-void launch_pairs_emit(int presort_bits, unsigned grid, cudaStream_t st, const uint4* rec, const unsigned* tile_pre,
-                       long long n, Count cno, unsigned dx, unsigned dxy, const PassPlan& plan, const int2* bounds,
-                       unsigned* keys, unsigned* vals, unsigned* counts, unsigned ld, unsigned* packed0 = nullptr) {
-  switch (presort_bits) {
-#define PG_CASE(B)                                                                                        \
-  case B:                                                                                                 \
-    pdl_launch(false, k_pairs_emit<B>, grid, RS_THREADS, sizeof(PeSmem), st, rec, tile_pre, n, cno, dx, dxy, plan, \
-               bounds, keys, vals, counts, ld, packed0);                                                  \
-    break;
-    PG_CASE(0) PG_CASE(1) PG_CASE(2) PG_CASE(3) PG_CASE(4) PG_CASE(5) PG_CASE(6) PG_CASE(7) PG_CASE(8) PG_CASE(9)
-#undef PG_CASE
-    default: break;
-  }
-}
-
-void launch_scatter_presorted(int bits, unsigned ntiles, cudaStream_t st, const unsigned* kin, const unsigned* vin,
-                              unsigned* ko, unsigned* vo, Count n, int shift, const unsigned* hist,
-                              const unsigned* offs, unsigned ld) {
-  switch (bits) {
-#define PG_CASE(B) \
-  case B: k_scatter_presorted<B><<<ntiles, RS_THREADS, 0, st>>>(kin, vin, ko, vo, n, shift, hist, offs, ld); break;
-    PG_CASE(1) PG_CASE(2) PG_CASE(3) PG_CASE(4) PG_CASE(5) PG_CASE(6) PG_CASE(7) PG_CASE(8) PG_CASE(9)
-#undef PG_CASE
-    default: break;
-  }
 }
 
 // PGRID_SYNC_DEBUG=1: synchronise after every launch so a fault names its kernel.
@@ -305,6 +228,10 @@ void ktimer_reset(cudaStream_t st) {
 
 #define LAUNCHED(name, st)                                                                         \
   do {                                                                                             \
+    const cudaError_t le_ = g_launch_err;                                                          \
+    g_launch_err = cudaSuccess;                                                                    \
+    if (le_ != cudaSuccess)                                                                        \
+      return fail(PG_CUDA_ERROR, "launch of %s failed: %s", name, cudaGetErrorString(le_));       \
     CU(cudaGetLastError());                                                                        \
     if (ktimes_on()) cudaEventRecord(g_kt.next(name), st);                                         \
     if (sync_debug()) {                                                                            \
@@ -385,22 +312,18 @@ int pg_builder_create(int device, pg_builder** out) {
   for (auto& e : b->ev) CU(cudaEventCreate(&e));
   CU(cudaMallocHost(&b->h_scalars, 4 * sizeof(unsigned long long)));
   CU(cudaFuncSetAttribute(k_boxes_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem)));
-  CU(set_emit_smem<0>()); CU(set_emit_smem<1>()); CU(set_emit_smem<2>()); CU(set_emit_smem<3>());
-  CU(set_emit_smem<4>()); CU(set_emit_smem<5>()); CU(set_emit_smem<6>()); CU(set_emit_smem<7>());
-  CU(set_emit_smem<8>()); CU(set_emit_smem<9>());
+  CU(cudaFuncSetAttribute(k_pairs_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PeSmem)));
   CU(set_scatter_smem<1>()); CU(set_scatter_smem<2>()); CU(set_scatter_smem<3>());
   CU(set_scatter_smem<4>()); CU(set_scatter_smem<5>()); CU(set_scatter_smem<6>());
   CU(set_scatter_smem<7>()); CU(set_scatter_smem<8>()); CU(set_scatter_smem<9>());
   for (auto f : {k_partition_send<1>, k_partition_send<2>, k_partition_send<3>, k_partition_send<4>})
     CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs_smem_bytes()));
+#if PGRID_FUSED_DISPATCH
   for (auto f : {k_pairs_send<1>, k_pairs_send<2>, k_pairs_send<3>, k_pairs_send<4>})
     CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SendSmem)));
   CU(cudaFuncSetAttribute(k_coarse_from_boxes, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PLAN_MAX_BUCKETS));
   CU(cudaFuncSetAttribute(k_coarse_big, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * PLAN_MAX_BUCKETS));
-  for (auto f : {k_radix_scatter_wc<1>, k_radix_scatter_wc<2>, k_radix_scatter_wc<3>, k_radix_scatter_wc<4>,
-                 k_radix_scatter_wc<5>, k_radix_scatter_wc<6>, k_radix_scatter_wc<7>, k_radix_scatter_wc<8>,
-                 k_radix_scatter_wc<9>})
-    CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(WcSmem)));
+#endif
   *out = b;
   return PG_OK;
 }
@@ -731,7 +654,7 @@ namespace {
 int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned* keys0, unsigned* vals0,
                unsigned* keys1, unsigned* vals1, unsigned* vals_final, Count cno, uint64_t cap, unsigned* hist,
                unsigned* counts, cudaStream_t st, const unsigned** sorted_keys_out, unsigned* keys2 = nullptr,
-               unsigned* vals2 = nullptr, bool presorted0 = false, const unsigned* packed0 = nullptr) {
+               unsigned* vals2 = nullptr, const unsigned* packed0 = nullptr) {
   // grids are sized for `cap` pairs; the kernels read the actual count from `cno`
   const unsigned ntiles = (unsigned)((cap + RS_TILE - 1) / RS_TILE);
   const unsigned ld = (ntiles + 3) & ~3u;
@@ -767,19 +690,9 @@ int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned
                  hist + p * kMaxBins);
       LAUNCHED("k_scan_tile_counts", st);
     }
-    if (p == 0 && presorted0) {
-      launch_scatter_presorted(plan.bits[p], ntiles, st, kin, vin, ko, vo, cno, plan.shift[p], hist + p * kMaxBins,
-                               counts, ld);
-      LAUNCHED("k_scatter_presorted", st);
-    } else if (wc_on()) {
-      launch_radix_scatter_wc(plan.bits[p], ntiles, st, kin, vin, ko, vo, cno, plan.shift[p], hist + p * kMaxBins,
-                              counts, ld);
-      LAUNCHED("k_radix_scatter_wc", st);
-    } else {
-      launch_radix_scatter(plan.bits[p], ntiles, st, kin, vin, ko, vo, cno, plan.shift[p], hist + p * kMaxBins, counts,
-                           ld);
-      LAUNCHED("k_radix_scatter", st);
-    }
+    launch_radix_scatter(plan.bits[p], ntiles, st, kin, vin, ko, vo, cno, plan.shift[p], hist + p * kMaxBins, counts,
+                         ld);
+    LAUNCHED("k_radix_scatter", st);
     b->launches += 2;
     *sorted_keys_out = ko;
   }
@@ -860,22 +773,19 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
       pdl_launch(true, k_pair_tile_bounds, (rs_tiles + 7) / 8, 256, 0, st, b->rec.as<uint4>(), b->tile_pre, b->n,
                  cno, RS_TILE, pbounds, hist, (unsigned)(hist_bytes / 4));
       LAUNCHED("k_pair_tile_bounds", st);
-      // K2 writes its first-pass tile counts straight into the digit-major matrix
-      // with the presort, K2 leaves every tile sorted by the first digit (pass 0 then only moves
-      // digit runs); stage dumps (record=) need generation order, so they skip it
-      const bool presort = presort_on() && !(flags & PG_KEEP_STAGES) && !b->inv_fix;
-      // K2's first-pass counts two digits per word (the row scan unpacks them): PGRID_PACKED0=0 off
-      unsigned* packed0 = (!presort && !b->inv_fix && packed0_on() && plan.bits[0] >= 1)
+      // K2 writes its first-pass tile counts straight into the digit-major matrix, two digits
+      // per word (the row scan unpacks them): PGRID_PACKED0=0 off
+      unsigned* packed0 = (!b->inv_fix && packed0_on() && plan.bits[0] >= 1)
                               ? counts + (size_t)kMaxBins * ld : nullptr;
-      launch_pairs_emit(presort ? plan.bits[0] : 0, rs_tiles, st, b->rec.as<uint4>(), b->tile_pre, b->n, cno, dxu,
-                        dxyu, plan, pbounds, keysA, valsA, counts, ld, packed0);
+      pdl_launch(false, k_pairs_emit, rs_tiles, RS_THREADS, sizeof(PeSmem), st, b->rec.as<uint4>(), b->tile_pre, b->n,
+                 cno, dxu, dxyu, plan, pbounds, keysA, valsA, counts, ld, packed0);
       LAUNCHED("k_pairs_emit", st);
       b->launches += 2;
       // two-axis inverted boxes: their keys are rewritten, so pass 0 recounts its digits
       if ((rc = fix_inverted(b, keysA, st))) return rc;
       CU(cudaEventRecord(b->ev[1], st));
       if ((rc = run_passes(b, plan, !b->inv_fix, keysA, valsA, keysB, valsB, dO, cno, no, hist, counts, st, &sorted,
-                           nullptr, nullptr, presort, packed0)))
+                           nullptr, nullptr, packed0)))
         return rc;
     } else {
       CU(cudaEventRecord(b->ev[1], st));
@@ -1785,6 +1695,17 @@ int pg_partition_send(pg_builder* b, const uint32_t* keys, const uint32_t* vals,
   return PG_OK;
 }
 
+int pg_features(void) { return PGRID_FUSED_DISPATCH ? PG_FEATURE_FUSED_DISPATCH : 0; }
+
+#if !PGRID_FUSED_DISPATCH
+int pg_coarse_hist(pg_builder*, int, int, uint32_t*, void*) {
+  return fail(PG_STATE_ERROR, "libpgrid built without PGRID_FUSED_DISPATCH (expansion + dispatch kernel)");
+}
+int pg_pairs_send(pg_builder*, uint32_t, const uint32_t*, int, int, const uint32_t*, const uint64_t*,
+                  const uint64_t*, const uint64_t*, void*) {
+  return fail(PG_STATE_ERROR, "libpgrid built without PGRID_FUSED_DISPATCH (expansion + dispatch kernel)");
+}
+#else
 int pg_coarse_hist(pg_builder* b, int coarse_shift, int coarse_bins, uint32_t* coarse_hist, void* stream_) {
   if (!b || !b->counted) return fail(PG_STATE_ERROR, "pg_coarse_hist without a successful pg_count");
   if (!coarse_hist || coarse_bins < 1 || coarse_bins > PLAN_MAX_BUCKETS || coarse_shift < 0 || coarse_shift > 31)
@@ -1864,6 +1785,7 @@ int pg_pairs_send(pg_builder* b, uint32_t val_offset, const uint32_t* slab_of_bu
   b->launches = 2;
   return PG_OK;
 }
+#endif  // PGRID_FUSED_DISPATCH
 
 int pg_peer_put(const uint32_t* src, int64_t n, const uint64_t* dsts, int nranks, int64_t dst_offset, void* stream_) {
   if (!dsts || (n > 0 && !src)) return fail(PG_INVARIANT_ERROR, "null argument");

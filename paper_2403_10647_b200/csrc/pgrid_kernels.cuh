@@ -935,22 +935,6 @@ k_expand_pairs(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_
   }
 }
 
-// Standalone digit histogram (plugin-seam sort of arbitrary keys).
-__global__ void __launch_bounds__(256)
-k_digit_hist(const unsigned* __restrict__ keys, long long n, PassPlan plan, unsigned* __restrict__ hist) {
-  __shared__ unsigned sh_hist[kMaxPasses * kMaxBins];
-  for (int i = threadIdx.x; i < plan.npasses * kMaxBins; i += blockDim.x) sh_hist[i] = 0;
-  __syncthreads();
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const unsigned k = keys[i];
-    for (int ps = 0; ps < plan.npasses; ++ps)
-      atomicAdd(&sh_hist[ps * kMaxBins + ((k >> plan.shift[ps]) & ((1u << plan.bits[ps]) - 1u))], 1u);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < plan.npasses * kMaxBins; i += blockDim.x)
-    if (sh_hist[i]) atomicAdd(&hist[i], sh_hist[i]);
-}
-
 // ----------------------------------------------------------------------------------------
 // K3: stable LSD radix pass, reduce-then-scan:
 //   k_tile_counts       per-tile digit counts          counts[digit][tile]
@@ -972,26 +956,17 @@ constexpr int RS_ITEMS = 16;
 constexpr int RS_ITEMS = RS_ITEMS_OVERRIDE;
 #endif
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 pairs per tile
-constexpr int RS_DPT = kMaxBins / RS_THREADS;  // digits per thread in the per-digit phases
+constexpr int RS_DPT = 2;  // digits per thread in the per-digit phases (threads >= kMaxBins / 2 take none)
+static_assert(RS_THREADS * RS_DPT >= kMaxBins, "the per-digit phases need kMaxBins / 2 threads");
 #ifndef RS_MIN_CTAS_OVERRIDE
 constexpr int RS_MIN_CTAS = 4;
 #else
 constexpr int RS_MIN_CTAS = RS_MIN_CTAS_OVERRIDE;
 #endif  // 64 registers, 45 KB smem: 4 CTAs (32 warps) per SM
 
-#ifndef PGRID_SCATTER_KV
-#define PGRID_SCATTER_KV 0  // 1: packed (value << 32 | key) scatter -- measured slower (register spills)
-#endif
 struct RsSmem {
-  union {
-    // PGRID_SCATTER_KV: the tile in digit order as packed (value << 32 | key) words; the
-    // values' cp.async staging area aliases it (read into registers before the scatter)
-    unsigned long long kv[RS_TILE];
-    struct {
-      unsigned buf[RS_TILE];     // tile in digit order: keys, then values
-      unsigned vstage[RS_TILE];  // values in input order (cp.async staging)
-    };
-  };
+  unsigned buf[RS_TILE];     // tile in digit order: keys, then values
+  unsigned vstage[RS_TILE];  // values in input order (cp.async staging)
   unsigned short whist[RS_WARPS][kMaxBins];  // per-warp digit counts -> tile offset of (warp, digit)
   unsigned gbase[kMaxBins];                  // global position of buf[0] for each digit
   unsigned hsm[kMaxBins];                    // digit totals (staged)
@@ -1119,25 +1094,6 @@ k_tile_counts(const unsigned* __restrict__ keys, Count cno, DigitFn dig, int nbi
       const int b = i / TC_TILES, q = i % TC_TILES;
       if (t0 + q < ntiles) counts[(size_t)b * ld + t0 + q] = h[q][b];
     }
-  }
-}
-
-// K2 writes its first-pass counts tile-major (one coalesced row per CTA); transpose them to
-// the digit-major layout the row scan and the scatter use.
-__global__ void __launch_bounds__(256)
-k_transpose_counts(const unsigned* __restrict__ tm, Count cno, int nbins, unsigned* __restrict__ dm, unsigned ld) {
-  __shared__ unsigned blk[32][33];
-  const unsigned ntiles = (cno.get() + RS_TILE - 1) / RS_TILE;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  const unsigned t0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
-  for (int r = ty; r < 32; r += 8) {
-    const unsigned t = t0 + r, d = d0 + tx;
-    blk[r][tx] = (t < ntiles && d < (unsigned)nbins) ? tm[(size_t)t * kMaxBins + d] : 0u;
-  }
-  __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
-    const unsigned d = d0 + r, t = t0 + tx;
-    if (t < ntiles && d < (unsigned)nbins) dm[(size_t)d * ld + t] = blk[tx][r];
   }
 }
 
@@ -1357,7 +1313,6 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
   __syncthreads();
   // per digit (thread t owns digits 2t, 2t+1 -- one 32-bit word of every warp's u16 row):
   // warp offsets and tile counts of both digits in one pass over the rows
-  static_assert(RS_DPT == 2, "two digits per thread");
   unsigned* rows = reinterpret_cast<unsigned*>(&sm.whist[0][0]);
   unsigned tpk = 0;  // tile counts of both digits, packed (u16 lanes never carry: <= RS_TILE)
   if (tid < NB / 2) {
@@ -1439,41 +1394,6 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
     lpre += tc[q];
     hpre += hs[q];
   }
-#if PGRID_SCATTER_KV
-  if (!SRC_SMEM) cp_async_wait();
-  __syncthreads();
-  // ranks -> tile positions (the digits die here), values into registers (input order,
-  // conflict-free), then the staging area is free
-#pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j)
-    if (valid(j)) rank[j] += sm.whist[warp][dg[j]];
-  unsigned vreg[RS_ITEMS];
-#pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) vreg[j] = valid(j) ? sm.vstage[elem(j)] : 0u;
-  __syncthreads();
-  // (key, value) pairs: one stable 8-byte local scatter into digit order (key re-read from
-  // L1/L2), then a run-coalesced write-out of both arrays from the same positions
-#pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) {
-    if (valid(j)) {
-      sm.kv[rank[j]] = ((unsigned long long)vreg[j] << 32) | (SRC_SMEM ? ksrc[elem(j)] : __ldg(ksrc + elem(j)));
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < RS_ITEMS; ++r) {
-    const unsigned i = tid + r * RS_THREADS;
-    if (FULL || i < tvalid) {
-      const unsigned long long x = sm.kv[i];
-      const unsigned k = (unsigned)x;
-      const unsigned d = digit(k);
-      const unsigned g = sm.gbase[d] + i;
-      if (keys_out) keys_out[g] = TABLE ? k - __ldg(&kbase[d]) : k;
-      vals_out[g] = (unsigned)(x >> 32);
-    }
-  }
-}
-#else
   __syncthreads();
   // keys: stable local scatter into digit order (key re-read from L1/L2), run-coalesced write
 #pragma unroll
@@ -1519,7 +1439,6 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
   }
 }
 
-#endif
 
 template <int BITS, bool TABLE>
 __global__ void __launch_bounds__(RS_THREADS, RS_MIN_CTAS)
@@ -1667,214 +1586,6 @@ k_slab_plan(const unsigned* __restrict__ hists, int nranks, int nb, int shift, l
 }
 
 // ----------------------------------------------------------------------------------------
-// Write-combining radix scatter (the default bit-field pass). What bounds a pass is the
-// number of 32-byte sectors its warp stores touch, not its bytes: moving 19.86M pairs in
-// runs of 8 items takes 82 us when every run is one aligned sector and 152 us when runs
-// straddle sector boundaries (tools/micro/run_align.cu). A tile's run of a digit (~8 items
-// for 9-bit digits) starts anywhere, so k_radix_scatter writes ~2 partial sectors per run.
-// Here each CTA owns a contiguous chunk of tiles. Digit d's output for the chunk is one
-// contiguous range, so the CTA carries the unfinished tail sector of every digit (<= 7 keys
-// and values in shared memory) into the next tile, lays it out in front of that tile's run,
-// and writes whole aligned sectors only; partial sectors remain at chunk ends alone.
-// Ranking is k_radix_scatter's (bit-sliced ballots, stable in element order).
-// ----------------------------------------------------------------------------------------
-constexpr int WC_CARRY = 7;
-constexpr int WC_CAP = RS_TILE + kMaxBins * WC_CARRY;               // tile + carried items
-constexpr int WC_R = (WC_CAP + RS_THREADS - 1) / RS_THREADS;        // write-out items per thread
-constexpr int WC_MIN_CTAS = 3;
-struct WcSmem {
-  unsigned buf[WC_CAP];                      // digit-major blocks [carry | tile run]: keys, then values
-  unsigned carry_k[kMaxBins * WC_CARRY];     // tail sector of each digit, carried to the next tile
-  unsigned carry_v[kMaxBins * WC_CARRY];
-  unsigned short whist[RS_WARPS][kMaxBins];  // per-warp digit counts -> buffer offset of (warp, digit)
-  unsigned cbase[kMaxBins];                  // global position of buf[0] for digit d's block
-  unsigned wend[kMaxBins];                   // end of digit d's written range this tile
-  unsigned wsum[RS_WARPS];
-};
-
-template <int BITS, bool FULL>
-__device__ __forceinline__ void wc_scatter_tile(WcSmem& sm, const unsigned* __restrict__ keys_in,
-                                                const unsigned* __restrict__ vals_in, unsigned* __restrict__ keys_out,
-                                                unsigned* __restrict__ vals_out, unsigned tbase, unsigned tvalid,
-                                                unsigned tile, unsigned ld, int shift,
-                                                const unsigned* __restrict__ offs, const unsigned (&hpre)[RS_DPT],
-                                                unsigned (&cs)[RS_DPT], bool first, bool last) {
-  constexpr int NB = 1 << BITS;
-  constexpr unsigned DMASK = (unsigned)NB - 1u;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  auto elem = [&](int j) { return (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane; };
-  auto valid = [&](int j) { return FULL || elem(j) < tvalid; };
-  auto digit = [&](unsigned k) { return (k >> shift) & DMASK; };
-  {
-    unsigned* row = reinterpret_cast<unsigned*>(&sm.whist[warp][0]);
-#pragma unroll
-    for (int q = lane; q < (NB + 1) / 2; q += 32) row[q] = 0u;
-  }
-  unsigned kreg[RS_ITEMS], vreg[RS_ITEMS];
-#pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) {
-    kreg[j] = valid(j) ? __ldcs(keys_in + tbase + elem(j)) : 0u;
-    vreg[j] = valid(j) ? __ldcs(vals_in + tbase + elem(j)) : 0u;
-  }
-  unsigned pos[RS_ITEMS];
-#pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) pos[j] = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid(j));
-#pragma unroll
-  for (int b = 0; b < BITS; ++b) {
-#pragma unroll
-    for (int j = 0; j < RS_ITEMS; ++j) pos[j] = peers_step(pos[j], kreg[j], 1u << (shift + b));
-  }
-  __syncwarp();
-  const unsigned lt = lanemask_lt();
-#pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) {
-    const unsigned peers = valid(j) ? pos[j] : 0u;
-    const unsigned dj = digit(kreg[j]);
-    const int leader = __ffs(peers | (1u << lane)) - 1;
-    unsigned old = 0;
-    if (lane == leader && peers) {
-      old = sm.whist[warp][dj];
-      sm.whist[warp][dj] = (unsigned short)(old + __popc(peers));
-    }
-    old = __shfl_sync(0xffffffffu, old, leader);
-    pos[j] = old + __popc(peers & lt);  // rank among the warp's items of this digit
-    __syncwarp();
-  }
-  __syncthreads();
-  // per digit (owner thread): tile count n, run start s, block = carry [cs, s) + run [s, s+n)
-  unsigned n[RS_DPT], s[RS_DPT], cc[RS_DPT], msum = 0;
-#pragma unroll
-  for (int q = 0; q < RS_DPT; ++q) {
-    const int d = tid * RS_DPT + q;
-    unsigned run = 0;
-    s[q] = 0;
-    if (d < NB) {
-#pragma unroll
-      for (int w = 0; w < RS_WARPS; ++w) {
-        const unsigned c = sm.whist[w][d];
-        sm.whist[w][d] = (unsigned short)run;
-        run += c;
-      }
-      s[q] = hpre[q] + __ldg(&offs[(size_t)d * ld + tile]);
-    }
-    if (first) cs[q] = s[q];
-    n[q] = run;
-    cc[q] = s[q] - cs[q];
-    msum += cc[q] + run;
-  }
-  unsigned mtot;
-  unsigned B = block_excl_scan<RS_WARPS>(msum, sm.wsum, mtot);
-  unsigned Bq[RS_DPT];
-#pragma unroll
-  for (int q = 0; q < RS_DPT; ++q) {
-    const int d = tid * RS_DPT + q;
-    Bq[q] = B;
-    if (d < NB) {
-#pragma unroll
-      for (int w = 0; w < RS_WARPS; ++w) sm.whist[w][d] = (unsigned short)(sm.whist[w][d] + B + cc[q]);
-      const unsigned end = s[q] + n[q];
-      const unsigned we = last ? end : max(cs[q], end & ~7u);  // whole sectors only
-      sm.cbase[d] = cs[q] - B;
-      sm.wend[d] = we;
-      for (unsigned i = 0; i < cc[q]; ++i) sm.buf[B + i] = sm.carry_k[d * WC_CARRY + i];
-      cs[q] = we;
-    }
-    B += cc[q] + n[q];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) {
-    if (valid(j)) {
-      pos[j] += sm.whist[warp][digit(kreg[j])];
-      sm.buf[pos[j]] = kreg[j];
-    }
-  }
-  __syncthreads();
-  // keys out: buffer position i of digit d is global position cbase[d] + i; items past the
-  // written range become the digit's new carry. Digits are kept (10 bits each) for the values.
-  unsigned dpk[(WC_R + 2) / 3];
-#pragma unroll
-  for (int r = 0; r < WC_R; ++r) {
-    const unsigned i = tid + r * RS_THREADS;
-    if (r % 3 == 0) dpk[r / 3] = 0u;
-    if (i < mtot) {
-      const unsigned k = sm.buf[i];
-      const unsigned d = digit(k);
-      dpk[r / 3] |= d << (10 * (r % 3));
-      const unsigned g = sm.cbase[d] + i, we = sm.wend[d];
-      if (g < we) keys_out[g] = k;
-      else sm.carry_k[d * WC_CARRY + (g - we)] = k;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j)
-    if (valid(j)) sm.buf[pos[j]] = vreg[j];
-#pragma unroll
-  for (int q = 0; q < RS_DPT; ++q) {
-    const int d = tid * RS_DPT + q;
-    if (d < NB)
-      for (unsigned i = 0; i < cc[q]; ++i) sm.buf[Bq[q] + i] = sm.carry_v[d * WC_CARRY + i];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < WC_R; ++r) {
-    const unsigned i = tid + r * RS_THREADS;
-    if (i < mtot) {
-      const unsigned d = (dpk[r / 3] >> (10 * (r % 3))) & 1023u;
-      const unsigned g = sm.cbase[d] + i, we = sm.wend[d];
-      if (g < we) vals_out[g] = sm.buf[i];
-      else sm.carry_v[d * WC_CARRY + (g - we)] = sm.buf[i];
-    }
-  }
-  // the next tile touches buf / cbase / wend / carries only after its ranking barrier
-}
-
-template <int BITS>
-__global__ void __launch_bounds__(RS_THREADS, WC_MIN_CTAS)
-k_radix_scatter_wc(const unsigned* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
-                   unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, Count cno, int shift,
-                   const unsigned* __restrict__ hist, const unsigned* __restrict__ offs, unsigned ld) {
-  constexpr int NB = 1 << BITS;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  WcSmem& sm = *reinterpret_cast<WcSmem*>(smem_raw);
-  const unsigned no = cno.get();
-  const unsigned ntiles = (no + RS_TILE - 1) / RS_TILE;
-  const unsigned t0 = (unsigned)((unsigned long long)ntiles * blockIdx.x / gridDim.x);
-  const unsigned t1 = (unsigned)((unsigned long long)ntiles * (blockIdx.x + 1) / gridDim.x);
-  if (t0 >= t1) return;
-  const int tid = threadIdx.x;
-  // per-digit state lives in the registers of the digit's owner thread
-  unsigned hpre[RS_DPT], cs[RS_DPT];
-  {
-    unsigned hs[RS_DPT], hsum = 0, htot;
-#pragma unroll
-    for (int q = 0; q < RS_DPT; ++q) {
-      const int d = tid * RS_DPT + q;
-      hs[q] = d < NB ? __ldg(&hist[d]) : 0u;
-      hsum += hs[q];
-      cs[q] = 0;
-    }
-    unsigned p = block_excl_scan<RS_WARPS>(hsum, sm.wsum, htot);
-#pragma unroll
-    for (int q = 0; q < RS_DPT; ++q) {
-      hpre[q] = p;
-      p += hs[q];
-    }
-  }
-  for (unsigned tile = t0; tile < t1; ++tile) {
-    const unsigned tbase = tile * (unsigned)RS_TILE;
-    const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
-    if (tvalid == (unsigned)RS_TILE)
-      wc_scatter_tile<BITS, true>(sm, keys_in, vals_in, keys_out, vals_out, tbase, tvalid, tile, ld, shift, offs,
-                                  hpre, cs, tile == t0, tile + 1 == t1);
-    else
-      wc_scatter_tile<BITS, false>(sm, keys_in, vals_in, keys_out, vals_out, tbase, tvalid, tile, ld, shift, offs,
-                                   hpre, cs, tile == t0, tile + 1 == t1);
-  }
-}
-
-// ----------------------------------------------------------------------------------------
 // K2: pair expansion on radix-sort tiles. Each CTA expands RS_TILE pairs, writes them in
 // generation (object-major) order with 16-byte stores, and counts the tile's first-pass
 // digits (the per-tile counts the first radix pass needs, so that pass skips its own
@@ -1887,101 +1598,10 @@ struct PeSmem {
   int warpmax[2 * RS_WARPS + 1];
 };
 static_assert(sizeof(ObjCache) >= RS_TILE * 4, "the object cache doubles as the value transpose buffer");
-// the presort keeps its values and per-warp counters in the object cache
-constexpr bool kPresortFits = sizeof(ObjCache) >= RS_TILE * 4 + RS_WARPS * kMaxBins * 2 + RS_WARPS * 4;
-
-// K2 with the first radix pass's local sort fused in (PRESORT = that pass's digit bits): the
-// tile's pairs are ranked by the first digit exactly as k_radix_scatter ranks a tile (stable,
-// element order) and written back to the tile's own slots in digit order, so the first pass
-// only has to move whole digit runs (k_scatter_presorted, no ranking). Shared memory reuses
-// the expansion's dead slots (keys) and object cache (values, per-warp counters).
-template <int BITS>
-__device__ __forceinline__ void presort_tile(const unsigned* __restrict__ skey, const unsigned* __restrict__ sval,
-                                             unsigned short (*whist)[kMaxBins], unsigned* wsum, unsigned p0,
-                                             unsigned tvalid, int shift, unsigned* __restrict__ keys,
-                                             unsigned* __restrict__ vals, unsigned* __restrict__ counts0, unsigned ld,
-                                             unsigned tile) {
-  constexpr int NB = 1 << BITS;
-  constexpr unsigned DMASK = (unsigned)NB - 1u;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  auto elem = [&](int j) { return (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane; };
-  auto valid = [&](int j) { return elem(j) < tvalid; };
-  {
-    unsigned* row = reinterpret_cast<unsigned*>(&whist[warp][0]);
-#pragma unroll
-    for (int q = lane; q < NB / 2; q += 32) row[q] = 0u;
-  }
-  unsigned dg[RS_ITEMS];
-#pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) dg[j] = valid(j) ? (skey[elem(j)] >> shift) & DMASK : 0u;
-  unsigned pm[RS_ITEMS];
-#pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) pm[j] = __ballot_sync(0xffffffffu, valid(j));
-#pragma unroll
-  for (int b = 0; b < BITS; ++b) {
-#pragma unroll
-    for (int j = 0; j < RS_ITEMS; ++j) pm[j] = peers_step(pm[j], dg[j], 1u << b);
-  }
-  __syncwarp();
-  const unsigned lt = lanemask_lt();
-  unsigned rank[RS_ITEMS];
-#pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) {
-    const unsigned peers = valid(j) ? pm[j] : 0u;
-    const int leader = __ffs(peers | (1u << lane)) - 1;
-    unsigned old = 0;
-    if (lane == leader && peers) {
-      old = whist[warp][dg[j]];
-      whist[warp][dg[j]] = (unsigned short)(old + __popc(peers));
-    }
-    old = __shfl_sync(0xffffffffu, old, leader);
-    rank[j] = old + __popc(peers & lt);
-    __syncwarp();
-  }
-  __syncthreads();
-  unsigned tc[RS_DPT], tsum = 0;
-#pragma unroll
-  for (int q = 0; q < RS_DPT; ++q) {
-    const int d = tid * RS_DPT + q;
-    unsigned run = 0;
-    if (d < NB) {
-#pragma unroll
-      for (int w = 0; w < RS_WARPS; ++w) {
-        const unsigned c = whist[w][d];
-        whist[w][d] = (unsigned short)run;
-        run += c;
-      }
-    }
-    tc[q] = run;
-    tsum += run;
-  }
-  unsigned ttot;
-  unsigned lpre = block_excl_scan<RS_WARPS>(tsum, wsum, ttot);
-#pragma unroll
-  for (int q = 0; q < RS_DPT; ++q) {
-    const int d = tid * RS_DPT + q;
-    if (d < NB) {
-#pragma unroll
-      for (int w = 0; w < RS_WARPS; ++w) whist[w][d] = (unsigned short)(whist[w][d] + lpre);
-      counts0[(size_t)d * ld + tile] = tc[q];
-    }
-    lpre += tc[q];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) {
-    if (valid(j)) {
-      const unsigned pos = p0 + rank[j] + whist[warp][dg[j]];
-      keys[pos] = skey[elem(j)];
-      vals[pos] = sval[elem(j)];
-    }
-  }
-}
 
 #ifndef K2_MIN_CTAS
 #define K2_MIN_CTAS (1024 / RS_THREADS)
 #endif
-template <int PRESORT>
 __global__ void __launch_bounds__(RS_THREADS, K2_MIN_CTAS)
 k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre, long long n, Count cno,
              unsigned dx, unsigned dxy, PassPlan plan, const int2* __restrict__ bounds, unsigned* __restrict__ keys, unsigned* __restrict__ vals,
@@ -2000,25 +1620,6 @@ k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pr
   expand_tile<RS_THREADS, RS_ITEMS>(rec, n, p0, pend, dx, dxy, tile_pre, bounds, sm.slot, sm.warpmax, &sm.oc, key, own);
   const unsigned pbase = p0 + (unsigned)tid * RS_ITEMS;
   const int nvalid = pend > pbase ? (int)min((unsigned)RS_ITEMS, pend - pbase) : 0;
-  if (PRESORT > 0 && kPresortFits) {
-    // the tile in element (generation) order: keys in the dead slots, values in the cache
-    unsigned* skey = reinterpret_cast<unsigned*>(sm.slot);
-    unsigned* ocw = reinterpret_cast<unsigned*>(&sm.oc);  // the whole object cache as words
-    unsigned* sval = ocw;
-    auto* whist = reinterpret_cast<unsigned short(*)[kMaxBins]>(ocw + RS_TILE);
-    unsigned* wsum = ocw + RS_TILE + RS_WARPS * kMaxBins / 2;
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < RS_ITEMS / 4; ++q) {
-      reinterpret_cast<uint4*>(skey)[tid * (RS_ITEMS / 4) + q] =
-          make_uint4(key[4 * q], key[4 * q + 1], key[4 * q + 2], key[4 * q + 3]);
-      reinterpret_cast<uint4*>(sval)[tid * (RS_ITEMS / 4) + q] =
-          make_uint4(own[4 * q], own[4 * q + 1], own[4 * q + 2], own[4 * q + 3]);
-    }
-    __syncthreads();
-    presort_tile<PRESORT>(skey, sval, whist, wsum, p0, pend - p0, plan.shift[0], keys, vals, counts0, ld, blockIdx.x);
-    return;
-  }
   // transpose through shared memory (the expansion's slots and object cache are dead): a
   // thread's 16 consecutive pairs leave as 16-byte chunks striped over the CTA, so every
   // warp store is 512 contiguous bytes; chunk index c is XOR-swizzled against bank conflicts
@@ -2072,6 +1673,10 @@ k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pr
 }
 
 
+#ifndef PGRID_FUSED_DISPATCH
+#define PGRID_FUSED_DISPATCH 0  // expansion + slab dispatch in one kernel: measured slower, not shipped
+#endif
+#if PGRID_FUSED_DISPATCH
 // ----------------------------------------------------------------------------------------
 // Sharded build, fused dispatch: pair expansion + slab partition + peer stores in ONE kernel.
 // Each CTA claims the next 4096-pair tile from a ticket, expands it exactly as K2 does, ranks
@@ -2225,77 +1830,7 @@ k_coarse_big(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pr
     if (hsh[b]) atomicAdd(&coarse[b], hsh[b]);
 }
 
-// First radix pass over tiles that K2 already sorted by the pass's digit (k_pairs_emit<BITS>):
-// every digit run of a tile moves as a block to digit_start + tile_prefix; no ranking.
-template <int BITS>
-__global__ void __launch_bounds__(RS_THREADS, 6)
-k_scatter_presorted(const unsigned* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
-                    unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, Count cno, int shift,
-                    const unsigned* __restrict__ hist, const unsigned* __restrict__ offs, unsigned ld) {
-  constexpr int NB = 1 << BITS;
-  constexpr unsigned DMASK = (unsigned)NB - 1u;
-  __shared__ unsigned short dgt[RS_TILE];
-  __shared__ __align__(16) unsigned vst[RS_TILE];
-  __shared__ unsigned gbase[kMaxBins];
-  __shared__ unsigned wsum[RS_WARPS];
-  const unsigned no = cno.get();
-  const unsigned tile = blockIdx.x;
-  const unsigned tbase = tile * (unsigned)RS_TILE;
-  if (tbase >= no) return;
-  const unsigned tvalid = min((unsigned)RS_TILE, no - tbase);
-  const int tid = threadIdx.x;
-  for (unsigned e = tid; e < tvalid; e += RS_THREADS) cp_async4(&vst[e], vals_in + tbase + e);
-  cp_async_commit();
-  unsigned k[RS_ITEMS];
-#pragma unroll
-  for (int r = 0; r < RS_ITEMS; ++r) {
-    const unsigned e = tid + r * RS_THREADS;
-    k[r] = e < tvalid ? __ldg(keys_in + tbase + e) : 0u;
-    dgt[e] = (unsigned short)((k[r] >> shift) & DMASK);
-  }
-  // digit starts: exclusive prefix of the global histogram
-  unsigned hs[RS_DPT], hsum = 0;
-#pragma unroll
-  for (int q = 0; q < RS_DPT; ++q) {
-    const int d = tid * RS_DPT + q;
-    hs[q] = d < NB ? __ldg(&hist[d]) : 0u;
-    hsum += hs[q];
-  }
-  unsigned htot;
-  unsigned hpre = block_excl_scan<RS_WARPS>(hsum, wsum, htot);  // (its barriers also publish dgt)
-  unsigned hp[RS_DPT];
-#pragma unroll
-  for (int q = 0; q < RS_DPT; ++q) {
-    hp[q] = hpre;
-    hpre += hs[q];
-  }
-  // run starts: gbase[d] = global position of the tile's first d-item, minus its tile index
-#pragma unroll
-  for (int q = 0; q < RS_DPT; ++q) {
-    const int d = tid * RS_DPT + q;
-    if (d < NB) gbase[d] = hp[q];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < RS_ITEMS; ++r) {
-    const unsigned e = tid + r * RS_THREADS;
-    if (e < tvalid) {
-      const unsigned d = dgt[e];
-      if (e == 0 || dgt[e - 1] != d) gbase[d] = gbase[d] + __ldg(&offs[(size_t)d * ld + tile]) - e;
-    }
-  }
-  cp_async_wait();
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < RS_ITEMS; ++r) {
-    const unsigned e = tid + r * RS_THREADS;
-    if (e < tvalid) {
-      const unsigned g = gbase[(k[r] >> shift) & DMASK] + e;
-      keys_out[g] = k[r];
-      vals_out[g] = vst[e];
-    }
-  }
-}
+#endif  // PGRID_FUSED_DISPATCH
 
 // ----------------------------------------------------------------------------------------
 // K4: G from the sorted cell ids (RLE -> NonEmptyCells scatter -> ExclusiveSum, fused)

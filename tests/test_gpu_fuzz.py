@@ -140,7 +140,9 @@ def test_fuzz_sharded_emulated(block):
         if want is None or isinstance(want, str) or len(mesh.triangles) < 2:
             continue
         world = int(rng.integers(1, 9))
-        for mode in ("p2p", "fused"):
+        from paper_2403_10647_b200 import _native
+        fused = ("fused",) if _native.features() & _native.PG_FEATURE_FUSED_DISPATCH else ()
+        for mode in ("copy", "p2p") + fused:
             G, O = D.run_emulated(D.CudaOps, mesh.vertices, mesh.triangles, spec, world, exchange=mode)
             assert np.array_equal(G, want[0]) and np.array_equal(O, want[1]), (block, mode, world, spec)
         done += 1

@@ -83,7 +83,7 @@ g, _ = builders.build_compact(mesh, spec)
 check("build_compact", g.G, g.O, mesh, spec)
 
 # sharded orchestration, 4 emulated ranks on this device
-for exchange in ("copy", "p2p", "fused"):
+for exchange in ("copy", "p2p") + (("fused",) if _native.features() & _native.PG_FEATURE_FUSED_DISPATCH else ()):
     G, O = D.run_emulated(D.CudaOps, mesh.vertices, mesh.triangles, spec, 4, exchange=exchange)
     check(f"sharded x4 {exchange}", G, O, mesh, spec)
 torch.cuda.synchronize()
