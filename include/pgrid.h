@@ -246,6 +246,10 @@ int pg_slab_plan(const uint32_t *hists, int nranks, int nbuckets, int bucket_shi
 
 /* Wait for the device work (and PG_HOST_OUTPUT copies) of the last pg_finish on b. */
 int pg_wait(pg_builder *b);
+/* The reference's six phase times (BuildReport.phase_ms, builders.py:46-54: count, scan,
+ * pairgen, sort, rle, finalize; device milliseconds) of the last pg_count + pg_finish on b,
+ * e.g. after a PG_ASYNC finish and pg_wait (waits for it if needed). */
+int pg_phase_times(pg_builder *b, float *phase_ms);
 
 /* Profiling aid: with PGRID_KTIMES=1 in the environment, every launch of the calling thread's
  * last pg_count + pg_finish is bracketed by events; this writes "kernel microseconds" lines

@@ -38,7 +38,7 @@ NPHASES = 6
 EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
            "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_finish_baseline",
            "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_partition_counts", "pg_partition_send", "pg_peer_put", "pg_slab_plan", "pg_count_result",
-           "pg_peer_put_count", "pg_coarse_hist", "pg_pairs_send", "pg_count_stats", "pg_features",
+           "pg_peer_put_count", "pg_coarse_hist", "pg_pairs_send", "pg_count_stats", "pg_features", "pg_phase_times",
            "pg_build_async",
            "pg_build_wait", "pg_host_register",
            "pg_host_unregister", "pg_host_alloc", "pg_host_free", "pg_last_launch_count",
@@ -122,6 +122,8 @@ def load():
         lib.pg_host_free.argtypes = [vp]
         lib.pg_last_launch_count.argtypes = [vp]
         lib.pg_last_error.restype = ctypes.c_char_p
+        lib.pg_phase_times.argtypes = [vp, ctypes.POINTER(ctypes.c_float)]
+        lib.pg_phase_times.restype = ctypes.c_int
         lib.pg_features.argtypes = []
         lib.pg_features.restype = ctypes.c_int
         for name in ("pg_builder_create", "pg_count", "pg_finish", "pg_stage",
@@ -232,6 +234,12 @@ class Builder:
     def wait(self):
         """Wait for the last finish (PG_ASYNC) including its host-output copies."""
         check(self._lib.pg_wait(self._h))
+
+    def phase_times(self):
+        """The six reference phases (device ms) of the last count + finish on this builder."""
+        out = (ctypes.c_float * NPHASES)()
+        check(self._lib.pg_phase_times(self._h, out))
+        return list(out)
 
     def finish_baseline(self, algo, G, O, flags=0, stream=None):
         """algo 1 = sorted grid, 2 = compact grid (builders.py:172-231); returns (phases, max_task_work)."""

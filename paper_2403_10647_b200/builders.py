@@ -269,8 +269,10 @@ class BuildPipeline:
                 return build_parallel(mesh, spec, device=self.device)
             O = O[:no]
         self._learn(no)
-        ms = {p: 0.0 for p in PHASES}
-        ms["count"] = count_ms
+        # all six phases (builders.py:46-54): the device times of this build's kernels (its
+        # events), the host time of the submit (copy enqueue + count) added to "count"
+        ms = dict(zip(PHASES, (float(x) for x in b.phase_times())))
+        ms["count"] += count_ms
         report = BuildReport("parallel", no=no, max_task_work=PAIRGEN_OPS_PER_PAIR if no else 0,
                              total_work=PAIRGEN_OPS_PER_PAIR * no, phase_ms=ms)
         return CompactGrid(spec, G, O), report

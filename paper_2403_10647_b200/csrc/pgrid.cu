@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys / ncu --nvtx
+
 #include "../../include/pgrid.h"
 #include "pgrid_kernels.cuh"
 #include "pgrid_dda.cuh"
@@ -24,6 +26,12 @@ using namespace pgrid;
 namespace {
 
 thread_local std::string g_err;
+
+// One NVTX range per C-ABI call (the host side of a build in a timeline profile).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // PGRID_PDL: 0 launches the build's kernel chain without programmatic dependent launch, 1 uses
 // it for every link, 2 only for the glue kernels (scans, bounds), 3 only for the bulk passes.
@@ -292,6 +300,7 @@ struct pg_builder {
   bool inv_fix = false;
   DevBuf inv;
   int64_t stats[6] = {};  // PG_STATS: raw statistics of the last count (pg_count_stats)
+  bool phases_ready = false;  // ev[0..4] bracket the phases of the last pg_finish
   // G / O of the last pg_build_async (pg_build_wait's host-counted rebuild)
   uint32_t* g_G = nullptr;
   uint32_t* g_O = nullptr;
@@ -567,6 +576,7 @@ void drop_graph(pg_builder* b) {
 
 int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64_t n, const pg_spec* spec,
              uint32_t flags, void* stream_, uint64_t* no_out) {
+  NvtxRange nvtx_("pg_count");
   if (!b || !spec || !no_out) return fail(PG_INVARIANT_ERROR, "null argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   CU(cudaSetDevice(b->device));
@@ -701,6 +711,8 @@ int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned
 
 }  // namespace
 
+int phase_times(pg_builder* b, float* phase_ms);
+
 // Pair expansion -> radix passes -> G for the last counted mesh. `cno` carries the pair
 // count (host value, or device pointer for the sync-free build); every buffer and grid is
 // sized for `no` = its capacity bound.
@@ -813,26 +825,33 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
     if (no) CU(cudaMemcpyAsync(O, dO, no * 4, cudaMemcpyDeviceToHost, st));
   }
   CU(cudaEventRecord(b->ev[4], st));
+  b->phases_ready = true;
   if (phase_ms || ((flags & PG_HOST_OUTPUT) && !(flags & PG_ASYNC))) CU(cudaEventSynchronize(b->ev[4]));
-  if (phase_ms) {
-    float t01 = 0, t12 = 0, t23 = 0, t34 = 0;
-    CU(cudaEventElapsedTime(&t01, b->ev[0], b->ev[1]));
-    CU(cudaEventElapsedTime(&t12, b->ev[1], b->ev[2]));
-    CU(cudaEventElapsedTime(&t23, b->ev[2], b->ev[3]));
-    CU(cudaEventElapsedTime(&t34, b->ev[3], b->ev[4]));
-    float t_k1 = 0.f;
-    if (b->k1_timed) CU(cudaEventElapsedTime(&t_k1, b->ev[5], b->ev[6]));
-    phase_ms[0] = t_k1;  // count: K1 device time (callers add their H2D / readback around it)
-    phase_ms[1] = 0.f;  // scan: fused into count (K1)
-    phase_ms[2] = t01;  // pairgen: tile bounds + K2 (+ first-pass tile counts)
-    phase_ms[3] = t12;  // sort: onesweep passes
-    phase_ms[4] = 0.f;  // rle: fused into finalize (K4)
-    phase_ms[5] = t23 + t34;  // finalize: K4 (+ D2H of G/O for host outputs)
-  }
+  if (phase_ms) return phase_times(b, phase_ms);
+  return PG_OK;
+}
+
+// The reference's six phases (builders.py:46-54) from the events of the last pg_count +
+// pg_finish (their work must have completed).
+int phase_times(pg_builder* b, float* phase_ms) {
+  float t01 = 0, t12 = 0, t23 = 0, t34 = 0;
+  CU(cudaEventElapsedTime(&t01, b->ev[0], b->ev[1]));
+  CU(cudaEventElapsedTime(&t12, b->ev[1], b->ev[2]));
+  CU(cudaEventElapsedTime(&t23, b->ev[2], b->ev[3]));
+  CU(cudaEventElapsedTime(&t34, b->ev[3], b->ev[4]));
+  float t_k1 = 0.f;
+  if (b->k1_timed) CU(cudaEventElapsedTime(&t_k1, b->ev[5], b->ev[6]));
+  phase_ms[0] = t_k1;  // count: K1 device time (callers add their H2D / readback around it)
+  phase_ms[1] = 0.f;  // scan: fused into count (K1)
+  phase_ms[2] = t01;  // pairgen: tile bounds + K2 (+ first-pass tile counts)
+  phase_ms[3] = t12;  // sort: the radix passes
+  phase_ms[4] = 0.f;  // rle: fused into finalize (K4)
+  phase_ms[5] = t23 + t34;  // finalize: K4 (+ D2H of G/O for host outputs)
   return PG_OK;
 }
 
 int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* stream_, float* phase_ms) {
+  NvtxRange nvtx_("pg_finish");
   if (!b || !b->counted) return fail(PG_STATE_ERROR, "pg_finish without a successful pg_count");
   CU(cudaSetDevice(b->device));
   drop_graph(b);
@@ -852,6 +871,7 @@ int pg_finish(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, void* str
 // exceeded o_capacity (G/O are then invalid: grow O and rebuild).
 int pg_build_async(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64_t n, const pg_spec* spec,
                    uint32_t* G, uint32_t* O, uint64_t o_capacity, void* stream_) {
+  NvtxRange nvtx_("pg_build_async");
   if (!b || !spec || !G) return fail(PG_INVARIANT_ERROR, "null argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   CU(cudaSetDevice(b->device));
@@ -916,6 +936,7 @@ int pg_build_async(pg_builder* b, const double* V, int64_t nv, const int32_t* T,
 }
 
 int pg_build_wait(pg_builder* b, uint64_t* no_out) {
+  NvtxRange nvtx_("pg_build_wait");
   if (!b || !b->gst) return fail(PG_STATE_ERROR, "no asynchronous build in flight");
   CU(cudaSetDevice(b->device));
   CU(cudaStreamSynchronize(b->gst));
@@ -940,6 +961,7 @@ int pg_build_wait(pg_builder* b, uint64_t* no_out) {
 // (per-cell counters, scan, slot claims, per-cell canonical sort). Same G/O as pg_finish.
 int pg_finish_baseline(pg_builder* b, int algo, uint32_t* G, uint32_t* O, uint32_t flags, void* stream_,
                        float* phase_ms, uint64_t* max_task_work) {
+  NvtxRange nvtx_("pg_finish_baseline");
   if (!b || !b->counted) return fail(PG_STATE_ERROR, "pg_finish_baseline without a successful pg_count");
   if (b->deferred) return fail(PG_STATE_ERROR, "pg_finish_baseline after a PG_DEFER count");
   if (algo != 1 && algo != 2) return fail(PG_INVARIANT_ERROR, "algo must be 1 (sorted) or 2 (compact)");
@@ -1085,6 +1107,7 @@ int pg_finish_baseline(pg_builder* b, int algo, uint32_t* G, uint32_t* O, uint32
 }
 
 int pg_stage(pg_builder* b, int stage, void* dst, uint32_t flags, void* stream_) {
+  NvtxRange nvtx_("pg_stage");
   if (!b || !b->counted) return fail(PG_STATE_ERROR, "no build to read stages from");
   if (b->deferred) return fail(PG_STATE_ERROR, "pg_stage after a PG_DEFER count");
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
@@ -1119,6 +1142,7 @@ int pg_stage(pg_builder* b, int stage, void* dst, uint32_t flags, void* stream_)
 
 int pg_radix_sort_pairs(pg_builder* b, const uint32_t* keys, const uint32_t* vals, uint32_t* keys_out,
                         uint32_t* vals_out, int64_t n, int key_bits, uint32_t flags, void* stream_) {
+  NvtxRange nvtx_("pg_radix_sort_pairs");
   if (!b) return fail(PG_INVARIANT_ERROR, "null builder");
   if (key_bits < 0 || key_bits > 32) return fail(PG_INVARIANT_ERROR, "key_bits must be in [0, 32]");
   if (n < 0) return fail(PG_INVARIANT_ERROR, "negative length");
@@ -1172,6 +1196,7 @@ int pg_radix_sort_pairs(pg_builder* b, const uint32_t* keys, const uint32_t* val
 // ---------------------------------------------------------------------------------------
 int pg_pairs(pg_builder* b, uint32_t* keys, uint32_t* vals, uint32_t val_offset, int coarse_shift, int coarse_bins,
              uint32_t* coarse_hist, void* stream_) {
+  NvtxRange nvtx_("pg_pairs");
   if (!b || !b->counted) return fail(PG_STATE_ERROR, "pg_pairs without a successful pg_count");
   if (coarse_hist && (coarse_bins < 1 || coarse_bins > 3 * OC_CAP))
     return fail(PG_INVARIANT_ERROR, "coarse_bins must be in [1, %d]", 3 * OC_CAP);
@@ -1206,6 +1231,7 @@ int pg_pairs(pg_builder* b, uint32_t* keys, uint32_t* vals, uint32_t val_offset,
 int pg_partition(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int64_t n, const uint32_t* slab_of_bucket,
                  int bucket_shift, int nslabs, const uint32_t* slab_base, uint32_t* keys_out, uint32_t* vals_out,
                  uint32_t* slab_counts, void* stream_) {
+  NvtxRange nvtx_("pg_partition");
   if (!b) return fail(PG_INVARIANT_ERROR, "null builder");
   if (nslabs < 1 || nslabs > 16) return fail(PG_INVARIANT_ERROR, "nslabs must be in [1, 16]");
   if (n < 0 || n > kMaxScan) return fail(PG_SIZE_ERROR, "partition of %lld pairs exceeds the size limit", (long long)n);
@@ -1239,6 +1265,7 @@ int pg_partition(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int6
 
 int pg_sort_cells(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int64_t n, int64_t ncells, uint32_t* G,
                   uint32_t* O, void* stream_) {
+  NvtxRange nvtx_("pg_sort_cells");
   if (!b) return fail(PG_INVARIANT_ERROR, "null builder");
   if (ncells < 1 || ncells > kMaxScan) return fail(PG_SIZE_ERROR, "ncells out of range");
   if (n < 0 || n > kMaxScan) return fail(PG_SIZE_ERROR, "sort of %lld pairs exceeds the size limit", (long long)n);
@@ -1322,6 +1349,7 @@ int pg_dda_prepare(pg_builder* b, const double* V, int64_t nv, const int32_t* T,
 int pg_dda_cast(pg_builder* b, const uint32_t* G, const uint32_t* O, int64_t no, const pg_spec* spec,
                 const double* origins, const double* dirs, const double* t_max, int64_t nrays, int64_t* ids,
                 double* ts, uint32_t flags, void* stream_) {
+  NvtxRange nvtx_("pg_dda_cast");
   if (!b || !spec) return fail(PG_INVARIANT_ERROR, "null argument");
   if (b->dda_ntri < 0) return fail(PG_STATE_ERROR, "pg_dda_cast before a successful pg_dda_prepare");
   if (nrays < 0 || no < 0) return fail(PG_INVARIANT_ERROR, "negative size");
@@ -1397,6 +1425,7 @@ int pg_dda_cast(pg_builder* b, const uint32_t* G, const uint32_t* O, int64_t no,
 }
 
 int pg_grid_stats(pg_builder* b, const uint32_t* G, uint32_t flags, void* stream_, uint64_t* out) {
+  NvtxRange nvtx_("pg_grid_stats");
   if (!b || !out) return fail(PG_INVARIANT_ERROR, "null argument");
   if (!b->counted) return fail(PG_STATE_ERROR, "pg_grid_stats before pg_count");
   if (b->deferred) return fail(PG_STATE_ERROR, "pg_grid_stats after a PG_DEFER count");
@@ -1437,6 +1466,7 @@ int pg_grid_stats(pg_builder* b, const uint32_t* G, uint32_t flags, void* stream
 
 int pg_mesh_bounds(pg_builder* b, const double* V, int64_t nv, uint32_t flags, void* stream_, double* lo,
                    double* hi) {
+  NvtxRange nvtx_("pg_mesh_bounds");
   if (!b || !lo || !hi) return fail(PG_INVARIANT_ERROR, "null argument");
   if (nv <= 0) return fail(PG_INVARIANT_ERROR, "cannot bound an empty mesh");
   if (!V) return fail(PG_INVARIANT_ERROR, "null vertex array");
@@ -1483,6 +1513,14 @@ int pg_wait(pg_builder* b) {
   return PG_OK;
 }
 
+int pg_phase_times(pg_builder* b, float* phase_ms) {
+  if (!b || !phase_ms) return fail(PG_INVARIANT_ERROR, "null argument");
+  if (!b->phases_ready) return fail(PG_STATE_ERROR, "pg_phase_times without a pg_finish");
+  CU(cudaSetDevice(b->device));
+  CU(cudaEventSynchronize(b->ev[4]));
+  return phase_times(b, phase_ms);
+}
+
 int pg_kernel_timing(int on) {
   g_ktimes = on ? 1 : 0;
   return PG_OK;
@@ -1506,6 +1544,7 @@ int pg_kernel_times(char* buf, int len) {
 }
 
 int pg_load_obj(pg_builder* b, const uint8_t* bytes, uint64_t nbytes, uint32_t flags, void* stream_, int64_t* out) {
+  NvtxRange nvtx_("pg_load_obj");
   if (!b || !out) return fail(PG_INVARIANT_ERROR, "null argument");
   if (nbytes && !bytes) return fail(PG_INVARIANT_ERROR, "null byte buffer");
   if (nbytes >= (1ull << 32)) return fail(PG_SIZE_ERROR, "OBJ input of %llu bytes exceeds 4 GiB", (unsigned long long)nbytes);
@@ -1627,6 +1666,7 @@ int pg_obj_fetch(pg_builder* b, double* V, int32_t* T, uint32_t flags, void* str
 
 int pg_partition_counts(pg_builder* b, const uint32_t* keys, int64_t n, const uint32_t* slab_of_bucket,
                         int bucket_shift, int nslabs, uint32_t* slab_counts, void* stream_) {
+  NvtxRange nvtx_("pg_partition_counts");
   if (!b) return fail(PG_INVARIANT_ERROR, "null builder");
   if (nslabs < 1 || nslabs > 16) return fail(PG_INVARIANT_ERROR, "nslabs must be in [1, 16]");
   if (n < 0 || n > kMaxScan) return fail(PG_SIZE_ERROR, "partition of %lld pairs exceeds the size limit", (long long)n);
@@ -1663,6 +1703,7 @@ int pg_partition_counts(pg_builder* b, const uint32_t* keys, int64_t n, const ui
 int pg_partition_send(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int64_t n,
                       const uint32_t* slab_of_bucket, int bucket_shift, int nslabs, const uint32_t* slab_base,
                       const uint64_t* dst_keys, const uint64_t* dst_vals, const uint64_t* dst_offset, void* stream_) {
+  NvtxRange nvtx_("pg_partition_send");
   if (!b || !dst_keys || !dst_vals || !dst_offset) return fail(PG_INVARIANT_ERROR, "null argument");
   if (b->part_n != n) return fail(PG_STATE_ERROR, "pg_partition_send without pg_partition_counts on these pairs");
   if (nslabs < 1 || nslabs > 16) return fail(PG_INVARIANT_ERROR, "nslabs must be in [1, 16]");

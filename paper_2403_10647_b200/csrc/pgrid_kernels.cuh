@@ -25,6 +25,18 @@
 
 namespace pgrid {
 
+// Checked builds (-DPGRID_CHECKED=1, `make checked`): every computed shared / global index of
+// the hot kernels is bounds-checked on the device and a violation traps, so the launch fails
+// and the caller sees a CUDA error. The GPU test suite runs against this build as well
+// (tools/checked_tests.sh) in place of compute-sanitizer, which this GPU pool does not allow.
+#ifndef PGRID_CHECKED
+#define PGRID_CHECKED 0
+#endif
+#define PG_ASSERT(c)                   \
+  do {                                 \
+    if (PGRID_CHECKED && !(c)) __trap(); \
+  } while (0)
+
 // ----------------------------------------------------------------------------------------
 // common helpers
 // ----------------------------------------------------------------------------------------
@@ -341,6 +353,7 @@ k_inverted_pairs(const double* __restrict__ V, const int* __restrict__ T, DevSpe
       }
       if (keys) {
         const unsigned p = off + (unsigned)rel;
+        PG_ASSERT(rel < cnt && (unsigned long long)off + (unsigned long long)rel < (1ull << 32));
         if (coarse) {
           atomicSub(&coarse[keys[p] >> coarse_shift], 1u);
           atomicAdd(&coarse[(unsigned)c >> coarse_shift], 1u);
@@ -627,6 +640,7 @@ __device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long 
     warpmax[2 * (THREADS / 32)] = (int)(__ldg(&tile_pre[olo / K1_TILE]) + r0.w);  // olo's absolute offset
   }
   auto start = [&](long long o, const uint4& r, unsigned tp) {
+    PG_ASSERT(tp + r.w >= p0 && tp + r.w - p0 < (unsigned)TILE);
     atomicMax(&slot[slot_at(tp + r.w - p0)], (int)o);  // zero-count triangles share the next start; max wins
     const long long ci = o - olo;
     if (ci < OC_CAP) {
@@ -1092,7 +1106,10 @@ k_tile_counts(const unsigned* __restrict__ keys, Count cno, DigitFn dig, int nbi
   } else {
     for (int i = tid; i < nbins * TC_TILES; i += RS_THREADS) {
       const int b = i / TC_TILES, q = i % TC_TILES;
-      if (t0 + q < ntiles) counts[(size_t)b * ld + t0 + q] = h[q][b];
+      if (t0 + q < ntiles) {
+        PG_ASSERT(t0 + q < ld);
+        counts[(size_t)b * ld + t0 + q] = h[q][b];
+      }
     }
   }
 }
@@ -1400,6 +1417,7 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
   for (int j = 0; j < RS_ITEMS; ++j) {
     if (valid(j)) {
       rank[j] += sm.whist[warp][dg[j]];  // rank -> tile position
+      PG_ASSERT(rank[j] < tvalid);
       sm.buf[rank[j]] = ksrc[elem(j)];
     }
   }
@@ -1414,6 +1432,7 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
       const unsigned k = sm.buf[i];
       const unsigned d = digit(k);
       gpos[r] = sm.gbase[d] + i;
+      PG_ASSERT(P2P || gpos[r] < htot);
       if (P2P) {
         dpk[r / 8] |= d << (4 * (r % 8));
         p2p->k[d][gpos[r]] = k - __ldg(&kbase[d]);
@@ -1873,7 +1892,10 @@ k_cell_offsets(const unsigned* __restrict__ sorted, Count cno, unsigned ncells, 
       const unsigned i = base + j * G_THREADS + tid;
       const unsigned up = __shfl_up_sync(0xffffffffu, k[j], 1);
       const unsigned prev = lane == 0 ? pk[j] : up;
-      if (i < i1 && (i == 0 || prev != k[j])) mark[k[j] - c0] = i;
+      if (i < i1 && (i == 0 || prev != k[j])) {
+        PG_ASSERT(k[j] >= c0 && k[j] < c1);
+        mark[k[j] - c0] = i;
+      }
     }
   }
   __syncthreads();

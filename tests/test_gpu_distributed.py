@@ -241,6 +241,7 @@ def test_emulated_fused_dispatch_cfg2_hash(hashes):
     assert len(O) == h["no"] and sha(G) == h["G_sha256"] and sha(O) == h["O_sha256"]
 
 
+@needs_fused
 @pytest.mark.parametrize("scene,n,dims", [("walls", 20000, None), ("skewed", 20000, (50, 40, 30)),
                                           ("lognormal", 50000, None), ("uniform", 30000, (4096, 2, 3)),
                                           ("walls", 5000, (1, 1, 7)), ("uniform", 30000, (97, 1, 1))])
@@ -259,7 +260,7 @@ def test_coarse_hist_from_boxes_matches_pairs(scene, n, dims):
     assert np.array_equal(h1, ops.to_numpy(h2)) and int(h1.sum()) == no
 
 
-@pytest.mark.parametrize("mode", ["copy", "p2p", "fused"])
+@pytest.mark.parametrize("mode", ["copy", "p2p", pytest.param("fused", marks=needs_fused)])
 def test_emulated_more_ranks_than_triangles(mode):
     """Empty shards (N < P) on the device paths: the device NO of an empty count is 0."""
     for n in (1, 3, 7):
