@@ -649,6 +649,28 @@ def main():
     e2e_sec = (time.perf_counter() - t0) / e2e_steps
     e2e_parity &= hashlib.sha256(g.G.tobytes()).hexdigest() == hashlib.sha256(grid.G.tobytes()).hexdigest()
     e2e_parity &= hashlib.sha256(g.O.tobytes()).hexdigest() == hashlib.sha256(grid.O.tobytes()).hexdigest()
+    # a soup's index array (T[i][k] = 3i + k, checked exactly by the C ABI) is not transferred
+    soup = bool(n >= (1 << 16) and nv >= 3 * n and
+                np.array_equal(Th.reshape(-1), np.arange(3 * n, dtype=np.int32)))
+    h2d_bytes = int(Vh.nbytes + (0 if soup else Th.nbytes))
+    # the single call's copy bound: the same bytes moved alone (pinned H2D of V, T; D2H of
+    # G, O), serialised as a build must (outputs exist only after the inputs)
+    dbuf = torch.empty(Vh.nbytes + Th.nbytes, dtype=torch.uint8, device=dev)
+    gh = _native.pinned_pool.empty(ncells + 1, np.uint32)
+    oh = _native.pinned_pool.empty(no, np.uint32)
+    cb = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dbuf[:Vh.nbytes].copy_(torch.from_numpy(Vh.view(np.uint8).reshape(-1)), non_blocking=True)
+        dbuf[Vh.nbytes:].copy_(torch.from_numpy(Th.view(np.uint8).reshape(-1)), non_blocking=True)
+        torch.from_numpy(gh.view(np.uint8)).copy_(dbuf[:gh.nbytes], non_blocking=True)
+        torch.from_numpy(oh.view(np.uint8)).copy_(dbuf[gh.nbytes:gh.nbytes + oh.nbytes], non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        cb.append(e0.elapsed_time(e1))
+    copy_bound_ms = statistics.median(cb)
+    del dbuf, gh, oh
     _native.host_unregister(Vh)
     _native.host_unregister(Th)
     # the drop-in call as a reference caller makes it: plain (pageable) numpy arrays, one
@@ -706,12 +728,15 @@ def main():
                     for k, v in kern.items()},
         "glue_us_per_build": glue,
         "e2e": {"value": round(1.0 / e2e_sec * world, 3), "unit": "builds/s",
-                "h2d_bytes_per_step": int(Vh.nbytes + Th.nbytes),
+                "h2d_bytes_per_step": h2d_bytes,
+                "h2d_note": ("V only: T is the implicit soup 0, 1, 2, ... (checked on the host, regenerated by K1)"
+                             if soup else "V and T"),
                 "d2h_bytes_per_step": int(grid.G.nbytes + 4 * max(pipe.capacity or 0, len(grid.O))),
                 "ms_per_step": round(e2e_sec * 1e3, 2),
                 "api": "builders.BuildPipeline (2 slots, no host round trip per build: build i+1's H2D follows build i's at once; O read back at the pipeline's pair capacity)",
                 "parity": "bit-exact vs build_parallel" if e2e_parity else "MISMATCH",
                 "sequential_build_parallel_ms": round(statistics.median(seq_t) * 1e3, 2),
+                "single_call_copy_bound_ms": round(copy_bound_ms, 2),
                 "pageable_build_parallel": {
                     "ms_per_step": round(statistics.median(page_t) * 1e3, 2),
                     "builds_per_s": round(1.0 / statistics.median(page_t), 3),

@@ -7,6 +7,11 @@
 
 #include <algorithm>
 #include <climits>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -32,6 +37,113 @@ struct NvtxRange {
   explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
   ~NvtxRange() { nvtxRangePop(); }
 };
+
+// Persistent host threads for parallel memcpy (the pageable-input staging path): one copy
+// call splits [src, src + n) into equal parts, the caller copies part 0, the workers the
+// rest. A single memcpy thread moves ~10 GB/s; the PCIe link takes ~55 GB/s.
+class HostCopyPool {
+ public:
+  static HostCopyPool& get() {
+    static HostCopyPool* pool = new HostCopyPool();  // never destroyed: its threads live on
+    return *pool;
+  }
+  void copy(void* dst, const void* src, size_t n) {
+    char* d = static_cast<char*>(dst);
+    const char* s = static_cast<const char*>(src);
+    run(n, [d, s](size_t off, size_t len) { memcpy(d + off, s + off, len); });
+  }
+  // fn(offset, length) over equal parts of [0, n) (64-byte multiples), in parallel
+  void run(size_t n, std::function<void(size_t, size_t)> fn) {
+    std::lock_guard<std::mutex> one(call_m_);  // one job at a time (builders on many threads)
+    const int parts = (int)std::min<size_t>(workers_.size() + 1, std::max<size_t>(1, n >> 20));
+    if (parts <= 1) {
+      if (n) fn(0, n);
+      return;
+    }
+    const size_t per = (n / parts + 63) & ~size_t(63);
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      fn_ = std::move(fn);
+      n_ = n;
+      per_ = per;
+      parts_ = parts;
+      pending_ = parts - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn_(0, std::min(per, n));
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+  }
+
+ private:
+  HostCopyPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int nw = (int)std::min(15u, hw > 1 ? hw - 1 : 0u);
+    for (int i = 0; i < nw; ++i) workers_.emplace_back([this, i] { loop(i + 1); });
+    for (auto& t : workers_) t.detach();  // live for the process
+  }
+  void loop(int part) {
+    uint64_t seen = 0;
+    for (;;) {
+      size_t off, len;
+      std::function<void(size_t, size_t)>* fn;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (part >= parts_) continue;
+        off = per_ * (size_t)part;
+        len = off < n_ ? std::min(per_, n_ - off) : 0;
+        fn = &fn_;
+      }
+      if (len) (*fn)(off, len);
+      {
+        std::lock_guard<std::mutex> lk(m_);
+        if (--pending_ == 0) done_.notify_one();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex call_m_, m_;
+  std::condition_variable cv_, done_;
+  std::function<void(size_t, size_t)> fn_;
+  size_t n_ = 0, per_ = 0;
+  int parts_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+};
+
+// A triangle soup's index array is T[i][k] = 3i + k, i.e. the flat array is 0, 1, 2, ...
+// (gen_scene and unshared-vertex exports; geometry.py:206-207). It carries no information,
+// so a host mesh whose T is exactly that is not copied: K1 regenerates the indices. Checked
+// exactly, in parallel on the host pool.
+bool is_soup_indices(const int32_t* T, int64_t n, int64_t nv) {
+  if (n < (1 << 16) || nv < 3 * n) return false;
+  std::atomic<bool> ok{true};
+  HostCopyPool::get().run((size_t)n * 3 * sizeof(int32_t), [&](size_t off, size_t len) {
+    const int32_t* t = T + off / 4;
+    const int32_t base = (int32_t)(off / 4);
+    const size_t m = len / 4;
+    bool good = true;
+    for (size_t j = 0; j < m && good; j += 4096) {
+      const size_t e = std::min(m, j + 4096);
+      int32_t bad = 0;
+      for (size_t q = j; q < e; ++q) bad |= t[q] ^ (base + (int32_t)q);
+      good = bad == 0 && ok.load(std::memory_order_relaxed);
+    }
+    if (!good) ok.store(false, std::memory_order_relaxed);
+  });
+  return ok.load();
+}
+
+bool is_pageable(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
 
 // PGRID_PDL: 0 launches the build's kernel chain without programmatic dependent launch, 1 uses
 // it for every link, 2 only for the glue kernels (scans, bounds), 3 only for the bulk passes.
@@ -257,6 +369,13 @@ struct pg_builder {
   unsigned long long* h_scalars = nullptr;  // pinned: [0] NO, [1] error flags
   // inputs staged on device for PG_HOST_INPUT
   DevBuf in_v, in_t;
+  // pageable host inputs: a ring of page-locked staging chunks, filled by the host copy pool
+  // while the previous chunks' DMA runs (stage_ev[i] = chunk i's copy done)
+  static constexpr int kStageBufs = 4;
+  static constexpr size_t kStageBytes = 16u << 20;
+  unsigned char* stage_h[kStageBufs] = {};
+  cudaEvent_t stage_ev[kStageBufs] = {};
+  int stage_next = 0;
   // K1 outputs / scratch
   DevBuf rec, k1_sync;
   // pair buffers and sort scratch
@@ -343,6 +462,10 @@ void pg_builder_destroy(pg_builder* b) {
   for (auto& e : b->ev)
     if (e) cudaEventDestroy(e);
   if (b->h_scalars) cudaFreeHost(b->h_scalars);
+  for (int i = 0; i < pg_builder::kStageBufs; ++i) {
+    if (b->stage_ev[i]) cudaEventSynchronize(b->stage_ev[i]), cudaEventDestroy(b->stage_ev[i]);
+    if (b->stage_h[i]) cudaFreeHost(b->stage_h[i]);
+  }
   if (b->gexec) cudaGraphExecDestroy(b->gexec);
   if (b->g_in) cudaEventDestroy(b->g_in);
   if (b->g_out) cudaEventDestroy(b->g_out);
@@ -383,6 +506,36 @@ int pg_last_launch_count(pg_builder* b) { return b ? b->launches : 0; }
 namespace {
 
 // Validation + builder state for a build of (n triangles, spec); fills the device spec.
+// Host -> device copy of caller memory. Page-locked sources go straight to the DMA engine.
+// Pageable ones (a plain numpy array, the reference caller's case) would make the driver stage
+// them at a few GB/s; instead the host copy pool fills a ring of page-locked 16 MB chunks in
+// parallel while the previous chunks are in flight, so host copy and PCIe transfer overlap.
+int h2d(pg_builder* b, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (!bytes) return PG_OK;
+  if (!is_pageable(src) || bytes <= (1u << 20)) {
+    CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    return PG_OK;
+  }
+  for (int i = 0; i < pg_builder::kStageBufs; ++i) {
+    if (!b->stage_h[i]) {
+      CU(cudaHostAlloc(reinterpret_cast<void**>(&b->stage_h[i]), pg_builder::kStageBytes, cudaHostAllocDefault));
+      CU(cudaEventCreateWithFlags(&b->stage_ev[i], cudaEventDisableTiming));
+      CU(cudaEventRecord(b->stage_ev[i], st));
+    }
+  }
+  HostCopyPool& pool = HostCopyPool::get();
+  for (size_t off = 0; off < bytes; off += pg_builder::kStageBytes) {
+    const size_t len = std::min(pg_builder::kStageBytes, bytes - off);
+    const int k = b->stage_next;
+    b->stage_next = (k + 1) % pg_builder::kStageBufs;
+    CU(cudaEventSynchronize(b->stage_ev[k]));  // that chunk's previous DMA has landed
+    pool.copy(b->stage_h[k], static_cast<const char*>(src) + off, len);
+    CU(cudaMemcpyAsync(static_cast<char*>(dst) + off, b->stage_h[k], len, cudaMemcpyHostToDevice, st));
+    CU(cudaEventRecord(b->stage_ev[k], st));
+  }
+  return PG_OK;
+}
+
 // late_ncells: the host-counted path reports ncells > 2^30 after the count checks, where the
 // reference does (its G scan, builders.py:130, runs last); the device-count paths check it here.
 int count_setup(pg_builder* b, int64_t nv, int64_t n, const pg_spec* spec, DevSpec& ds, bool late_ncells = false) {
@@ -463,8 +616,21 @@ struct InvStats {
   unsigned long long kept, inverted, negative, zero, positive;
   bool cells_ok;
 };
+// K1 ran on an implicit soup (no index array on the device): write it out for the paths
+// that gather through T
+int materialize_T(pg_builder* b, cudaStream_t st) {
+  if (b->last_T) return PG_OK;
+  int rc;
+  if ((rc = b->in_t.ensure((size_t)b->n * 3 * sizeof(int32_t)))) return rc;
+  k_soup_indices<<<1184, 256, 0, st>>>(b->in_t.as<int>(), 3 * b->n);
+  CU(cudaGetLastError());
+  b->last_T = b->in_t.as<int32_t>();
+  return PG_OK;
+}
+
 int resolve_inverted(pg_builder* b, InvStats& r) {
   int rc;
+  if ((rc = materialize_T(b, nullptr))) return rc;
   const size_t head = 256;
   if ((rc = b->inv.ensure(head + (size_t)std::max<int64_t>(b->n, 1) * 4))) return rc;
   unsigned long long* out = b->inv.as<unsigned long long>(16);
@@ -606,11 +772,15 @@ int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64
   const int32_t* dT = T;
   if (flags & PG_HOST_INPUT) {
     if ((rc = b->in_v.ensure((size_t)nv * 3 * sizeof(double)))) return rc;
-    if ((rc = b->in_t.ensure((size_t)n * 3 * sizeof(int32_t)))) return rc;
-    CU(cudaMemcpyAsync(b->in_v.p, V, (size_t)nv * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(b->in_t.p, T, (size_t)n * 3 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    if (is_soup_indices(T, n, nv)) {
+      dT = nullptr;  // the implicit soup: 12 bytes per triangle not transferred
+    } else {
+      if ((rc = b->in_t.ensure((size_t)n * 3 * sizeof(int32_t)))) return rc;
+      if ((rc = h2d(b, b->in_t.p, T, (size_t)n * 3 * sizeof(int32_t), st))) return rc;
+      dT = b->in_t.as<int32_t>();
+    }
+    if ((rc = h2d(b, b->in_v.p, V, (size_t)nv * 3 * sizeof(double), st))) return rc;
     dV = b->in_v.as<double>();
-    dT = b->in_t.as<int32_t>();
   }
   if ((rc = count_enqueue(b, dV, nv, dT, n, ds, st))) return rc;
   if (flags & PG_DEFER) {

@@ -314,6 +314,12 @@ __device__ __forceinline__ unsigned tri_offset(const uint4* __restrict__ rec, co
   return __ldg(&tile_pre[o / K1_TILE]) + __ldg(&rec[o].w);
 }
 
+// the index array of an implicit soup (T[i][k] = 3i + k), for the rare paths that read T
+__global__ void k_soup_indices(int* __restrict__ T, long long count) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x)
+    T[i] = (int)i;
+}
+
 // numpy's `//` on int64 (floor division), as _make_cell_ids uses it (builders.py:111-112)
 __device__ __forceinline__ long long floordiv_i64(long long a, long long b) {
   const long long q = a / b;
@@ -382,18 +388,21 @@ k_boxes_count(const double* __restrict__ V, long long nv, const int* __restrict_
   const bool full = tcount == K1_TILE;
   // speculative soup staging is in range only if the tile's vertex rows exist
   const bool spec_v = bulk_ok && full && 3 * (tbase + K1_TILE) <= nv;
+  // T == nullptr: an implicit soup (the host found T[i][k] == 3i + k and did not copy it)
   if (bulk_ok && full) {
     if (tid == 0) {
       mbar_init(&sm.bar, 1);
-      const unsigned tb = K1_TILE * 3 * sizeof(int), vb = spec_v ? K1_TILE * 9 * sizeof(double) : 0u;
+      const unsigned tb = T ? K1_TILE * 3 * sizeof(int) : 0u, vb = spec_v ? K1_TILE * 9 * sizeof(double) : 0u;
       mbar_expect_tx(&sm.bar, tb + vb);
-      bulk_g2s(sm.t, T + 3 * tbase, tb, &sm.bar);
+      if (T) bulk_g2s(sm.t, T + 3 * tbase, tb, &sm.bar);
       if (spec_v) bulk_g2s(sm.v, V + 9 * tbase, vb, &sm.bar);
     }
+    if (!T)
+      for (int q = tid; q < 3 * tcount; q += K1_THREADS) sm.t[q] = (int)(3 * tbase + q);
     __syncthreads();  // barrier initialised before anyone waits on it
     mbar_wait(&sm.bar, 0);
   } else {
-    for (int q = tid; q < 3 * tcount; q += K1_THREADS) sm.t[q] = __ldg(T + 3 * tbase + q);
+    for (int q = tid; q < 3 * tcount; q += K1_THREADS) sm.t[q] = T ? __ldg(T + 3 * tbase + q) : (int)(3 * tbase + q);
     __syncthreads();
   }
   // soup test over the whole tile (index 3*i+k == 3*(tbase+i)+k) and index validation

@@ -369,3 +369,29 @@ def test_no_above_2_32_on_device_count_paths():
         pipe.result()
     again, _ = pipe.result()
     assert grids_equal(want, again)
+
+
+def test_host_input_soup_and_near_soup():
+    """Host meshes whose index array is exactly the soup 0, 1, 2, ... skip its transfer (K1
+    regenerates it); a single different index must take the copied path. Pageable and
+    page-locked inputs, against the oracle."""
+    mesh = gen_scene("lognormal", 300_000, 5)
+    spec = spec_for_mesh(mesh)
+    V = np.ascontiguousarray(mesh.vertices).copy()
+    T = np.ascontiguousarray(mesh.triangles).copy()
+    G, O = oracle.build_parallel(V, T, spec)
+    grid, _ = builders.build_parallel(TriangleMesh(V, T), spec)          # pageable, implicit soup
+    assert np.array_equal(grid.G, G) and np.array_equal(grid.O, O)
+    T2 = T.copy()
+    T2[123_457, 1], T2[200_001, 2] = T2[200_001, 2], T2[123_457, 1]      # not a soup any more
+    G2, O2 = oracle.build_parallel(V, T2, spec)
+    grid, _ = builders.build_parallel(TriangleMesh(V, T2), spec)
+    assert np.array_equal(grid.G, G2) and np.array_equal(grid.O, O2)
+    _native.host_register(V)
+    _native.host_register(T)
+    try:                                                                  # page-locked inputs
+        grid, _ = builders.build_parallel(TriangleMesh(V, T), spec)
+        assert np.array_equal(grid.G, G) and np.array_equal(grid.O, O)
+    finally:
+        _native.host_unregister(V)
+        _native.host_unregister(T)

@@ -67,19 +67,27 @@ torch.cuda.empty_cache()
 
 states = []
 for r in range(P):
+    # every rank holds only its shard, as a local soup (vertex rows 3lo..3hi, indices from 0),
+    # as bench.py's ranks generate it (scenes.gen_shard)
     lo, hi = D.shard_range(n, r, P)
-    states.append(D.ShardState(D.CudaOps(), Vd, Td[lo:hi], lo, spec, r, P))
+    Tr = (Td[lo:hi] - 3 * lo).contiguous()
+    states.append(D.ShardState(D.CudaOps(), Vd[3 * lo:3 * hi], Tr, lo, spec, r, P))
 ex = D.EmulatedExchange(torch, torch.device("cuda", 0), P)
 rows = []
-for rep in range(a.reps):
+cap = None
+for rep in range(a.reps + 1):
+    # rep 0: host-checked counts (the verdict; learns the pair capacity); then deferred counts
+    # (PG_DEFER: no host round trip inside K1), as the steady-state sharded build runs them
     t = {r: {} for r in range(P)}
     hists, stats = [], []
     for r, s in enumerate(states):
-        st_r, t[r]["k1"] = timed(lambda: s.phase_count_only())
+        st_r, t[r]["k1"] = timed(lambda: s.phase_count_only(cap))
         stats.append(st_r)
         h, t[r]["k2_hist"] = timed(lambda: s.phase_pairs())
         hists.append(h)
-    D.count_verdict(np.sum(stats, axis=0), states[0].ncells)
+    if cap is None:
+        D.count_verdict(np.sum(stats, axis=0), states[0].ncells)
+        cap = int(max(s.no for s in states) * 1.25) + 4096
     hist = np.sum([s.ops.to_numpy(h).astype(np.int64) for s, h in zip(states, hists)], axis=0)
     plan = D.plan_slabs(hist, states[0].ncells, P)
     counts = []
@@ -94,7 +102,8 @@ for rep in range(a.reps):
         nrecv[r], t[r]["partition_send"] = timed(lambda: s.phase_send(matrix, dk, dv))
     for r, s in enumerate(states):
         _, t[r]["slab_sort_k4"] = timed(lambda: s.phase_sort(*ex.received(r, nrecv[r])))
-    rows.append(t)
+    if rep:
+        rows.append(t)
 
 med = {r: {k: float(np.median([rows[i][r][k] for i in range(a.reps)])) for k in rows[0][r]} for r in range(P)}
 send_bytes = [int(8 * (matrix[r].sum() - matrix[r][r])) for r in range(P)]
