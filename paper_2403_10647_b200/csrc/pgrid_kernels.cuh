@@ -1864,7 +1864,11 @@ k_coarse_big(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pr
 // K4: G from the sorted cell ids (RLE -> NonEmptyCells scatter -> ExclusiveSum, fused)
 // ----------------------------------------------------------------------------------------
 constexpr int G_THREADS = 256;
+#ifndef G_ITEMS_OVERRIDE
 constexpr int G_ITEMS = 16;
+#else
+constexpr int G_ITEMS = G_ITEMS_OVERRIDE;
+#endif
 constexpr int G_TILE = G_THREADS * G_ITEMS;  // cells per CTA
 
 // G[c] = #pairs with cell < c = lower_bound(sorted, c). Each CTA owns cells [c0, c0+G_TILE):
