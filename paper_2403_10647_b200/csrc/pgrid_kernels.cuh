@@ -144,6 +144,13 @@ __device__ __forceinline__ double floor_quot(double x, double c, double rc) {
 __device__ __forceinline__ unsigned clip_axis(long long v, int dim) {
   return v < 0 ? 0u : (v > (long long)(dim - 1) ? (unsigned)(dim - 1) : (unsigned)v);
 }
+// clip_axis(np_floor_i64(f), dim) for an already floored f (floor_quot's result), without the
+// 64-bit integer detour: NaN and |f| >= 2^63 cast to INT64_MIN on x86 and clip to 0, a negative
+// f clips to 0, the rest to min(f, dim - 1) -- all exact in f64 (f is integral). K1 is issue-
+// bound next to its HBM stream, so the six per-triangle conversions are kept short.
+__device__ __forceinline__ unsigned cell_of(double f, double dmax) {
+  return (f >= 0.0 && f < 9223372036854775808.0) ? (unsigned)fmin(f, dmax) : 0u;
+}
 
 // Warp-cooperative 32-ary lower_bound: smallest i in [0, n] with load(i) >= x (load(n) = +inf).
 // 5 rounds of 32 parallel probes cover 2^25 elements; each round is one L2/HBM latency.
@@ -240,8 +247,9 @@ __device__ __forceinline__ void tri_box_raw(const double* a, const double* b, co
     const double mx = fmax(fmax(x0, x1), x2);
     keep &= !nan && (mx >= s.lo[k]) && (mn <= s.hi[k]);
     // one IEEE subtract, one IEEE divide, floor (gridcore.py:161-162)
-    lo[k] = clip_axis(np_floor_i64(floor_quot(__dsub_rn(mn, s.lo[k]), s.cell[k], s.rcell[k])), s.dims[k]);
-    hi[k] = clip_axis(np_floor_i64(floor_quot(__dsub_rn(mx, s.lo[k]), s.cell[k], s.rcell[k])), s.dims[k]);
+    const double dmax = (double)(s.dims[k] - 1);
+    lo[k] = cell_of(floor_quot(__dsub_rn(mn, s.lo[k]), s.cell[k], s.rcell[k]), dmax);
+    hi[k] = cell_of(floor_quot(__dsub_rn(mx, s.lo[k]), s.cell[k], s.rcell[k]), dmax);
   }
 }
 
