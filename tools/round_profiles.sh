@@ -10,5 +10,5 @@ CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1"
 $CMD > gpurun_out/${R}_plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches.csv $CMD > gpurun_out/${R}_ncu_launch.log 2>&1
 python tools/prof_build.py --builds 1 > gpurun_out/${R}_plain2.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"k_" -s 14 -c 14 -o gpurun_out/${R}_full python tools/prof_build.py --builds 1 > gpurun_out/${R}_ncu_full.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:"k_" -s ${NK:-14} -c ${NK:-14} -o gpurun_out/${R}_full python tools/prof_build.py --builds 1 > gpurun_out/${R}_ncu_full.log 2>&1
 echo done
