@@ -12,6 +12,8 @@
 #include <functional>
 #include <mutex>
 #include <thread>
+
+#include <unistd.h>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -55,7 +57,9 @@ class HostCopyPool {
   // fn(offset, length) over equal parts of [0, n) (64-byte multiples), in parallel
   void run(size_t n, std::function<void(size_t, size_t)> fn) {
     std::lock_guard<std::mutex> one(call_m_);  // one job at a time (builders on many threads)
-    const int parts = (int)std::min<size_t>(workers_.size() + 1, std::max<size_t>(1, n >> 20));
+    // a forked child inherits this object but not the worker threads: work alone there
+    const size_t nw = getpid() == pid_ ? workers_.size() : 0;
+    const int parts = (int)std::min<size_t>(nw + 1, std::max<size_t>(1, n >> 20));
     if (parts <= 1) {
       if (n) fn(0, n);
       return;
@@ -77,7 +81,7 @@ class HostCopyPool {
   }
 
  private:
-  HostCopyPool() {
+  HostCopyPool() : pid_(getpid()) {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     const int nw = (int)std::min(15u, hw > 1 ? hw - 1 : 0u);
     for (int i = 0; i < nw; ++i) workers_.emplace_back([this, i] { loop(i + 1); });
@@ -104,6 +108,7 @@ class HostCopyPool {
       }
     }
   }
+  const pid_t pid_;
   std::vector<std::thread> workers_;
   std::mutex call_m_, m_;
   std::condition_variable cv_, done_;
