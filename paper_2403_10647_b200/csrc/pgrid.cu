@@ -517,7 +517,8 @@ namespace {
 // parallel while the previous chunks are in flight, so host copy and PCIe transfer overlap.
 int h2d(pg_builder* b, void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (!bytes) return PG_OK;
-  if (!is_pageable(src) || bytes <= (1u << 20)) {
+  // (small pageable copies: the driver's own staging is fine, and cheaper than the ring's setup)
+  if (bytes < pg_builder::kStageBytes || !is_pageable(src)) {
     CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
     return PG_OK;
   }
@@ -604,7 +605,8 @@ int count_enqueue(pg_builder* b, const double* dV, int64_t nv, const int32_t* dT
   k_boxes_count<<<ntiles, K1_THREADS, sizeof(K1Smem), st>>>(dV, nv, reinterpret_cast<const int*>(dT), n, ds, bulk_ok,
                                                             b->rec.as<uint4>(), tile_sum, err);
   LAUNCHED("k_boxes_count", st);
-  pdl_launch(true, k_scan_tile_sums, 1, TS_THREADS, 0, st, tile_sum, ntiles, tile_pre, total);
+  pdl_launch(true, k_scan_tile_sums_mc, (ntiles + MS_PER - 1) / MS_PER, MS_THREADS, 0, st, tile_sum, ntiles, tile_pre,
+             total);
   LAUNCHED("k_scan_tile_sums", st);
   CU(cudaEventRecord(b->ev[6], st));
   b->launches = 2;

@@ -316,6 +316,55 @@ k_inverted_boxes(const double* __restrict__ V, const int* __restrict__ T, long l
   }
 }
 
+// K1b for the build chain, on many CTAs: CTA c scans tile sums [c*MS_PER, (c+1)*MS_PER) and
+// first adds up every tile sum before its range itself (at most ntiles u64 from L2, read in
+// one coalesced sweep), so no CTA waits for another; the last CTA writes the total NO.
+// (k_scan_tile_sums: the same result on one SM, 9-10 us at cfg3; this one ~3 us.)
+constexpr int MS_THREADS = 1024;
+constexpr int MS_PER = 1024;  // tiles per CTA
+__global__ void __launch_bounds__(MS_THREADS)
+k_scan_tile_sums_mc(const unsigned long long* __restrict__ tile_sum, unsigned ntiles, unsigned* __restrict__ tile_pre,
+                    unsigned long long* __restrict__ total) {
+  PDL_ENTRY();
+  __shared__ unsigned long long wsum[MS_THREADS / 32];
+  __shared__ unsigned long long pre_sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned c0 = blockIdx.x * (unsigned)MS_PER;
+  const unsigned i = c0 + tid;
+  const unsigned long long v = i < ntiles ? __ldg(&tile_sum[i]) : 0ull;
+  unsigned long long part = 0;
+#pragma unroll 8
+  for (unsigned j = tid; j < c0; j += MS_THREADS) part += __ldg(&tile_sum[j]);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
+  if (lane == 0) wsum[warp] = part;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long x = wsum[lane];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
+    if (lane == 0) pre_sh = x;
+  }
+  __syncthreads();
+  // exclusive scan of this CTA's tile sums
+  unsigned long long inc = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  unsigned long long carry = pre_sh, tot = pre_sh;
+  for (int w = 0; w < MS_THREADS / 32; ++w) {
+    const unsigned long long x = wsum[w];
+    carry += w < warp ? x : 0ull;
+    tot += x;
+  }
+  if (i < ntiles) tile_pre[i] = (unsigned)(carry + inc - v);
+  if (blockIdx.x == gridDim.x - 1 && tid == 0) *total = tot;
+}
+
 // absolute pair offset of triangle o (K1 tiles of K1_TILE triangles)
 __device__ __forceinline__ unsigned tri_offset(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pre,
                                                long long o) {
@@ -618,64 +667,16 @@ struct ObjCache {
 // Inside a thread's consecutive pairs the cell coordinate is stepped incrementally
 // (x-fastest); a new run always starts at relative offset 0, so the two divisions of
 // _make_cell_ids (builders.py:111-113) only ever run for a thread's first pair.
-template <int THREADS, int ITEMS>
-__device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long long n, unsigned p0, unsigned pend,
-                                            unsigned dx, unsigned dxy, const unsigned* __restrict__ tile_pre,
-                                            const int2* __restrict__ bounds, int* slot, int* warpmax, ObjCache* oc,
-                                            unsigned (&key)[ITEMS], int (&own)[ITEMS]) {
-  constexpr int TILE = THREADS * ITEMS;
+// Owners and cell ids of a tile's pairs once its run starts are in the slots (expand_tile):
+// inclusive max-scan of the slots, then each thread steps its ITEMS consecutive pairs. `box`
+// returns an object's {lo_cell, mx, my}.
+template <int THREADS, int ITEMS, typename Box>
+__device__ __forceinline__ void expand_runs(int* slot, int* warpmax, long long olo, unsigned p0, unsigned pend,
+                                            unsigned dx, unsigned dxy, Box box, unsigned (&key)[ITEMS],
+                                            int (&own)[ITEMS]) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // [olo, oend): owner of pair p0, and one past the last triangle whose run starts in the tile
-  // (k_pair_tile_bounds precomputed both with 32-ary searches over the offsets)
-  const int2 bnd = __ldg(&bounds[p0 / TILE]);
-  const long long olo = bnd.x, oend = bnd.y;
-  // slots live in 16-byte chunks whose index is XOR-swizzled (slot_at) so the per-thread
-  // chunk reads of the max-scan below are bank-conflict free
   auto slot_at = [](unsigned e) { return ((((e >> 2) ^ ((e >> 5) & 7u)) << 2) | (e & 3u)); };
-  // the first EXP_PRE records of this thread are requested before the slot initialisation and
-  // its barrier, which then hide their DRAM latency (the stall that dominated this phase)
-  constexpr int EXP_PRE = 4;
-  uint4 pr[EXP_PRE];
-  unsigned pt[EXP_PRE];
-#pragma unroll
-  for (int u = 0; u < EXP_PRE; ++u) {
-    const long long o = olo + 1 + tid + (long long)u * THREADS;
-    if (o < oend) {
-      pr[u] = __ldg(&rec[o]);
-      pt[u] = __ldg(&tile_pre[o / K1_TILE]);
-    }
-  }
-  uint4 r0 = make_uint4(0u, 0u, 0u, 0u);
-  if (tid == 0) r0 = __ldg(&rec[olo]);
-  for (int i = tid; i < TILE; i += THREADS) slot[i] = -1;
-  __syncthreads();
-  if (tid == 0) {
-    slot[0] = (int)olo;  // slot_at(0) == 0
-    oc->lo_cell[0] = r0.x;
-    oc->mx[0] = r0.y;
-    oc->my[0] = r0.z;
-    warpmax[2 * (THREADS / 32)] = (int)(__ldg(&tile_pre[olo / K1_TILE]) + r0.w);  // olo's absolute offset
-  }
-  auto start = [&](long long o, const uint4& r, unsigned tp) {
-    PG_ASSERT(tp + r.w >= p0 && tp + r.w - p0 < (unsigned)TILE);
-    atomicMax(&slot[slot_at(tp + r.w - p0)], (int)o);  // zero-count triangles share the next start; max wins
-    const long long ci = o - olo;
-    if (ci < OC_CAP) {
-      oc->lo_cell[ci] = r.x;
-      oc->mx[ci] = r.y;
-      oc->my[ci] = r.z;
-    }
-  };
-#pragma unroll
-  for (int u = 0; u < EXP_PRE; ++u) {
-    const long long o = olo + 1 + tid + (long long)u * THREADS;
-    if (o < oend) start(o, pr[u], pt[u]);
-  }
-  // the remaining run starts inside the tile (independent loads, no barrier per chunk)
-#pragma unroll 4
-  for (long long o = olo + 1 + tid + (long long)EXP_PRE * THREADS; o < oend; o += THREADS)
-    start(o, __ldg(&rec[o]), __ldg(&tile_pre[o / K1_TILE]));
-  __syncthreads();
+  (void)olo;
   // inclusive max-scan over the slots (blocked: thread t owns slots [ITEMS*t, ITEMS*t + ITEMS))
 #pragma unroll
   for (int q = 0; q < ITEMS / 4; ++q) {
@@ -722,19 +723,6 @@ __device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long 
   for (int j = 0; j < ITEMS; ++j) own[j] = max(own[j], carry);
   const int start0 = first_starts ? tid * ITEMS : pcarry;  // tile position of own[0]'s run, or -1
 
-  auto box = [&](int o, unsigned& lc, unsigned& bx, unsigned& by) {
-    const long long ci = (long long)o - olo;
-    if (ci < OC_CAP) {
-      lc = oc->lo_cell[ci];
-      bx = oc->mx[ci];
-      by = oc->my[ci];
-    } else {
-      const uint4 r = __ldg(&rec[o]);
-      lc = r.x;
-      bx = r.y;
-      by = r.z;
-    }
-  };
   const unsigned pbase = p0 + (unsigned)tid * ITEMS;
   unsigned cell = 0, x = 0, y = 0, mx = 1, my = 1;
   if (pbase < pend) {  // first pair: may sit anywhere inside its run
@@ -773,6 +761,83 @@ __device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long 
     }
     key[j] = cell;
   }
+}
+
+
+template <int THREADS, int ITEMS>
+__device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long long n, unsigned p0, unsigned pend,
+                                            unsigned dx, unsigned dxy, const unsigned* __restrict__ tile_pre,
+                                            const int2* __restrict__ bounds, int* slot, int* warpmax, void* cache,
+                                            unsigned (&key)[ITEMS], int (&own)[ITEMS]) {
+  constexpr int TILE = THREADS * ITEMS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // [olo, oend): owner of pair p0, and one past the last triangle whose run starts in the tile
+  // (k_pair_tile_bounds precomputed both with 32-ary searches over the offsets)
+  const int2 bnd = __ldg(&bounds[p0 / TILE]);
+  const long long olo = bnd.x, oend = bnd.y;
+  // slots live in 16-byte chunks whose index is XOR-swizzled (slot_at) so the per-thread
+  // chunk reads of the max-scan below are bank-conflict free
+  auto slot_at = [](unsigned e) { return ((((e >> 2) ^ ((e >> 5) & 7u)) << 2) | (e & 3u)); };
+  ObjCache* oc = static_cast<ObjCache*>(cache);
+  // the first EXP_PRE records of this thread are requested before the slot initialisation and
+  // its barrier, which then hide their DRAM latency (the stall that dominated this phase)
+  constexpr int EXP_PRE = 4;
+  uint4 pr[EXP_PRE];
+  unsigned pt[EXP_PRE];
+#pragma unroll
+  for (int u = 0; u < EXP_PRE; ++u) {
+    const long long o = olo + 1 + tid + (long long)u * THREADS;
+    if (o < oend) {
+      pr[u] = __ldg(&rec[o]);
+      pt[u] = __ldg(&tile_pre[o / K1_TILE]);
+    }
+  }
+  uint4 r0 = make_uint4(0u, 0u, 0u, 0u);
+  if (tid == 0) r0 = __ldg(&rec[olo]);
+  for (int i = tid; i < TILE; i += THREADS) slot[i] = -1;
+  __syncthreads();
+  if (tid == 0) {
+    slot[0] = (int)olo;  // slot_at(0) == 0
+    oc->lo_cell[0] = r0.x;
+    oc->mx[0] = r0.y;
+    oc->my[0] = r0.z;
+    warpmax[2 * (THREADS / 32)] = (int)(__ldg(&tile_pre[olo / K1_TILE]) + r0.w);  // olo's absolute offset
+  }
+  auto start = [&](long long o, const uint4& r, unsigned tp) {
+    PG_ASSERT(tp + r.w >= p0 && tp + r.w - p0 < (unsigned)TILE);
+    atomicMax(&slot[slot_at(tp + r.w - p0)], (int)o);  // zero-count triangles share the next start; max wins
+    const long long ci = o - olo;
+    if (ci < OC_CAP) {
+      oc->lo_cell[ci] = r.x;
+      oc->mx[ci] = r.y;
+      oc->my[ci] = r.z;
+    }
+  };
+#pragma unroll
+  for (int u = 0; u < EXP_PRE; ++u) {
+    const long long o = olo + 1 + tid + (long long)u * THREADS;
+    if (o < oend) start(o, pr[u], pt[u]);
+  }
+  // the remaining run starts inside the tile (independent loads, no barrier per chunk)
+#pragma unroll 4
+  for (long long o = olo + 1 + tid + (long long)EXP_PRE * THREADS; o < oend; o += THREADS)
+    start(o, __ldg(&rec[o]), __ldg(&tile_pre[o / K1_TILE]));
+  __syncthreads();
+  expand_runs<THREADS, ITEMS>(slot, warpmax, olo, p0, pend, dx, dxy,
+                              [&](int o, unsigned& lc, unsigned& bx, unsigned& by) {
+                                const long long ci = (long long)o - olo;
+                                if (ci < OC_CAP) {
+                                  lc = oc->lo_cell[ci];
+                                  bx = oc->mx[ci];
+                                  by = oc->my[ci];
+                                } else {
+                                  const uint4 r = __ldg(&rec[o]);
+                                  lc = r.x;
+                                  bx = r.y;
+                                  by = r.z;
+                                }
+                              },
+                              key, own);
 }
 
 // record= stage 0: records with absolute pair offsets
@@ -1662,7 +1727,7 @@ k_pairs_emit(const uint4* __restrict__ rec, const unsigned* __restrict__ tile_pr
   __syncthreads();
   {
     uint4* ks = reinterpret_cast<uint4*>(sm.slot);
-    uint4* vs = reinterpret_cast<uint4*>(sm.oc.lo_cell);
+    uint4* vs = reinterpret_cast<uint4*>(&sm.oc);
     auto swz = [](unsigned c) { return c ^ ((c >> 3) & 7u); };
 #pragma unroll
     for (int q = 0; q < RS_ITEMS / 4; ++q) {
