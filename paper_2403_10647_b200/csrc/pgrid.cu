@@ -381,6 +381,11 @@ struct pg_builder {
   unsigned char* stage_h[kStageBufs] = {};
   cudaEvent_t stage_ev[kStageBufs] = {};
   int stage_next = 0;
+  // page-locked V of an implicit soup: copied in chunks on a copy stream, K1 launched per
+  // chunk as it lands (chunk_ev[i] = chunk i copied)
+  static constexpr int kMaxChunks = 32;
+  cudaStream_t cst = nullptr;
+  cudaEvent_t chunk_ev[kMaxChunks] = {};
   // K1 outputs / scratch
   DevBuf rec, k1_sync;
   // pair buffers and sort scratch
@@ -471,6 +476,9 @@ void pg_builder_destroy(pg_builder* b) {
     if (b->stage_ev[i]) cudaEventSynchronize(b->stage_ev[i]), cudaEventDestroy(b->stage_ev[i]);
     if (b->stage_h[i]) cudaFreeHost(b->stage_h[i]);
   }
+  for (auto& e : b->chunk_ev)
+    if (e) cudaEventDestroy(e);
+  if (b->cst) cudaStreamSynchronize(b->cst), cudaStreamDestroy(b->cst);
   if (b->gexec) cudaGraphExecDestroy(b->gexec);
   if (b->g_in) cudaEventDestroy(b->g_in);
   if (b->g_out) cudaEventDestroy(b->g_out);
@@ -580,8 +588,15 @@ int count_setup(pg_builder* b, int64_t nv, int64_t n, const pg_spec* spec, DevSp
 
 // K1 + cross-tile scan on device-resident V/T (n >= 1); NO and the error flags are copied
 // to the pinned b->h_scalars asynchronously (read them after the stream is synchronised).
+// V chunks of an implicit soup copied on b->cst: chunk i holds triangles [ch[i], ch[i + 1])
+// (multiples of K1_TILE) and b->chunk_ev[i] marks its arrival
+struct Chunks {
+  int count = 0;
+  int64_t tri[pg_builder::kMaxChunks + 1];
+};
+
 int count_enqueue(pg_builder* b, const double* dV, int64_t nv, const int32_t* dT, int64_t n, const DevSpec& ds,
-                  cudaStream_t st, bool readback = true) {
+                  cudaStream_t st, bool readback = true, const Chunks* chunks = nullptr) {
   const unsigned ntiles = (unsigned)((n + K1_TILE - 1) / K1_TILE);
   int rc;
   b->last_V = dV;
@@ -602,9 +617,22 @@ int count_enqueue(pg_builder* b, const double* dV, int64_t nv, const int32_t* dT
   CU(cudaEventRecord(b->ev[5], st));
   // TMA bulk staging needs 16-byte aligned sources
   const int bulk_ok = ((reinterpret_cast<uintptr_t>(dV) | reinterpret_cast<uintptr_t>(dT)) & 15) == 0;
-  k_boxes_count<<<ntiles, K1_THREADS, sizeof(K1Smem), st>>>(dV, nv, reinterpret_cast<const int*>(dT), n, ds, bulk_ok,
-                                                            b->rec.as<uint4>(), tile_sum, err);
-  LAUNCHED("k_boxes_count", st);
+  if (chunks) {
+    // K1 on each chunk as soon as its copy has landed (the copy of the next overlaps it)
+    for (int i = 0; i < chunks->count; ++i) {
+      const unsigned t0 = (unsigned)(chunks->tri[i] / K1_TILE);
+      const unsigned t1 = (unsigned)((chunks->tri[i + 1] + K1_TILE - 1) / K1_TILE);
+      CU(cudaStreamWaitEvent(st, b->chunk_ev[i], 0));
+      if (t1 > t0)
+        k_boxes_count<<<t1 - t0, K1_THREADS, sizeof(K1Smem), st>>>(dV, nv, nullptr, n, ds, bulk_ok, b->rec.as<uint4>(),
+                                                                  tile_sum, err, t0);
+      LAUNCHED("k_boxes_count", st);
+    }
+  } else {
+    k_boxes_count<<<ntiles, K1_THREADS, sizeof(K1Smem), st>>>(dV, nv, reinterpret_cast<const int*>(dT), n, ds,
+                                                              bulk_ok, b->rec.as<uint4>(), tile_sum, err);
+    LAUNCHED("k_boxes_count", st);
+  }
   pdl_launch(true, k_scan_tile_sums_mc, (ntiles + MS_PER - 1) / MS_PER, MS_THREADS, 0, st, tile_sum, ntiles, tile_pre,
              total);
   LAUNCHED("k_scan_tile_sums", st);
@@ -777,19 +805,49 @@ int pg_count(pg_builder* b, const double* V, int64_t nv, const int32_t* T, int64
   if (!V || !T) return fail(PG_INVARIANT_ERROR, "null mesh arrays");
   const double* dV = V;
   const int32_t* dT = T;
+  Chunks chunks;
   if (flags & PG_HOST_INPUT) {
-    if ((rc = b->in_v.ensure((size_t)nv * 3 * sizeof(double)))) return rc;
+    // V first: a page-locked V streams over PCIe while the host checks T for the implicit soup
+    const size_t vbytes = (size_t)nv * 3 * sizeof(double);
+    if ((rc = b->in_v.ensure(vbytes))) return rc;
+    const bool chunked = vbytes >= (64u << 20) && !is_pageable(V);
+    if (chunked) {
+      // page-locked V: chunks of ~64 MB (whole K1 tiles of a soup) on the copy stream
+      if (!b->cst) {
+        CU(cudaStreamCreateWithFlags(&b->cst, cudaStreamNonBlocking));
+        for (auto& e : b->chunk_ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
+      CU(cudaEventRecord(b->chunk_ev[0], st));  // the copies follow earlier work on st
+      CU(cudaStreamWaitEvent(b->cst, b->chunk_ev[0], 0));
+      const int64_t per = std::max<int64_t>(K1_TILE, ((int64_t)(64u << 20) / 72 / K1_TILE) * K1_TILE);
+      chunks.count = (int)std::min<int64_t>(pg_builder::kMaxChunks, (n + per - 1) / per);
+      const int64_t step = ((n + chunks.count - 1) / chunks.count + K1_TILE - 1) / K1_TILE * K1_TILE;
+      for (int i = 0; i <= chunks.count; ++i) chunks.tri[i] = std::min<int64_t>(n, (int64_t)i * step);
+      for (int i = 0; i < chunks.count; ++i) {
+        // rows 3 * tri[i] .. 3 * tri[i + 1]; the last chunk also carries rows past 3n
+        const size_t r0 = (size_t)chunks.tri[i] * 3, r1 = i + 1 < chunks.count ? (size_t)chunks.tri[i + 1] * 3 : (size_t)nv;
+        if (r1 > r0)
+          CU(cudaMemcpyAsync(b->in_v.as<double>() + 3 * r0, V + 3 * r0, (r1 - r0) * 24, cudaMemcpyHostToDevice,
+                             b->cst));
+        CU(cudaEventRecord(b->chunk_ev[i], b->cst));
+      }
+    } else if ((rc = h2d(b, b->in_v.p, V, vbytes, st))) {
+      return rc;
+    }
+    dV = b->in_v.as<double>();
     if (is_soup_indices(T, n, nv)) {
       dT = nullptr;  // the implicit soup: 12 bytes per triangle not transferred
     } else {
+      if (chunked) {  // an indexed mesh: K1 needs every vertex row
+        CU(cudaStreamWaitEvent(st, b->chunk_ev[chunks.count - 1], 0));
+        chunks.count = 0;
+      }
       if ((rc = b->in_t.ensure((size_t)n * 3 * sizeof(int32_t)))) return rc;
       if ((rc = h2d(b, b->in_t.p, T, (size_t)n * 3 * sizeof(int32_t), st))) return rc;
       dT = b->in_t.as<int32_t>();
     }
-    if ((rc = h2d(b, b->in_v.p, V, (size_t)nv * 3 * sizeof(double), st))) return rc;
-    dV = b->in_v.as<double>();
   }
-  if ((rc = count_enqueue(b, dV, nv, dT, n, ds, st))) return rc;
+  if ((rc = count_enqueue(b, dV, nv, dT, n, ds, st, true, chunks.count ? &chunks : nullptr))) return rc;
   if (flags & PG_DEFER) {
     // no host round trip: the sharded building blocks run on the device count, bounded by
     // the capacity the caller passed in *no_out; pg_count_result checks it afterwards

@@ -434,12 +434,12 @@ k_inverted_pairs(const double* __restrict__ V, const int* __restrict__ T, DevSpe
 __global__ void __launch_bounds__(K1_THREADS)
 k_boxes_count(const double* __restrict__ V, long long nv, const int* __restrict__ T, long long n, DevSpec s,
               int bulk_ok, uint4* __restrict__ rec, unsigned long long* __restrict__ tile_sum,
-              unsigned* __restrict__ err) {
+              unsigned* __restrict__ err, unsigned tile0 = 0) {
   PDL_ENTRY();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   K1Smem& sm = *reinterpret_cast<K1Smem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned tile = blockIdx.x;
+  const unsigned tile = tile0 + blockIdx.x;  // tile0: launches per copied chunk of an implicit soup
   const long long tbase = (long long)tile * K1_TILE;
   const int tcount = (int)min((long long)K1_TILE, n - tbase);
   const bool full = tcount == K1_TILE;

@@ -395,3 +395,41 @@ def test_host_input_soup_and_near_soup():
     finally:
         _native.host_unregister(V)
         _native.host_unregister(T)
+
+
+def test_pinned_soup_chunked_copy_with_k1_per_chunk(hashes):
+    """A page-locked soup of >= 64 MB of vertices is copied in chunks on a copy stream and K1
+    runs on each chunk as it lands (cfg2: 1M triangles, 72 MB); an indexed variant of the same
+    mesh takes the whole-V path. Golden hash / oracle."""
+    h = hashes["cfg2"]
+    mesh, spec = scene_from_recipe(h["recipe"])
+    V = np.ascontiguousarray(mesh.vertices).copy()
+    T = np.ascontiguousarray(mesh.triangles).copy()
+    assert V.nbytes >= 64 << 20
+    _native.host_register(V)
+    _native.host_register(T)
+    try:
+        for _ in range(2):
+            grid, rep = builders.build_parallel(TriangleMesh(V, T), spec)
+            assert sha(grid.G) == h["G_sha256"] and sha(grid.O) == h["O_sha256"] and rep.no == h["no"]
+        pipe = builders.BuildPipeline(depth=2)
+        for _ in range(3):
+            pipe.submit(TriangleMesh(V, T), spec)
+            if len(pipe) == 2:
+                g, _ = pipe.result()
+                assert sha(g.G) == h["G_sha256"] and sha(g.O) == h["O_sha256"]
+        while len(pipe):
+            g, _ = pipe.result()
+            assert sha(g.G) == h["G_sha256"] and sha(g.O) == h["O_sha256"]
+        T2 = T.copy()
+        T2[0, 0], T2[-1, 2] = T2[-1, 2], T2[0, 0]        # not a soup: K1 waits for every row
+        _native.host_register(T2)
+        try:
+            G2, O2 = oracle.build_parallel(V, T2, spec)
+            grid, _ = builders.build_parallel(TriangleMesh(V, T2), spec)
+            assert np.array_equal(grid.G, G2) and np.array_equal(grid.O, O2)
+        finally:
+            _native.host_unregister(T2)
+    finally:
+        _native.host_unregister(V)
+        _native.host_unregister(T)
