@@ -1130,10 +1130,10 @@ struct DigitFn {
   }
 };
 
-// Upsweep of a radix pass: per-tile digit counts, TC_TILES tiles per CTA so every digit row
-// of the digit-major matrix receives TC_TILES consecutive entries (a full 32-byte sector).
+// Upsweep of a radix pass: per-tile digit counts, TC_TILES tiles per CTA (each digit row of
+// the digit-major matrix receives TC_TILES consecutive entries).
 #ifndef TC_TILES_OVERRIDE
-constexpr int TC_TILES = 4;
+constexpr int TC_TILES = 2;  // 2 tiles per CTA: 48 registers (4: 78, 1: 32); measured best (r2_ab_upsweep_tiles)
 #else
 constexpr int TC_TILES = TC_TILES_OVERRIDE;
 #endif

@@ -1,5 +1,6 @@
 #!/bin/bash
-# compute-sanitizer over every device path of libpgrid (tools/sanitize_drive.py), one tool at
+# compute-sanitizer (CLOSED on this GPU pool: see profiles/r2_compute_sanitizer_closed.txt;
+# tools/checked_tests.sh is the stand-in) over every device path of libpgrid (tools/sanitize_drive.py), one tool at
 # a time, only our kernels checked (mangled names in namespace pgrid). Summaries land in
 # gpurun_out/sanitize_<tool>.log; copy them to profiles/ for the record.
 #   bash tools/sanitize.sh [tools...]      (default: memcheck racecheck synccheck initcheck)
