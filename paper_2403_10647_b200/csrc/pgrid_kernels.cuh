@@ -1541,8 +1541,15 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
 }
 
 
+// 9-bit digits: 3 CTAs/SM with 80 registers (no spill) beat 4 with 64 (127 vs 129 us per
+// pass at cfg3); narrower digits keep 4 (102 vs 104-106 us), r2_ab_k4_rs_occupancy.txt
+#ifndef RS_MIN_CTAS_OVERRIDE
+constexpr int rs_min_ctas(int bits) { return bits >= 9 ? 3 : 4; }
+#else
+constexpr int rs_min_ctas(int) { return RS_MIN_CTAS_OVERRIDE; }
+#endif
 template <int BITS, bool TABLE>
-__global__ void __launch_bounds__(RS_THREADS, RS_MIN_CTAS)
+__global__ void __launch_bounds__(RS_THREADS, rs_min_ctas(BITS))
 k_radix_scatter(const unsigned* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
                 unsigned* __restrict__ keys_out, unsigned* __restrict__ vals_out, Count cno, int shift,
                 const unsigned* __restrict__ hist, const unsigned* __restrict__ offs, unsigned ld,
@@ -1948,7 +1955,10 @@ constexpr int G_TILE = G_THREADS * G_ITEMS;  // cells per CTA
 // its key range [i0, i1) comes from k_key_tile_bounds; every first occurrence of a cell marks
 // its run start; a block suffix-min fills empty cells with the next run start (or i1).
 // The last CTA also writes the sentinel G[ncells] = NO (builders.py:131-133).
-__global__ void __launch_bounds__(G_THREADS)
+#ifndef K4_MIN_CTAS
+#define K4_MIN_CTAS 8  // 32 registers, 8 CTAs/SM: 60.4 vs 64.5 us at cfg3 (r2_ab_k4_rs_occupancy.txt)
+#endif
+__global__ void __launch_bounds__(G_THREADS, K4_MIN_CTAS)
 k_cell_offsets(const unsigned* __restrict__ sorted, Count cno, unsigned ncells, const unsigned* __restrict__ kb,
                unsigned* __restrict__ G) {
   PDL_ENTRY();
