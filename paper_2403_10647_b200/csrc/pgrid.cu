@@ -633,8 +633,13 @@ int count_enqueue(pg_builder* b, const double* dV, int64_t nv, const int32_t* dT
                                                               bulk_ok, b->rec.as<uint4>(), tile_sum, err);
     LAUNCHED("k_boxes_count", st);
   }
-  pdl_launch(true, k_scan_tile_sums_mc, (ntiles + MS_PER - 1) / MS_PER, MS_THREADS, 0, st, tile_sum, ntiles, tile_pre,
-             total);
+  // every CTA of the many-CTA scan re-reads the sums before its range (ntiles^2 / 2048 words
+  // in all): for up to 256K tiles (134M triangles) that is <= 256 MB of L2 reads; beyond, one CTA
+  if (ntiles <= (1u << 18))
+    pdl_launch(true, k_scan_tile_sums_mc, (ntiles + MS_PER - 1) / MS_PER, MS_THREADS, 0, st, tile_sum, ntiles,
+               tile_pre, total);
+  else
+    pdl_launch(true, k_scan_tile_sums, 1, TS_THREADS, 0, st, tile_sum, ntiles, tile_pre, total);
   LAUNCHED("k_scan_tile_sums", st);
   CU(cudaEventRecord(b->ev[6], st));
   b->launches = 2;
