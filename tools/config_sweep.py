@@ -19,10 +19,13 @@ ap.add_argument("--steps", type=int, default=10)
 ap.add_argument("--only", default="")
 a = ap.parse_args()
 hashes = json.load(open(os.path.join(ROOT, "tests", "golden", "hashes.json")))["scenes"]
+big = json.load(open(os.path.join(ROOT, "tests", "golden", "hashes_big.json")))["scenes"]
+hashes.update({{"cfg5": "cfg5_1gpu", "cfg5a": "cfg5a_1gpu"}.get(k, k): v for k, v in big.items()})
 runs = [("cfg1", "uniform", 100_000, 5.0), ("cfg2", "lognormal", 1_000_000, 5.0), ("cfg3", "arch", 10_000_000, 4.0),
         ("cfg3u", "uniform", 10_000_000, 5.0)]
 runs += [(f"cfg4_d{d}", "uniform", 10_000_000, float(d)) for d in (1, 2, 4, 8, 16, 32, 64)]
-runs += [("cfg5_1gpu", "uniform", 100_000_000, 5.0)]   # config 5's scene on one B200
+runs += [("cfg5_1gpu", "uniform", 100_000_000, 5.0),   # config 5's scenes on one B200
+         ("cfg5a_1gpu", "arch", 100_000_000, 4.0)]
 if a.only:
     runs = [r for r in runs if r[0] in a.only.split(",")]
 b = _native.Builder(0)
@@ -32,7 +35,7 @@ for name, kind, n, dens in runs:
     key = (kind, n)
     if key not in cache:
         cache.clear()
-        m = (scenes.gen_uniform_chunked(n, 7) if n > 20_000_000 else
+        m = (scenes.gen_scene_large(kind, n, 7, dens) if n > 20_000_000 else
              scenes.gen_scene(kind, n, 7, dens if kind in ("lognormal", "arch") else 5.0))
         cache[key] = (m, torch.from_numpy(m.vertices.copy()).cuda(), torch.from_numpy(m.triangles.copy()).cuda())
     mesh, Vd, Td = cache[key]
