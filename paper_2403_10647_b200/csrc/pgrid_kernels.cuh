@@ -1350,6 +1350,17 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
   auto elem = [&](int j) { return (unsigned)warp * (RS_ITEMS * 32) + j * 32 + lane; };
   auto valid = [&](int j) { return FULL || elem(j) < tvalid; };
 
+#ifndef PGRID_KEYS_FIRST
+#define PGRID_KEYS_FIRST 1
+#endif
+  // the tile's keys are requested first: the ranking waits on them (the DRAM round trip that
+  // heads the pass's stall profile), everything else below overlaps their flight
+  const unsigned* ksrc = SRC_SMEM ? keys_in : keys_in + tbase;
+  unsigned dg[RS_ITEMS];
+  if (PGRID_KEYS_FIRST && !SRC_SMEM) {
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) dg[j] = valid(j) ? __ldg(ksrc + elem(j)) : 0u;
+  }
   // the per-digit inputs of this tile (L2 hits: digit totals and this tile's column of the
   // scanned count matrix) are copied into shared memory now, so their latency hides behind
   // the ranking without holding registers
@@ -1373,15 +1384,18 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
     }
     cp_async_commit();
   }
-  const unsigned* ksrc = SRC_SMEM ? keys_in : keys_in + tbase;
   {
     unsigned* row = reinterpret_cast<unsigned*>(&sm.whist[warp][0]);
 #pragma unroll
     for (int q = lane; q < NB / 2; q += 32) row[q] = 0u;
   }
-  unsigned dg[RS_ITEMS];
+  if (PGRID_KEYS_FIRST && !SRC_SMEM) {
 #pragma unroll
-  for (int j = 0; j < RS_ITEMS; ++j) dg[j] = valid(j) ? digit(SRC_SMEM ? ksrc[elem(j)] : __ldg(ksrc + elem(j))) : 0u;
+    for (int j = 0; j < RS_ITEMS; ++j) dg[j] = valid(j) ? digit(dg[j]) : 0u;
+  } else {
+#pragma unroll
+    for (int j = 0; j < RS_ITEMS; ++j) dg[j] = valid(j) ? digit(SRC_SMEM ? ksrc[elem(j)] : __ldg(ksrc + elem(j))) : 0u;
+  }
   // peers (same-digit lanes) per item: bit-sliced ballots, items interleaved for ILP
   unsigned pm[RS_ITEMS];
 #pragma unroll

@@ -30,14 +30,14 @@ def random_case(rng):
     if rng.random() < 0.3:                       # poison a few coordinates
         idx = rng.integers(0, len(V), max(1, len(V) // 500))
         V[idx, rng.integers(0, 3, len(idx))] = rng.choice([np.nan, np.inf, -np.inf, 1e300, -1e300], len(idx))
+    lo, hi = np.nanmin(np.where(np.isfinite(V), V, np.nan), 0), np.nanmax(np.where(np.isfinite(V), V, np.nan), 0)
+    lo, hi = np.nan_to_num(lo), np.nan_to_num(hi, nan=1.0)
     if rng.random() < 0.2 and kind != "indexed":  # boxes inverted on two axes (the reference builds them)
         for t in rng.choice(len(T), max(1, len(T) // 1000), replace=False):
             a, b, c = T[t]
             V[b] = V[a]
             V[c] = V[a] + 1e-9
             V[b, rng.choice(3, 2, replace=False)] = rng.choice([np.inf, 1e300])
-    lo, hi = np.nanmin(np.where(np.isfinite(V), V, np.nan), 0), np.nanmax(np.where(np.isfinite(V), V, np.nan), 0)
-    lo, hi = np.nan_to_num(lo), np.nan_to_num(hi, nan=1.0)
     span = np.maximum(hi - lo, 1e-6)
     if rng.random() < 0.4:                       # a sub-box: many triangles dropped or clipped
         a = lo + rng.random(3) * 0.5 * span
@@ -54,8 +54,8 @@ def two_axis_inverted(mesh, spec):
     """Does a kept box invert on exactly two axes (the reference's sorted / compact builders
     leave its pairs uninitialised; the GPU versions raise)?"""
     lo, hi, keep = oracle.cell_boxes(mesh.vertices, mesh.triangles, spec)
-    inv = (hi.astype(np.int64) < lo).sum(axis=1)
-    return bool(np.any(keep & (inv == 2)))
+    e = hi.astype(np.int64) - lo + 1
+    return bool(np.any(keep & (e.prod(axis=1) > 0) & (e < 0).any(axis=1)))
 
 
 def oracle_or_error(mesh, spec):
