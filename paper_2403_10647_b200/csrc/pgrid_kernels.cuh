@@ -1353,6 +1353,13 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
 #ifndef PGRID_KEYS_FIRST
 #define PGRID_KEYS_FIRST 1
 #endif
+#ifndef PGRID_KEYS_REG
+#define PGRID_KEYS_REG 1
+#endif
+  // KREG: the keys stay in registers (digits extracted where used), no re-read for the local
+  // scatter: 8-bit pass 102 -> 96 us (r2_ab_keys_reg.txt; values through registers instead of
+  // the cp.async staging measured slower at every load point)
+  constexpr bool KREG = PGRID_KEYS_REG && PGRID_KEYS_FIRST && !SRC_SMEM && !TABLE;
   // the tile's keys are requested first: the ranking waits on them (the DRAM round trip that
   // heads the pass's stall profile), everything else below overlaps their flight
   const unsigned* ksrc = SRC_SMEM ? keys_in : keys_in + tbase;
@@ -1389,7 +1396,8 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
 #pragma unroll
     for (int q = lane; q < NB / 2; q += 32) row[q] = 0u;
   }
-  if (PGRID_KEYS_FIRST && !SRC_SMEM) {
+  if (KREG) {
+  } else if (PGRID_KEYS_FIRST && !SRC_SMEM) {
 #pragma unroll
     for (int j = 0; j < RS_ITEMS; ++j) dg[j] = valid(j) ? digit(dg[j]) : 0u;
   } else {
@@ -1403,8 +1411,9 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
 #pragma unroll
   for (int b = 0; b < BITS; ++b) {
 #pragma unroll
-    for (int j = 0; j < RS_ITEMS; ++j) pm[j] = peers_step(pm[j], dg[j], 1u << b);
+    for (int j = 0; j < RS_ITEMS; ++j) pm[j] = peers_step(pm[j], dg[j], KREG ? 1u << (b + shift) : 1u << b);
   }
+  auto dig_of = [&](int j) -> unsigned { return KREG ? (dg[j] >> shift) & DMASK : dg[j]; };
   __syncwarp();
   const unsigned lt = lanemask_lt();
   unsigned rank[RS_ITEMS];
@@ -1414,8 +1423,8 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
     const int leader = __ffs(peers | (1u << lane)) - 1;  // invalid lanes: themselves
     unsigned old = 0;
     if (lane == leader && peers) {
-      old = sm.whist[warp][dg[j]];
-      sm.whist[warp][dg[j]] = (unsigned short)(old + __popc(peers));
+      old = sm.whist[warp][dig_of(j)];
+      sm.whist[warp][dig_of(j)] = (unsigned short)(old + __popc(peers));
     }
     old = __shfl_sync(0xffffffffu, old, leader);
     rank[j] = old + __popc(peers & lt);
@@ -1512,9 +1521,9 @@ __device__ __forceinline__ void radix_scatter_tile(RsSmem& sm, const unsigned* _
 #pragma unroll
   for (int j = 0; j < RS_ITEMS; ++j) {
     if (valid(j)) {
-      rank[j] += sm.whist[warp][dg[j]];  // rank -> tile position
+      rank[j] += sm.whist[warp][dig_of(j)];  // rank -> tile position
       PG_ASSERT(rank[j] < tvalid);
-      sm.buf[rank[j]] = ksrc[elem(j)];
+      sm.buf[rank[j]] = KREG ? dg[j] : ksrc[elem(j)];
     }
   }
   __syncthreads();
