@@ -693,11 +693,11 @@ def main():
         return ktime.get(name, {"ms_per_launch": 0.0, "launches": 0, "ms_per_build": 0.0})
     # algorithmic bytes per launch: K1 reads T and V, writes a 16-byte record per
     # triangle; K2 reads the records and writes the (cell, object) pairs; every radix scatter
-    # reads and writes 8 bytes per pair; the last pass with G (k_radix_scatter_g) reads 8 bytes
-    # per pair and writes the 4-byte object id and G; K4 (when the last pass writes keys) reads
-    # the sorted cells and writes G
+    # reads and writes 8 bytes per pair; K4L (k_bucket_sort, the MSD-first finish) reads the
+    # bucket-sorted pairs and writes O and G; K4 (the classic finish, PGRID_LOCAL=0) reads the
+    # sorted cells and writes G
     alg = {"k_boxes_count": 12 * n + 24 * nv + 16 * n, "k_pairs_emit": 16 * n + 8 * no,
-           "k_radix_scatter": 16 * no, "k_radix_scatter_g": 12 * no + 4 * (ncells + 1),
+           "k_radix_scatter": 16 * no, "k_bucket_sort": 12 * no + 4 * (ncells + 1),
            "k_cell_offsets": 4 * no + 4 * (ncells + 1)}
     kern = {k: {"alg_bytes": v} for k, v in alg.items() if k in ktime}
     for k, v in kern.items():

@@ -252,6 +252,41 @@ PassPlan make_plan(int key_bits, int max_digit_bits) {
   return pl;
 }
 
+// The MSD-first finish (k_bucket_sort): PGRID_LOCAL=0 turns it off (classic LSD + K4);
+// PGRID_LOCAL_ITEMS = the mean pairs per bucket the bucket width is chosen for (256: L = 9 at cfg3).
+int local_env(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+bool local_on() {
+  static const bool on = local_env("PGRID_LOCAL", 1) != 0;
+  return on;
+}
+int local_items() {
+  static const int v = std::max(1, local_env("PGRID_LOCAL_ITEMS", 256));
+  return v;
+}
+
+// Passes over the key's top bits [lo, key_bits) only (the MSD-first finish sorts [0, lo))
+PassPlan make_plan_above(int lo, int key_bits, int max_digit_bits) {
+  PassPlan pl = make_plan(key_bits - lo, max_digit_bits);
+  for (int i = 0; i < pl.npasses; ++i) pl.shift[i] += lo;
+  return pl;
+}
+
+// Bucket width L of the MSD-first finish, or -1 for the classic LSD + K4 finish: buckets of
+// 2^L cells hold about local_items() pairs on average (L <= 11: a bucket is one warp's serial
+// work; at least one radix pass above it).
+constexpr int kMinLocalBits = 2, kMaxLocalBits = 10;
+int local_bits(int key_bits, int64_t ncells, uint64_t no, uint32_t flags) {
+  if (!local_on() || (flags & PG_KEEP_STAGES) || key_bits <= kMinLocalBits || no == 0) return -1;
+  int L = kMinLocalBits;
+  while (L < kMaxLocalBits && L + 1 < key_bits &&
+         ((double)no * (double)(1ull << (L + 1)) <= (double)local_items() * ncells))
+    ++L;
+  return L;
+}
+
 int bit_length(uint64_t v) {
   int b = 0;
   while (v >> b) ++b;
@@ -266,6 +301,31 @@ void launch_scatter_bits(unsigned ntiles, cudaStream_t st, const unsigned* kin, 
                          const unsigned* dtable, const unsigned* kbase) {
   pdl_launch(false, k_radix_scatter<BITS, TABLE>, ntiles, RS_THREADS, rs_smem_bytes(), st, kin, vin, ko, vo, n, shift,
              hist, offs, ld, dtable, kbase);
+}
+
+// K4L over cell tiles of 8 buckets of 2^lbits cells (lbits 2..10)
+template <int L>
+int launch_bucket_sort_l(unsigned tiles, cudaStream_t st, const unsigned* keys, const unsigned* vals, Count cno,
+                         unsigned ncells, const unsigned* kb, unsigned* G, unsigned* O) {
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute(k_bucket_sort<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_smem_bytes(L)));
+    CU(cudaFuncSetAttribute(k_bucket_sort<L>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            (int)cudaSharedmemCarveoutMaxShared));
+    attr = true;
+  }
+  pdl_launch(false, k_bucket_sort<L>, tiles, BK_THREADS, bk_smem_bytes(L), st, keys, vals, cno, ncells, kb, G, O);
+  return PG_OK;
+}
+int launch_bucket_sort(int lbits, unsigned tiles, cudaStream_t st, const unsigned* keys, const unsigned* vals,
+                       Count cno, unsigned ncells, const unsigned* kb, unsigned* G, unsigned* O) {
+  switch (lbits) {
+#define PG_BK(l) \
+  case l: return launch_bucket_sort_l<l>(tiles, st, keys, vals, cno, ncells, kb, G, O);
+    PG_BK(2) PG_BK(3) PG_BK(4) PG_BK(5) PG_BK(6) PG_BK(7) PG_BK(8) PG_BK(9) PG_BK(10)
+#undef PG_BK
+    default: return fail(PG_INVARIANT_ERROR, "bucket width 2^%d", lbits);
+  }
 }
 
 // bit-field digits of 1..9 bits, or (dtable != null) slab-table digits of 1..4 bits
@@ -898,13 +958,14 @@ int pg_count_result(pg_builder* b, uint64_t* no_out) {
 namespace {
 
 // LSD passes over (keys0, vals0), ping-ponging with (keys1, vals1); the last pass writes its
-// values straight into vals_final (O). hist (plan.npasses x 512) must already be filled;
+// values straight into vals_final (O; null: into the ping-pong buffer, *sorted_vals_out). hist (plan.npasses x 512) must already be filled;
 // `counts` holds one [digit][tile] matrix (row stride ld), already filled for pass 0 when
 // counts0_ready (K2 emits them).
 int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned* keys0, unsigned* vals0,
                unsigned* keys1, unsigned* vals1, unsigned* vals_final, Count cno, uint64_t cap, unsigned* hist,
                unsigned* counts, cudaStream_t st, const unsigned** sorted_keys_out, unsigned* keys2 = nullptr,
-               unsigned* vals2 = nullptr, const unsigned* packed0 = nullptr) {
+               unsigned* vals2 = nullptr, const unsigned* packed0 = nullptr,
+               const unsigned** sorted_vals_out = nullptr) {
   // grids are sized for `cap` pairs; the kernels read the actual count from `cno`
   const unsigned ntiles = (unsigned)((cap + RS_TILE - 1) / RS_TILE);
   const unsigned ld = (ntiles + 3) & ~3u;
@@ -912,6 +973,7 @@ int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned
   // read-only and passes >= 2 use buffer 2 in its place
   unsigned* kbuf[2] = {keys0, keys1};
   unsigned* vbuf[2] = {vals0, vals1};
+  if (sorted_vals_out) *sorted_vals_out = vals0;
   for (int p = 0; p < plan.npasses; ++p) {
     const bool last = p == plan.npasses - 1;
     if (p == 1 && keys2) {
@@ -921,7 +983,7 @@ int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned
     unsigned* kin = kbuf[p & 1];
     unsigned* vin = vbuf[p & 1];
     unsigned* ko = kbuf[(p + 1) & 1];
-    unsigned* vo = last ? vals_final : vbuf[(p + 1) & 1];
+    unsigned* vo = (last && vals_final) ? vals_final : vbuf[(p + 1) & 1];
     // with a packed region (packed0), every pass's tile counts travel two digits per word
     const bool packed = packed0 != nullptr && plan.bits[p] >= 1;
     if (p > 0 || !counts0_ready) {
@@ -945,6 +1007,7 @@ int run_passes(pg_builder* b, const PassPlan& plan, bool counts0_ready, unsigned
     LAUNCHED("k_radix_scatter", st);
     b->launches += 2;
     *sorted_keys_out = ko;
+    if (sorted_vals_out) *sorted_vals_out = vo;
   }
   return PG_OK;
 }
@@ -959,7 +1022,10 @@ int phase_times(pg_builder* b, float* phase_ms);
 int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStream_t st, float* phase_ms, Count cno,
                 uint64_t no) {
   const int64_t ncells = b->ncells;
-  const PassPlan plan = make_plan(b->key_bits, kMaxDigitBits);
+  // MSD-first finish (lb >= 0): the passes sort by the bucket key >> lb, k_bucket_sort the rest
+  const int lb = local_bits(b->key_bits, ncells, no, flags);
+  const PassPlan plan = lb >= 0 ? make_plan_above(lb, b->key_bits, kMaxDigitBits) : make_plan(b->key_bits, kMaxDigitBits);
+  const unsigned* svals = nullptr;
   int rc;
   unsigned* dG = G;
   unsigned* dO = O;
@@ -984,7 +1050,9 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
   const unsigned g_tiles = (unsigned)((ncells + G_TILE - 1) / G_TILE);
   const size_t hist_bytes = align_up(kMaxPasses * kMaxBins * 4);
   const size_t pb_bytes = align_up((size_t)std::max(rs_tiles, k2_tiles) * 8 + 8);
-  const size_t kb_bytes = align_up((size_t)(g_tiles + 1) * 4);
+  // cell-tile bounds: K4's tiles, or k_bucket_sort's (8 buckets of 2^lb cells)
+  const size_t bk_tiles = lb >= 0 ? (size_t)((ncells + (8 << lb) - 1) / (8 << lb)) : 0;
+  const size_t kb_bytes = align_up((std::max<size_t>(g_tiles, bk_tiles) + 1) * 4);
   if ((rc = b->sort_sync.ensure(hist_bytes + pb_bytes + kb_bytes + (size_t)((rs_tiles + 3) & ~3u) * kMaxBins * 6)))
     return rc;
   unsigned* hist = b->sort_sync.as<unsigned>(0);
@@ -1036,8 +1104,8 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
       // two-axis inverted boxes: their keys are rewritten, so pass 0 recounts its digits
       if ((rc = fix_inverted(b, keysA, st))) return rc;
       CU(cudaEventRecord(b->ev[1], st));
-      if ((rc = run_passes(b, plan, !b->inv_fix, keysA, valsA, keysB, valsB, dO, cno, no, hist, counts, st, &sorted,
-                           nullptr, nullptr, packed0)))
+      if ((rc = run_passes(b, plan, !b->inv_fix, keysA, valsA, keysB, valsB, lb >= 0 ? nullptr : dO, cno, no, hist,
+                           counts, st, &sorted, nullptr, nullptr, packed0, &svals)))
         return rc;
     } else {
       CU(cudaEventRecord(b->ev[1], st));
@@ -1047,17 +1115,28 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
   }
   CU(cudaEventRecord(b->ev[2], st));
   {
-    // narrow K4's bound searches with the last pass's digit totals (when a sort ran)
+    // searches narrowed with the last pass's digit totals (when a sort ran)
     const int lp = plan.npasses - 1;
     const bool top = lp >= 0 && no > 0 && ncells > 1;
-    pdl_launch(true, k_key_tile_bounds, (g_tiles + 1 + 7) / 8, 256, 0, st, sorted, cno, G_TILE, (unsigned)ncells,
-               g_tiles + 1, kbounds, top ? hist + lp * kMaxBins : nullptr, top ? plan.shift[lp] : 0,
-               top ? 1 << plan.bits[lp] : 0);
+    const unsigned* th = top ? hist + lp * kMaxBins : nullptr;
+    const int tsh = top ? plan.shift[lp] : 0, tbins = top ? 1 << plan.bits[lp] : 0;
+    if (lb >= 0) {
+      const unsigned step = 8u << lb, tiles = (unsigned)((ncells + step - 1) / step);
+      pdl_launch(true, k_key_tile_bounds, (tiles + 1 + 7) / 8, 256, 0, st, sorted, cno, step, (unsigned)ncells,
+                 tiles + 1, kbounds, th, tsh, tbins);
+      LAUNCHED("k_key_tile_bounds", st);
+      if ((rc = launch_bucket_sort(lb, tiles, st, sorted, svals, cno, (unsigned)ncells, kbounds, dG, dO))) return rc;
+      LAUNCHED("k_bucket_sort", st);
+      b->launches += 2;
+    } else {
+      pdl_launch(true, k_key_tile_bounds, (g_tiles + 1 + 7) / 8, 256, 0, st, sorted, cno, G_TILE, (unsigned)ncells,
+                 g_tiles + 1, kbounds, th, tsh, tbins);
+      LAUNCHED("k_key_tile_bounds", st);
+      pdl_launch(false, k_cell_offsets, g_tiles, G_THREADS, 0, st, sorted, cno, (unsigned)ncells, kbounds, dG);
+      LAUNCHED("k_cell_offsets", st);
+      b->launches += 2;
+    }
   }
-  LAUNCHED("k_key_tile_bounds", st);
-  pdl_launch(false, k_cell_offsets, g_tiles, G_THREADS, 0, st, sorted, cno, (unsigned)ncells, kbounds, dG);
-  LAUNCHED("k_cell_offsets", st);
-  b->launches += 2;
   b->sorted_keys = sorted;
   CU(cudaEventRecord(b->ev[3], st));
   if (flags & PG_HOST_OUTPUT) {

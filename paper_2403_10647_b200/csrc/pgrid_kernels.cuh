@@ -2073,6 +2073,268 @@ k_cell_offsets(const unsigned* __restrict__ sorted, Count cno, unsigned ncells, 
 }
 
 // ----------------------------------------------------------------------------------------
+// K4L: the last sort level fused with G (the MSD-first finish). The radix passes covered only
+// the key's top bits [L, key_bits), so the pairs arrive sorted by their bucket key >> L
+// (stably: generation order inside a bucket), and a bucket's pairs occupy the same index range
+// in O as in the input. Each CTA owns 8 buckets = 2^(L+3) cells [c0, c0 + 2^(L+3)) and their
+// pairs [i0, i1) (k_key_tile_bounds: the lower bound is exact at bucket boundaries):
+//   1. count its pairs per cell (shared-memory histogram, coalesced key reads),
+//   2. scan the counts: G for its cells (the reference's RLE -> scatter -> ExclusiveSum,
+//      builders.py:126-134); the counts become every cell's next O slot, and the buckets'
+//      pair ranges fall out of the same scan,
+//   3. in rounds of whole buckets (<= BK_CAP pairs; a larger bucket in slices), stage the
+//      round's keys in shared memory, let warp w rank bucket w (stable: 32 pairs at a time,
+//      bit-sliced ballots over the low L bits, the lowest lane of a cell's peers advances its
+//      slot) into shared-memory positions, then move the round's values to O with coalesced
+//      loads. Generation order is kept inside a cell, exactly as the stable LSD pass it
+//      replaces (primitives.py:97-113).
+// This replaces the last radix pass with its upsweep and row scan, the key write-back, and K4.
+// ----------------------------------------------------------------------------------------
+constexpr int BK_THREADS = 256;
+constexpr int BK_WARPS = BK_THREADS / 32;  // one bucket per warp
+#ifndef BK_CAP_OVERRIDE
+constexpr unsigned BK_CAP = 2048;          // pairs per round
+#else
+constexpr unsigned BK_CAP = BK_CAP_OVERRIDE;
+#endif
+constexpr unsigned BK_SORT_MAX = 32;       // largest cell sorted by one thread (else: ballot ranking)
+// dynamic shared memory: cnt[2^(L+3)] | pos[BK_CAP] | key[BK_CAP] (u16, relative to c0)
+__host__ __device__ constexpr size_t bk_smem_bytes(int L) { return 4u * (1u << (L + 3)) + 4u * BK_CAP + 2u * BK_CAP; }
+
+#ifndef BK_MIN_CTAS
+#define BK_MIN_CTAS 5  // 48 registers: 5 CTAs/SM (r2_ab_bucket_*.txt)
+#endif
+template <int L>
+__global__ void __launch_bounds__(BK_THREADS, BK_MIN_CTAS)
+k_bucket_sort(const unsigned* __restrict__ keys, const unsigned* __restrict__ vals, Count cno, unsigned ncells,
+              const unsigned* __restrict__ kb, unsigned* __restrict__ G, unsigned* __restrict__ O) {
+  PDL_ENTRY();
+  constexpr unsigned NCB = 1u << L, NC = NCB * BK_WARPS;
+  constexpr int NG = NC >= 1024 ? (int)(NC / 1024) : 1;  // groups of 1024 cells: thread t owns 4t..4t+3
+  static_assert(L >= 2 && L <= 10, "bucket width");
+  extern __shared__ __align__(16) unsigned bk_dyn[];
+  unsigned* cnt = bk_dyn;
+  unsigned* pos = bk_dyn + NC;
+  unsigned short* key = reinterpret_cast<unsigned short*>(bk_dyn + NC + BK_CAP);
+
+  __shared__ unsigned wsum[NG][BK_WARPS];
+  __shared__ unsigned bst[BK_WARPS + 1];
+  __shared__ unsigned bmax[BK_WARPS];  // the largest cell count of each bucket
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned no = cno.get();
+  const unsigned c0 = blockIdx.x * NC;
+  const unsigned i0 = __ldg(&kb[blockIdx.x]), i1 = __ldg(&kb[blockIdx.x + 1]);
+  for (unsigned q = tid * 4; q < NC; q += BK_THREADS * 4) *reinterpret_cast<uint4*>(cnt + q) = make_uint4(0, 0, 0, 0);
+  if (tid < BK_WARPS) bmax[tid] = 0;
+  __syncthreads();
+  // 1. histogram. The first BK_CAP pairs (keys and values) are loaded once, up front: they are
+  // also the first round's data (step 3), so a CTA with <= BK_CAP pairs reads HBM once
+  constexpr int RV = BK_CAP / BK_THREADS;
+  unsigned kv[RV], vv[RV];
+#pragma unroll
+  for (int j = 0; j < RV; ++j) {
+    const unsigned i = i0 + j * BK_THREADS + tid;
+    kv[j] = i < i1 ? __ldg(keys + i) : 0u;
+    vv[j] = i < i1 ? __ldg(vals + i) : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < RV; ++j) {
+    if (i0 + j * BK_THREADS + tid < i1) {
+      PG_ASSERT(kv[j] >= c0 && kv[j] - c0 < NC);
+      atomicAdd(&cnt[kv[j] - c0], 1u);
+    }
+  }
+  for (unsigned base = i0 + BK_CAP; base < i1; base += 8 * BK_THREADS) {
+    unsigned k[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const unsigned i = base + j * BK_THREADS + tid;
+      k[j] = i < i1 ? __ldg(keys + i) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (base + j * BK_THREADS + tid < i1) {
+        PG_ASSERT(k[j] >= c0 && k[j] - c0 < NC);
+        atomicAdd(&cnt[k[j] - c0], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  // 2. exclusive scan of the counts, offset by i0: every group's warp scan at once (sums
+  // first, the counts are re-read for the offsets), one barrier
+  unsigned sum[NG], inc[NG];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    const unsigned q = (unsigned)(g * BK_THREADS + tid) * 4;
+    const uint4 a = q < NC ? reinterpret_cast<const uint4*>(cnt)[g * BK_THREADS + tid] : make_uint4(0, 0, 0, 0);
+    sum[g] = a.x + a.y + a.z + a.w;
+    inc[g] = sum[g];
+  }
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const unsigned o = __shfl_up_sync(0xffffffffu, inc[g], d);
+      if (lane >= d) inc[g] += o;
+    }
+  }
+  if (lane == 31) {
+#pragma unroll
+    for (int g = 0; g < NG; ++g) wsum[g][warp] = inc[g];
+  }
+  __syncthreads();
+  unsigned carry = i0;
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    unsigned wpre = 0, gtot = 0;
+#pragma unroll
+    for (int w = 0; w < BK_WARPS; ++w) {
+      const unsigned x = wsum[g][w];
+      wpre += w < warp ? x : 0u;
+      gtot += x;
+    }
+    const unsigned q = (unsigned)(g * BK_THREADS + tid) * 4;
+    if (q < NC) {
+      const uint4 a = reinterpret_cast<const uint4*>(cnt)[g * BK_THREADS + tid];
+      const unsigned v0 = carry + wpre + inc[g] - sum[g];
+      const uint4 v = make_uint4(v0, v0 + a.x, v0 + a.x + a.y, v0 + a.x + a.y + a.z);
+      reinterpret_cast<uint4*>(cnt)[g * BK_THREADS + tid] = v;  // the thread's own cells
+      const unsigned c = c0 + q;
+      if (c + 4 <= ncells) {
+        *reinterpret_cast<uint4*>(G + c) = v;
+      } else {
+        if (c < ncells) G[c] = v.x;
+        if (c + 1 < ncells) G[c + 1] = v.y;
+        if (c + 2 < ncells) G[c + 2] = v.z;
+      }
+      if ((q & (NCB - 1)) == 0) bst[q / NCB] = v0;  // a bucket's first cell (NCB >= 4)
+      const unsigned m = max(max(a.x, a.y), max(a.z, a.w));
+      if constexpr (NCB >= 128) {  // the warp's 128 cells lie in one bucket (and all of it runs here)
+        const unsigned wm = __reduce_max_sync(0xffffffffu, m);
+        if (lane == 0 && wm > 1) atomicMax(&bmax[q / NCB], wm);
+      } else {
+        if (m > 1) atomicMax(&bmax[q / NCB], m);
+      }
+    }
+    carry += gtot;
+  }
+  if (tid == 0) bst[BK_WARPS] = i1;
+  if (blockIdx.x == gridDim.x - 1 && tid == 0) G[ncells] = no;
+  __syncthreads();
+  // 3. rounds of whole buckets (or slices of one bucket larger than BK_CAP)
+  const unsigned lt = lanemask_lt();
+  __shared__ unsigned round[4];  // the round's end, first and past-last bucket, fast path
+  unsigned rb = i0;               // the round's first pair
+  while (rb < i1) {
+    if (tid == 0) {
+      int ba = 0;
+      while (ba < BK_WARPS && bst[ba + 1] <= rb) ++ba;  // skip finished / empty buckets
+      int bb = ba + 1;
+      unsigned re = min(bst[ba + 1], rb + BK_CAP);
+      if (re == bst[ba + 1]) {
+        while (bb < BK_WARPS && bst[bb + 1] - rb <= BK_CAP) ++bb;
+        re = bst[bb];
+      }
+      // whole buckets whose cells hold <= BK_SORT_MAX pairs each: slots by shared atomics,
+      // then each cell's values sorted back into generation order
+      unsigned m = 0;
+      for (int q = ba; q < bb; ++q) m = max(m, bmax[q]);
+      round[0] = re;
+      round[1] = (unsigned)ba;
+      round[2] = (unsigned)bb;
+      round[3] = bst[ba] == rb && re == bst[bb] && m <= BK_SORT_MAX;
+    }
+    __syncthreads();
+    const unsigned re = round[0];
+    const int ba = (int)round[1], bb = (int)round[2];
+    const bool fast = round[3] != 0;
+    const unsigned rn = re - rb;
+    if (rb != i0) {  // (the first round's pairs are already in registers)
+#pragma unroll
+      for (int j = 0; j < RV; ++j) {
+        const unsigned e = j * BK_THREADS + tid;
+        kv[j] = e < rn ? __ldg(keys + rb + e) : 0u;
+        vv[j] = e < rn ? __ldg(vals + rb + e) : 0u;
+      }
+    }
+    if (fast) {
+      // a cell's pairs come from distinct triangles in generation (= ascending value) order,
+      // so any slot order inside the cell followed by ranking its values is the stable order
+#pragma unroll
+      for (int j = 0; j < RV; ++j) {
+        const unsigned e = j * BK_THREADS + tid;
+        if (e < rn) {
+          const unsigned slot = atomicAdd(&cnt[kv[j] - c0], 1u) - rb;
+          PG_ASSERT(slot < rn);
+          pos[slot] = vv[j];
+        }
+      }
+      __syncthreads();
+      // each pair's rank inside its cell = the cell's values below its own (a cell holds
+      // <= BK_SORT_MAX pairs); the previous cell's slot counter is final: the cell's start
+#pragma unroll
+      for (int j = 0; j < RV; ++j) {
+        const unsigned e = j * BK_THREADS + tid;
+        if (e < rn) {
+          const unsigned c = kv[j] - c0, v = vv[j];
+          const unsigned s0 = c ? cnt[c - 1] : i0, s1 = cnt[c];
+          unsigned r = 0;
+          if (s1 - s0 > 1) {
+            for (unsigned x = s0; x < s1; ++x) r += pos[x - rb] < v;
+          }
+          O[s0 + r] = v;
+        }
+      }
+      __syncthreads();
+      rb = re;
+      continue;
+    }
+#pragma unroll
+    for (int j = 0; j < RV; ++j) {
+      const unsigned e = j * BK_THREADS + tid;
+      if (e < rn) key[e] = (unsigned short)(kv[j] - c0);
+    }
+    __syncthreads();
+    // warp w ranks bucket ba + w of the round (its pairs in [max(bst, rb), min(bst', re)))
+    if (ba + warp < bb) {
+      const int bk = ba + warp;
+      const unsigned s = max(bst[bk], rb) - rb, t = min(bst[bk + 1], re) - rb;
+      for (unsigned base = s; base < t; base += 32) {
+        const unsigned e = base + lane;
+        const bool ok = e < t;
+        const unsigned k = ok ? key[e] : 0u;
+        unsigned pm = __ballot_sync(0xffffffffu, ok);
+#pragma unroll 5  // (a full unroll at L = 10 crashes ptxas 12.9's register allocator)
+        for (int bit = 0; bit < L; ++bit) pm = peers_step(pm, k, 1u << bit);
+        const unsigned peers = ok ? pm : 0u;
+        const int leader = __ffs(peers | (1u << lane)) - 1;
+        unsigned old = 0;
+        if (ok && lane == leader) {
+          PG_ASSERT((k >> L) == (unsigned)bk);
+          old = cnt[k];
+          cnt[k] = old + __popc(peers);
+        }
+        old = __shfl_sync(0xffffffffu, old, leader);
+        if (ok) {
+          PG_ASSERT(old + __popc(peers & lt) >= bst[bk] && old + __popc(peers & lt) < bst[bk + 1]);
+          pos[e] = old + __popc(peers & lt);
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // the round's values into O: coalesced loads, stores inside the round's buckets
+#pragma unroll
+    for (int j = 0; j < RV; ++j) {
+      const unsigned e = j * BK_THREADS + tid;
+      if (e < rn) O[pos[e]] = vv[j];
+    }
+    __syncthreads();
+    rb = re;
+  }
+}
+
+// ----------------------------------------------------------------------------------------
 // The paper's comparison builders: "sorted" and "compact" grids
 // (builders.py:172-231). Both walk each triangle's whole cell box in one thread, which is
 // exactly the per-object load imbalance Alg. 1 removes; they produce the same

@@ -188,12 +188,18 @@ def test_launch_count_is_native():
     """The build runs our kernels: K1 + K2 + passes + K4 launches are reported."""
     mesh = gen_scene("uniform", 20000, 1)
     spec = spec_for_mesh(mesh)
-    builders.build_parallel(mesh, spec)
+    g, _ = builders.build_parallel(mesh, spec)
     b = _native.thread_builder()
     nbits = int(spec.ncells - 1).bit_length()
-    passes = (nbits + 8) // 9                         # 9-bit digits
-    # K1 + tile scan, tile bounds + K2, K4 + its bounds, and count/scan/scatter per pass
-    # (pass 0 counted by K2)
+    no = len(g.O)
+    # the MSD-first finish: buckets of 2^L cells (~256 pairs each, 2 <= L <= 10), passes over
+    # the top nbits - L bits, then k_bucket_sort (pgrid.cu local_bits)
+    L = 2
+    while L < 10 and L + 1 < nbits and no * (1 << (L + 1)) <= 256 * spec.ncells:
+        L += 1
+    passes = (nbits - L + 8) // 9                     # <= 9-bit digits
+    # K1 + tile scan, tile bounds + K2, count/scan/scatter per pass (pass 0 counted by K2),
+    # and k_bucket_sort + its bounds
     assert b.launches() == 5 + 3 * passes
 
 
