@@ -55,6 +55,10 @@ extern "C" {
                                   statistics are kept for pg_count_stats and the caller combines
                                   every rank's into the global verdict (the reference's checks
                                   apply to the whole mesh, not to one shard) */
+#define PG_GEN_ORDER 256u      /* pg_sort_cells_flags: the pairs are in generation order, so the
+                                  values ascend inside every cell (distinct triangle ids, object-
+                                  major emission): the MSD-first finish may rank a cell's pairs
+                                  by value instead of by position */
 
 /* Grid specification: the exact host doubles of GridSpec (gridcore.py:36-57). */
 typedef struct {
@@ -192,6 +196,9 @@ int pg_partition(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int6
                  uint32_t *slab_counts, void *stream);
 int pg_sort_cells(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int64_t n,
                   int64_t ncells, uint32_t *G, uint32_t *O, void *stream);
+/* pg_sort_cells with flags: PG_GEN_ORDER (the sharded build's received slab, rank-ordered) */
+int pg_sort_cells_flags(pg_builder *b, const uint32_t *keys, const uint32_t *vals, int64_t n,
+                        int64_t ncells, uint32_t flags, uint32_t *G, uint32_t *O, void *stream);
 
 /* Device-side small collectives of the sharded build over peer memory (no NCCL call, no host
  * round trip between the pair expansion and the slab plan; replaces the all-reduce of the

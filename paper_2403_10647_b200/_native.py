@@ -31,12 +31,13 @@ PG_CHECK = 16
 PG_ASYNC = 32
 PG_DEFER = 64
 PG_STATS = 128
+PG_GEN_ORDER = 256
 
 NPHASES = 6
 
 # every symbol include/pgrid.h declares (checked by tests/test_boundary.py)
 EXPORTS = ("pg_builder_create", "pg_builder_destroy", "pg_count", "pg_finish", "pg_stage",
-           "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_finish_baseline",
+           "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_sort_cells_flags", "pg_finish_baseline",
            "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_partition_counts", "pg_partition_send", "pg_peer_put", "pg_slab_plan", "pg_count_result",
            "pg_peer_put_count", "pg_coarse_hist", "pg_pairs_send", "pg_count_stats", "pg_features", "pg_phase_times",
            "pg_build_async",
@@ -91,6 +92,7 @@ def load():
         lib.pg_pairs.argtypes = [vp, vp, vp, u32, ctypes.c_int, ctypes.c_int, vp, vp]
         lib.pg_partition.argtypes = [vp, vp, vp, i64, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp]
         lib.pg_sort_cells.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp]
+        lib.pg_sort_cells_flags.argtypes = [vp, vp, vp, i64, i64, u32, vp, vp, vp]
         lib.pg_finish_baseline.argtypes = [vp, ctypes.c_int, vp, vp, u32, vp, ctypes.POINTER(ctypes.c_float),
                                            ctypes.POINTER(u64)]
         lib.pg_dda_prepare.argtypes = [vp, vp, i64, vp, i64, u32, vp]
@@ -127,7 +129,7 @@ def load():
         lib.pg_features.argtypes = []
         lib.pg_features.restype = ctypes.c_int
         for name in ("pg_builder_create", "pg_count", "pg_finish", "pg_stage",
-                     "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells",
+                     "pg_radix_sort_pairs", "pg_pairs", "pg_partition", "pg_sort_cells", "pg_sort_cells_flags",
                      "pg_finish_baseline", "pg_count_stats", "pg_dda_prepare", "pg_dda_cast", "pg_grid_stats", "pg_mesh_bounds", "pg_kernel_times", "pg_load_obj", "pg_obj_fetch", "pg_wait", "pg_kernel_timing", "pg_partition_counts", "pg_partition_send", "pg_peer_put", "pg_slab_plan",
            "pg_build_async", "pg_build_wait", "pg_host_register", "pg_host_unregister", "pg_host_alloc", "pg_host_free",
                      "pg_last_launch_count"):
@@ -345,9 +347,9 @@ class Builder:
                                           arr(*[int(x) for x in dst_vals]), arr(*[int(x) for x in dst_offset]),
                                           stream))
 
-    def sort_cells(self, keys, vals, n, ncells, G, O, stream=None):
-        check(self._lib.pg_sort_cells(self._h, ptr(keys), ptr(vals), int(n), int(ncells), ptr(G),
-                                      ptr(O), stream))
+    def sort_cells(self, keys, vals, n, ncells, G, O, stream=None, flags=0):
+        check(self._lib.pg_sort_cells_flags(self._h, ptr(keys), ptr(vals), int(n), int(ncells), flags, ptr(G),
+                                            ptr(O), stream))
 
 
 _tls = threading.local()

@@ -306,7 +306,7 @@ void launch_scatter_bits(unsigned ntiles, cudaStream_t st, const unsigned* kin, 
 // K4L over cell tiles of 8 buckets of 2^lbits cells (lbits 2..10)
 template <int L>
 int launch_bucket_sort_l(unsigned tiles, cudaStream_t st, const unsigned* keys, const unsigned* vals, Count cno,
-                         unsigned ncells, const unsigned* kb, unsigned* G, unsigned* O) {
+                         unsigned ncells, const unsigned* kb, unsigned* G, unsigned* O, int vals_ascend) {
   static bool attr = false;
   if (!attr) {
     CU(cudaFuncSetAttribute(k_bucket_sort<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_smem_bytes(L)));
@@ -314,14 +314,15 @@ int launch_bucket_sort_l(unsigned tiles, cudaStream_t st, const unsigned* keys, 
                             (int)cudaSharedmemCarveoutMaxShared));
     attr = true;
   }
-  pdl_launch(false, k_bucket_sort<L>, tiles, BK_THREADS, bk_smem_bytes(L), st, keys, vals, cno, ncells, kb, G, O);
+  pdl_launch(false, k_bucket_sort<L>, tiles, BK_THREADS, bk_smem_bytes(L), st, keys, vals, cno, ncells, kb, G, O,
+             vals_ascend);
   return PG_OK;
 }
 int launch_bucket_sort(int lbits, unsigned tiles, cudaStream_t st, const unsigned* keys, const unsigned* vals,
-                       Count cno, unsigned ncells, const unsigned* kb, unsigned* G, unsigned* O) {
+                       Count cno, unsigned ncells, const unsigned* kb, unsigned* G, unsigned* O, bool vals_ascend) {
   switch (lbits) {
 #define PG_BK(l) \
-  case l: return launch_bucket_sort_l<l>(tiles, st, keys, vals, cno, ncells, kb, G, O);
+  case l: return launch_bucket_sort_l<l>(tiles, st, keys, vals, cno, ncells, kb, G, O, vals_ascend ? 1 : 0);
     PG_BK(2) PG_BK(3) PG_BK(4) PG_BK(5) PG_BK(6) PG_BK(7) PG_BK(8) PG_BK(9) PG_BK(10)
 #undef PG_BK
     default: return fail(PG_INVARIANT_ERROR, "bucket width 2^%d", lbits);
@@ -1051,7 +1052,7 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
   const size_t hist_bytes = align_up(kMaxPasses * kMaxBins * 4);
   const size_t pb_bytes = align_up((size_t)std::max(rs_tiles, k2_tiles) * 8 + 8);
   // cell-tile bounds: K4's tiles, or k_bucket_sort's (8 buckets of 2^lb cells)
-  const size_t bk_tiles = lb >= 0 ? (size_t)((ncells + (8 << lb) - 1) / (8 << lb)) : 0;
+  const size_t bk_tiles = lb >= 0 ? (size_t)((ncells + (BK_WARPS << lb) - 1) / (BK_WARPS << lb)) : 0;
   const size_t kb_bytes = align_up((std::max<size_t>(g_tiles, bk_tiles) + 1) * 4);
   if ((rc = b->sort_sync.ensure(hist_bytes + pb_bytes + kb_bytes + (size_t)((rs_tiles + 3) & ~3u) * kMaxBins * 6)))
     return rc;
@@ -1121,11 +1122,13 @@ int finish_impl(pg_builder* b, uint32_t* G, uint32_t* O, uint32_t flags, cudaStr
     const unsigned* th = top ? hist + lp * kMaxBins : nullptr;
     const int tsh = top ? plan.shift[lp] : 0, tbins = top ? 1 << plan.bits[lp] : 0;
     if (lb >= 0) {
-      const unsigned step = 8u << lb, tiles = (unsigned)((ncells + step - 1) / step);
+      const unsigned step = (unsigned)BK_WARPS << lb, tiles = (unsigned)((ncells + step - 1) / step);
       pdl_launch(true, k_key_tile_bounds, (tiles + 1 + 7) / 8, 256, 0, st, sorted, cno, step, (unsigned)ncells,
                  tiles + 1, kbounds, th, tsh, tbins);
       LAUNCHED("k_key_tile_bounds", st);
-      if ((rc = launch_bucket_sort(lb, tiles, st, sorted, svals, cno, (unsigned)ncells, kbounds, dG, dO))) return rc;
+      // K2's pairs are in generation order: values ascend inside every cell
+      if ((rc = launch_bucket_sort(lb, tiles, st, sorted, svals, cno, (unsigned)ncells, kbounds, dG, dO, true)))
+        return rc;
       LAUNCHED("k_bucket_sort", st);
       b->launches += 2;
     } else {
@@ -1584,6 +1587,11 @@ int pg_partition(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int6
 
 int pg_sort_cells(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int64_t n, int64_t ncells, uint32_t* G,
                   uint32_t* O, void* stream_) {
+  return pg_sort_cells_flags(b, keys, vals, n, ncells, 0, G, O, stream_);
+}
+
+int pg_sort_cells_flags(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int64_t n, int64_t ncells,
+                        uint32_t flags, uint32_t* G, uint32_t* O, void* stream_) {
   NvtxRange nvtx_("pg_sort_cells");
   if (!b) return fail(PG_INVARIANT_ERROR, "null builder");
   if (ncells < 1 || ncells > kMaxScan) return fail(PG_SIZE_ERROR, "ncells out of range");
@@ -1591,7 +1599,10 @@ int pg_sort_cells(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   CU(cudaSetDevice(b->device));
   drop_graph(b);
-  const PassPlan plan = make_plan(bit_length((uint64_t)(ncells - 1)), kMaxDigitBits);
+  // the MSD-first finish (K4L) as in finish_impl; arbitrary values take its stable path
+  const int key_bits = bit_length((uint64_t)(ncells - 1));
+  const int lb = local_bits(key_bits, ncells, (uint64_t)n, 0);
+  const PassPlan plan = lb >= 0 ? make_plan_above(lb, key_bits, kMaxDigitBits) : make_plan(key_bits, kMaxDigitBits);
   const size_t sec = align_up(std::max<size_t>((size_t)n * 4, 16));
   int rc;
   if ((rc = b->pairs.ensure(4 * sec))) return rc;
@@ -1601,29 +1612,45 @@ int pg_sort_cells(pg_builder* b, const uint32_t* keys, const uint32_t* vals, int
   unsigned* vB = b->pairs.as<unsigned>(3 * sec);
   const unsigned rs_tiles = (unsigned)((n + RS_TILE - 1) / RS_TILE);
   const unsigned g_tiles = (unsigned)((ncells + G_TILE - 1) / G_TILE);
+  const unsigned step = lb >= 0 ? (unsigned)BK_WARPS << lb : (unsigned)G_TILE;
+  const unsigned tiles = (unsigned)((ncells + step - 1) / step);
   const size_t hist_bytes = align_up(kMaxPasses * kMaxBins * 4);
-  const size_t kb_bytes = align_up((size_t)(g_tiles + 1) * 4);
+  const size_t kb_bytes = align_up((size_t)(std::max(g_tiles, tiles) + 1) * 4);
   if ((rc = b->sort_sync.ensure(hist_bytes + kb_bytes + (size_t)((rs_tiles + 3) & ~3u) * kMaxBins * 4))) return rc;
   unsigned* hist = b->sort_sync.as<unsigned>(0);
   unsigned* kbounds = b->sort_sync.as<unsigned>(hist_bytes);
   unsigned* counts = b->sort_sync.as<unsigned>(hist_bytes + kb_bytes);
+  const Count cn{nullptr, (unsigned)n};
   const unsigned* sorted = keys;
+  const unsigned* svals = vals;
   if (n > 0) {
     if (plan.npasses == 0) {
-      CU(cudaMemcpyAsync(O, vals, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+      if (lb < 0) CU(cudaMemcpyAsync(O, vals, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
     } else {
       CU(cudaMemsetAsync(hist, 0, hist_bytes, st));
       // pass 0 reads the caller's (const) pairs; later passes ping-pong in the workspace
-      if ((rc = run_passes(b, plan, false, const_cast<unsigned*>(keys), const_cast<unsigned*>(vals), kB, vB, O,
-                           Count{nullptr, (unsigned)n}, (uint64_t)n, hist, counts, st, &sorted, kA, vA)))
+      if ((rc = run_passes(b, plan, false, const_cast<unsigned*>(keys), const_cast<unsigned*>(vals), kB, vB,
+                           lb >= 0 ? nullptr : O, cn, (uint64_t)n, hist, counts, st, &sorted, kA, vA, nullptr,
+                           &svals)))
         return rc;
     }
   }
-  k_key_tile_bounds<<<(g_tiles + 1 + 7) / 8, 256, 0, st>>>(sorted, Count{nullptr, (unsigned)n}, G_TILE,
-                                                          (unsigned)ncells, g_tiles + 1, kbounds);
+  const int lp = plan.npasses - 1;
+  const bool top = lp >= 0 && n > 0 && ncells > 1;
+  const unsigned* th = top ? hist + lp * kMaxBins : nullptr;
+  const int tsh = top ? plan.shift[lp] : 0, tbins = top ? 1 << plan.bits[lp] : 0;
+  pdl_launch(true, k_key_tile_bounds, (tiles + 1 + 7) / 8, 256, 0, st, sorted, cn, step, (unsigned)ncells, tiles + 1,
+             kbounds, th, tsh, tbins);
   LAUNCHED("k_key_tile_bounds", st);
-  k_cell_offsets<<<g_tiles, G_THREADS, 0, st>>>(sorted, Count{nullptr, (unsigned)n}, (unsigned)ncells, kbounds, G);
-  LAUNCHED("k_cell_offsets", st);
+  if (lb >= 0) {
+    if ((rc = launch_bucket_sort(lb, tiles, st, sorted, svals, cn, (unsigned)ncells, kbounds, G, O,
+                                 (flags & PG_GEN_ORDER) != 0)))
+      return rc;
+    LAUNCHED("k_bucket_sort", st);
+  } else {
+    pdl_launch(false, k_cell_offsets, g_tiles, G_THREADS, 0, st, sorted, cn, (unsigned)ncells, kbounds, G);
+    LAUNCHED("k_cell_offsets", st);
+  }
   b->launches += 2;
   return PG_OK;
 }

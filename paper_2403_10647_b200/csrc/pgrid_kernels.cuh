@@ -2090,7 +2090,11 @@ k_cell_offsets(const unsigned* __restrict__ sorted, Count cno, unsigned ncells, 
 //      replaces (primitives.py:97-113).
 // This replaces the last radix pass with its upsweep and row scan, the key write-back, and K4.
 // ----------------------------------------------------------------------------------------
+#ifndef BK_THREADS_OVERRIDE
 constexpr int BK_THREADS = 256;
+#else
+constexpr int BK_THREADS = BK_THREADS_OVERRIDE;
+#endif
 constexpr int BK_WARPS = BK_THREADS / 32;  // one bucket per warp
 #ifndef BK_CAP_OVERRIDE
 constexpr unsigned BK_CAP = 2048;          // pairs per round
@@ -2107,10 +2111,11 @@ __host__ __device__ constexpr size_t bk_smem_bytes(int L) { return 4u * (1u << (
 template <int L>
 __global__ void __launch_bounds__(BK_THREADS, BK_MIN_CTAS)
 k_bucket_sort(const unsigned* __restrict__ keys, const unsigned* __restrict__ vals, Count cno, unsigned ncells,
-              const unsigned* __restrict__ kb, unsigned* __restrict__ G, unsigned* __restrict__ O) {
+              const unsigned* __restrict__ kb, unsigned* __restrict__ G, unsigned* __restrict__ O, int vals_ascend) {
   PDL_ENTRY();
   constexpr unsigned NCB = 1u << L, NC = NCB * BK_WARPS;
-  constexpr int NG = NC >= 1024 ? (int)(NC / 1024) : 1;  // groups of 1024 cells: thread t owns 4t..4t+3
+  constexpr unsigned GC = 4u * BK_THREADS;  // cells per group: thread t owns 4t..4t+3 of each
+  constexpr int NG = NC >= GC ? (int)(NC / GC) : 1;
   static_assert(L >= 2 && L <= 10, "bucket width");
   extern __shared__ __align__(16) unsigned bk_dyn[];
   unsigned* cnt = bk_dyn;
@@ -2209,7 +2214,7 @@ k_bucket_sort(const unsigned* __restrict__ keys, const unsigned* __restrict__ va
       }
       if ((q & (NCB - 1)) == 0) bst[q / NCB] = v0;  // a bucket's first cell (NCB >= 4)
       const unsigned m = max(max(a.x, a.y), max(a.z, a.w));
-      if constexpr (NCB >= 128) {  // the warp's 128 cells lie in one bucket (and all of it runs here)
+      if constexpr (NCB >= 128 && NC >= GC) {  // the warp's 128 cells lie in one bucket (all lanes here)
         const unsigned wm = __reduce_max_sync(0xffffffffu, m);
         if (lane == 0 && wm > 1) atomicMax(&bmax[q / NCB], wm);
       } else {
@@ -2235,14 +2240,14 @@ k_bucket_sort(const unsigned* __restrict__ keys, const unsigned* __restrict__ va
         while (bb < BK_WARPS && bst[bb + 1] - rb <= BK_CAP) ++bb;
         re = bst[bb];
       }
-      // whole buckets whose cells hold <= BK_SORT_MAX pairs each: slots by shared atomics,
-      // then each cell's values sorted back into generation order
+      // whole buckets whose cells hold <= BK_SORT_MAX pairs each, values ascending in
+      // generation order (vals_ascend): slots by shared atomics, ranks by value
       unsigned m = 0;
       for (int q = ba; q < bb; ++q) m = max(m, bmax[q]);
       round[0] = re;
       round[1] = (unsigned)ba;
       round[2] = (unsigned)bb;
-      round[3] = bst[ba] == rb && re == bst[bb] && m <= BK_SORT_MAX;
+      round[3] = vals_ascend && bst[ba] == rb && re == bst[bb] && m <= BK_SORT_MAX;
     }
     __syncthreads();
     const unsigned re = round[0];

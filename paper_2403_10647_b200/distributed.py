@@ -866,8 +866,11 @@ class CudaOps:
         self.b.partition_send(keys, vals, n, self._ptab, shift, nslabs, self._pbase, dst_keys, dst_vals,
                               dst_offset, self._sp())
 
-    def sort_cells(self, keys, vals, n, ncells):
+    def sort_cells(self, keys, vals, n, ncells, gen_order=True):
         G = self._buf("G", ncells + 1)
         O = self._buf("O", n)
-        self.b.sort_cells(keys, vals, n, ncells, G, O, self._sp())
+        # the received slab is in generation order (stable partition, rank-ordered receive):
+        # the MSD-first finish may rank a cell's pairs by triangle id
+        self.b.sort_cells(keys, vals, n, ncells, G, O, self._sp(),
+                          flags=_native.PG_GEN_ORDER if gen_order else 0)
         return G, O

@@ -80,7 +80,7 @@ class NumpyOps:
         counts = np.bincount(slab, minlength=nslabs).astype(np.int64)
         return ko, np.asarray(vals, np.uint32)[order], counts
 
-    def sort_cells(self, keys, vals, n, ncells):
+    def sort_cells(self, keys, vals, n, ncells, gen_order=True):
         keys = self.to_numpy(keys)
         vals = self.to_numpy(vals)
         ks, vs = oracle.radix_sort_pairs(keys, vals, int(ncells - 1).bit_length())

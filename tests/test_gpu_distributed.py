@@ -106,15 +106,26 @@ def test_partition_kernel_is_stable_and_rebased():
     assert np.array_equal(ops.to_numpy(ko), (keys[order] - plan.cell_lo[slab[order]]).astype(np.uint32))
 
 
+@pytest.mark.parametrize("gen_order", [False, True])
 @pytest.mark.parametrize("ncells", [1, 2, 1000, 1 << 17, 3_000_001])
-def test_sort_cells_matches_oracle(ncells):
+def test_sort_cells_matches_oracle(ncells, gen_order):
+    """Arbitrary values (stable by position) and generation-ordered ones (PG_GEN_ORDER: values
+    ascend inside a cell, the MSD-first finish ranks them by value)."""
     ops = D.CudaOps()
     rng = np.random.default_rng(ncells)
     n = 200_000
     keys = rng.integers(0, ncells, n).astype(np.uint32)
     vals = rng.integers(0, 1 << 30, n).astype(np.uint32)
+    if gen_order:   # object-major emission: ids ascend along the pairs, distinct inside a cell
+        vals = np.sort(vals)
+        keys = keys[np.lexsort((keys, vals))]
+        _, first = np.unique(np.stack([keys, vals]), axis=1, return_index=True)
+        keep = np.zeros(n, bool)
+        keep[first] = True
+        keys, vals = keys[keep], vals[keep]
+        n = len(keys)
     G, O = ops.sort_cells(torch.from_numpy(keys.view(np.int32)).cuda(),
-                          torch.from_numpy(vals.view(np.int32)).cuda(), n, ncells)
+                          torch.from_numpy(vals.view(np.int32)).cuda(), n, ncells, gen_order=gen_order)
     ks, vs = oracle.radix_sort_pairs(keys, vals, int(ncells - 1).bit_length())
     Gr = np.zeros(ncells + 1, np.uint32)
     Gr[1:] = np.cumsum(np.bincount(ks.astype(np.int64), minlength=ncells))
