@@ -352,7 +352,7 @@ def run_sharded(args, world, rank, local):
             kt.setdefault(name, []).append(us * 1e-3)
     _native.kernel_timing(False)
     peak, peak_kind = peaks()
-    sc_name = "k_radix_scatter_wc" if "k_radix_scatter_wc" in kt else "k_radix_scatter"
+    sc_name = "k_radix_scatter"
     sc = kt.get(sc_name, [])
     sc_ms = float(np.mean(sc)) if sc else 0.0
     sc_bytes = 16 * no_local
