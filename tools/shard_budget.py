@@ -28,6 +28,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg5")
 ap.add_argument("--world", type=int, default=8)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--ktimes", action="store_true", help="per-kernel times of every rank's K2 + histogram (last rep)")
+ap.add_argument("--reverse", action="store_true", help="run the emulated ranks in reverse order")
 a = ap.parse_args()
 kind, n, seed, density = scenes.CONFIGS[a.config]
 mesh = scenes.gen_scene_large(kind, n, seed, density) if n > 20_000_000 else scenes.gen_scene(kind, n, seed, density)
@@ -79,12 +81,20 @@ for rep in range(a.reps + 1):
     # rep 0: host-checked counts (the verdict; learns the pair capacity); then deferred counts
     # (PG_DEFER: no host round trip inside K1), as the steady-state sharded build runs them
     t = {r: {} for r in range(P)}
-    hists, stats = [], []
-    for r, s in enumerate(states):
+    order = list(range(P))[::-1] if a.reverse else list(range(P))
+    stats = [None] * P
+    hists = [None] * P
+    for r in order:
+        s = states[r]
         st_r, t[r]["k1"] = timed(lambda: s.phase_count_only(cap))
-        stats.append(st_r)
+        stats[r] = st_r
+        if a.ktimes and rep == a.reps:
+            _native.kernel_timing(True)
         h, t[r]["k2_hist"] = timed(lambda: s.phase_pairs())
-        hists.append(h)
+        if a.ktimes and rep == a.reps:
+            print("rank", r, [(k, round(us, 1)) for k, us in _native.kernel_times()], file=sys.stderr)
+            _native.kernel_timing(False)
+        hists[r] = h
     if cap is None:
         D.count_verdict(np.sum(stats, axis=0), states[0].ncells)
         cap = int(max(s.no for s in states) * 1.25) + 4096
