@@ -2283,9 +2283,19 @@ k_bucket_sort(const unsigned* __restrict__ keys, const unsigned* __restrict__ va
         if (e < rn) {
           const unsigned c = kv[j] - c0, v = vv[j];
           const unsigned s0 = c ? cnt[c - 1] : i0, s1 = cnt[c];
+          // (cells of 1-4 pairs without a loop: 98% of the multi-pair cells in every config)
+          const unsigned nc = s1 - s0;
           unsigned r = 0;
-          if (s1 - s0 > 1) {
-            for (unsigned x = s0; x < s1; ++x) r += pos[x - rb] < v;
+          if (nc > 1) {
+            const unsigned* p = pos + (s0 - rb);
+            r = (p[0] < v) + (p[1] < v);
+            if (nc > 2) {
+              r += p[2] < v;
+              if (nc > 3) {
+                r += p[3] < v;
+                for (unsigned x = 4; x < nc; ++x) r += p[x] < v;
+              }
+            }
           }
           O[s0 + r] = v;
         }
