@@ -792,6 +792,13 @@ __device__ __forceinline__ void expand_tile(const uint4* __restrict__ rec, long 
       pt[u] = __ldg(&tile_pre[o / K1_TILE]);
     }
   }
+#ifndef PGRID_K2_PREF
+#define PGRID_K2_PREF 1
+#endif
+  if (PGRID_K2_PREF) {  // the later records towards L2 now (no registers held), loaded below
+    for (long long o = olo + 1 + tid + (long long)EXP_PRE * THREADS; o < oend; o += THREADS)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(rec + o));
+  }
   uint4 r0 = make_uint4(0u, 0u, 0u, 0u);
   if (tid == 0) r0 = __ldg(&rec[olo]);
   for (int i = tid; i < TILE; i += THREADS) slot[i] = -1;
