@@ -2085,15 +2085,20 @@ k_cell_offsets(const unsigned* __restrict__ sorted, Count cno, unsigned ncells, 
 // (stably: generation order inside a bucket), and a bucket's pairs occupy the same index range
 // in O as in the input. Each CTA owns 8 buckets = 2^(L+3) cells [c0, c0 + 2^(L+3)) and their
 // pairs [i0, i1) (k_key_tile_bounds: the lower bound is exact at bucket boundaries):
-//   1. count its pairs per cell (shared-memory histogram, coalesced key reads),
+//   1. count its pairs per cell (shared-memory histogram; the first BK_CAP pairs' keys and
+//      values are loaded once, into registers, for step 3 too),
 //   2. scan the counts: G for its cells (the reference's RLE -> scatter -> ExclusiveSum,
 //      builders.py:126-134); the counts become every cell's next O slot, and the buckets'
-//      pair ranges fall out of the same scan,
-//   3. in rounds of whole buckets (<= BK_CAP pairs; a larger bucket in slices), stage the
-//      round's keys in shared memory, let warp w rank bucket w (stable: 32 pairs at a time,
-//      bit-sliced ballots over the low L bits, the lowest lane of a cell's peers advances its
-//      slot) into shared-memory positions, then move the round's values to O with coalesced
-//      loads. Generation order is kept inside a cell, exactly as the stable LSD pass it
+//      pair ranges and largest cell counts fall out of the same scan,
+//   3. in rounds of whole buckets (<= BK_CAP pairs; a larger bucket in slices):
+//      - fast path (vals_ascend: the pairs are in generation order, so a cell's values are
+//        distinct, ascending triangle ids; cells <= BK_SORT_MAX pairs): every pair takes a slot
+//        in its cell with a shared atomic and parks its value there; its rank in the cell is
+//        the number of the cell's values below its own; O[cell start + rank] = value;
+//      - stable path (any values): the round's keys staged in shared memory, warp w ranks
+//        bucket w 32 pairs at a time (bit-sliced ballots over the low L bits, the lowest lane
+//        of a cell's peers advances its slot), then the round's values move to O.
+//      Either way generation order is kept inside a cell, exactly as the stable LSD pass it
 //      replaces (primitives.py:97-113).
 // This replaces the last radix pass with its upsweep and row scan, the key write-back, and K4.
 // ----------------------------------------------------------------------------------------
@@ -2108,7 +2113,7 @@ constexpr unsigned BK_CAP = 2048;          // pairs per round
 #else
 constexpr unsigned BK_CAP = BK_CAP_OVERRIDE;
 #endif
-constexpr unsigned BK_SORT_MAX = 32;       // largest cell sorted by one thread (else: ballot ranking)
+constexpr unsigned BK_SORT_MAX = 32;       // largest cell ranked by value (else: ballot ranking)
 // dynamic shared memory: cnt[2^(L+3)] | pos[BK_CAP] | key[BK_CAP] (u16, relative to c0)
 __host__ __device__ constexpr size_t bk_smem_bytes(int L) { return 4u * (1u << (L + 3)) + 4u * BK_CAP + 2u * BK_CAP; }
 
