@@ -30,6 +30,8 @@ ap.add_argument("--world", type=int, default=8)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--ktimes", action="store_true", help="per-kernel times of every rank's K2 + histogram (last rep)")
 ap.add_argument("--reverse", action="store_true", help="run the emulated ranks in reverse order")
+ap.add_argument("--reverse-timed", action="store_true",
+                help="allocate in rank order (rep 0) but time the ranks in reverse order")
 a = ap.parse_args()
 kind, n, seed, density = scenes.CONFIGS[a.config]
 mesh = scenes.gen_scene_large(kind, n, seed, density) if n > 20_000_000 else scenes.gen_scene(kind, n, seed, density)
@@ -81,7 +83,7 @@ for rep in range(a.reps + 1):
     # rep 0: host-checked counts (the verdict; learns the pair capacity); then deferred counts
     # (PG_DEFER: no host round trip inside K1), as the steady-state sharded build runs them
     t = {r: {} for r in range(P)}
-    order = list(range(P))[::-1] if a.reverse else list(range(P))
+    order = list(range(P))[::-1] if (a.reverse or (a.reverse_timed and rep > 0)) else list(range(P))
     stats = [None] * P
     hists = [None] * P
     for r in order:
