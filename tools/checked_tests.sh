@@ -10,4 +10,4 @@ echo "checked rc=$?" >> gpurun_out/checked_pytest.log
 PGRID_LIB=$PWD/paper_2403_10647_b200/_lib/libpgrid_checked.so timeout 900 python tools/sanitize_drive.py \
   > gpurun_out/checked_drive.log 2>&1
 echo "drive rc=$?" >> gpurun_out/checked_drive.log
-tail -3 gpurun_out/checked_pytest.log gpurun_out/checked_drive.log
+tail -n 3 gpurun_out/checked_pytest.log gpurun_out/checked_drive.log
