@@ -2243,23 +2243,29 @@ k_bucket_sort(const unsigned* __restrict__ keys, const unsigned* __restrict__ va
   __shared__ unsigned round[4];  // the round's end, first and past-last bucket, fast path
   unsigned rb = i0;               // the round's first pair
   while (rb < i1) {
-    if (tid == 0) {
-      int ba = 0;
-      while (ba < BK_WARPS && bst[ba + 1] <= rb) ++ba;  // skip finished / empty buckets
+    if (warp == 0) {  // lane b looks at bucket b: one load each, ballots instead of a serial walk
+      const bool in = lane < BK_WARPS;
+      const unsigned e1 = in ? bst[lane + 1] : 0xffffffffu;  // bucket lane's end
+      const unsigned bm = in ? bmax[lane] : 0u;
+      // first bucket not finished (every bucket ending <= rb is done or empty)
+      const int ba = __ffs(__ballot_sync(0xffffffffu, in && e1 > rb)) - 1;
+      const unsigned eba = __shfl_sync(0xffffffffu, e1, ba);
       int bb = ba + 1;
-      unsigned re = min(bst[ba + 1], rb + BK_CAP);
-      if (re == bst[ba + 1]) {
-        while (bb < BK_WARPS && bst[bb + 1] - rb <= BK_CAP) ++bb;
-        re = bst[bb];
+      unsigned re = min(eba, rb + BK_CAP);
+      if (re == eba) {  // whole buckets: extend while they fit in BK_CAP pairs
+        const unsigned fit = __ballot_sync(0xffffffffu, in && lane >= ba && e1 - rb <= BK_CAP);
+        bb = ba + __ffs(~(fit >> ba)) - 1;  // the run of fitting buckets from ba
+        re = __shfl_sync(0xffffffffu, e1, bb - 1);
       }
       // whole buckets whose cells hold <= BK_SORT_MAX pairs each, values ascending in
       // generation order (vals_ascend): slots by shared atomics, ranks by value
-      unsigned m = 0;
-      for (int q = ba; q < bb; ++q) m = max(m, bmax[q]);
-      round[0] = re;
-      round[1] = (unsigned)ba;
-      round[2] = (unsigned)bb;
-      round[3] = vals_ascend && bst[ba] == rb && re == bst[bb] && m <= BK_SORT_MAX;
+      const unsigned m = __reduce_max_sync(0xffffffffu, lane >= ba && lane < bb ? bm : 0u);
+      if (lane == 0) {
+        round[0] = re;
+        round[1] = (unsigned)ba;
+        round[2] = (unsigned)bb;
+        round[3] = vals_ascend && bst[ba] == rb && re == bst[bb] && m <= BK_SORT_MAX;
+      }
     }
     __syncthreads();
     const unsigned re = round[0];
