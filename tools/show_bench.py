@@ -1,4 +1,5 @@
-import json, sys
+import json, signal, sys
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)  # quiet when piped into head
 for line in open(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/bench.log"):
     line = line.strip()
     if not line.startswith("{"):
