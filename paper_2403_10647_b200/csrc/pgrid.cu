@@ -307,13 +307,15 @@ void launch_scatter_bits(unsigned ntiles, cudaStream_t st, const unsigned* kin, 
 template <int L>
 int launch_bucket_sort_l(unsigned tiles, cudaStream_t st, const unsigned* keys, const unsigned* vals, Count cno,
                          unsigned ncells, const unsigned* kb, unsigned* G, unsigned* O, int vals_ascend) {
-  static_assert(bk_smem_bytes(10) <= 48 * 1024, "K4L's dynamic shared memory needs no opt-in");
-  // the shared-memory carveout preference (5 CTAs/SM at 28 KB each), once per device
+  // the shared-memory carveout preference (5 CTAs/SM at 28 KB each) and, for tiles above 48 KB
+  // (only in BK_CAP variants), the opt-in: once per device
   static std::atomic<unsigned long long> done{0};
   int dev = 0;
   CU(cudaGetDevice(&dev));
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(done.load() & bit)) {
+    if constexpr (bk_smem_bytes(L) > 48 * 1024)
+      CU(cudaFuncSetAttribute(k_bucket_sort<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bk_smem_bytes(L)));
     CU(cudaFuncSetAttribute(k_bucket_sort<L>, cudaFuncAttributePreferredSharedMemoryCarveout,
                             (int)cudaSharedmemCarveoutMaxShared));
     done.fetch_or(bit);
