@@ -1,7 +1,7 @@
 mkdir -p gpurun_out
 : > gpurun_out/ab.log
 L=paper_2403_10647_b200/_lib
-for lib in libpgrid.so libpgrid_c4k.so libpgrid_c3k.so libpgrid.so libpgrid_c4k.so libpgrid_c3k.so; do
+for lib in libpgrid_prev.so libpgrid.so libpgrid_prev.so libpgrid.so; do
   echo "== $lib" >> gpurun_out/ab.log
   PGRID_LIB=$PWD/$L/$lib PGRID_KTIMES=1 timeout 300 python tools/ktimes.py >> gpurun_out/ab.log 2>&1
   PGRID_LIB=$PWD/$L/$lib timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ab_one.log 2>&1
